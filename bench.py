@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark: one projective-dynamics frame (30 local/global PD iterations) of the
+390K-tet synthetic sweater (BASELINE.json configs[2], "C3"), dt = 1/150 s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one frame.  value = whole-job tet-iters/s = N * nE * iterations * K /
+(max over ranks of the device time of the K frames).  Under torchrun (N > 1)
+every rank simulates its own copy of the scene (weak scaling, no data-path
+collective; the domain-decomposed multi-GPU step is tracked in DESIGN.md).
+
+`--impl reference` times the CPU oracle (numpy/scipy restatement of the
+reference `pd_step`, direct SuperLU solve) on the host cores, one PD iteration
+of the same scene per step (a bounded sample).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALG_BYTES_LOCAL = {"fp32": 70.0, "fp64": 125.0}   # SURVEY.md 8d, per tet-iteration
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
+    p.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    p.add_argument("--iterations", type=int, default=30)
+    p.add_argument("--tol", type=float, default=None)
+    p.add_argument("--no-flush", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-iters", type=int, default=3)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, ValueError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(sc, sample_iters):
+    """Oracle (numpy/scipy restatement of the reference pd_step, direct solve) on the host."""
+    from oracle import pd_oracle as orc
+    m = sc.mesh
+    gs, gv = sc.gammas.gamma_s, sc.gammas.gamma_v
+    K = orc.assemble_K(m.tets, m.shape_grad, m.volume, gs, gv, m.node_mass, sc.dt, m.n_nodes)
+    free = np.setdiff1d(np.arange(m.n_nodes), sc.pins)
+    solver = orc.GlobalSolver(K, free, sc.pins)
+    t0 = time.perf_counter()
+    orc.pd_step(m.nodes.copy(), np.zeros_like(m.nodes), sc.dt, m.tets, m.shape_grad, m.volume, gs, gv,
+                m.node_mass, solver, sc.pins, sc.pin_targets, sc.forces, sample_iters)
+    el = time.perf_counter() - t0
+    return {"value": m.n_elements * sample_iters / el, "unit": "tet-iters/s", "cores": 1,
+            "kind": "port",
+            "sample": f"{sample_iters} PD iterations of one {sc.name} frame (direct SuperLU global "
+                      f"solve, factorization excluded), {el:.1f} s on {os.cpu_count()} host cores "
+                      f"(numpy/scipy, effectively 1 core)",
+            "ms_per_frame_extrapolated": el / sample_iters * 30 * 1e3}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import pd_oracle as orc
+    from paper_2405_12484_b200 import scenes
+    sc = scenes.make_scene(args.config)
+    m = sc.mesh
+    gs, gv = sc.gammas.gamma_s, sc.gammas.gamma_v
+    K = orc.assemble_K(m.tets, m.shape_grad, m.volume, gs, gv, m.node_mass, sc.dt, m.n_nodes)
+    free = np.setdiff1d(np.arange(m.n_nodes), sc.pins)
+    solver = orc.GlobalSolver(K, free, sc.pins)
+    x, v = m.nodes.copy(), np.zeros_like(m.nodes)
+    per = 1   # PD iterations per bounded step
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        x2, v2 = orc.pd_step(x, v, sc.dt, m.tets, m.shape_grad, m.volume, gs, gv, m.node_mass, solver,
+                             sc.pins, sc.pin_targets, sc.forces, per)
+        el = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(el)
+        x, v = x2, v2
+    tot = sum(times)
+    val = m.n_elements * per * len(times) / tot
+    line = {
+        "impl": "reference", "metric": "tet-iters/s (PD local+global), 390K-tet sweater",
+        "value": val, "unit": "tet-iters/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3 * 30 / per,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": sc.name, "n_tets": m.n_elements,
+                                         "n_nodes": m.n_nodes, "pd_iterations": 30, "dt": sc.dt,
+                                         "solver": "direct (SuperLU)"},
+        "cpu_baseline": {"value": val, "unit": "tet-iters/s", "cores": 1, "kind": "port",
+                         "sample": f"{per} PD iteration of one frame per step, CPU oracle port "
+                                   f"({os.cpu_count()} host cores available, 1 used)"},
+        "e2e": {"value": val, "unit": "tet-iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2405_12484_b200 import _abi, pdsolver, scenes
+
+    sc = scenes.make_scene(args.config)
+    m = sc.mesh
+    ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s,
+                       sc.gammas.gamma_v, sc.pins, sc.dt, precision=args.precision,
+                       tol=args.tol if args.tol else pdsolver.DEFAULT_TOL[args.precision],
+                       device=local)
+    stream = torch.cuda.Stream()          # a real (non-default) stream shared with the library
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_state(m.nodes)
+    ctx.set_pin_targets(sc.pin_targets)
+    ctx.set_forces(sc.forces)
+    its = args.iterations
+
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32,
+                                                   device="cuda")
+    for _ in range(args.warmup):
+        ctx.step_async(its)
+    ctx.sync()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-timed frames (inputs resident), L2 flushed between frames
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    barrier()
+    clk.start()
+    time.sleep(0.3)
+    for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        starts[k].record(stream)
+        ctx.step_async(its)
+        ends[k].record(stream)
+    ctx.sync()
+    barrier()
+    clocks = clk.stop()
+    frame_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot_ms = sum(frame_ms)
+    st = ctx.stats()
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside
+    hf = torch.empty((m.n_nodes, 3), dtype=torch.float64, pin_memory=True).numpy()
+    hp = torch.empty((len(sc.pins), 3), dtype=torch.float64, pin_memory=True).numpy()
+    hx = torch.empty((m.n_nodes, 3), dtype=torch.float64, pin_memory=True).numpy()
+    hf[:] = sc.forces
+    hp[:] = sc.pin_targets
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        ctx.set_forces(hf)
+        ctx.set_pin_targets(hp)
+        ctx.step(its)
+        ctx.get_state(want_x=True, want_v=False, out_x=hx)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    h2d = hf.nbytes + hp.nbytes
+    d2h = hx.nbytes
+
+    # ---- per-kernel split (events around every launch, one extra frame, not in the timed region)
+    local_ms, global_ms, prof_frame_ms = ctx.profile_step(its)
+
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([tot_ms, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, e2e_s = float(t[0]), float(t[1])
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    nE = m.n_elements
+    value = world * nE * its * args.steps / (tot_ms * 1e-3)
+    e2e_val = world * nE * its * args.steps / e2e_s
+    peak, peak_kind = measured_peak()
+    alg = ALG_BYTES_LOCAL[args.precision] * nE
+    achieved = alg / (local_ms * 1e-3) / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(sc, args.cpu_sample_iters)
+    line = {
+        "metric": "tet-iters/s (PD local+global), 390K-tet sweater",
+        "value": value,
+        "unit": "tet-iters/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic",
+        "config": {"workload": sc.name, "n_tets": nE, "n_nodes": m.n_nodes, "pd_iterations": its,
+                   "dt": sc.dt, "solver": "direct-equivalent (device CG to tol)",
+                   "tol": ctx_tol(args), "parallelism": f"replicas x{world}",
+                   "l2": "flushed between frames" if flush is not None else "not flushed"},
+        "e2e": {"value": e2e_val, "unit": "tet-iters/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3 / args.steps},
+        "gpu_launches": args.steps * (2 * its + 2),
+        "roofline": {"bound": "hbm", "kernel": "k_local (PD local step)", "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "alg_bytes_per_launch": alg,
+                     "local_ms_per_launch": local_ms, "global_ms_per_launch": global_ms,
+                     "profiled_frame_ms": prof_frame_ms},
+        "clocks": clocks,
+        "solver_stats": {"cg_iters_last_frame": st["cg_iters_total"], "pcg_blocks": st["pcg_blocks"],
+                         "robust_elements_cum": st["robust"]},
+        "paper_ms_per_frame": 604.0,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def ctx_tol(args):
+    from paper_2405_12484_b200 import pdsolver
+    return args.tol if args.tol else pdsolver.DEFAULT_TOL[args.precision]
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,129 @@
+/*
+ * vkpd -- B200 (sm_100a) projective-dynamics step for the volumetric
+ * homogenized knit model (arXiv 2405.12484).  Plain C ABI: host pointers and
+ * sizes only, no PyTorch / CUDA types in the signatures (streams travel as
+ * `void*` = cudaStream_t).
+ *
+ * Each entry point replaces one reference interface (paths relative to
+ * /root/reference/pkg/src/volknit/):
+ *
+ *   vkpd_create           VolumeMesh operators + assemble_global + GlobalSolver(...)
+ *                         construction: pdsolver.py:42-56, 201-223, 734-742
+ *   vkpd_set_state /      SimState x, v (pdsolver.py:180-198)
+ *   vkpd_get_state
+ *   vkpd_set_pin_targets  SimState.pin_targets / per-step pin path (pdsolver.py:750-751)
+ *   vkpd_set_forces       per-step external forces (pdsolver.py:744-752)
+ *   vkpd_step             pd_step (pdsolver.py:257-304), no colliders
+ *   vkpd_elastic_rhs      elastic_rhs (pdsolver.py:59-71)
+ *   vkpd_global_solve     GlobalSolver.solve (pdsolver.py:225-246)
+ *   vkpd_apply_K          the assembled K (pdsolver.py:42-56) applied to a vector
+ *   vkpd_batch_projections material.batch_projections (material.py:395-407)
+ *
+ * Error convention (mirrors the reference's exceptions):
+ *   VKPD_OK          0
+ *   VKPD_EINVAL      1  invalid argument            -> ValueError
+ *   VKPD_ENONFINITE  2  non-finite positions at PD iteration *failed_iter
+ *                       -> RuntimeError("projective step produced non-finite
+ *                          positions at iteration {it}")
+ *   VKPD_ECUDA       3  CUDA error / no device       -> RuntimeError
+ * vkpd_last_error() returns a thread-local message for the last failure.
+ *
+ * A context is not re-entrant; one context per device per process.
+ */
+#ifndef VKPD_H
+#define VKPD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VKPD_OK 0
+#define VKPD_EINVAL 1
+#define VKPD_ENONFINITE 2
+#define VKPD_ECUDA 3
+
+#define VKPD_FP32 32
+#define VKPD_FP64 64
+
+typedef struct vkpd_ctx vkpd_ctx;
+
+typedef struct {
+    int64_t n_nodes;
+    int64_t n_tets;
+    const int64_t* tets;        /* (n_tets, 4) node ids, positive orientation        */
+    const double* shape_grad;   /* (n_tets, 4, 3) rest shape gradients (volmesh.py:87-91) */
+    const double* volume;       /* (n_tets,)  rest volumes, > 0                          */
+    const double* node_mass;    /* (n_nodes,) lumped masses                             */
+    const double* gamma_s;      /* (n_tets,)  >= 0                                       */
+    const double* gamma_v;      /* (n_tets,)  >= 0                                       */
+    const int64_t* pins;        /* (n_pins,) unique node ids, may be NULL if n_pins = 0  */
+    int64_t n_pins;
+    double dt;                  /* > 0 */
+} vkpd_mesh_desc;
+
+typedef struct {
+    int precision;     /* VKPD_FP32 or VKPD_FP64                                         */
+    double tol;        /* global-step relative residual tolerance (<= 0: default)        */
+    int max_iters;     /* CG iteration cap per global solve (<= 0: default 1000)         */
+    int device;        /* CUDA device ordinal                                            */
+    int pcg_blocks;    /* CTAs of the persistent solver (<= 0: one per SM)               */
+    int use_graph;     /* capture a whole frame in a CUDA graph (1, default) or not (0)  */
+} vkpd_config;
+
+typedef struct {
+    int n_pd_iters;            /* PD iterations of the last frame                         */
+    int cg_iters[256];         /* CG iterations of each global solve of the last frame     */
+    int cg_iters_total;
+    unsigned int robust;       /* elements re-solved on the robust scalar SL(3) path       */
+    unsigned int fallback;     /* robust path fell back to uniform scaling (warned)        */
+    int pcg_blocks;
+    int ell_width;
+    int64_t n_free;
+} vkpd_stats;
+
+const char* vkpd_last_error(void);
+int vkpd_device_count(int* count);
+
+int vkpd_create(const vkpd_mesh_desc* mesh, const vkpd_config* cfg, vkpd_ctx** out);
+/* matrix-only context: GlobalSolver(K, free, pins) with K in CSR (pdsolver.py:205-223);
+ * supports vkpd_global_solve / vkpd_apply_K / vkpd_get_matrix_csr only */
+int vkpd_create_matrix(int64_t n, const int64_t* indptr, const int64_t* indices, const double* data,
+                       const int64_t* pins, int64_t n_pins, const vkpd_config* cfg, vkpd_ctx** out);
+/* the device-assembled K as CSR in caller node order (free rows; all rows without pins).
+ * Call with indptr = NULL to query *nnz first. */
+int vkpd_get_matrix_csr(vkpd_ctx* ctx, int64_t* indptr, int64_t* indices, double* data, int64_t* nnz);
+void vkpd_destroy(vkpd_ctx* ctx);
+/* run subsequent work on this cudaStream_t (NULL: the context's own stream) */
+int vkpd_set_stream(vkpd_ctx* ctx, void* stream);
+void* vkpd_get_stream(vkpd_ctx* ctx);
+
+int vkpd_set_state(vkpd_ctx* ctx, const double* x, const double* v);      /* (nV,3) each; v may be NULL (= 0) */
+int vkpd_get_state(vkpd_ctx* ctx, double* x, double* v);                  /* either may be NULL */
+int vkpd_set_pin_targets(vkpd_ctx* ctx, const double* targets);           /* (n_pins,3) */
+int vkpd_set_forces(vkpd_ctx* ctx, const double* forces);                 /* (nV,3) or NULL = none */
+
+/* one implicit-Euler step by `iterations` local/global rounds; blocks until done.
+ * On VKPD_ENONFINITE the state is left as it was before the step. */
+int vkpd_step(vkpd_ctx* ctx, int iterations, double damping, int* failed_iter);
+/* same step, enqueued without waiting; vkpd_sync() reports the outcome */
+int vkpd_step_async(vkpd_ctx* ctx, int iterations, double damping);
+int vkpd_sync(vkpd_ctx* ctx, int* failed_iter);
+/* one frame launched kernel by kernel with CUDA events around every local-step and
+ * global-step launch (measurement only): average durations in ms */
+int vkpd_profile_step(vkpd_ctx* ctx, int iterations, double damping, double* local_ms,
+                      double* global_ms, double* frame_ms);
+
+int vkpd_elastic_rhs(vkpd_ctx* ctx, const double* x, double* rhs, double* F, double* R, double* V);
+int vkpd_global_solve(vkpd_ctx* ctx, const double* B, const double* pin_vals, double* X, int k);
+int vkpd_apply_K(vkpd_ctx* ctx, const double* X, double* Y);
+int vkpd_get_stats(vkpd_ctx* ctx, vkpd_stats* st);
+
+int vkpd_batch_projections(int precision, int64_t n, const double* F, double* R, double* V,
+                           unsigned int* n_robust, unsigned int* n_fallback);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VKPD_H */

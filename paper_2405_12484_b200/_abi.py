@@ -1,0 +1,294 @@
+"""ctypes binding of the C-ABI library `lib/libvkpd.so` (declared in include/vkpd.h).
+
+The library is the only compute path: if it is missing, or no CUDA device is
+visible, every entry point raises -- there is no host fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libvkpd.so")
+
+VKPD_OK, VKPD_EINVAL, VKPD_ENONFINITE, VKPD_ECUDA = 0, 1, 2, 3
+PRECISION = {"fp32": 32, "fp64": 64, 32: 32, 64: 64}
+
+EXPORTS = (
+    "vkpd_last_error", "vkpd_device_count", "vkpd_create", "vkpd_destroy", "vkpd_set_stream",
+    "vkpd_get_stream", "vkpd_set_state", "vkpd_get_state", "vkpd_set_pin_targets",
+    "vkpd_set_forces", "vkpd_step", "vkpd_step_async", "vkpd_sync", "vkpd_profile_step",
+    "vkpd_elastic_rhs", "vkpd_global_solve", "vkpd_apply_K", "vkpd_get_stats",
+    "vkpd_batch_projections", "vkpd_create_matrix", "vkpd_get_matrix_csr",
+)
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [
+        ("n_nodes", C.c_int64), ("n_tets", C.c_int64), ("tets", C.c_void_p),
+        ("shape_grad", C.c_void_p), ("volume", C.c_void_p), ("node_mass", C.c_void_p),
+        ("gamma_s", C.c_void_p), ("gamma_v", C.c_void_p), ("pins", C.c_void_p),
+        ("n_pins", C.c_int64), ("dt", C.c_double),
+    ]
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("precision", C.c_int), ("tol", C.c_double), ("max_iters", C.c_int), ("device", C.c_int),
+        ("pcg_blocks", C.c_int), ("use_graph", C.c_int),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("n_pd_iters", C.c_int), ("cg_iters", C.c_int * 256), ("cg_iters_total", C.c_int),
+        ("robust", C.c_uint), ("fallback", C.c_uint), ("pcg_blocks", C.c_int),
+        ("ell_width", C.c_int), ("n_free", C.c_int64),
+    ]
+
+
+_lib = None
+
+
+def load():
+    """Load the shared library (once).  Raises ImportError when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"vkpd CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+    lib = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    I = C.c_int
+    sig = {
+        "vkpd_last_error": (C.c_char_p, []),
+        "vkpd_device_count": (I, [C.POINTER(I)]),
+        "vkpd_create": (I, [C.POINTER(MeshDesc), C.POINTER(Config), C.POINTER(P)]),
+        "vkpd_destroy": (None, [P]),
+        "vkpd_set_stream": (I, [P, P]),
+        "vkpd_get_stream": (P, [P]),
+        "vkpd_set_state": (I, [P, P, P]),
+        "vkpd_get_state": (I, [P, P, P]),
+        "vkpd_set_pin_targets": (I, [P, P]),
+        "vkpd_set_forces": (I, [P, P]),
+        "vkpd_step": (I, [P, I, C.c_double, C.POINTER(I)]),
+        "vkpd_step_async": (I, [P, I, C.c_double]),
+        "vkpd_sync": (I, [P, C.POINTER(I)]),
+        "vkpd_profile_step": (I, [P, I, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double)]),
+        "vkpd_elastic_rhs": (I, [P, P, P, P, P, P]),
+        "vkpd_global_solve": (I, [P, P, P, P, I]),
+        "vkpd_apply_K": (I, [P, P, P]),
+        "vkpd_get_stats": (I, [P, C.POINTER(Stats)]),
+        "vkpd_batch_projections": (I, [I, C.c_int64, P, P, P, C.POINTER(C.c_uint), C.POINTER(C.c_uint)]),
+        "vkpd_create_matrix": (I, [C.c_int64, P, P, P, P, C.c_int64, C.POINTER(Config), C.POINTER(P)]),
+        "vkpd_get_matrix_csr": (I, [P, P, P, P, C.POINTER(C.c_int64)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class NonFiniteError(RuntimeError):
+    pass
+
+
+def check(rc):
+    if rc == VKPD_OK:
+        return
+    msg = load().vkpd_last_error().decode(errors="replace")
+    if rc == VKPD_EINVAL:
+        raise ValueError(msg)
+    if rc == VKPD_ENONFINITE:
+        raise NonFiniteError(msg)
+    raise RuntimeError(f"vkpd CUDA failure: {msg}")
+
+
+def ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None:
+        a = a.reshape(shape)
+    return a
+
+
+def device_count():
+    n = C.c_int(0)
+    load().vkpd_device_count(C.byref(n))
+    return n.value
+
+
+def batch_projections(F, precision="fp64"):
+    lib = load()
+    F = f64(F).reshape(-1, 3, 3)
+    R = np.empty_like(F)
+    V = np.empty_like(F)
+    nr, nf = C.c_uint(0), C.c_uint(0)
+    check(lib.vkpd_batch_projections(PRECISION[precision], F.shape[0], ptr(F), ptr(R), ptr(V),
+                                     C.byref(nr), C.byref(nf)))
+    if nf.value:
+        import logging
+        logging.getLogger("paper_2405_12484_b200.material").warning(
+            "volume projection Newton failed for %d elements, using uniform scaling", nf.value)
+    return R, V
+
+
+class Context:
+    """Owns one `vkpd_ctx` (device-resident scene)."""
+
+    def __init__(self, nodes_count, tets, shape_grad, volume, node_mass, gamma_s, gamma_v, pins,
+                 dt, precision="fp32", tol=0.0, max_iters=0, device=0, pcg_blocks=0, use_graph=True):
+        self.lib = load()
+        self._keep = dict(
+            tets=np.ascontiguousarray(tets, dtype=np.int64).reshape(-1, 4),
+            G=f64(shape_grad).reshape(-1, 4, 3),
+            vol=f64(volume).reshape(-1),
+            mass=None if node_mass is None else f64(node_mass).reshape(-1),
+            gs=f64(gamma_s).reshape(-1),
+            gv=f64(gamma_v).reshape(-1),
+            pins=np.ascontiguousarray(pins, dtype=np.int64).reshape(-1),
+        )
+        k = self._keep
+        self.n = int(nodes_count)
+        self.n_tets = k["tets"].shape[0]
+        self.n_pins = k["pins"].shape[0]
+        if k["mass"] is None:
+            raise ValueError("mesh node masses not lumped yet")
+        d = MeshDesc(self.n, self.n_tets, ptr(k["tets"]), ptr(k["G"]), ptr(k["vol"]), ptr(k["mass"]),
+                     ptr(k["gs"]), ptr(k["gv"]), ptr(k["pins"]) if self.n_pins else None,
+                     self.n_pins, float(dt))
+        cfg = Config(PRECISION[precision], float(tol), int(max_iters), int(device), int(pcg_blocks),
+                     1 if use_graph else 0)
+        h = C.c_void_p()
+        check(self.lib.vkpd_create(C.byref(d), C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.precision = precision
+        self.dt = float(dt)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.vkpd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:     # noqa: BLE001 - interpreter shutdown
+            pass
+
+    # -- state
+    def set_stream(self, stream_ptr):
+        check(self.lib.vkpd_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def set_state(self, x, v=None):
+        x = f64(x, (self.n, 3))
+        v = None if v is None else f64(v, (self.n, 3))
+        check(self.lib.vkpd_set_state(self.h, ptr(x), ptr(v)))
+
+    def get_state(self, want_x=True, want_v=True, out_x=None):
+        x = (np.empty((self.n, 3)) if out_x is None else out_x) if want_x else None
+        v = np.empty((self.n, 3)) if want_v else None
+        check(self.lib.vkpd_get_state(self.h, ptr(x), ptr(v)))
+        return x, v
+
+    def set_pin_targets(self, t):
+        if self.n_pins:
+            check(self.lib.vkpd_set_pin_targets(self.h, ptr(f64(t, (self.n_pins, 3)))))
+
+    def set_forces(self, f):
+        check(self.lib.vkpd_set_forces(self.h, None if f is None else ptr(f64(f, (self.n, 3)))))
+
+    def step(self, iterations, damping=1.0):
+        fi = C.c_int(-1)
+        rc = self.lib.vkpd_step(self.h, int(iterations), float(damping), C.byref(fi))
+        check(rc)
+
+    def step_async(self, iterations, damping=1.0):
+        check(self.lib.vkpd_step_async(self.h, int(iterations), float(damping)))
+
+    def sync(self):
+        fi = C.c_int(-1)
+        check(self.lib.vkpd_sync(self.h, C.byref(fi)))
+
+    def profile_step(self, iterations, damping=1.0):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        check(self.lib.vkpd_profile_step(self.h, int(iterations), float(damping), C.byref(a),
+                                         C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    # -- parity entry points
+    def elastic_rhs(self, x, with_frv=True):
+        x = f64(x, (self.n, 3))
+        rhs = np.empty((self.n, 3))
+        F = R = V = None
+        if with_frv:
+            F, R, V = (np.empty((self.n_tets, 3, 3)) for _ in range(3))
+        check(self.lib.vkpd_elastic_rhs(self.h, ptr(x), ptr(rhs), ptr(F), ptr(R), ptr(V)))
+        return rhs, F, R, V
+
+    def global_solve(self, B, pin_vals):
+        B = f64(B)
+        if B.ndim == 1:
+            B = B[:, None]
+        k = B.shape[1]
+        P = f64(pin_vals).reshape(self.n_pins, k) if self.n_pins else np.zeros((0, k))
+        X = np.empty_like(B)
+        check(self.lib.vkpd_global_solve(self.h, ptr(B), ptr(P), ptr(X), int(k)))
+        return X
+
+    def apply_K(self, X):
+        X = f64(X, (self.n, 3))
+        Y = np.empty_like(X)
+        check(self.lib.vkpd_apply_K(self.h, ptr(X), ptr(Y)))
+        return Y
+
+    def matrix_csr(self):
+        nnz = C.c_int64(0)
+        check(self.lib.vkpd_get_matrix_csr(self.h, None, None, None, C.byref(nnz)))
+        indptr = np.empty(self.n + 1, dtype=np.int64)
+        indices = np.empty(nnz.value, dtype=np.int64)
+        data = np.empty(nnz.value)
+        check(self.lib.vkpd_get_matrix_csr(self.h, ptr(indptr), ptr(indices), ptr(data), C.byref(nnz)))
+        return indptr, indices, data
+
+    def stats(self):
+        st = Stats()
+        check(self.lib.vkpd_get_stats(self.h, C.byref(st)))
+        n = st.n_pd_iters
+        return dict(cg_iters=list(st.cg_iters[:n]), cg_iters_total=st.cg_iters_total,
+                    robust=st.robust, fallback=st.fallback, pcg_blocks=st.pcg_blocks,
+                    ell_width=st.ell_width, n_free=st.n_free)
+
+
+class MatrixContext(Context):
+    """Matrix-only device context: `GlobalSolver(K, free, pins)` (pdsolver.py:205-246)."""
+
+    def __init__(self, K, pins, precision="fp64", tol=0.0, max_iters=0, device=0, pcg_blocks=0):
+        import scipy.sparse as sp
+        self.lib = load()
+        K = sp.csr_matrix(K)
+        K.sort_indices()
+        self.n = K.shape[0]
+        self.n_tets = 0
+        pins = np.ascontiguousarray(pins, dtype=np.int64).reshape(-1)
+        self.n_pins = len(pins)
+        self._keep = dict(indptr=np.ascontiguousarray(K.indptr, dtype=np.int64),
+                          indices=np.ascontiguousarray(K.indices, dtype=np.int64),
+                          data=f64(K.data), pins=pins)
+        k = self._keep
+        cfg = Config(PRECISION[precision], float(tol), int(max_iters), int(device), int(pcg_blocks), 0)
+        h = C.c_void_p()
+        check(self.lib.vkpd_create_matrix(self.n, ptr(k["indptr"]), ptr(k["indices"]), ptr(k["data"]),
+                                          ptr(pins) if self.n_pins else None, self.n_pins,
+                                          C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.precision = precision

@@ -1,0 +1,167 @@
+// PD local step (K2) and the projection kernel.
+//
+// One thread per tet: gather the four corner positions, F = Ds Dm^-1
+// (volmesh.py:115-118), rotation-variant SVD (material.py:127-137), volume
+// projection of the singular values (material.py:343-392, float64), then
+//   P = gs R + gv V = U diag(gs + gv s) W^T                    (pdsolver.py:67)
+// and the per-corner contributions 2 V P g_n                  (pdsolver.py:68)
+// written to a corner-major buffer `corner[a * nE + e]`; a deterministic
+// node-centric gather (no float atomics) sums them later in tet order.
+//
+// MODE_RESID writes 2V (P - (gs+gv) F) g_n instead: summed over a node and
+// added to (m/dt^2)(xhat - x) it is exactly b - K x, the global-step residual
+// at the current iterate (the `-K x` part is the frozen-projection Hessian
+// applied to x).  That lets the global step solve for the correction in
+// residual form, which is what makes float32 storage accurate enough.
+#pragma once
+
+#include "sl3.cuh"
+#include "svd3.cuh"
+#include "vk_common.cuh"
+
+namespace vk {
+
+enum LocalMode { MODE_RHS = 0, MODE_RESID = 1 };
+
+struct ProjStats {
+    unsigned int robust;     // elements re-solved on the scalar path
+    unsigned int fallback;   // robust path fell back to uniform scaling
+};
+
+__device__ __forceinline__ void count_path(ProjStats* st, int path) {
+    if (st == nullptr) return;
+    const unsigned int m1 = __ballot_sync(__activemask(), path >= 1);
+    const unsigned int m2 = __ballot_sync(__activemask(), path == 2);
+    const int lane = threadIdx.x & 31;
+    const unsigned int lead = __ffs(__activemask()) - 1;
+    if (lane == (int)lead) {
+        if (m1) atomicAdd(&st->robust, (unsigned int)__popc(m1));
+        if (m2) atomicAdd(&st->fallback, (unsigned int)__popc(m2));
+    }
+}
+
+// F -> (U, d, W) with P = U diag(d_i) W^T for d_i = a + b * s_i.  Returns path id.
+template <typename T>
+__device__ __forceinline__ int project_element(const T (&F)[3][3], T (&U)[3][3], T (&W)[3][3],
+                                               T (&sig)[3], double (&s)[3]) {
+    svd3_rv(F, U, sig, W);
+    const double sd[3] = {(double)sig[0], (double)sig[1], (double)sig[2]};
+    return sl3::project(sd, s);
+}
+
+// out = U diag(d) W^T
+template <typename T>
+__device__ __forceinline__ void udw(const T (&U)[3][3], const T (&d)[3], const T (&W)[3][3], T (&out)[3][3]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            out[i][j] = U[i][0] * d[0] * W[j][0] + U[i][1] * d[1] * W[j][1] + U[i][2] * d[2] * W[j][2];
+}
+
+template <typename T>
+struct LocalArgs {
+    int nE;
+    const int4* tets;            // internal node ids
+    const T* G;                  // 9 planes of nE: rows 1..3 of the shape gradient (= Dm^-1 rows)
+    const T* w;                  // 2 planes of nE: 2 V gs, 2 V gv
+    const vec4_t<T>* x;          // positions, internal order
+    vec4_t<T>* corner;           // 4 planes of nE
+    ProjStats* stats;
+    double* F_out;               // optional (nE,3,3) (RHS mode only)
+    double* R_out;
+    double* V_out;
+};
+
+template <typename T, int MODE, bool WITH_FRV>
+__global__ void __launch_bounds__(128) k_local(LocalArgs<T> a) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= a.nE) return;
+    const int nE = a.nE;
+    const int4 t = __ldg(&a.tets[e]);
+    T g[3][3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) g[k / 3][k % 3] = a.G[(size_t)k * nE + e];
+    const T ws = a.w[e], wv = a.w[(size_t)nE + e];
+    const vec4_t<T> x0 = ldg4(&a.x[t.x]);
+    const vec4_t<T> x1 = ldg4(&a.x[t.y]);
+    const vec4_t<T> x2 = ldg4(&a.x[t.z]);
+    const vec4_t<T> x3 = ldg4(&a.x[t.w]);
+    // edges x_n - x_0 (n = 1..3) as rows e[n-1][:]
+    const T ed[3][3] = {{x1.x - x0.x, x1.y - x0.y, x1.z - x0.z},
+                        {x2.x - x0.x, x2.y - x0.y, x2.z - x0.z},
+                        {x3.x - x0.x, x3.y - x0.y, x3.z - x0.z}};
+    T F[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            F[i][j] = ed[0][i] * g[0][j] + ed[1][i] * g[1][j] + ed[2][i] * g[2][j];
+
+    T U[3][3], W[3][3], sig[3];
+    double s[3];
+    const int path = project_element(F, U, W, sig, s);
+    count_path(a.stats, path);
+
+    const T d[3] = {ws + wv * (T)s[0], ws + wv * (T)s[1], ws + wv * (T)s[2]};
+    T P[3][3];
+    udw(U, d, W, P);
+    if (MODE == MODE_RESID) {
+        const T c = ws + wv;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) P[i][j] -= c * F[i][j];
+    }
+    if (WITH_FRV) {
+        const T one[3] = {T(1), T(1), T(1)};
+        const T sv[3] = {(T)s[0], (T)s[1], (T)s[2]};
+        T R[3][3], V[3][3];
+        udw(U, one, W, R);
+        udw(U, sv, W, V);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            a.F_out[(size_t)e * 9 + k] = (double)F[k / 3][k % 3];
+            a.R_out[(size_t)e * 9 + k] = (double)R[k / 3][k % 3];
+            a.V_out[(size_t)e * 9 + k] = (double)V[k / 3][k % 3];
+        }
+    }
+    // f_n = P g_n for n = 1..3, f_0 = -(f_1 + f_2 + f_3)
+    T f[3][3];
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) f[n][i] = P[i][0] * g[n][0] + P[i][1] * g[n][1] + P[i][2] * g[n][2];
+    st4(&a.corner[e], make4<T>(-(f[0][0] + f[1][0] + f[2][0]), -(f[0][1] + f[1][1] + f[2][1]),
+                               -(f[0][2] + f[1][2] + f[2][2]), T(0)));
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+        st4(&a.corner[(size_t)(n + 1) * nE + e], make4<T>(f[n][0], f[n][1], f[n][2], T(0)));
+}
+
+// Stateless projections of a batch of F (material.py:395-407): (R, V).
+template <typename T>
+__global__ void __launch_bounds__(128) k_project(int n, const double* __restrict__ Fin, double* R, double* V,
+                                                 ProjStats* stats) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    T F[3][3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) F[k / 3][k % 3] = (T)Fin[(size_t)e * 9 + k];
+    T U[3][3], W[3][3], sig[3];
+    double s[3];
+    const int path = project_element(F, U, W, sig, s);
+    count_path(stats, path);
+    const T one[3] = {T(1), T(1), T(1)};
+    const T sv[3] = {(T)s[0], (T)s[1], (T)s[2]};
+    T Rm[3][3], Vm[3][3];
+    udw(U, one, W, Rm);
+    udw(U, sv, W, Vm);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        R[(size_t)e * 9 + k] = (double)Rm[k / 3][k % 3];
+        V[(size_t)e * 9 + k] = (double)Vm[k / 3][k % 3];
+    }
+}
+
+}  // namespace vk

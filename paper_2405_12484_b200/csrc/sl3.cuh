@@ -1,0 +1,286 @@
+// Volume (SL(3)) projection in singular-value space, per thread, in float64.
+//
+//   min |s - sigma|^2  s.t.  s0 s1 s2 = 1,  s_i >= 0.01
+//
+// Restates, per element, the reference's batched solve
+// `sl3_sigma_project_batch` (material.py:343-392) with its KKT Newton
+// `_sl3_batch_newton` (309-340), and the robust multi-start scalar path
+// `sl3_sigma_project` (242-287) with `_sl3_solve_clamping` (217-239) and
+// `_sl3_newton_free` (171-214).  All thresholds are the reference's, verbatim;
+// the arithmetic is always float64 (also in the fp32 build), so the branch
+// decisions (second start, "suspicious" re-solve, clamping) are the
+// reference's decisions for the same sigma.
+//
+// Deviation (documented in DESIGN.md): a singular 4x4 KKT Jacobian fails only
+// that element's Newton (ok = false); the reference's batched
+// `np.linalg.solve` raises for the whole batch and re-solves every element on
+// the scalar path.
+#pragma once
+
+#include <math.h>
+
+#include "vk_common.cuh"
+
+namespace vk {
+namespace sl3 {
+
+constexpr double kFloor = 0.01;     // material.py:25
+constexpr double kTol = 1e-12;      // material.py:30
+constexpr int kIters = 20;          // material.py:29
+
+VK_HD double nanmax(double m, double a) { return (a > m || a != a) ? a : m; }
+
+VK_HD void pairprod(const double (&s)[3], double (&p)[3]) {
+    p[0] = s[1] * s[2];
+    p[1] = s[0] * s[2];
+    p[2] = s[0] * s[1];
+}
+
+// Gaussian elimination with partial pivoting on an n x n system (n <= 4);
+// false when a pivot is exactly zero (LAPACK gesv info > 0).
+VK_HD bool gesv(double (&A)[4][4], double (&b)[4], int n) {
+    for (int k = 0; k < n; ++k) {
+        int piv = k;
+        double best = fabs(A[k][k]);
+        for (int i = k + 1; i < n; ++i) {
+            const double v = fabs(A[i][k]);
+            if (v > best) { best = v; piv = i; }
+        }
+        if (piv != k) {
+            for (int j = 0; j < 4; ++j) { const double t = A[k][j]; A[k][j] = A[piv][j]; A[piv][j] = t; }
+            const double t = b[k]; b[k] = b[piv]; b[piv] = t;
+        }
+        if (A[k][k] == 0.0) return false;
+        const double inv = 1.0 / A[k][k];
+        for (int i = k + 1; i < n; ++i) {
+            const double f = A[i][k] * inv;
+            if (f != 0.0) {
+                for (int j = k + 1; j < n; ++j) A[i][j] -= f * A[k][j];
+                b[i] -= f * b[k];
+            }
+        }
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        double v = b[k];
+        for (int j = k + 1; j < n; ++j) v -= A[k][j] * b[j];
+        b[k] = v / A[k][k];
+    }
+    return true;
+}
+
+// One element of `_sl3_batch_newton` (material.py:309-340): unclamped KKT
+// Newton on (s, lam) from start s; returns ok.
+VK_HD bool kkt_newton(const double (&sig)[3], double (&s)[3], double& lam) {
+    double p[3];
+    pairprod(s, p);
+    const double denom = fmax(p[0] * p[0] + p[1] * p[1] + p[2] * p[2], 1e-300);
+    lam = (s[0] * s[1] * s[2] - 1.0) / denom;
+    for (int it = 0; it < kIters; ++it) {
+        pairprod(s, p);
+        double r[4];
+        for (int i = 0; i < 3; ++i) r[i] = s[i] - sig[i] + lam * p[i];
+        r[3] = s[0] * s[1] * s[2] - 1.0;
+        double rn = 0.0;
+        for (int i = 0; i < 4; ++i) rn = nanmax(rn, fabs(r[i]));
+        if (rn < kTol) break;
+        double J[4][4] = {{1.0, lam * s[2], lam * s[1], p[0]},
+                          {lam * s[2], 1.0, lam * s[0], p[1]},
+                          {lam * s[1], lam * s[0], 1.0, p[2]},
+                          {p[0], p[1], p[2], 0.0}};
+        double d[4] = {-r[0], -r[1], -r[2], -r[3]};
+        if (!gesv(J, d, 4)) return false;
+        s[0] += d[0]; s[1] += d[1]; s[2] += d[2];
+        lam += d[3];
+    }
+    pairprod(s, p);
+    double r3 = 0.0;
+    for (int i = 0; i < 3; ++i) r3 = nanmax(r3, fabs(s[i] - sig[i] + lam * p[i]));
+    const double rc = fabs(s[0] * s[1] * s[2] - 1.0);
+    const bool fin = isfinite(s[0]) && isfinite(s[1]) && isfinite(s[2]);
+    return (nanmax(r3, rc) < 1e-10) && fin;
+}
+
+VK_HD double sq3(const double (&a)[3], const double (&b)[3]) {
+    const double d0 = a[0] - b[0], d1 = a[1] - b[1], d2 = a[2] - b[2];
+    return d0 * d0 + d1 * d1 + d2 * d2;
+}
+VK_HD double nanmin3(const double (&a)[3]) {
+    double m = a[0];
+    for (int i = 1; i < 3; ++i) m = (a[i] < m || a[i] != a[i]) ? a[i] : m;
+    return m;
+}
+VK_HD int argmin3(const double (&a)[3]) {
+    int j = 0;
+    if (a[1] < a[j]) j = 1;
+    if (a[2] < a[j]) j = 2;
+    return j;
+}
+
+// residual of the frozen-entry system (material.py:163-168), max-norm over free + constraint
+VK_HD double free_resnorm(const double (&sig)[3], const double (&s)[3], double lam,
+                                               const bool (&fr)[3]) {
+    double p[3];
+    pairprod(s, p);
+    double rn = fabs(s[0] * s[1] * s[2] - 1.0);
+    for (int i = 0; i < 3; ++i)
+        if (fr[i]) rn = nanmax(rn, fabs(s[i] - sig[i] + lam * p[i]));
+    return rn;
+}
+
+// `_sl3_newton_free` (material.py:171-214)
+VK_HDNI bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, const bool (&fr)[3]) {
+    int idx[3], nf = 0;
+    for (int i = 0; i < 3; ++i) if (fr[i]) idx[nf++] = i;
+    if (nf == 0) return false;
+    for (int it = 0; it < kIters; ++it) {
+        const double rn = free_resnorm(sig, s, lam, fr);
+        if (rn < kTol) return true;
+        double p[3];
+        pairprod(s, p);
+        double J[4][4] = {{0.0}};
+        double d[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int a = 0; a < nf; ++a) {
+            const int i = idx[a];
+            for (int b = 0; b < nf; ++b) {
+                const int j = idx[b];
+                J[a][b] = (i == j) ? 1.0 : lam * s[3 - i - j];
+            }
+            J[a][nf] = p[i];
+            J[nf][a] = p[i];
+            d[a] = -(s[i] - sig[i] + lam * p[i]);
+        }
+        d[nf] = -(s[0] * s[1] * s[2] - 1.0);
+        if (!gesv(J, d, nf + 1)) return false;
+        double step = 1.0;
+        double sn[3], ln = lam;
+        for (int t = 0; t < 6; ++t) {
+            sn[0] = s[0]; sn[1] = s[1]; sn[2] = s[2];
+            for (int a = 0; a < nf; ++a) sn[idx[a]] = s[idx[a]] + step * d[a];
+            ln = lam + step * d[nf];
+            const double rn_new = free_resnorm(sig, sn, ln, fr);
+            if (rn_new < rn || rn_new < kTol) break;
+            step *= 0.5;
+        }
+        s[0] = sn[0]; s[1] = sn[1]; s[2] = sn[2];
+        lam = ln;
+    }
+    return free_resnorm(sig, s, lam, fr) < 1e-10;
+}
+
+// `_sl3_solve_clamping` (material.py:217-239); returns false for "None"
+VK_HDNI bool solve_clamping(const double (&sig)[3], double (&s)[3], double& lam) {
+    bool fr[3] = {true, true, true};
+    for (int round = 0; round < 3; ++round) {
+        for (int i = 0; i < 3; ++i) if (!fr[i]) s[i] = kFloor;
+        if (!newton_free(sig, s, lam, fr)) return false;
+        bool viol[3], any = false;
+        for (int i = 0; i < 3; ++i) { viol[i] = fr[i] && (s[i] < kFloor - 1e-12); any |= viol[i]; }
+        if (!any) return true;
+        int nfree = 0, last = -1;
+        for (int i = 0; i < 3; ++i) { fr[i] = fr[i] && !viol[i]; if (fr[i]) { ++nfree; last = i; } }
+        if (nfree == 1) {
+            s[0] = s[1] = s[2] = kFloor;
+            s[last] = 1.0 / (kFloor * kFloor);
+            double p[3];
+            pairprod(s, p);
+            lam = (sig[last] - s[last]) / p[last];
+            return true;
+        }
+    }
+    return false;
+}
+
+// `sl3_sigma_project` (material.py:242-287); returns ok (false = uniform-scaling fallback)
+VK_HDNI bool project_robust(const double (&sig)[3], double (&out)[3]) {
+    double starts[4][3];
+    int ns = 0;
+    for (int i = 0; i < 3; ++i) starts[0][i] = fmax(sig[i], kFloor);
+    starts[1][0] = starts[1][1] = starts[1][2] = 1.0;
+    ns = 2;
+    const double prod = sig[0] * sig[1] * sig[2];
+    if (prod > 1e-12) {
+        const double c = cbrt(prod);
+        for (int i = 0; i < 3; ++i) starts[ns][i] = fmax(sig[i] / c, kFloor);
+        ++ns;
+    }
+    if (prod > 1.0) {
+        const int j = argmin3(sig);
+        double others = 1.0;
+        for (int i = 0; i < 3; ++i) if (i != j) others *= sig[i];
+        if (others > 1e-12) {
+            for (int i = 0; i < 3; ++i) starts[ns][i] = fmax(sig[i], kFloor);
+            starts[ns][j] = fmax(1.0 / others, kFloor);
+            ++ns;
+        }
+    }
+    bool have = false;
+    double best = 0.0;
+    for (int k = 0; k < ns; ++k) {
+        double s[3] = {starts[k][0], starts[k][1], starts[k][2]};
+        double p[3];
+        pairprod(s, p);
+        const double den = p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
+        double lam = den > 1e-300 ? (s[0] * s[1] * s[2] - 1.0) / den : 0.0;
+        if (!solve_clamping(sig, s, lam)) continue;
+        if (nanmin3(s) < kFloor - 1e-9 || fabs(s[0] * s[1] * s[2] - 1.0) > 1e-8) continue;
+        const double obj = sq3(s, sig);
+        if (!have || obj < best - 1e-15) {
+            have = true;
+            best = obj;
+            out[0] = s[0]; out[1] = s[1]; out[2] = s[2];
+        }
+    }
+    if (have) return true;
+    double s[3];
+    for (int i = 0; i < 3; ++i) s[i] = fmax(fabs(sig[i]), kFloor);
+    for (int r = 0; r < 3; ++r) {
+        const double c = cbrt(s[0] * s[1] * s[2]);
+        for (int i = 0; i < 3; ++i) s[i] = fmax(s[i] / c, kFloor);
+    }
+    out[0] = s[0]; out[1] = s[1]; out[2] = s[2];
+    return false;
+}
+
+// Per-element `sl3_sigma_project_batch` (material.py:343-392).
+// Returns 0 = batch Newton result, 1 = robust path, 2 = robust path fell back
+// to uniform scaling (the reference logs a warning).
+VK_HD int project(const double (&sig)[3], double (&s)[3]) {
+    for (int i = 0; i < 3; ++i) s[i] = fmax(sig[i], kFloor);
+    double lam;
+    const bool ok = kkt_newton(sig, s, lam);
+    bool feas = ok && (nanmin3(s) >= kFloor - 1e-12);
+    double obj = feas ? sq3(s, sig) : INFINITY;
+    const double prod = sig[0] * sig[1] * sig[2];
+    if (prod > 1.0) {
+        const int j = argmin3(sig);
+        const double others = prod / fmax(sig[j], 1e-300);
+        double s2[3];
+        for (int i = 0; i < 3; ++i) s2[i] = fmax(sig[i], kFloor);
+        s2[j] = fmax(1.0 / fmax(others, 1e-12), kFloor);
+        double lam2;
+        const bool ok2 = kkt_newton(sig, s2, lam2);
+        const double obj2 = sq3(s2, sig);
+        if (ok2 && nanmin3(s2) >= kFloor - 1e-12 && obj2 < obj - 1e-15) {
+            s[0] = s2[0]; s[1] = s2[1]; s[2] = s2[2];
+            obj = obj2;
+            feas = true;
+        }
+    }
+    double mn = nanmin3(sig);
+    double mx = fmax(fmax(fabs(sig[0]), fabs(sig[1])), fabs(sig[2]));
+    bool odd = !feas || (mn < 0.2) || (mx > 5.0);
+    if (!odd && prod > 1e-12) {
+        const double c = cbrt(fmax(prod, 1e-300));
+        const double r0 = sig[0] / c, r1 = sig[1] / c, r2 = sig[2] / c;
+        if (fmin(fmin(r0, r1), r2) >= kFloor) {
+            const double oref = (r0 - sig[0]) * (r0 - sig[0]) + (r1 - sig[1]) * (r1 - sig[1]) +
+                                (r2 - sig[2]) * (r2 - sig[2]);
+            odd = obj > oref + 1e-12;
+        }
+    }
+    if (!odd) return 0;
+    return project_robust(sig, s) ? 1 : 2;
+}
+
+}  // namespace sl3
+}  // namespace vk

@@ -1,0 +1,368 @@
+// Global step (K1/K6/K7 of SURVEY.md section 2): matrix assembly, step
+// prologue/epilogue and the persistent preconditioned-CG kernel.
+//
+// Node order on the device ("internal"): free nodes first, in the caller's
+// order, then the pinned nodes in pin order.  The scalar global matrix
+// K = M/dt^2 + sum_e 2V(gs+gv) G G^T (pdsolver.py:42-56) is kept as K_ff in
+// column-major ELL over the free rows (free columns only), so pinned values
+// are eliminated exactly as GlobalSolver does (pdsolver.py:210-229).
+#pragma once
+
+#include "vk_common.cuh"
+
+namespace vk {
+
+// ---------------------------------------------------------------------------
+// K_ff assembly, one thread per free row; deterministic (incidences in tet order).
+template <typename T>
+struct AssembleArgs {
+    int nF, nE, ell_w;
+    const int* inc_ptr;          // (n+1) per internal node
+    const int* inc_code;         // a * nE + e, sorted by e
+    const int4* tets;            // internal ids
+    const double* G;             // (nE,4,3) float64 shape gradients (host layout)
+    const double* wsum;          // (nE) 2 V (gs + gv)
+    const double* m_dt2;         // (n) m / dt^2, internal order
+    const int* ell_col;          // [s * nF + i]
+    T* ell_val;
+    T* inv_diag;                 // (nF)
+    double* diag64;              // (nF) float64 diagonal (A-Jacobi / reference-compat paths)
+    // K_fp in CSR over free rows (columns are pin slots 0..nP-1)
+    const int* fp_ptr;
+    const int* fp_col;
+    T* fp_val;
+    int n_free_cols_base;        // = nF: internal id of the first pinned node
+};
+
+template <typename T>
+__global__ void k_assemble(AssembleArgs<T> a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.nF) return;
+    const int b0 = a.inc_ptr[i], b1 = a.inc_ptr[i + 1];
+    double diag = a.m_dt2[i];
+    for (int s = 0; s < a.ell_w; ++s) {
+        const int col = a.ell_col[(size_t)s * a.nF + i];
+        double v = 0.0;
+        if (col >= 0) {
+            for (int k = b0; k < b1; ++k) {
+                const int code = a.inc_code[k];
+                const int e = code % a.nE, an = code / a.nE;
+                const int4 t = a.tets[e];
+                const int nodes[4] = {t.x, t.y, t.z, t.w};
+                for (int bn = 0; bn < 4; ++bn) {
+                    if (nodes[bn] == col) {
+                        const double* g = a.G + (size_t)e * 12;
+                        v += a.wsum[e] * (g[an * 3 + 0] * g[bn * 3 + 0] + g[an * 3 + 1] * g[bn * 3 + 1] +
+                                          g[an * 3 + 2] * g[bn * 3 + 2]);
+                    }
+                }
+            }
+            if (col == i) { v += diag; diag = v; }
+        }
+        a.ell_val[(size_t)s * a.nF + i] = (T)v;
+    }
+    a.inv_diag[i] = (T)(1.0 / diag);
+    a.diag64[i] = diag;
+    for (int k = a.fp_ptr[i]; k < a.fp_ptr[i + 1]; ++k) {
+        const int col = a.n_free_cols_base + a.fp_col[k];
+        double v = 0.0;
+        for (int kk = b0; kk < b1; ++kk) {
+            const int code = a.inc_code[kk];
+            const int e = code % a.nE, an = code / a.nE;
+            const int4 t = a.tets[e];
+            const int nodes[4] = {t.x, t.y, t.z, t.w};
+            for (int bn = 0; bn < 4; ++bn)
+                if (nodes[bn] == col) {
+                    const double* g = a.G + (size_t)e * 12;
+                    v += a.wsum[e] * (g[an * 3 + 0] * g[bn * 3 + 0] + g[an * 3 + 1] * g[bn * 3 + 1] +
+                                      g[an * 3 + 2] * g[bn * 3 + 2]);
+                }
+        }
+        a.fp_val[k] = (T)v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Step prologue (pdsolver.py:249-254, 283-289):
+//   x_start = x, v_start = v, xhat = x + dt v + dt^2 m^-1 f (m^-1 := 0 where m = 0),
+//   x = xhat on free nodes, x = pin target on pinned nodes.
+template <typename T>
+__global__ void k_prologue(int n, int nF, T dt, const T* __restrict__ dt2_inv_m, const vec4_t<T>* __restrict__ f,
+                           const vec4_t<T>* __restrict__ pin_tgt, vec4_t<T>* x, vec4_t<T>* v,
+                           vec4_t<T>* x_start, vec4_t<T>* v_start, vec4_t<T>* xhat, int* fail_iter) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *fail_iter = 0x7fffffff;
+    if (i >= n) return;
+    const vec4_t<T> xi = x[i], vi = v[i];
+    x_start[i] = xi;
+    v_start[i] = vi;
+    const T c = dt2_inv_m[i];
+    vec4_t<T> fi = make4<T>(T(0), T(0), T(0), T(0));
+    if (f != nullptr) fi = f[i];
+    const vec4_t<T> xh = make4<T>(xi.x + dt * vi.x + c * fi.x, xi.y + dt * vi.y + c * fi.y,
+                                  xi.z + dt * vi.z + c * fi.z, T(0));
+    xhat[i] = xh;
+    x[i] = (i < nF) ? xh : pin_tgt[i - nF];
+}
+
+// Step epilogue (pdsolver.py:302): v = damping (x - x_start) / dt.
+template <typename T>
+__global__ void k_epilogue(int n, T damp_over_dt, const vec4_t<T>* __restrict__ x,
+                           const vec4_t<T>* __restrict__ x_start, vec4_t<T>* v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const vec4_t<T> a = x[i], b = x_start[i];
+    v[i] = make4<T>(damp_over_dt * (a.x - b.x), damp_over_dt * (a.y - b.y), damp_over_dt * (a.z - b.z), T(0));
+}
+
+// Restore the step's input state after a non-finite abort.
+template <typename T>
+__global__ void k_restore(int n, vec4_t<T>* x, vec4_t<T>* v, const vec4_t<T>* x_start, const vec4_t<T>* v_start) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    x[i] = x_start[i];
+    v[i] = v_start[i];
+}
+
+// rhs_i = sum over incidences of corner contributions (tet order) -- the
+// `np.add.at` of pdsolver.py:69-70, without atomics.  All n nodes.
+template <typename T>
+__global__ void k_gather(int n, const int* __restrict__ inc_ptr, const int* __restrict__ inc_code,
+                         const vec4_t<T>* __restrict__ corner, vec4_t<T>* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    T sx = 0, sy = 0, sz = 0;
+    for (int k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
+        const vec4_t<T> c = ldg4(&corner[inc_code[k]]);
+        sx += c.x; sy += c.y; sz += c.z;
+    }
+    out[i] = make4<T>(sx, sy, sz, T(0));
+}
+
+// ---------------------------------------------------------------------------
+// Persistent Jacobi-preconditioned CG on K_ff for the three coordinate
+// columns at once (one scalar recurrence per column), launched cooperatively
+// with one grid barrier per half-iteration.  The search direction is double
+// buffered so the "p = z + beta p" update fuses into the SpMV phase.
+//
+// init == INIT_PD:  r = sum_inc corner + (m/dt^2)(xhat - x)  (= b - K x at the
+//                   current PD iterate, free rows), solve K_ff dx = r, x += dx.
+// init == INIT_RHS: r = rhs (caller-assembled b_f - K_fp pins), x0 = 0, the
+//                   solution is left in dx (GlobalSolver.solve drop-in).
+// Stops when sum_c |r_c|^2 <= tol^2 * scale^2 (scale^2 = |M/dt^2 xhat|^2 for
+// INIT_PD, |r0|^2 for INIT_RHS) or after max_iters.
+enum PcgInit { INIT_PD = 0, INIT_RHS = 1 };
+
+template <typename T>
+struct PcgArgs {
+    int nF, ell_w;
+    const int* ell_col;
+    const T* ell_val;
+    const T* inv_diag;
+    const int* inc_ptr;
+    const int* inc_code;
+    const vec4_t<T>* corner;
+    const T* m_dt2;
+    const vec4_t<T>* xhat;
+    const vec4_t<T>* rhs;
+    vec4_t<T>* x;
+    vec4_t<T>* r;
+    vec4_t<T>* z;
+    vec4_t<T>* p0;
+    vec4_t<T>* p1;
+    vec4_t<T>* q;
+    vec4_t<T>* dx;
+    double* partials;            // gridDim.x * 8
+    double* scal;                // 16 published scalars
+    GridBar* bar;
+    int* iters_out;              // iteration count of this solve
+    int* fail_iter;              // atomicMin'd with pd_iter on non-finite output
+    int pd_iter;
+    double tol;
+    int max_iters;
+    int init;
+};
+
+// scal layout
+enum { S_RZ = 0, S_RZP = 3, S_PQ = 6, S_RR = 9, S_BB = 10 };
+
+template <int NV>
+__device__ __forceinline__ void reduce_partials(const double* partials, double* out, double* smem) {
+    // deterministic: fixed strided assignment + fixed-order block sum
+    double v[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] += partials[b * 8 + k];
+    block_sum<NV>(v, smem);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) out[k] = v[k];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
+    __shared__ double smem[32 * 8];
+    __shared__ double s_out[8];
+    const int nF = a.nF;
+    const int chunk = (nF + gridDim.x - 1) / gridDim.x;
+    const int row0 = blockIdx.x * chunk;
+    const int row1 = min(nF, row0 + chunk);
+    double* scal = a.scal;
+
+    // ---- init: residual, z = D^-1 r, p0 = 0, dx = 0
+    {
+        double acc[5] = {0, 0, 0, 0, 0};     // rz x3, rr, bb
+        for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+            T rx, ry, rz;
+            if (a.init == INIT_PD) {
+                rx = 0; ry = 0; rz = 0;
+                for (int k = a.inc_ptr[i]; k < a.inc_ptr[i + 1]; ++k) {
+                    const vec4_t<T> c = ld4(&a.corner[a.inc_code[k]]);
+                    rx += c.x; ry += c.y; rz += c.z;
+                }
+                const T m = a.m_dt2[i];
+                const vec4_t<T> xh = a.xhat[i], xi = a.x[i];
+                rx += m * (xh.x - xi.x);
+                ry += m * (xh.y - xi.y);
+                rz += m * (xh.z - xi.z);
+                const double bx = (double)m * xh.x, by = (double)m * xh.y, bz = (double)m * xh.z;
+                acc[4] += bx * bx + by * by + bz * bz;
+            } else {
+                const vec4_t<T> b = a.rhs[i];
+                rx = b.x; ry = b.y; rz = b.z;
+                acc[4] += (double)rx * rx + (double)ry * ry + (double)rz * rz;
+            }
+            const T d = a.inv_diag[i];
+            const vec4_t<T> zi = make4<T>(d * rx, d * ry, d * rz, T(0));
+            a.r[i] = make4<T>(rx, ry, rz, T(0));
+            a.z[i] = zi;
+            a.p0[i] = make4<T>(T(0), T(0), T(0), T(0));
+            a.dx[i] = make4<T>(T(0), T(0), T(0), T(0));
+            acc[0] += (double)rx * zi.x;
+            acc[1] += (double)ry * zi.y;
+            acc[2] += (double)rz * zi.z;
+            acc[3] += (double)rx * rx + (double)ry * ry + (double)rz * rz;
+        }
+        block_sum<5>(acc, smem);
+        if (threadIdx.x == 0)
+            for (int k = 0; k < 5; ++k) a.partials[blockIdx.x * 8 + k] = acc[k];
+        grid_sync(a.bar, [&]() {
+            reduce_partials<5>(a.partials, s_out, smem);
+            if (threadIdx.x == 0) {
+                for (int c = 0; c < 3; ++c) { scal[S_RZ + c] = s_out[c]; scal[S_RZP + c] = 1.0; }
+                scal[S_RR] = s_out[3];
+                scal[S_BB] = s_out[4];
+            }
+        });
+    }
+
+    int it = 0;
+    for (;; ++it) {
+        const double rr = ((volatile double*)scal)[S_RR];
+        const double bb = ((volatile double*)scal)[S_BB];
+        if (!(rr > a.tol * a.tol * bb) || it >= a.max_iters) break;   // also stops on NaN
+        double beta[3];
+        for (int c = 0; c < 3; ++c)
+            beta[c] = (it == 0) ? 0.0 : ((volatile double*)scal)[S_RZ + c] / ((volatile double*)scal)[S_RZP + c];
+        const T bx = (T)beta[0], by = (T)beta[1], bz = (T)beta[2];
+        const vec4_t<T>* pold = (it & 1) ? a.p1 : a.p0;
+        vec4_t<T>* pnew = (it & 1) ? a.p0 : a.p1;
+        // ---- phase A: p_new = z + beta p_old; q = K_ff p_new
+        {
+            double acc[3] = {0, 0, 0};
+            for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+                T qx = 0, qy = 0, qz = 0;
+                for (int s = 0; s < a.ell_w; ++s) {
+                    const int col = __ldg(&a.ell_col[(size_t)s * nF + i]);
+                    if (col < 0) break;
+                    const T kv = __ldg(&a.ell_val[(size_t)s * nF + i]);
+                    const vec4_t<T> zc = ld4(&a.z[col]);
+                    const vec4_t<T> pc = ld4(&pold[col]);
+                    qx += kv * (zc.x + bx * pc.x);
+                    qy += kv * (zc.y + by * pc.y);
+                    qz += kv * (zc.z + bz * pc.z);
+                }
+                const vec4_t<T> zi = ld4(&a.z[i]);
+                const vec4_t<T> pi = ld4(&pold[i]);
+                const vec4_t<T> pn = make4<T>(zi.x + bx * pi.x, zi.y + by * pi.y, zi.z + bz * pi.z, T(0));
+                pnew[i] = pn;
+                a.q[i] = make4<T>(qx, qy, qz, T(0));
+                acc[0] += (double)pn.x * qx;
+                acc[1] += (double)pn.y * qy;
+                acc[2] += (double)pn.z * qz;
+            }
+            block_sum<3>(acc, smem);
+            if (threadIdx.x == 0)
+                for (int k = 0; k < 3; ++k) a.partials[blockIdx.x * 8 + k] = acc[k];
+            grid_sync(a.bar, [&]() {
+                reduce_partials<3>(a.partials, s_out, smem);
+                if (threadIdx.x == 0)
+                    for (int c = 0; c < 3; ++c) scal[S_PQ + c] = s_out[c];
+            });
+        }
+        // ---- phase B: dx += alpha p; r -= alpha q; z = D^-1 r
+        {
+            double alpha[3];
+            for (int c = 0; c < 3; ++c) {
+                const double pq = ((volatile double*)scal)[S_PQ + c];
+                alpha[c] = pq != 0.0 ? ((volatile double*)scal)[S_RZ + c] / pq : 0.0;
+            }
+            const T ax = (T)alpha[0], ay = (T)alpha[1], az = (T)alpha[2];
+            double acc[4] = {0, 0, 0, 0};
+            for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+                const vec4_t<T> pn = ld4(&pnew[i]);
+                const vec4_t<T> qi = ld4(&a.q[i]);
+                vec4_t<T> d = ld4(&a.dx[i]);
+                vec4_t<T> ri = ld4(&a.r[i]);
+                d.x += ax * pn.x; d.y += ay * pn.y; d.z += az * pn.z;
+                ri.x -= ax * qi.x; ri.y -= ay * qi.y; ri.z -= az * qi.z;
+                const T dg = a.inv_diag[i];
+                const vec4_t<T> zi = make4<T>(dg * ri.x, dg * ri.y, dg * ri.z, T(0));
+                a.dx[i] = d;
+                a.r[i] = ri;
+                a.z[i] = zi;
+                acc[0] += (double)ri.x * zi.x;
+                acc[1] += (double)ri.y * zi.y;
+                acc[2] += (double)ri.z * zi.z;
+                acc[3] += (double)ri.x * ri.x + (double)ri.y * ri.y + (double)ri.z * ri.z;
+            }
+            block_sum<4>(acc, smem);
+            if (threadIdx.x == 0)
+                for (int k = 0; k < 4; ++k) a.partials[blockIdx.x * 8 + k] = acc[k];
+            grid_sync(a.bar, [&]() {
+                reduce_partials<4>(a.partials, s_out, smem);
+                if (threadIdx.x == 0) {
+                    for (int c = 0; c < 3; ++c) {
+                        scal[S_RZP + c] = scal[S_RZ + c];
+                        scal[S_RZ + c] = s_out[c];
+                    }
+                    scal[S_RR] = s_out[3];
+                }
+            });
+        }
+    }
+    // ---- finish: x += dx (PD mode), finite check
+    if (a.init == INIT_PD) {
+        bool bad = false;
+        for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+            const vec4_t<T> d = ld4(&a.dx[i]);
+            vec4_t<T> xi = a.x[i];
+            xi.x += d.x; xi.y += d.y; xi.z += d.z;
+            a.x[i] = xi;
+            bad |= !(isfinite(xi.x) && isfinite(xi.y) && isfinite(xi.z));
+        }
+        if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, a.pd_iter);
+    } else {
+        bool bad = false;
+        for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+            const vec4_t<T> d = ld4(&a.dx[i]);
+            bad |= !(isfinite(d.x) && isfinite(d.y) && isfinite(d.z));
+        }
+        if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, a.pd_iter);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.iters_out = it;
+}
+
+}  // namespace vk

@@ -1,0 +1,143 @@
+// Common device helpers for the PD step library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cuda/atomic>
+
+namespace vk {
+
+template <typename T> struct Vec4;
+template <> struct Vec4<float> { using type = float4; };
+template <> struct Vec4<double> { using type = double4; };
+template <typename T> using vec4_t = typename Vec4<T>::type;
+
+template <typename T> __device__ __forceinline__ vec4_t<T> make4(T a, T b, T c, T d);
+template <> __device__ __forceinline__ float4 make4<float>(float a, float b, float c, float d) {
+    return make_float4(a, b, c, d);
+}
+template <> __device__ __forceinline__ double4 make4<double>(double a, double b, double c, double d) {
+    return make_double4(a, b, c, d);
+}
+
+// 16-B (float4) / 32-B (double4) vector load through the read-only path.
+__device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+    double4 r;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+// plain (coherent) vector load for data written earlier in the same kernel
+__device__ __forceinline__ float4 ld4(const float4* p) { return *p; }
+__device__ __forceinline__ double4 ld4(const double4* p) {
+    double4 r;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st4(float4* p, float4 v) { *p = v; }
+__device__ __forceinline__ void st4(double4* p, double4 v) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
+
+#define VK_HD __host__ __device__ __forceinline__
+#define VK_HDNI __host__ __device__ __noinline__
+
+template <typename T> VK_HD T rsqrt_(T x);
+template <> VK_HD float rsqrt_<float>(float x) {
+#ifdef __CUDA_ARCH__
+    return rsqrtf(x);
+#else
+    return 1.0f / sqrtf(x);
+#endif
+}
+template <> VK_HD double rsqrt_<double>(double x) {
+#ifdef __CUDA_ARCH__
+    return rsqrt(x);
+#else
+    return 1.0 / sqrt(x);
+#endif
+}
+
+template <typename T> struct Eps;
+template <> struct Eps<float> { static constexpr float v = 1.1920929e-7f; };
+template <> struct Eps<double> { static constexpr double v = 2.220446049250313e-16; };
+
+// ---------------------------------------------------------------------------
+// Grid-wide barrier for a cooperatively launched (co-resident) grid.
+//
+// Sense-reversing counter + generation word.  The last CTA to arrive runs
+// `on_last` (a deterministic grid reduction over per-CTA partials, fixed
+// order) before releasing everyone, so the reduced scalars are published by
+// the barrier itself.  A bounded spin turns a lost CTA into a trap instead
+// of a hang.
+struct GridBar {
+    unsigned int count;
+    unsigned int gen;
+};
+
+template <typename OnLast>
+__device__ __forceinline__ void grid_sync(GridBar* bar, OnLast on_last) {
+    __syncthreads();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+        cuda::atomic_ref<unsigned int, cuda::thread_scope_device> gen(bar->gen);
+        cuda::atomic_ref<unsigned int, cuda::thread_scope_device> cnt(bar->count);
+        unsigned int g = gen.load(cuda::memory_order_relaxed);
+        __threadfence();
+        unsigned int arrived = cnt.fetch_add(1u, cuda::memory_order_acq_rel);
+        s_last = (arrived == gridDim.x - 1) ? 1 : 0;
+        if (!s_last) {
+            unsigned long long spins = 0;
+            while (gen.load(cuda::memory_order_acquire) == g) {
+                if (++spins > (1ull << 31)) __trap();
+                if (spins > 64) __nanosleep(20);
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    if (s_last) {
+        on_last();                    // whole CTA participates
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            cuda::atomic_ref<unsigned int, cuda::thread_scope_device> gen(bar->gen);
+            cuda::atomic_ref<unsigned int, cuda::thread_scope_device> cnt(bar->count);
+            __threadfence();
+            cnt.store(0u, cuda::memory_order_relaxed);
+            gen.fetch_add(1u, cuda::memory_order_release);
+        }
+        __syncthreads();
+    }
+}
+
+struct NoOp { __device__ void operator()() const {} };
+
+// Block-wide sum of NV doubles per thread; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* >= 32*NV */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) smem[warp * NV + k] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < NV; ++k) {
+            double a = 0.0;
+            for (int w = 0; w < nw; ++w) a += smem[w * NV + k];
+            v[k] = a;
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace vk

@@ -1,0 +1,893 @@
+// vkpd: C-ABI host runtime of the B200 projective-dynamics step.
+//
+// Owns the device-resident mesh, material, matrix and state of one scene and
+// drives a frame as  prologue -> iterations x (local step, persistent CG) ->
+// epilogue,  captured once into a CUDA graph and replayed per frame.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/vkpd.h"
+#include "local_step.cuh"
+#include "solver.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e__ = (call);                                                                  \
+        if (e__ != cudaSuccess)                                                                    \
+            return fail(VKPD_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__));           \
+    } while (0)
+
+template <typename X>
+struct DBuf {
+    X* p = nullptr;
+    size_t n = 0;
+    ~DBuf() { if (p) cudaFree(p); }
+    cudaError_t alloc(size_t count) {
+        if (p) { cudaFree(p); p = nullptr; }
+        n = count;
+        if (count == 0) return cudaSuccess;
+        return cudaMalloc(&p, count * sizeof(X));
+    }
+    cudaError_t upload(const X* h, size_t count, cudaStream_t s) {
+        return cudaMemcpyAsync(p, h, count * sizeof(X), cudaMemcpyHostToDevice, s);
+    }
+};
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------------------
+// layout conversion kernels: host (nV,3) float64 in caller order <-> device vec4 internal order
+template <typename T>
+__global__ void k_scatter_in(int n, const double* __restrict__ src, const int* __restrict__ int_of_orig,
+                             vk::vec4_t<T>* dst) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    dst[int_of_orig[j]] = vk::make4<T>((T)src[3 * j], (T)src[3 * j + 1], (T)src[3 * j + 2], T(0));
+}
+template <typename T>
+__global__ void k_gather_out(int n, const vk::vec4_t<T>* __restrict__ src, const int* __restrict__ int_of_orig,
+                             double* dst) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const vk::vec4_t<T> v = src[int_of_orig[j]];
+    dst[3 * j] = (double)v.x;
+    dst[3 * j + 1] = (double)v.y;
+    dst[3 * j + 2] = (double)v.z;
+}
+// plain vec4 rows (first m rows) from (m, 3) float64
+template <typename T>
+__global__ void k_rows_in(int m, const double* __restrict__ src, vk::vec4_t<T>* dst) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    dst[j] = vk::make4<T>((T)src[3 * j], (T)src[3 * j + 1], (T)src[3 * j + 2], T(0));
+}
+// out_f = B_f - K_fp P  (columns are packed 3-wide)
+template <typename T>
+__global__ void k_rhs_minus_fp(int nF, const vk::vec4_t<T>* __restrict__ Bint, const int* __restrict__ fp_ptr,
+                               const int* __restrict__ fp_col, const T* __restrict__ fp_val,
+                               const vk::vec4_t<T>* __restrict__ P, vk::vec4_t<T>* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    vk::vec4_t<T> b = Bint[i];
+    for (int k = fp_ptr[i]; k < fp_ptr[i + 1]; ++k) {
+        const T v = fp_val[k];
+        const vk::vec4_t<T> p = P[fp_col[k]];
+        b.x -= v * p.x; b.y -= v * p.y; b.z -= v * p.z;
+    }
+    out[i] = b;
+}
+// Y_f = K_ff X_f + K_fp X_p (free rows), Y_p = 0
+template <typename T>
+__global__ void k_apply_K(int n, int nF, int ell_w, const int* __restrict__ ell_col, const T* __restrict__ ell_val,
+                          const int* __restrict__ fp_ptr, const int* __restrict__ fp_col, const T* __restrict__ fp_val,
+                          const vk::vec4_t<T>* __restrict__ X, vk::vec4_t<T>* Y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (i >= nF) { Y[i] = vk::make4<T>(T(0), T(0), T(0), T(0)); return; }
+    T a = 0, b = 0, c = 0;
+    for (int s = 0; s < ell_w; ++s) {
+        const int col = ell_col[(size_t)s * nF + i];
+        if (col < 0) break;
+        const T v = ell_val[(size_t)s * nF + i];
+        const vk::vec4_t<T> x = X[col];
+        a += v * x.x; b += v * x.y; c += v * x.z;
+    }
+    for (int k = fp_ptr[i]; k < fp_ptr[i + 1]; ++k) {
+        const T v = fp_val[k];
+        const vk::vec4_t<T> x = X[nF + fp_col[k]];
+        a += v * x.x; b += v * x.y; c += v * x.z;
+    }
+    Y[i] = vk::make4<T>(a, b, c, T(0));
+}
+
+// ---------------------------------------------------------------------------
+struct CtxBase {
+    virtual ~CtxBase() {}
+    virtual int init(const vkpd_mesh_desc* d, const vkpd_config* c) = 0;
+    virtual int set_state(const double* x, const double* v) = 0;
+    virtual int get_state(double* x, double* v) = 0;
+    virtual int set_pin_targets(const double* t) = 0;
+    virtual int set_forces(const double* f) = 0;
+    virtual int step_async(int iterations, double damping) = 0;
+    virtual int sync(int* failed) = 0;
+    virtual int profile(int iterations, double damping, double* lms, double* gms, double* fms) = 0;
+    virtual int elastic_rhs(const double* x, double* rhs, double* F, double* R, double* V) = 0;
+    virtual int global_solve(const double* B, const double* P, double* X, int k) = 0;
+    virtual int apply_K(const double* X, double* Y) = 0;
+    virtual int stats(vkpd_stats* st) = 0;
+    virtual int init_matrix(int64_t n, const int64_t* indptr, const int64_t* indices, const double* data,
+                            const int64_t* pins, int64_t npins, const vkpd_config* c) = 0;
+    virtual int get_csr(int64_t* indptr, int64_t* indices, double* data, int64_t* nnz) = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    int device = 0;
+};
+
+template <typename T>
+struct Ctx : CtxBase {
+    using V4 = vk::vec4_t<T>;
+    int n = 0, nE = 0, nF = 0, nP = 0, ell_w = 0;
+    double dt = 0, tol = 0;
+    int max_iters = 1000;
+    int pcg_blocks = 0;
+    bool use_graph = true;
+    bool has_forces = false;
+    int n_sms = 0;
+    std::vector<int> int_of_orig_h;
+
+    // topology / material
+    DBuf<int4> tets;
+    DBuf<T> G, w, inv_diag, ell_val, fp_val, m_dt2, dt2_inv_m;
+    DBuf<int> ell_col, fp_ptr, fp_col, inc_ptr, inc_code, int_of_orig;
+    DBuf<double> diag64;
+    // state
+    DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
+    DBuf<double> partials, scal, stage;
+    DBuf<vk::GridBar> bar;
+    DBuf<int> iters, fail_iter;
+    DBuf<vk::ProjStats> pstats;
+    int* h_fail = nullptr;
+    int last_iterations = 0;
+
+    // graph cache
+    cudaGraphExec_t graph_exec = nullptr;
+    int graph_iters = -1;
+    double graph_damp = 0;
+    bool graph_forces = false;
+    bool graph_broken = false;
+
+    ~Ctx() override {
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        if (h_fail) cudaFreeHost(h_fail);
+        if (own_stream) cudaStreamDestroy(own_stream);
+    }
+
+    int init(const vkpd_mesh_desc* d, const vkpd_config* c) override {
+        n = (int)d->n_nodes;
+        nE = (int)d->n_tets;
+        nP = (int)d->n_pins;
+        dt = d->dt;
+        tol = c->tol > 0 ? c->tol : (sizeof(T) == 4 ? 1e-6 : 1e-12);
+        max_iters = c->max_iters > 0 ? c->max_iters : 1000;
+        use_graph = c->use_graph != 0;
+        if (n <= 0 || nE <= 0) return fail(VKPD_EINVAL, "empty mesh");
+        if (d->n_nodes > (1ll << 30) || 4ll * d->n_tets > (1ll << 31) - 1)
+            return fail(VKPD_EINVAL, "mesh too large for 32-bit indexing");
+        if (!(dt > 0.0)) return fail(VKPD_EINVAL, "dt must be positive");
+        if (d->node_mass == nullptr) return fail(VKPD_EINVAL, "mesh node masses not lumped yet");
+        for (int e = 0; e < nE; ++e) {
+            if (d->gamma_s[e] < 0.0 || d->gamma_v[e] < 0.0)
+                return fail(VKPD_EINVAL, "negative material coefficient");
+            if (!(d->volume[e] > 0.0)) return fail(VKPD_EINVAL, "non-positive element volume");
+            for (int k = 0; k < 4; ++k) {
+                const int64_t id = d->tets[4 * (size_t)e + k];
+                if (id < 0 || id >= n) return fail(VKPD_EINVAL, "tet node index out of range");
+            }
+        }
+        // internal order: free nodes (caller order), then pins (pin order)
+        std::vector<int> ioo(n, -1);
+        std::vector<char> pinned(n, 0);
+        for (int k = 0; k < nP; ++k) {
+            const int64_t id = d->pins[k];
+            if (id < 0 || id >= n) return fail(VKPD_EINVAL, "pin index out of range");
+            if (pinned[id]) return fail(VKPD_EINVAL, "duplicate pin index");
+            pinned[id] = 1;
+        }
+        nF = 0;
+        for (int j = 0; j < n; ++j) if (!pinned[j]) ioo[j] = nF++;
+        for (int k = 0; k < nP; ++k) ioo[d->pins[k]] = nF + k;
+        int_of_orig_h = ioo;
+        std::vector<int4> tets_h(nE);
+        for (int e = 0; e < nE; ++e)
+            tets_h[e] = make_int4(ioo[d->tets[4 * (size_t)e]], ioo[d->tets[4 * (size_t)e + 1]],
+                                  ioo[d->tets[4 * (size_t)e + 2]], ioo[d->tets[4 * (size_t)e + 3]]);
+        // incidences per internal node, tet order
+        std::vector<int> iptr(n + 1, 0);
+        for (int e = 0; e < nE; ++e) {
+            const int* t = &tets_h[e].x;
+            for (int a = 0; a < 4; ++a) iptr[t[a] + 1]++;
+        }
+        for (int i = 0; i < n; ++i) iptr[i + 1] += iptr[i];
+        std::vector<int> icode(iptr[n]), fillp(iptr.begin(), iptr.end() - 1);
+        for (int e = 0; e < nE; ++e) {
+            const int* t = &tets_h[e].x;
+            for (int a = 0; a < 4; ++a) icode[fillp[t[a]]++] = a * nE + e;
+        }
+        // neighbour sets of free rows -> ELL (free cols) + K_fp CSR (pin slots)
+        std::vector<std::vector<int>> nb(nF);
+        ell_w = 0;
+        std::vector<int> fptr(nF + 1, 0), fcol;
+        for (int i = 0; i < nF; ++i) {
+            std::vector<int>& s = nb[i];
+            s.push_back(i);
+            for (int k = iptr[i]; k < iptr[i + 1]; ++k) {
+                const int e = icode[k] % nE;
+                const int* t = &tets_h[e].x;
+                for (int a = 0; a < 4; ++a) s.push_back(t[a]);
+            }
+            std::sort(s.begin(), s.end());
+            s.erase(std::unique(s.begin(), s.end()), s.end());
+            int nfree = 0;
+            for (int col : s) {
+                if (col < nF) ++nfree;
+                else fcol.push_back(col - nF);
+            }
+            fptr[i + 1] = (int)fcol.size();
+            ell_w = std::max(ell_w, nfree);
+        }
+        std::vector<int> ecol((size_t)ell_w * nF, -1);
+        for (int i = 0; i < nF; ++i) {
+            int s = 0;
+            for (int col : nb[i])
+                if (col < nF) ecol[(size_t)s++ * nF + i] = col;
+        }
+        // per-node arrays in internal order
+        std::vector<double> mdt2(n);
+        std::vector<T> mdt2_t(n), dt2im(n);
+        for (int j = 0; j < n; ++j) {
+            const double m = d->node_mass[j];
+            mdt2[ioo[j]] = m / (dt * dt);
+            mdt2_t[ioo[j]] = (T)(m / (dt * dt));
+            dt2im[ioo[j]] = (T)(m > 0.0 ? dt * dt / m : 0.0);
+        }
+        // per-tet planes
+        std::vector<T> Gp((size_t)9 * nE), wp((size_t)2 * nE);
+        std::vector<double> wsum(nE);
+        for (int e = 0; e < nE; ++e) {
+            const double* g = d->shape_grad + (size_t)12 * e;
+            for (int k = 0; k < 9; ++k) Gp[(size_t)k * nE + e] = (T)g[3 + k];
+            const double vv = 2.0 * d->volume[e];
+            wp[e] = (T)(vv * d->gamma_s[e]);
+            wp[(size_t)nE + e] = (T)(vv * d->gamma_v[e]);
+            wsum[e] = vv * (d->gamma_s[e] + d->gamma_v[e]);
+        }
+
+        CK(cudaSetDevice(device));
+        CK(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+        stream = own_stream;
+        cudaStream_t s = stream;
+        CK(tets.alloc(nE)); CK(tets.upload(tets_h.data(), nE, s));
+        CK(G.alloc((size_t)9 * nE)); CK(G.upload(Gp.data(), Gp.size(), s));
+        CK(w.alloc((size_t)2 * nE)); CK(w.upload(wp.data(), wp.size(), s));
+        CK(inc_ptr.alloc(n + 1)); CK(inc_ptr.upload(iptr.data(), n + 1, s));
+        CK(inc_code.alloc(icode.size())); CK(inc_code.upload(icode.data(), icode.size(), s));
+        CK(int_of_orig.alloc(n)); CK(int_of_orig.upload(ioo.data(), n, s));
+        CK(ell_col.alloc(ecol.size())); CK(ell_col.upload(ecol.data(), ecol.size(), s));
+        CK(ell_val.alloc(ecol.size()));
+        CK(fp_ptr.alloc(nF + 1)); CK(fp_ptr.upload(fptr.data(), nF + 1, s));
+        CK(fp_col.alloc(std::max<size_t>(1, fcol.size())));
+        if (!fcol.empty()) CK(fp_col.upload(fcol.data(), fcol.size(), s));
+        CK(fp_val.alloc(std::max<size_t>(1, fcol.size())));
+        CK(inv_diag.alloc(nF));
+        CK(diag64.alloc(nF));
+        CK(m_dt2.alloc(n)); CK(m_dt2.upload(mdt2_t.data(), n, s));
+        CK(dt2_inv_m.alloc(n)); CK(dt2_inv_m.upload(dt2im.data(), n, s));
+        // assembly inputs (float64, freed after)
+        {
+            DBuf<double> G64, ws64, md64;
+            CK(G64.alloc((size_t)12 * nE)); CK(G64.upload(d->shape_grad, (size_t)12 * nE, s));
+            CK(ws64.alloc(nE)); CK(ws64.upload(wsum.data(), nE, s));
+            CK(md64.alloc(n)); CK(md64.upload(mdt2.data(), n, s));
+            vk::AssembleArgs<T> aa;
+            aa.nF = nF; aa.nE = nE; aa.ell_w = ell_w;
+            aa.inc_ptr = inc_ptr.p; aa.inc_code = inc_code.p; aa.tets = tets.p; aa.G = G64.p; aa.wsum = ws64.p;
+            aa.m_dt2 = md64.p; aa.ell_col = ell_col.p; aa.ell_val = ell_val.p; aa.inv_diag = inv_diag.p;
+            aa.diag64 = diag64.p; aa.fp_ptr = fp_ptr.p; aa.fp_col = fp_col.p; aa.fp_val = fp_val.p;
+            aa.n_free_cols_base = nF;
+            if (nF > 0) vk::k_assemble<T><<<cdiv(nF, 128), 128, 0, s>>>(aa);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(s));
+        }
+        return alloc_work(c);
+    }
+
+    int alloc_work(const vkpd_config* c) {
+        cudaStream_t s = stream;
+        for (DBuf<V4>* b : {&x, &v, &x_start, &v_start, &xhat, &tmp4a, &tmp4b}) {
+            CK(b->alloc(n));
+            CK(cudaMemsetAsync(b->p, 0, n * sizeof(V4), s));
+        }
+        CK(f.alloc(n));
+        CK(cudaMemsetAsync(f.p, 0, n * sizeof(V4), s));
+        CK(pin_tgt.alloc(std::max(1, nP)));
+        CK(cudaMemsetAsync(pin_tgt.p, 0, std::max(1, nP) * sizeof(V4), s));
+        CK(corner.alloc((size_t)4 * nE));
+        for (DBuf<V4>* b : {&r, &z, &p0, &p1, &q, &dx, &rhs}) {
+            CK(b->alloc(std::max(1, nF)));
+            CK(cudaMemsetAsync(b->p, 0, std::max(1, nF) * sizeof(V4), s));
+        }
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_pcg<T>, 512, 0));
+        if (occ < 1) return fail(VKPD_ECUDA, "persistent solver kernel cannot be resident");
+        pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : n_sms;
+        pcg_blocks = std::min(pcg_blocks, occ * n_sms);
+        pcg_blocks = std::max(1, std::min(pcg_blocks, cdiv(std::max(1, nF), 32)));
+        CK(partials.alloc((size_t)8 * pcg_blocks));
+        CK(scal.alloc(16));
+        CK(bar.alloc(1));
+        CK(cudaMemsetAsync(bar.p, 0, sizeof(vk::GridBar), s));
+        CK(iters.alloc(1024));
+        CK(cudaMemsetAsync(iters.p, 0, 1024 * sizeof(int), s));
+        CK(fail_iter.alloc(1));
+        CK(pstats.alloc(1));
+        CK(cudaMemsetAsync(pstats.p, 0, sizeof(vk::ProjStats), s));
+        CK(stage.alloc((size_t)3 * n));
+        CK(cudaHostAlloc(&h_fail, sizeof(int), cudaHostAllocDefault));
+        *h_fail = 0x7fffffff;
+        CK(cudaStreamSynchronize(s));
+        return VKPD_OK;
+    }
+
+
+    // Matrix-only context (GlobalSolver drop-in, pdsolver.py:205-223): K given as CSR.
+    int init_matrix(int64_t nn, const int64_t* indptr, const int64_t* indices, const double* data,
+                    const int64_t* pins, int64_t npins, const vkpd_config* c) override {
+        n = (int)nn;
+        nE = 0;
+        nP = (int)npins;
+        dt = 1.0;
+        tol = c->tol > 0 ? c->tol : (sizeof(T) == 4 ? 1e-6 : 1e-12);
+        max_iters = c->max_iters > 0 ? c->max_iters : 1000;
+        use_graph = false;
+        if (n <= 0) return fail(VKPD_EINVAL, "empty matrix");
+        std::vector<int> ioo(n, -1);
+        std::vector<char> pinned(n, 0);
+        for (int k = 0; k < nP; ++k) {
+            if (pins[k] < 0 || pins[k] >= n) return fail(VKPD_EINVAL, "pin index out of range");
+            if (pinned[pins[k]]) return fail(VKPD_EINVAL, "duplicate pin index");
+            pinned[pins[k]] = 1;
+        }
+        nF = 0;
+        for (int j = 0; j < n; ++j) if (!pinned[j]) ioo[j] = nF++;
+        for (int k = 0; k < nP; ++k) ioo[pins[k]] = nF + k;
+        int_of_orig_h = ioo;
+        std::vector<int> orig_of_int(n);
+        for (int j = 0; j < n; ++j) orig_of_int[ioo[j]] = j;
+        ell_w = 0;
+        std::vector<int> fptr(nF + 1, 0), fcol;
+        std::vector<T> fval;
+        std::vector<double> dg(nF, 0.0);
+        std::vector<std::vector<std::pair<int, double>>> rows(nF);
+        for (int i = 0; i < nF; ++i) {
+            const int j = orig_of_int[i];
+            for (int64_t k = indptr[j]; k < indptr[j + 1]; ++k) {
+                const int64_t cj = indices[k];
+                if (cj < 0 || cj >= n) return fail(VKPD_EINVAL, "matrix column out of range");
+                const int ci = ioo[cj];
+                if (ci < nF) rows[i].push_back({ci, data[k]});
+                else { fcol.push_back(ci - nF); fval.push_back((T)data[k]); }
+                if (ci == i) dg[i] += data[k];
+            }
+            std::sort(rows[i].begin(), rows[i].end());
+            fptr[i + 1] = (int)fcol.size();
+            ell_w = std::max(ell_w, (int)rows[i].size());
+            if (!(dg[i] > 0.0)) return fail(VKPD_EINVAL, "matrix diagonal must be positive");
+        }
+        std::vector<int> ecol((size_t)ell_w * nF, -1);
+        std::vector<T> evals((size_t)ell_w * nF, T(0)), idg(nF);
+        for (int i = 0; i < nF; ++i) {
+            for (size_t s2 = 0; s2 < rows[i].size(); ++s2) {
+                ecol[s2 * nF + i] = rows[i][s2].first;
+                evals[s2 * nF + i] = (T)rows[i][s2].second;
+            }
+            idg[i] = (T)(1.0 / dg[i]);
+        }
+        CK(cudaSetDevice(device));
+        CK(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+        stream = own_stream;
+        cudaStream_t s = stream;
+        CK(int_of_orig.alloc(n)); CK(int_of_orig.upload(ioo.data(), n, s));
+        CK(ell_col.alloc(ecol.size())); CK(ell_col.upload(ecol.data(), ecol.size(), s));
+        CK(ell_val.alloc(evals.size())); CK(ell_val.upload(evals.data(), evals.size(), s));
+        CK(fp_ptr.alloc(nF + 1)); CK(fp_ptr.upload(fptr.data(), nF + 1, s));
+        CK(fp_col.alloc(std::max<size_t>(1, fcol.size())));
+        CK(fp_val.alloc(std::max<size_t>(1, fcol.size())));
+        if (!fcol.empty()) { CK(fp_col.upload(fcol.data(), fcol.size(), s)); CK(fp_val.upload(fval.data(), fval.size(), s)); }
+        CK(inv_diag.alloc(nF)); CK(inv_diag.upload(idg.data(), nF, s));
+        CK(diag64.alloc(nF)); CK(diag64.upload(dg.data(), nF, s));
+        CK(m_dt2.alloc(n));
+        CK(dt2_inv_m.alloc(n));
+        CK(inc_ptr.alloc(n + 1));
+        CK(cudaMemsetAsync(inc_ptr.p, 0, (n + 1) * sizeof(int), s));
+        return alloc_work(c);
+    }
+
+    // K in CSR, caller node order, rows of free nodes only (all rows when there are no pins)
+    int get_csr(int64_t* indptr, int64_t* indices, double* data, int64_t* nnz) override {
+        std::vector<int> ecol((size_t)ell_w * nF), fptr(nF + 1), fcol(fp_col.n);
+        std::vector<T> evals((size_t)ell_w * nF), fval(fp_val.n);
+        CK(cudaStreamSynchronize(stream));
+        if (nF) {
+            CK(cudaMemcpy(ecol.data(), ell_col.p, ecol.size() * sizeof(int), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(evals.data(), ell_val.p, evals.size() * sizeof(T), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(fptr.data(), fp_ptr.p, fptr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(fcol.data(), fp_col.p, fcol.size() * sizeof(int), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(fval.data(), fp_val.p, fval.size() * sizeof(T), cudaMemcpyDeviceToHost));
+        }
+        std::vector<int> orig_of_int(n);
+        for (int j = 0; j < n; ++j) orig_of_int[int_of_orig_h[j]] = j;
+        // count
+        int64_t total = 0;
+        std::vector<std::vector<std::pair<int64_t, double>>> rows(n);
+        for (int i = 0; i < nF; ++i) {
+            auto& r = rows[orig_of_int[i]];
+            for (int s2 = 0; s2 < ell_w; ++s2) {
+                const int col = ecol[(size_t)s2 * nF + i];
+                if (col < 0) break;
+                r.push_back({orig_of_int[col], (double)evals[(size_t)s2 * nF + i]});
+            }
+            for (int k = fptr[i]; k < fptr[i + 1]; ++k) r.push_back({orig_of_int[nF + fcol[k]], (double)fval[k]});
+            std::sort(r.begin(), r.end());
+            total += (int64_t)r.size();
+        }
+        *nnz = total;
+        if (!indptr) return VKPD_OK;     // size query
+        int64_t pos = 0;
+        indptr[0] = 0;
+        for (int j = 0; j < n; ++j) {
+            for (auto& kv : rows[j]) { indices[pos] = kv.first; data[pos] = kv.second; ++pos; }
+            indptr[j + 1] = pos;
+        }
+        return VKPD_OK;
+    }
+
+    int upload_nodes(const double* h, V4* dst) {
+        CK(cudaMemcpyAsync(stage.p, h, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, stream));
+        k_scatter_in<T><<<cdiv(n, 256), 256, 0, stream>>>(n, stage.p, int_of_orig.p, dst);
+        CK(cudaGetLastError());
+        return VKPD_OK;
+    }
+    int download_nodes(const V4* src, double* h) {
+        k_gather_out<T><<<cdiv(n, 256), 256, 0, stream>>>(n, src, int_of_orig.p, stage.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h, stage.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        return VKPD_OK;
+    }
+
+    int set_state(const double* hx, const double* hv) override {
+        int rc = upload_nodes(hx, x.p);
+        if (rc) return rc;
+        if (hv) rc = upload_nodes(hv, v.p);
+        else CK(cudaMemsetAsync(v.p, 0, n * sizeof(V4), stream));
+        if (rc) return rc;
+        CK(cudaStreamSynchronize(stream));
+        return VKPD_OK;
+    }
+    int get_state(double* hx, double* hv) override {
+        if (hx) { int rc = download_nodes(x.p, hx); if (rc) return rc; }
+        if (hv) { int rc = download_nodes(v.p, hv); if (rc) return rc; }
+        return VKPD_OK;
+    }
+    int set_pin_targets(const double* t) override {
+        if (nP == 0) return VKPD_OK;
+        CK(cudaMemcpyAsync(stage.p, t, sizeof(double) * 3 * nP, cudaMemcpyHostToDevice, stream));
+        k_rows_in<T><<<cdiv(nP, 256), 256, 0, stream>>>(nP, stage.p, pin_tgt.p);
+        CK(cudaGetLastError());
+        return VKPD_OK;
+    }
+    int set_forces(const double* hf) override {
+        if (hf == nullptr) { has_forces = false; return VKPD_OK; }
+        has_forces = true;
+        return upload_nodes(hf, f.p);
+    }
+
+    vk::LocalArgs<T> local_args(const V4* xin) {
+        vk::LocalArgs<T> la;
+        la.nE = nE; la.tets = tets.p; la.G = G.p; la.w = w.p; la.x = xin; la.corner = corner.p;
+        la.stats = pstats.p; la.F_out = la.R_out = la.V_out = nullptr;
+        return la;
+    }
+    vk::PcgArgs<T> pcg_args(int init, int pd_iter, int* iters_slot) {
+        vk::PcgArgs<T> pa;
+        pa.nF = nF; pa.ell_w = ell_w; pa.ell_col = ell_col.p; pa.ell_val = ell_val.p; pa.inv_diag = inv_diag.p;
+        pa.inc_ptr = inc_ptr.p; pa.inc_code = inc_code.p; pa.corner = corner.p; pa.m_dt2 = m_dt2.p;
+        pa.xhat = xhat.p; pa.rhs = rhs.p; pa.x = x.p; pa.r = r.p; pa.z = z.p; pa.p0 = p0.p; pa.p1 = p1.p;
+        pa.q = q.p; pa.dx = dx.p; pa.partials = partials.p; pa.scal = scal.p; pa.bar = bar.p;
+        pa.iters_out = iters_slot; pa.fail_iter = fail_iter.p; pa.pd_iter = pd_iter; pa.tol = tol;
+        pa.max_iters = max_iters; pa.init = init;
+        return pa;
+    }
+    cudaError_t launch_pcg(const vk::PcgArgs<T>& pa) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(pcg_blocks);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, vk::k_pcg<T>, pa);
+    }
+
+    // enqueue one frame on `stream`; events (optional) bracket local / global launches
+    int enqueue_frame(int iterations, double damping, std::vector<cudaEvent_t>* ev) {
+        const int nb = cdiv(n, 256);
+        vk::k_prologue<T><<<nb, 256, 0, stream>>>(n, nF, (T)dt, dt2_inv_m.p, has_forces ? f.p : nullptr,
+                                                  pin_tgt.p, x.p, v.p, x_start.p, v_start.p, xhat.p,
+                                                  fail_iter.p);
+        CK(cudaGetLastError());
+        const vk::LocalArgs<T> la = local_args(x.p);
+        for (int it = 0; it < iterations; ++it) {
+            if (ev) CK(cudaEventRecord((*ev)[3 * it], stream));
+            vk::k_local<T, vk::MODE_RESID, false><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+            CK(cudaGetLastError());
+            if (ev) CK(cudaEventRecord((*ev)[3 * it + 1], stream));
+            if (nF > 0) CK(launch_pcg(pcg_args(vk::INIT_PD, it, iters.p + it)));
+            if (ev) CK(cudaEventRecord((*ev)[3 * it + 2], stream));
+        }
+        vk::k_epilogue<T><<<nb, 256, 0, stream>>>(n, (T)(damping / dt), x.p, x_start.p, v.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h_fail, fail_iter.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        return VKPD_OK;
+    }
+
+    int build_graph(int iterations, double damping) {
+        if (graph_exec) { cudaGraphExecDestroy(graph_exec); graph_exec = nullptr; }
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_frame(iterations, damping, nullptr);
+        cudaError_t e = cudaStreamEndCapture(stream, &g);
+        if (rc != VKPD_OK || e != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            graph_broken = true;
+            return VKPD_OK;     // fall back to direct launches
+        }
+        e = cudaGraphInstantiate(&graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            graph_exec = nullptr;
+            graph_broken = true;
+            return VKPD_OK;
+        }
+        graph_iters = iterations;
+        graph_damp = damping;
+        graph_forces = has_forces;
+        return VKPD_OK;
+    }
+
+    int step_async(int iterations, double damping) override {
+        if (iterations < 0 || iterations > 1024) return fail(VKPD_EINVAL, "iterations must be in [0, 1024]");
+        last_iterations = iterations;
+        if (use_graph && !graph_broken) {
+            if (!graph_exec || graph_iters != iterations || graph_damp != damping || graph_forces != has_forces) {
+                int rc = build_graph(iterations, damping);
+                if (rc) return rc;
+            }
+            if (graph_exec) {
+                CK(cudaGraphLaunch(graph_exec, stream));
+                return VKPD_OK;
+            }
+        }
+        return enqueue_frame(iterations, damping, nullptr);
+    }
+
+    int sync(int* failed) override {
+        CK(cudaStreamSynchronize(stream));
+        const int fi = *h_fail;
+        if (failed) *failed = fi == 0x7fffffff ? -1 : fi;
+        if (fi != 0x7fffffff) {
+            vk::k_restore<T><<<cdiv(n, 256), 256, 0, stream>>>(n, x.p, v.p, x_start.p, v_start.p);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(stream));
+            *h_fail = 0x7fffffff;
+            char buf[128];
+            snprintf(buf, sizeof buf, "projective step produced non-finite positions at iteration %d", fi);
+            return fail(VKPD_ENONFINITE, buf);
+        }
+        return VKPD_OK;
+    }
+
+    int profile(int iterations, double damping, double* lms, double* gms, double* fms) override {
+        std::vector<cudaEvent_t> ev(3 * iterations + 2);
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(ev[3 * iterations], stream));
+        int rc = enqueue_frame(iterations, damping, &ev);
+        CK(cudaEventRecord(ev[3 * iterations + 1], stream));
+        CK(cudaStreamSynchronize(stream));
+        double lsum = 0, gsum = 0;
+        for (int it = 0; it < iterations; ++it) {
+            float a = 0, b = 0;
+            CK(cudaEventElapsedTime(&a, ev[3 * it], ev[3 * it + 1]));
+            CK(cudaEventElapsedTime(&b, ev[3 * it + 1], ev[3 * it + 2]));
+            lsum += a; gsum += b;
+        }
+        float fr = 0;
+        CK(cudaEventElapsedTime(&fr, ev[3 * iterations], ev[3 * iterations + 1]));
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (lms) *lms = iterations ? lsum / iterations : 0;
+        if (gms) *gms = iterations ? gsum / iterations : 0;
+        if (fms) *fms = fr;
+        if (rc) return rc;
+        int failed = -1;
+        return sync(&failed);
+    }
+
+    int elastic_rhs(const double* hx, double* hrhs, double* F, double* R, double* Vv) override {
+        int rc = upload_nodes(hx, tmp4a.p);
+        if (rc) return rc;
+        vk::LocalArgs<T> la = local_args(tmp4a.p);
+        DBuf<double> dF, dR, dV;
+        const bool frv = F || R || Vv;
+        if (frv) {
+            CK(dF.alloc((size_t)9 * nE)); CK(dR.alloc((size_t)9 * nE)); CK(dV.alloc((size_t)9 * nE));
+            la.F_out = dF.p; la.R_out = dR.p; la.V_out = dV.p;
+            vk::k_local<T, vk::MODE_RHS, true><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+        } else {
+            vk::k_local<T, vk::MODE_RHS, false><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+        }
+        CK(cudaGetLastError());
+        vk::k_gather<T><<<cdiv(n, 256), 256, 0, stream>>>(n, inc_ptr.p, inc_code.p, corner.p, tmp4b.p);
+        CK(cudaGetLastError());
+        rc = download_nodes(tmp4b.p, hrhs);
+        if (rc) return rc;
+        const size_t bytes = sizeof(double) * 9 * nE;
+        if (F) CK(cudaMemcpy(F, dF.p, bytes, cudaMemcpyDeviceToHost));
+        if (R) CK(cudaMemcpy(R, dR.p, bytes, cudaMemcpyDeviceToHost));
+        if (Vv) CK(cudaMemcpy(Vv, dV.p, bytes, cudaMemcpyDeviceToHost));
+        return VKPD_OK;
+    }
+
+    int global_solve(const double* B, const double* P, double* X, int k) override {
+        if (k <= 0) return fail(VKPD_EINVAL, "need at least one right-hand side column");
+        std::vector<double> b3((size_t)3 * n), p3((size_t)3 * std::max(1, nP)), x3((size_t)3 * n);
+        int bad = 0;
+        for (int c0 = 0; c0 < k; c0 += 3) {
+            const int kc = std::min(3, k - c0);
+            std::fill(b3.begin(), b3.end(), 0.0);
+            std::fill(p3.begin(), p3.end(), 0.0);
+            for (int j = 0; j < n; ++j)
+                for (int c = 0; c < kc; ++c) b3[3 * (size_t)j + c] = B[(size_t)j * k + c0 + c];
+            for (int j = 0; j < nP; ++j)
+                for (int c = 0; c < kc; ++c) p3[3 * (size_t)j + c] = P[(size_t)j * k + c0 + c];
+            int rc = upload_nodes(b3.data(), tmp4a.p);
+            if (rc) return rc;
+            if (nP) {
+                CK(cudaMemcpyAsync(stage.p, p3.data(), sizeof(double) * 3 * nP, cudaMemcpyHostToDevice, stream));
+                k_rows_in<T><<<cdiv(nP, 256), 256, 0, stream>>>(nP, stage.p, tmp4b.p);
+                CK(cudaGetLastError());
+            }
+            if (nF > 0) {
+                k_rhs_minus_fp<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, tmp4a.p, fp_ptr.p, fp_col.p, fp_val.p,
+                                                                    tmp4b.p, rhs.p);
+                CK(cudaGetLastError());
+                CK(launch_pcg(pcg_args(vk::INIT_RHS, 0, iters.p + 1023)));
+                // assemble internal vector [dx (free) ; P (pinned)] in tmp4a
+                CK(cudaMemcpyAsync(tmp4a.p, dx.p, sizeof(V4) * nF, cudaMemcpyDeviceToDevice, stream));
+            }
+            if (nP) CK(cudaMemcpyAsync(tmp4a.p + nF, tmp4b.p, sizeof(V4) * nP, cudaMemcpyDeviceToDevice, stream));
+            rc = download_nodes(tmp4a.p, x3.data());
+            if (rc) return rc;
+            for (int j = 0; j < n; ++j)
+                for (int c = 0; c < kc; ++c) {
+                    const double vv = x3[3 * (size_t)j + c];
+                    X[(size_t)j * k + c0 + c] = vv;
+                    bad |= !std::isfinite(vv);
+                }
+        }
+        (void)bad;
+        return VKPD_OK;
+    }
+
+    int apply_K(const double* hX, double* hY) override {
+        int rc = upload_nodes(hX, tmp4a.p);
+        if (rc) return rc;
+        k_apply_K<T><<<cdiv(n, 256), 256, 0, stream>>>(n, nF, ell_w, ell_col.p, ell_val.p, fp_ptr.p, fp_col.p,
+                                                       fp_val.p, tmp4a.p, tmp4b.p);
+        CK(cudaGetLastError());
+        return download_nodes(tmp4b.p, hY);
+    }
+
+    int stats(vkpd_stats* st) override {
+        std::memset(st, 0, sizeof(*st));
+        CK(cudaStreamSynchronize(stream));
+        const int ni = std::min(last_iterations, 256);
+        st->n_pd_iters = ni;
+        if (ni > 0) CK(cudaMemcpy(st->cg_iters, iters.p, sizeof(int) * ni, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < ni; ++i) st->cg_iters_total += st->cg_iters[i];
+        vk::ProjStats ps;
+        CK(cudaMemcpy(&ps, pstats.p, sizeof(ps), cudaMemcpyDeviceToHost));
+        st->robust = ps.robust;
+        st->fallback = ps.fallback;
+        st->pcg_blocks = pcg_blocks;
+        st->ell_width = ell_w;
+        st->n_free = nF;
+        return VKPD_OK;
+    }
+};
+
+}  // namespace
+
+struct vkpd_ctx {
+    std::unique_ptr<CtxBase> impl;
+};
+
+extern "C" {
+
+const char* vkpd_last_error(void) { return g_err.c_str(); }
+
+int vkpd_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *count = 0;
+        return fail(VKPD_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    *count = c;
+    return VKPD_OK;
+}
+
+int vkpd_create(const vkpd_mesh_desc* mesh, const vkpd_config* cfg, vkpd_ctx** out) {
+    if (!mesh || !cfg || !out) return fail(VKPD_EINVAL, "null argument");
+    if (!mesh->tets || !mesh->shape_grad || !mesh->volume || !mesh->gamma_s || !mesh->gamma_v)
+        return fail(VKPD_EINVAL, "missing mesh array");
+    if (mesh->n_pins > 0 && !mesh->pins) return fail(VKPD_EINVAL, "missing pin array");
+    int count = 0;
+    if (vkpd_device_count(&count) != VKPD_OK || count == 0)
+        return fail(VKPD_ECUDA, "no CUDA device available (the vkpd library has no CPU path)");
+    if (cfg->device < 0 || cfg->device >= count) return fail(VKPD_EINVAL, "bad device ordinal");
+    std::unique_ptr<vkpd_ctx> c(new vkpd_ctx);
+    if (cfg->precision == VKPD_FP32) c->impl.reset(new Ctx<float>());
+    else if (cfg->precision == VKPD_FP64) c->impl.reset(new Ctx<double>());
+    else return fail(VKPD_EINVAL, "precision must be 32 or 64");
+    c->impl->device = cfg->device;
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return fail(VKPD_ECUDA, "cudaSetDevice failed");
+    int rc = c->impl->init(mesh, cfg);
+    if (rc != VKPD_OK) return rc;
+    *out = c.release();
+    return VKPD_OK;
+}
+
+int vkpd_create_matrix(int64_t n, const int64_t* indptr, const int64_t* indices, const double* data,
+                       const int64_t* pins, int64_t n_pins, const vkpd_config* cfg, vkpd_ctx** out) {
+    if (!indptr || !indices || !data || !cfg || !out || (n_pins > 0 && !pins))
+        return fail(VKPD_EINVAL, "null argument");
+    int count = 0;
+    if (vkpd_device_count(&count) != VKPD_OK || count == 0)
+        return fail(VKPD_ECUDA, "no CUDA device available (the vkpd library has no CPU path)");
+    if (cfg->device < 0 || cfg->device >= count) return fail(VKPD_EINVAL, "bad device ordinal");
+    std::unique_ptr<vkpd_ctx> c(new vkpd_ctx);
+    if (cfg->precision == VKPD_FP32) c->impl.reset(new Ctx<float>());
+    else if (cfg->precision == VKPD_FP64) c->impl.reset(new Ctx<double>());
+    else return fail(VKPD_EINVAL, "precision must be 32 or 64");
+    c->impl->device = cfg->device;
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return fail(VKPD_ECUDA, "cudaSetDevice failed");
+    int rc = c->impl->init_matrix(n, indptr, indices, data, pins, n_pins, cfg);
+    if (rc != VKPD_OK) return rc;
+    *out = c.release();
+    return VKPD_OK;
+}
+
+int vkpd_get_matrix_csr(vkpd_ctx* ctx, int64_t* indptr, int64_t* indices, double* data, int64_t* nnz) {
+    if (!ctx || !nnz) return fail(VKPD_EINVAL, "null argument");
+    cudaSetDevice(ctx->impl->device);
+    return ctx->impl->get_csr(indptr, indices, data, nnz);
+}
+
+void vkpd_destroy(vkpd_ctx* ctx) { delete ctx; }
+
+int vkpd_set_stream(vkpd_ctx* ctx, void* stream) {
+    if (!ctx) return fail(VKPD_EINVAL, "null context");
+    ctx->impl->stream = stream ? (cudaStream_t)stream : ctx->impl->own_stream;
+    return VKPD_OK;
+}
+void* vkpd_get_stream(vkpd_ctx* ctx) { return ctx ? (void*)ctx->impl->stream : nullptr; }
+
+#define CTX_CALL(expr)                                                                             \
+    do {                                                                                           \
+        if (!ctx) return fail(VKPD_EINVAL, "null context");                                       \
+        cudaSetDevice(ctx->impl->device);                                                          \
+        return ctx->impl->expr;                                                                    \
+    } while (0)
+
+int vkpd_set_state(vkpd_ctx* ctx, const double* x, const double* v) {
+    if (!x) return fail(VKPD_EINVAL, "null positions");
+    CTX_CALL(set_state(x, v));
+}
+int vkpd_get_state(vkpd_ctx* ctx, double* x, double* v) { CTX_CALL(get_state(x, v)); }
+int vkpd_set_pin_targets(vkpd_ctx* ctx, const double* t) {
+    if (!t) return fail(VKPD_EINVAL, "null pin targets");
+    CTX_CALL(set_pin_targets(t));
+}
+int vkpd_set_forces(vkpd_ctx* ctx, const double* f) { CTX_CALL(set_forces(f)); }
+int vkpd_step_async(vkpd_ctx* ctx, int iterations, double damping) { CTX_CALL(step_async(iterations, damping)); }
+int vkpd_sync(vkpd_ctx* ctx, int* failed_iter) { CTX_CALL(sync(failed_iter)); }
+int vkpd_step(vkpd_ctx* ctx, int iterations, double damping, int* failed_iter) {
+    if (!ctx) return fail(VKPD_EINVAL, "null context");
+    int rc = vkpd_step_async(ctx, iterations, damping);
+    if (rc) return rc;
+    return vkpd_sync(ctx, failed_iter);
+}
+int vkpd_profile_step(vkpd_ctx* ctx, int iterations, double damping, double* lms, double* gms, double* fms) {
+    CTX_CALL(profile(iterations, damping, lms, gms, fms));
+}
+int vkpd_elastic_rhs(vkpd_ctx* ctx, const double* x, double* rhs, double* F, double* R, double* V) {
+    if (!x || !rhs) return fail(VKPD_EINVAL, "null buffer");
+    CTX_CALL(elastic_rhs(x, rhs, F, R, V));
+}
+int vkpd_global_solve(vkpd_ctx* ctx, const double* B, const double* P, double* X, int k) {
+    if (!B || !X) return fail(VKPD_EINVAL, "null buffer");
+    CTX_CALL(global_solve(B, P, X, k));
+}
+int vkpd_apply_K(vkpd_ctx* ctx, const double* X, double* Y) {
+    if (!X || !Y) return fail(VKPD_EINVAL, "null buffer");
+    CTX_CALL(apply_K(X, Y));
+}
+int vkpd_get_stats(vkpd_ctx* ctx, vkpd_stats* st) {
+    if (!st) return fail(VKPD_EINVAL, "null stats");
+    CTX_CALL(stats(st));
+}
+
+int vkpd_batch_projections(int precision, int64_t n, const double* F, double* R, double* V,
+                           unsigned int* n_robust, unsigned int* n_fallback) {
+    if (n < 0 || (n > 0 && (!F || !R || !V))) return fail(VKPD_EINVAL, "bad arguments");
+    if (precision != VKPD_FP32 && precision != VKPD_FP64) return fail(VKPD_EINVAL, "precision must be 32 or 64");
+    int count = 0;
+    if (vkpd_device_count(&count) != VKPD_OK || count == 0)
+        return fail(VKPD_ECUDA, "no CUDA device available (the vkpd library has no CPU path)");
+    for (int64_t i = 0; i < 9 * n; ++i)
+        if (!std::isfinite(F[i])) return fail(VKPD_EINVAL, "non-finite deformation gradient in batch");
+    if (n == 0) return VKPD_OK;
+    DBuf<double> dF, dR, dV;
+    DBuf<vk::ProjStats> st;
+    CK(dF.alloc((size_t)9 * n)); CK(dR.alloc((size_t)9 * n)); CK(dV.alloc((size_t)9 * n));
+    CK(st.alloc(1));
+    CK(cudaMemset(st.p, 0, sizeof(vk::ProjStats)));
+    CK(cudaMemcpy(dF.p, F, sizeof(double) * 9 * n, cudaMemcpyHostToDevice));
+    if (precision == VKPD_FP32) vk::k_project<float><<<cdiv(n, 128), 128>>>((int)n, dF.p, dR.p, dV.p, st.p);
+    else vk::k_project<double><<<cdiv(n, 128), 128>>>((int)n, dF.p, dR.p, dV.p, st.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(R, dR.p, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(V, dV.p, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost));
+    vk::ProjStats hs;
+    CK(cudaMemcpy(&hs, st.p, sizeof(hs), cudaMemcpyDeviceToHost));
+    if (n_robust) *n_robust = hs.robust;
+    if (n_fallback) *n_fallback = hs.fallback;
+    return VKPD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,347 @@
+"""Drop-in projective-dynamics API backed by the B200 (sm_100a) library.
+
+Mirrors the reference simulator surface (`/root/reference/pkg/src/volknit/pdsolver.py`):
+
+  SimState                       pdsolver.py:180-198
+  assemble_global(mesh, g, dt)   pdsolver.py:42-56     (assembled on the GPU, returned as CSC)
+  elastic_rhs(mesh, g, x)        pdsolver.py:59-71     (GPU local step + deterministic gather)
+  GlobalSolver(K, free, pins)    pdsolver.py:201-246   (GPU persistent CG; `.solve(B, pin_vals)`)
+  pd_step(state, mesh, g, ...)   pdsolver.py:257-304
+  simulate_mesh(mesh, g, ...)    pdsolver.py:710-763
+  pd_objective / elastic_energy  pdsolver.py:74-82, 307-312 (diagnostics, projections on GPU)
+
+Same argument names, meaning and error behaviour: ValueError for invalid input,
+RuntimeError("... non-finite positions at iteration {it}") on blow-up, any
+object with `.solve(B, pin_vals)` accepted as `solver=`.  All arithmetic runs
+in the CUDA library; nothing here falls back to the CPU.
+
+Extra keyword arguments (not in the reference): `precision` ("fp32" default,
+"fp64"), `tol` (relative residual of each global solve) and `max_iters`.
+
+Solver modes: "direct" is the exact global step (the reference's SuperLU),
+realised as a persistent CG on the device driven to `tol`; "cms" is the
+reference's component-mode subspace + A-Jacobi path (see `cms.py`).
+"""
+
+from __future__ import annotations
+
+import logging
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _abi
+from .material import MaterialField
+
+log = logging.getLogger(__name__)
+
+PD_ITERS_DEFAULT = 30       # pdsolver.py:23
+JACOBI_OMEGA = 0.75         # pdsolver.py:24
+CONTACT_STIFFNESS = 1e4     # pdsolver.py:25
+
+DEFAULT_TOL = {"fp32": 1e-6, "fp64": 1e-12}
+
+
+@dataclass
+class SimState:
+    """Forward-simulation state; pinned nodes track their targets exactly (`pdsolver.py:180-198`)."""
+
+    x: np.ndarray
+    v: np.ndarray
+    dt: float
+    pins: np.ndarray = field(default_factory=lambda: np.empty(0, dtype=int))
+    pin_targets: np.ndarray = None
+    colliders: tuple = ()
+
+    def __post_init__(self):
+        self.x = np.asarray(self.x, dtype=float).reshape(-1, 3).copy()
+        self.v = np.asarray(self.v, dtype=float).reshape(-1, 3).copy()
+        self.pins = np.asarray(self.pins, dtype=int)
+        if self.pin_targets is None and len(self.pins):
+            self.pin_targets = self.x[self.pins].copy()
+        if self.dt <= 0.0:
+            raise ValueError("dt must be positive")
+
+
+def _check_inputs(mesh, gammas, dt):
+    if dt <= 0.0:
+        raise ValueError("dt must be positive")
+    if np.any(np.asarray(gammas.gamma_s) < 0.0) or np.any(np.asarray(gammas.gamma_v) < 0.0):
+        raise ValueError("negative material coefficient")
+    if getattr(mesh, "node_mass", None) is None:
+        raise ValueError("mesh node masses not lumped yet")
+
+
+# ---------------------------------------------------------------------------
+# device contexts (one per scene configuration), cached by array identity
+
+_CACHE = {}
+_CACHE_MAX = 8
+
+
+def _key(mesh, gammas, dt, pins, precision, tol, max_iters):
+    arrs = (mesh.tets, mesh.shape_grad, mesh.volume, mesh.node_mass, gammas.gamma_s, gammas.gamma_v)
+    ident = tuple((id(a), a.__array_interface__["data"][0], a.shape) for a in map(np.asarray, arrs))
+    pins = np.asarray(pins, dtype=np.int64)
+    return (ident, float(dt), pins.tobytes(), precision, tol, max_iters)
+
+
+def invalidate_cache():
+    """Drop cached device contexts (call after editing mesh/material arrays in place)."""
+    _CACHE.clear()
+
+
+def device_context(mesh, gammas, dt, pins=(), precision="fp32", tol=None, max_iters=0):
+    """Device-resident scene for (mesh, gammas, dt, pins); created once and cached."""
+    _check_inputs(mesh, gammas, dt)
+    tol = DEFAULT_TOL[precision] if tol is None else float(tol)
+    k = _key(mesh, gammas, dt, pins, precision, tol, max_iters)
+    ctx = _CACHE.get(k)
+    if ctx is None:
+        if len(_CACHE) >= _CACHE_MAX:
+            _CACHE.pop(next(iter(_CACHE)))
+        ctx = _abi.Context(mesh.n_nodes if hasattr(mesh, "n_nodes") else len(mesh.nodes), mesh.tets,
+                           mesh.shape_grad, mesh.volume, mesh.node_mass, gammas.gamma_s,
+                           gammas.gamma_v, pins, dt, precision=precision, tol=tol,
+                           max_iters=max_iters)
+        _CACHE[k] = ctx
+    return ctx
+
+
+# ---------------------------------------------------------------------------
+# assembly and local step
+
+
+def assemble_global(mesh, gammas, dt, precision="fp64"):
+    """Scalar global matrix K = M/dt^2 + sum_e 2 V_e (gs + gv) G G^T (`pdsolver.py:42-56`).
+
+    Assembled on the device (deterministic node-centric sum) and returned as a
+    scipy CSC matrix for callers that want the matrix itself.
+    """
+    ctx = device_context(mesh, gammas, dt, (), precision)
+    indptr, indices, data = ctx.matrix_csr()
+    n = ctx.n
+    return sp.csr_matrix((data, indices, indptr), shape=(n, n)).tocsc()
+
+
+def elastic_rhs(mesh, gammas, x, precision="fp64"):
+    """Local-step rhs sum_e 2 V_e G^T (gs R + gv V) and (F, R, V) (`pdsolver.py:59-71`)."""
+    m = mesh
+    if getattr(m, "node_mass", None) is None:
+        m = _MassShim(mesh)
+    ctx = device_context(m, gammas, 1.0, (), precision)
+    rhs, F, R, V = ctx.elastic_rhs(np.asarray(x, dtype=float).reshape(-1, 3))
+    return rhs, F, R, V
+
+
+class _MassShim:
+    """elastic_rhs does not need masses; give the context unit masses."""
+
+    def __init__(self, mesh):
+        self.tets, self.shape_grad, self.volume = mesh.tets, mesh.shape_grad, mesh.volume
+        self.n_nodes = mesh.nodes.shape[0]
+        self.nodes = mesh.nodes
+        self.node_mass = _MassShim._ones(self.n_nodes)
+
+    _ones_cache = {}
+
+    @staticmethod
+    def _ones(n):
+        a = _MassShim._ones_cache.get(n)
+        if a is None:
+            a = _MassShim._ones_cache[n] = np.ones(n)
+        return a
+
+
+def elastic_energy(mesh, gammas, x, FRV=None, precision="fp64"):
+    """sum_e V_e (gs |F - R|^2 + gv |F - V|^2) (`pdsolver.py:74-82`), projections on the GPU."""
+    if FRV is None:
+        _, F, R, V = elastic_rhs(mesh, gammas, x, precision)
+    else:
+        F, R, V = FRV
+    ds = np.sum((F - R) ** 2, axis=(1, 2))
+    dv = np.sum((F - V) ** 2, axis=(1, 2))
+    return float(np.sum(mesh.volume * (gammas.gamma_s * ds + gammas.gamma_v * dv)))
+
+
+def pd_objective(state_or_x, mesh, gammas, xhat, dt, precision="fp64"):
+    """Inertia plus elastic potential minimized by one implicit step (`pdsolver.py:307-312`)."""
+    x = state_or_x.x if isinstance(state_or_x, SimState) else np.asarray(state_or_x)
+    d = x - xhat
+    inertia = 0.5 / dt ** 2 * float(np.sum(mesh.node_mass[:, None] * d * d))
+    return inertia + elastic_energy(mesh, gammas, x, precision=precision)
+
+
+def _predicted(state, forces, mesh):
+    """xhat = x + dt v + dt^2 m^-1 f, m^-1 := 0 where m = 0 (`pdsolver.py:249-254`)."""
+    inv_m = np.zeros(mesh.n_nodes)
+    pos = mesh.node_mass > 0.0
+    inv_m[pos] = 1.0 / mesh.node_mass[pos]
+    f = np.zeros_like(state.x) if forces is None else np.asarray(forces, dtype=float)
+    return state.x + state.dt * state.v + state.dt ** 2 * inv_m[:, None] * f
+
+
+# ---------------------------------------------------------------------------
+# global solver
+
+
+class GlobalSolver:
+    """Solves K X = B with pinned values eliminated (`pdsolver.py:201-246`).
+
+    `K` is any sparse SPD matrix (e.g. from `assemble_global`); it is uploaded
+    once and every `solve(B, pin_vals)` runs the device CG to `tol`.  Mode
+    "cms" routes through the component-mode subspace (`cms.CmsGlobalSolver`).
+    """
+
+    def __init__(self, K, free, pins, mode="direct", cms=None, refine_sweeps=0, aggregation=2,
+                 omega=JACOBI_OMEGA, chebyshev=False, precision="fp64", tol=None, max_iters=0):
+        if mode not in ("direct", "cms"):
+            raise ValueError(f"unknown solver mode {mode!r}")
+        self.K = K
+        self.free = np.asarray(free)
+        self.pins = np.asarray(pins, dtype=np.int64)
+        self.mode = mode
+        self.cms = cms
+        self.refine_sweeps = refine_sweeps
+        self.aggregation = aggregation
+        self.omega = omega
+        self.chebyshev = chebyshev
+        tol = DEFAULT_TOL[precision] if tol is None else tol
+        K = sp.csr_matrix(K)
+        n = K.shape[0]
+        expect_free = np.setdiff1d(np.arange(n), self.pins)
+        if len(expect_free) != len(self.free) or np.any(np.sort(self.free) != expect_free):
+            raise ValueError("free must be the complement of pins")
+        self._ctx = _abi.MatrixContext(K, self.pins, precision=precision, tol=tol, max_iters=max_iters)
+        if mode == "cms":
+            from .cms import CmsGlobalSolver
+            self._cms = CmsGlobalSolver(self._ctx, K, self.free, self.pins, cms, refine_sweeps,
+                                        aggregation, omega, chebyshev)
+
+    def solve(self, B, pin_vals):
+        B = np.asarray(B, dtype=float)
+        if self.mode == "cms":
+            return self._cms.solve(B, pin_vals)
+        return self._ctx.global_solve(B, pin_vals)
+
+
+# ---------------------------------------------------------------------------
+# stepping
+
+
+def pd_step(state, mesh, gammas, iterations=PD_ITERS_DEFAULT, forces=None, solver=None,
+            contact_stiffness=CONTACT_STIFFNESS, damping=1.0, precision="fp32", tol=None,
+            max_iters=0):
+    """One implicit-Euler step by local/global rounds (`pdsolver.py:257-304`); returns the state.
+
+    With `solver=None` the whole step (prologue, `iterations` x [local step,
+    device CG], epilogue) runs device-resident as one CUDA graph.  A caller
+    `solver` (anything with `.solve(B, pin_vals)`) keeps the reference's
+    host-driven loop with the local step on the GPU.
+    """
+    if state.colliders:
+        from .contact import pd_step_contact
+        return pd_step_contact(state, mesh, gammas, iterations, forces, contact_stiffness,
+                               damping, precision)
+    _check_inputs(mesh, gammas, state.dt)
+    if solver is not None and not isinstance(solver, _DeviceStep):
+        return _pd_step_host_solver(state, mesh, gammas, iterations, forces, solver, damping, precision)
+    ctx = device_context(mesh, gammas, state.dt, state.pins, precision, tol, max_iters)
+    ctx.set_state(state.x, state.v)
+    if len(state.pins):
+        ctx.set_pin_targets(state.pin_targets)
+    ctx.set_forces(forces)
+    try:
+        ctx.step(iterations, damping)
+    except _abi.NonFiniteError as exc:
+        raise RuntimeError(str(exc)) from None
+    x, v = ctx.get_state()
+    state.x, state.v = x, v
+    return state
+
+
+class _DeviceStep:
+    """Marker base for solvers that run inside the device-resident step."""
+
+
+def _pd_step_host_solver(state, mesh, gammas, iterations, forces, solver, damping, precision):
+    """Reference loop (`pdsolver.py:283-304`) with a caller-provided global solver."""
+    ctx = device_context(mesh, gammas, state.dt, (), "fp64" if precision == "fp64" else precision)
+    xhat = _predicted(state, forces, mesh)
+    x_start = state.x.copy()
+    x = xhat.copy()
+    if len(state.pins):
+        pin_vals = state.pin_targets
+        x[state.pins] = pin_vals
+    else:
+        pin_vals = np.empty((0, 3))
+    inertia = (mesh.node_mass[:, None] / state.dt ** 2) * xhat
+    for it in range(iterations):
+        rhs = ctx.elastic_rhs(x, with_frv=False)[0]
+        x = np.asarray(solver.solve(inertia + rhs, pin_vals), dtype=float)
+        if not np.all(np.isfinite(x)):
+            raise RuntimeError(f"projective step produced non-finite positions at iteration {it}")
+    state.v = damping * (x - x_start) / state.dt
+    state.x = x
+    return state
+
+
+def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=None, colliders=(),
+                  iterations=PD_ITERS_DEFAULT, solver_mode="direct", n_domains=2, modes_per_domain=20,
+                  refine_sweeps=30, aggregation=2, chebyshev=False, damping=1.0, polish_tol=None,
+                  x0=None, precision="fp32", tol=None, max_iters=0, labels=None):
+    """Run a forward simulation and return the frame stack (steps, nV, 3) (`pdsolver.py:710-763`).
+
+    pin_targets may be constant (nP, 3) or a per-step path (steps, nP, 3).
+    """
+    if polish_tol is not None:
+        raise NotImplementedError("newton_polish is outside the B200 hot path (SURVEY.md 8f)")
+    if solver_mode not in ("direct", "cms"):
+        raise ValueError(f"unknown solver mode {solver_mode!r}")
+    _check_inputs(mesh, gammas, dt)
+    pins = np.asarray(pins, dtype=int)
+    pin_path = None
+    if pin_targets is not None:
+        pin_targets = np.asarray(pin_targets, dtype=float)
+        if pin_targets.ndim == 3:
+            pin_path = pin_targets
+            pin_targets = pin_path[0]
+    state = SimState(x=mesh.nodes.copy() if x0 is None else np.asarray(x0, dtype=float).copy(),
+                     v=np.zeros_like(mesh.nodes), dt=dt, pins=pins, pin_targets=pin_targets,
+                     colliders=tuple(colliders))
+    if forces is not None:
+        forces = np.asarray(forces, dtype=float)
+        if forces.ndim == 2:
+            forces = np.broadcast_to(forces, (steps,) + forces.shape)
+    frames = np.empty((steps, mesh.n_nodes, 3))
+    if state.colliders:
+        for i in range(steps):
+            if pin_path is not None:
+                state.pin_targets = pin_path[i]
+            pd_step(state, mesh, gammas, iterations, None if forces is None else forces[i],
+                    damping=damping, precision=precision)
+            frames[i] = state.x
+        return frames
+    if solver_mode == "cms":
+        from .cms import simulate_cms
+        return simulate_cms(mesh, gammas, steps, dt, forces, state, pin_path, iterations,
+                            n_domains, modes_per_domain, refine_sweeps, aggregation, chebyshev,
+                            damping, precision, labels)
+    ctx = device_context(mesh, gammas, dt, pins, precision, tol, max_iters)
+    ctx.set_state(state.x, state.v)
+    if len(pins):
+        ctx.set_pin_targets(state.pin_targets)
+    const_forces = forces is not None and forces.strides[0] == 0      # broadcast (nV,3) input
+    ctx.set_forces(None if forces is None else forces[0])
+    for i in range(steps):
+        if pin_path is not None:
+            ctx.set_pin_targets(pin_path[i])
+        if forces is not None and not const_forces and i > 0:
+            ctx.set_forces(forces[i])
+        try:
+            ctx.step(iterations, damping)
+        except _abi.NonFiniteError as exc:
+            raise RuntimeError(str(exc)) from None
+        ctx.get_state(want_x=True, want_v=False, out_x=frames[i])
+    return frames

@@ -1,0 +1,180 @@
+"""Generate golden vectors by running the REAL reference (volknit) in the build container.
+
+Run from the repo root (needs /root/reference, which the GPU box does not have):
+
+    python tests/golden/make_golden.py [small|c2|c3|all]
+
+Outputs (committed) land next to this script.  Scenes come from
+`paper_2405_12484_b200.scenes` (seeded, bit-reproducible); the fixtures also
+store input checksums so the tests can prove the regenerated scene is the one
+the reference saw.  Per-fixture contents:
+
+  projections.npz  F batch (random / inverted / near-singular / clamp / t*I) and the
+                   reference `material.batch_projections` R, V; scalar
+                   `sl3_sigma_project` results on special sigma triples.
+  c1.npz           C1 swatch: `assemble_global` K (CSR), `elastic_rhs` at a perturbed
+                   x (rhs, F, R, V), `simulate_mesh(direct)` after 1 and 3 frames.
+  solvers.npz      C1 free-free K: `a_jacobi_refine` (agg 2/3, Chebyshev) from a seeded
+                   start, `build_cms(...).solve`, and `simulate_mesh(cms)` 1 frame.
+  c2.npz           C2 scarf: `simulate_mesh(direct)` frames 1, 10, 100 (f64).
+  c3.npz           C3 sweater: `simulate_mesh(direct)` frame 1, displacement as f32.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from volknit import material as ref_mat      # noqa: E402
+from volknit import pdsolver as ref_pd       # noqa: E402
+from volknit import volmesh as ref_vm        # noqa: E402
+
+from paper_2405_12484_b200 import scenes     # noqa: E402
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:32]
+
+
+def scene_digest(sc):
+    m = sc.mesh
+    return digest(m.nodes, m.tets.astype(np.int64), m.node_mass, sc.gammas.gamma_s,
+                  sc.gammas.gamma_v, sc.pins.astype(np.int64))
+
+
+def ref_mesh(sc):
+    m = sc.mesh
+    rm = ref_vm.VolumeMesh(nodes=m.nodes.copy(), tets=m.tets.copy(), cell_size=m.cell_size,
+                           origin=m.origin.copy(), node_grid=m.node_grid.copy(),
+                           voxels=m.voxels.copy(), tet_voxel=m.tet_voxel.copy())
+    rm.node_mass = m.node_mass.copy()
+    return rm
+
+
+def projection_batch(rng):
+    F = [np.eye(3) + 0.8 * rng.normal(size=(1500, 3, 3))]
+    inv = np.eye(3) + 0.3 * rng.normal(size=(200, 3, 3))
+    inv[:, :, 0] *= -1.0
+    F.append(inv)
+    # near-rank-deficient: scale one singular direction down
+    a = rng.normal(size=(100, 3, 3))
+    U, s, Vt = np.linalg.svd(a)
+    s[:, 2] = 10.0 ** rng.uniform(-7, -2, size=100)
+    F.append(U @ (s[:, :, None] * Vt))
+    # large stretches / compressions (suspicious band: min < 0.2 or max > 5)
+    d = np.exp(rng.uniform(-3.0, 2.0, size=(200, 3)))
+    Q1 = np.linalg.qr(rng.normal(size=(200, 3, 3)))[0]
+    Q2 = np.linalg.qr(rng.normal(size=(200, 3, 3)))[0]
+    F.append(Q1 @ (d[:, :, None] * np.swapaxes(Q2, 1, 2)))
+    # mild near-identity (the PD steady state)
+    F.append(np.eye(3) + 0.02 * rng.normal(size=(500, 3, 3)))
+    # uniform scalings incl. the symmetry-breaking band
+    F.append(np.stack([t * np.eye(3) for t in (0.5, 1.0, 1.5, 1.8, 1.95, 2.0, 2.5)]))
+    return np.concatenate(F)
+
+
+def make_projections():
+    rng = np.random.default_rng(20240817)
+    F = projection_batch(rng)
+    R, V = ref_mat.batch_projections(F)
+    sig_cases = np.array([
+        [2.0, 2.0, 2.0], [100.0, 100.0, 1e-5], [1.5, 1.5, 1.5], [0.5, 0.5, 0.5],
+        [3.0, 0.1, 0.05], [1.2, 0.9, 0.95], [7.0, 1.0, 0.2], [0.0, 0.0, 0.0],
+        [1.0, 1.0, -0.5], [40.0, 0.3, 0.001],
+    ])
+    sig_rand = np.exp(rng.uniform(-3.0, 1.5, size=(40, 3)))
+    sig_all = np.concatenate([sig_cases, sig_rand])
+    S, L, C, OK = [], [], [], []
+    for sg in sig_all:
+        s, lam, cl, ok = ref_mat.sl3_sigma_project(sg)
+        S.append(s); L.append(lam); C.append(cl); OK.append(ok)
+    np.savez_compressed(os.path.join(HERE, "projections.npz"), F=F, R=R, V=V, sigma=sig_all,
+                        s=np.array(S), lam=np.array(L), clamped=np.array(C), ok=np.array(OK))
+    print("projections", F.shape)
+
+
+def make_c1():
+    sc = scenes.c1_swatch()
+    rm = ref_mesh(sc)
+    K = ref_pd.assemble_global(rm, ref_mat.MaterialField(sc.gammas.gamma_s, sc.gammas.gamma_v),
+                               sc.dt).tocsr()
+    gam = ref_mat.MaterialField(sc.gammas.gamma_s, sc.gammas.gamma_v)
+    rng = np.random.default_rng(7)
+    xp = sc.mesh.nodes + 0.002 * rng.normal(size=sc.mesh.nodes.shape)
+    rhs, F, R, V = ref_pd.elastic_rhs(rm, gam, xp)
+    kw = dict(forces=sc.forces, pins=sc.pins, pin_targets=sc.pin_targets, iterations=30)
+    fr3 = ref_pd.simulate_mesh(rm, gam, 3, sc.dt, **kw)
+    st = ref_pd.SimState(x=sc.mesh.nodes, v=np.zeros_like(sc.mesh.nodes), dt=sc.dt,
+                         pins=sc.pins, pin_targets=sc.pin_targets)
+    xhat = ref_pd._predicted(st, sc.forces, rm)
+    np.savez_compressed(os.path.join(HERE, "c1.npz"), digest=scene_digest(sc),
+                        K_data=K.data, K_indices=K.indices, K_indptr=K.indptr,
+                        x_pert=xp, rhs=rhs, F=F, R=R, V=V, frames=fr3, xhat=xhat)
+    print("c1", fr3.shape)
+
+
+def make_solvers():
+    sc = scenes.c1_swatch()
+    rm = ref_mesh(sc)
+    gam = ref_mat.MaterialField(sc.gammas.gamma_s, sc.gammas.gamma_v)
+    K = ref_pd.assemble_global(rm, gam, sc.dt)
+    free = np.setdiff1d(np.arange(sc.n_nodes), sc.pins)
+    Kff = K[free][:, free].tocsc()
+    rng = np.random.default_rng(11)
+    b = rng.normal(size=len(free))
+    x0 = rng.normal(size=len(free))
+    out = {"digest": scene_digest(sc), "b": b, "x0": x0}
+    for agg in (2, 3):
+        x, info = ref_pd.a_jacobi_refine(Kff, b, x0, sweeps=7, aggregation=agg, omega=0.7)
+        out[f"aj{agg}_x"], out[f"aj{agg}_res"] = x, np.array(info["residuals"])
+    x, info = ref_pd.a_jacobi_refine(Kff, b, x0, sweeps=10, aggregation=2, chebyshev=True)
+    out["cheb_x"], out["cheb_res"] = x, np.array(info["residuals"])
+    x, info = ref_pd.a_jacobi_refine(Kff, b, x0, sweeps=60, aggregation=2, omega=2.5)
+    out["div_x"], out["div_res"], out["div_flag"] = x, np.array(info["residuals"]), info["diverged"]
+    cms = ref_pd.build_cms(Kff, rm, n_domains=2, modes_per_domain=12, free=free)
+    out["cms_x"] = cms.solve(b)
+    out["cms_nred"] = cms.K_red.shape[0]
+    kw = dict(forces=sc.forces, pins=sc.pins, pin_targets=sc.pin_targets, iterations=30)
+    out["cms_frame"] = ref_pd.simulate_mesh(rm, gam, 1, sc.dt, solver_mode="cms", n_domains=2,
+                                            modes_per_domain=12, refine_sweeps=30, **kw)[0]
+    np.savez_compressed(os.path.join(HERE, "solvers.npz"), **out)
+    print("solvers")
+
+
+def make_big(key, frames_keep, steps, f32_disp):
+    sc = scenes.make_scene(key)
+    rm = ref_mesh(sc)
+    gam = ref_mat.MaterialField(sc.gammas.gamma_s, sc.gammas.gamma_v)
+    t0 = time.time()
+    fr = ref_pd.simulate_mesh(rm, gam, steps, sc.dt, forces=sc.forces, pins=sc.pins,
+                              pin_targets=sc.pin_targets, iterations=30)
+    el = time.time() - t0
+    keep = {f"frame{k}": (fr[k - 1] - sc.mesh.nodes).astype(np.float32) if f32_disp else fr[k - 1]
+            for k in frames_keep}
+    np.savez_compressed(os.path.join(HERE, f"{key.lower()}.npz"), digest=scene_digest(sc),
+                        seconds=el, steps=steps, **keep)
+    print(key, "seconds", el)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "small"
+    if what in ("small", "all"):
+        make_projections()
+        make_c1()
+        make_solvers()
+    if what in ("c2", "all"):
+        make_big("C2", (1, 10, 100), 100, False)
+    if what in ("c3", "all"):
+        make_big("C3", (1,), 1, True)

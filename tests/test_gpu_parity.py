@@ -1,0 +1,261 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the reference's golden
+vectors and the CPU oracle, on the same seeded inputs.  Run with `-m gpu`."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from oracle import pd_oracle as orc
+from paper_2405_12484_b200 import material, pdsolver, scenes
+from paper_2405_12484_b200.material import MaterialField
+from paper_2405_12484_b200.volmesh import VolumeMesh
+from pdtest_helpers import golden, rel_l2, scene_digest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c1():
+    sc = scenes.c1_swatch()
+    assert scene_digest(sc) == str(golden("c1.npz")["digest"])
+    return sc
+
+
+def single_tet(mass=0.1):
+    nodes = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], dtype=float)
+    m = VolumeMesh(nodes, np.array([[0, 1, 2, 3]]))
+    m.node_mass = np.full(4, mass)
+    return m
+
+
+# ---------------------------------------------------------------------------
+# projections (material.py:395-407)
+
+
+@pytest.mark.parametrize("prec,tol_r,tol_v", [("fp64", 1e-11, 1e-10), ("fp32", 2e-4, 2e-4)])
+def test_batch_projections_match_reference(prec, tol_r, tol_v):
+    g = golden("projections.npz")
+    R, V = material.batch_projections(g["F"], precision=prec)
+    assert np.abs(R - g["R"]).max() < tol_r
+    assert np.abs(V - g["V"]).max() < tol_v
+
+
+def test_projection_known_answers():
+    phi = (1.0 + np.sqrt(5.0)) / 2.0
+    F = np.stack([t * np.eye(3) for t in (0.5, 1.5, 1.8)] + [np.diag([100.0, 100.0, 1e-5]),
+                                                            2.0 * np.eye(3), np.zeros((3, 3))])
+    R, V = material.batch_projections(F)
+    for k in range(3):
+        assert np.abs(V[k] - np.eye(3)).max() < 1e-9
+    assert np.abs(np.sort(np.linalg.svd(V[3], compute_uv=False)) - [0.01, 10.0, 10.0]).max() < 1e-6
+    assert np.abs(np.sort(np.linalg.svd(V[4], compute_uv=False)) - [phi ** -2, phi, phi]).max() < 1e-9
+    assert abs(np.linalg.det(V[5]) - 1.0) < 1e-6
+
+
+def test_projection_invariants_random(rng):
+    F = np.eye(3) + 0.8 * rng.normal(size=(4000, 3, 3))
+    R, V = material.batch_projections(F)
+    assert np.abs(np.linalg.det(V) - 1.0).max() < 1e-8
+    assert np.linalg.svd(V, compute_uv=False).min() >= 0.01 - 1e-8
+    assert np.abs(np.einsum("eij,ekj->eik", R, R) - np.eye(3)).max() < 1e-12
+    assert np.abs(np.linalg.det(R) - 1.0).max() < 1e-12
+
+
+def test_projection_rejects_nonfinite():
+    F = np.eye(3)[None].copy()
+    F[0, 0, 0] = np.nan
+    with pytest.raises(ValueError):
+        material.batch_projections(F)
+
+
+# ---------------------------------------------------------------------------
+# assembly and local step
+
+
+def test_assemble_global_matches_reference(c1):
+    g = golden("c1.npz")
+    K = pdsolver.assemble_global(c1.mesh, c1.gammas, c1.dt).tocsr()
+    Kr = sp.csr_matrix((g["K_data"], g["K_indices"], g["K_indptr"]), shape=K.shape)
+    assert abs(K - Kr).max() < 1e-12 * abs(Kr).max()
+    assert abs(K - K.T).max() < 1e-12 * abs(Kr).max()
+
+
+def test_assemble_rejects_bad_input(c1):
+    with pytest.raises(ValueError):
+        pdsolver.assemble_global(c1.mesh, c1.gammas, 0.0)
+    bad = MaterialField(-np.ones(c1.n_tets), np.ones(c1.n_tets))
+    with pytest.raises(ValueError):
+        pdsolver.assemble_global(c1.mesh, bad, 1e-3)
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-10), ("fp32", 5e-5)])
+def test_elastic_rhs_matches_reference(c1, prec, tol):
+    g = golden("c1.npz")
+    rhs, F, R, V = pdsolver.elastic_rhs(c1.mesh, c1.gammas, g["x_pert"], precision=prec)
+    scale = np.abs(g["rhs"]).max()
+    assert np.abs(rhs - g["rhs"]).max() < tol * scale
+    assert np.abs(F - g["F"]).max() < max(tol, 1e-12) * 10
+    assert np.abs(R - g["R"]).max() < tol * 10
+    assert np.abs(V - g["V"]).max() < tol * 10
+
+
+def test_elastic_rhs_is_deterministic(c1):
+    g = golden("c1.npz")
+    a = pdsolver.elastic_rhs(c1.mesh, c1.gammas, g["x_pert"], precision="fp32")[0]
+    b = pdsolver.elastic_rhs(c1.mesh, c1.gammas, g["x_pert"], precision="fp32")[0]
+    assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------------------
+# global solve (GlobalSolver drop-in)
+
+
+def test_global_solver_matches_direct(c1, rng):
+    K = orc.assemble_K(c1.mesh.tets, c1.mesh.shape_grad, c1.mesh.volume, c1.gammas.gamma_s,
+                       c1.gammas.gamma_v, c1.mesh.node_mass, c1.dt, c1.n_nodes)
+    free = np.setdiff1d(np.arange(c1.n_nodes), c1.pins)
+    ref = orc.GlobalSolver(K, free, c1.pins)
+    B = rng.normal(size=(c1.n_nodes, 3))
+    P = rng.normal(size=(len(c1.pins), 3))
+    X_ref = ref.solve(B, P)
+    gs = pdsolver.GlobalSolver(K, free, c1.pins, precision="fp64", tol=1e-13)
+    X = gs.solve(B, P)
+    assert rel_l2(X, X_ref) < 1e-10
+    assert np.array_equal(X[c1.pins], P)
+    # more than three columns are chunked
+    B5 = rng.normal(size=(c1.n_nodes, 5))
+    P5 = rng.normal(size=(len(c1.pins), 5))
+    assert rel_l2(gs.solve(B5, P5), ref.solve(B5, P5)) < 1e-10
+
+
+def test_global_solver_rejects_bad_mode(c1):
+    K = pdsolver.assemble_global(c1.mesh, c1.gammas, c1.dt)
+    with pytest.raises(ValueError):
+        pdsolver.GlobalSolver(K, np.arange(c1.n_nodes), np.empty(0, dtype=int), mode="lu")
+
+
+# ---------------------------------------------------------------------------
+# stepping (pdsolver.py:257-304, 710-763)
+
+
+@pytest.mark.parametrize("prec,tol_pos,tol_disp", [("fp64", 1e-10, 1e-8), ("fp32", 1e-5, 5e-3)])
+def test_c1_frames_match_reference(c1, prec, tol_pos, tol_disp):
+    g = golden("c1.npz")
+    fr = pdsolver.simulate_mesh(c1.mesh, c1.gammas, 3, c1.dt, forces=c1.forces, pins=c1.pins,
+                                pin_targets=c1.pin_targets, iterations=30, precision=prec)
+    x0 = c1.mesh.nodes
+    for k in range(3):
+        assert rel_l2(fr[k], g["frames"][k]) < tol_pos, k
+        assert rel_l2(fr[k] - x0, g["frames"][k] - x0) < tol_disp, k
+
+
+def test_rest_is_fixed_point():
+    sc = scenes.box_scene(6, 5, 3)
+    st = pdsolver.SimState(x=sc.mesh.nodes, v=np.zeros_like(sc.mesh.nodes), dt=1e-3)
+    pdsolver.pd_step(st, sc.mesh, sc.gammas, iterations=5, precision="fp64")
+    assert np.abs(st.x - sc.mesh.nodes).max() < 1e-12
+
+
+def test_free_fall_discrete_closed_form():
+    sc = scenes.box_scene(6, 5, 3)
+    mesh = sc.mesh
+    mesh.node_mass = np.full(mesh.n_nodes, 1e-3)
+    gam = MaterialField.uniform(mesh.n_elements, 5.0, 3.0)
+    dt, steps = 1e-3, 8
+    gvec = np.array([0.0, -9.8, 0.0])
+    frames = pdsolver.simulate_mesh(mesh, gam, steps, dt, forces=mesh.node_mass[:, None] * gvec,
+                                    iterations=3, precision="fp64")
+    for n in range(1, steps + 1):
+        expect = mesh.nodes + gvec * dt ** 2 * n * (n + 1) / 2.0
+        assert np.abs(frames[n - 1] - expect).max() < 1e-12
+
+
+def test_pinned_nodes_track_targets(c1):
+    pins = np.array([0, 1, 2])
+    tgt = c1.mesh.nodes[pins] + np.array([0.0, 0.01, 0.0])
+    for prec in ("fp64", "fp32"):
+        st = pdsolver.SimState(x=c1.mesh.nodes, v=np.zeros_like(c1.mesh.nodes), dt=1e-3, pins=pins,
+                               pin_targets=tgt)
+        pdsolver.pd_step(st, c1.mesh, c1.gammas, iterations=4, precision=prec)
+        assert np.abs(st.x[pins] - tgt).max() < (1e-14 if prec == "fp64" else 1e-7)
+
+
+def test_non_finite_abort_reports_iteration(c1):
+    class BadSolver:
+        def solve(self, b, pin_vals):
+            return np.full_like(b, np.nan)
+
+    st = pdsolver.SimState(x=c1.mesh.nodes, v=np.zeros_like(c1.mesh.nodes), dt=1e-3)
+    with pytest.raises(RuntimeError, match="iteration 0"):
+        pdsolver.pd_step(st, c1.mesh, c1.gammas, solver=BadSolver())
+
+
+def test_device_step_non_finite_abort_keeps_state(c1):
+    f = c1.forces.copy()
+    f[5, 1] = np.nan
+    st = pdsolver.SimState(x=c1.mesh.nodes, v=np.zeros_like(c1.mesh.nodes), dt=c1.dt, pins=c1.pins)
+    with pytest.raises(RuntimeError, match="iteration 0"):
+        pdsolver.pd_step(st, c1.mesh, c1.gammas, iterations=3, forces=f)
+    assert np.array_equal(st.x, c1.mesh.nodes)
+    # the context is still usable afterwards
+    pdsolver.pd_step(st, c1.mesh, c1.gammas, iterations=3, forces=c1.forces)
+    assert np.all(np.isfinite(st.x))
+
+
+def test_objective_monotone_with_device_solver(c1):
+    mesh, gam, dt = c1.mesh, c1.gammas, 1e-3
+    pins = c1.pins
+    tgt = mesh.nodes[pins]
+    st = pdsolver.SimState(x=1.002 * mesh.nodes, v=np.zeros_like(mesh.nodes), dt=dt, pins=pins,
+                           pin_targets=tgt)
+    xhat = pdsolver._predicted(st, None, mesh)
+    free = np.setdiff1d(np.arange(mesh.n_nodes), pins)
+    solver = pdsolver.GlobalSolver(pdsolver.assemble_global(mesh, gam, dt), free, pins, tol=1e-13)
+    x = xhat.copy()
+    x[pins] = tgt
+    objs = [pdsolver.pd_objective(x, mesh, gam, xhat, dt)]
+    for _ in range(10):
+        rhs, *_ = pdsolver.elastic_rhs(mesh, gam, x)
+        b = (mesh.node_mass[:, None] / dt ** 2) * xhat + rhs
+        x = solver.solve(b, tgt)
+        objs.append(pdsolver.pd_objective(x, mesh, gam, xhat, dt))
+    objs = np.array(objs)
+    assert np.all(np.diff(objs) <= 1e-10 * np.abs(objs[:-1]) + 1e-18)
+
+
+def test_bit_identical_reruns(c1):
+    kw = dict(forces=c1.forces, pins=c1.pins, pin_targets=c1.pin_targets, iterations=30)
+    a = pdsolver.simulate_mesh(c1.mesh, c1.gammas, 2, c1.dt, **kw)
+    pdsolver.invalidate_cache()
+    b = pdsolver.simulate_mesh(c1.mesh, c1.gammas, 2, c1.dt, **kw)
+    assert np.array_equal(a, b)
+
+
+def test_pin_path_and_per_step_forces(c1):
+    steps = 3
+    path = np.stack([c1.pin_targets + np.array([0.0, 0.0, 1e-3 * k]) for k in range(steps)])
+    fseq = np.stack([c1.forces * (1.0 + 0.1 * k) for k in range(steps)])
+    fr = pdsolver.simulate_mesh(c1.mesh, c1.gammas, steps, c1.dt, forces=fseq, pins=c1.pins,
+                                pin_targets=path, iterations=20, precision="fp64")
+    m = c1.mesh
+    ref = orc.simulate(m.nodes, m.tets, m.shape_grad, m.volume, c1.gammas.gamma_s, c1.gammas.gamma_v,
+                       m.node_mass, steps, c1.dt, forces=fseq, pins=c1.pins, pin_targets=path,
+                       iterations=20)
+    assert rel_l2(fr, ref) < 1e-10
+    assert np.abs(fr[:, c1.pins] - path).max() < 1e-14
+
+
+# ---------------------------------------------------------------------------
+# full-size parity (BASELINE configs)
+
+
+def test_c3_frame_matches_reference_fp32():
+    g = golden("c3.npz")
+    sc = scenes.c3_sweater()
+    assert scene_digest(sc) == str(g["digest"])
+    fr = pdsolver.simulate_mesh(sc.mesh, sc.gammas, 1, sc.dt, forces=sc.forces, pins=sc.pins,
+                                pin_targets=sc.pin_targets, iterations=30, precision="fp32")
+    ref = sc.mesh.nodes + g["frame1"].astype(np.float64)
+    assert rel_l2(fr[0], ref) < 1e-5
+    assert rel_l2(fr[0] - sc.mesh.nodes, g["frame1"]) < 1e-2
