@@ -36,33 +36,40 @@ VK_HD void pairprod(const double (&s)[3], double (&p)[3]) {
     p[2] = s[0] * s[1];
 }
 
-// Gaussian elimination with partial pivoting on an n x n system (n <= 4);
-// false when a pivot is exactly zero (LAPACK gesv info > 0).
-VK_HD bool gesv(double (&A)[4][4], double (&b)[4], int n) {
-    for (int k = 0; k < n; ++k) {
-        int piv = k;
-        double best = fabs(A[k][k]);
-        for (int i = k + 1; i < n; ++i) {
-            const double v = fabs(A[i][k]);
-            if (v > best) { best = v; piv = i; }
-        }
-        if (piv != k) {
-            for (int j = 0; j < 4; ++j) { const double t = A[k][j]; A[k][j] = A[piv][j]; A[piv][j] = t; }
-            const double t = b[k]; b[k] = b[piv]; b[piv] = t;
+// Fixed-size 4x4 solve with partial pivoting, fully unrolled so the matrix
+// stays in registers (row exchanges are conditional moves, pivot = first
+// largest magnitude as in LAPACK idamax).  false on an exactly zero pivot.
+VK_HD bool gesv4(double (&A)[4][4], double (&b)[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int i = k + 1; i < 4; ++i) {
+            const bool sw = fabs(A[i][k]) > fabs(A[k][k]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double a = A[k][j], c = A[i][j];
+                A[k][j] = sw ? c : a;
+                A[i][j] = sw ? a : c;
+            }
+            const double a = b[k], c = b[i];
+            b[k] = sw ? c : a;
+            b[i] = sw ? a : c;
         }
         if (A[k][k] == 0.0) return false;
         const double inv = 1.0 / A[k][k];
-        for (int i = k + 1; i < n; ++i) {
+#pragma unroll
+        for (int i = k + 1; i < 4; ++i) {
             const double f = A[i][k] * inv;
-            if (f != 0.0) {
-                for (int j = k + 1; j < n; ++j) A[i][j] -= f * A[k][j];
-                b[i] -= f * b[k];
-            }
+#pragma unroll
+            for (int j = k + 1; j < 4; ++j) A[i][j] -= f * A[k][j];
+            b[i] -= f * b[k];
         }
     }
-    for (int k = n - 1; k >= 0; --k) {
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
         double v = b[k];
-        for (int j = k + 1; j < n; ++j) v -= A[k][j] * b[j];
+#pragma unroll
+        for (int j = k + 1; j < 4; ++j) v -= A[k][j] * b[j];
         b[k] = v / A[k][k];
     }
     return true;
@@ -88,7 +95,7 @@ VK_HD bool kkt_newton(const double (&sig)[3], double (&s)[3], double& lam) {
                           {lam * s[1], lam * s[0], 1.0, p[2]},
                           {p[0], p[1], p[2], 0.0}};
         double d[4] = {-r[0], -r[1], -r[2], -r[3]};
-        if (!gesv(J, d, 4)) return false;
+        if (!gesv4(J, d)) return false;
         s[0] += d[0]; s[1] += d[1]; s[2] += d[2];
         lam += d[3];
     }
@@ -127,36 +134,38 @@ VK_HD double free_resnorm(const double (&sig)[3], const double (&s)[3], double l
     return rn;
 }
 
-// `_sl3_newton_free` (material.py:171-214)
+// `_sl3_newton_free` (material.py:171-214).  The reduced (nf+1) system is
+// solved embedded in the 4x4 one: frozen entries get an identity row/column
+// and a zero right-hand side, so their update is exactly zero.
 VK_HDNI bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, const bool (&fr)[3]) {
-    int idx[3], nf = 0;
-    for (int i = 0; i < 3; ++i) if (fr[i]) idx[nf++] = i;
+    const int nf = (int)fr[0] + (int)fr[1] + (int)fr[2];
     if (nf == 0) return false;
     for (int it = 0; it < kIters; ++it) {
         const double rn = free_resnorm(sig, s, lam, fr);
         if (rn < kTol) return true;
         double p[3];
         pairprod(s, p);
-        double J[4][4] = {{0.0}};
-        double d[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int a = 0; a < nf; ++a) {
-            const int i = idx[a];
-            for (int b = 0; b < nf; ++b) {
-                const int j = idx[b];
-                J[a][b] = (i == j) ? 1.0 : lam * s[3 - i - j];
+        double J[4][4], d[4];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double v = (i == j) ? 1.0 : lam * s[3 - i - j];
+                J[i][j] = (fr[i] && fr[j]) ? v : (i == j ? 1.0 : 0.0);
             }
-            J[a][nf] = p[i];
-            J[nf][a] = p[i];
-            d[a] = -(s[i] - sig[i] + lam * p[i]);
+            J[i][3] = fr[i] ? p[i] : 0.0;
+            J[3][i] = fr[i] ? p[i] : 0.0;
+            d[i] = fr[i] ? -(s[i] - sig[i] + lam * p[i]) : 0.0;
         }
-        d[nf] = -(s[0] * s[1] * s[2] - 1.0);
-        if (!gesv(J, d, nf + 1)) return false;
+        J[3][3] = 0.0;
+        d[3] = -(s[0] * s[1] * s[2] - 1.0);
+        if (!gesv4(J, d)) return false;
         double step = 1.0;
-        double sn[3], ln = lam;
+        double sn[3] = {s[0], s[1], s[2]}, ln = lam;
         for (int t = 0; t < 6; ++t) {
-            sn[0] = s[0]; sn[1] = s[1]; sn[2] = s[2];
-            for (int a = 0; a < nf; ++a) sn[idx[a]] = s[idx[a]] + step * d[a];
-            ln = lam + step * d[nf];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) sn[i] = fr[i] ? s[i] + step * d[i] : s[i];
+            ln = lam + step * d[3];
             const double rn_new = free_resnorm(sig, sn, ln, fr);
             if (rn_new < rn || rn_new < kTol) break;
             step *= 0.5;

@@ -264,8 +264,10 @@ __global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
         const double bb = ((volatile double*)scal)[S_BB];
         if (!(rr > a.tol * a.tol * bb) || it >= a.max_iters) break;   // also stops on NaN
         double beta[3];
-        for (int c = 0; c < 3; ++c)
-            beta[c] = (it == 0) ? 0.0 : ((volatile double*)scal)[S_RZ + c] / ((volatile double*)scal)[S_RZP + c];
+        for (int c = 0; c < 3; ++c) {
+            const double rzp = ((volatile double*)scal)[S_RZP + c];
+            beta[c] = (it == 0 || rzp == 0.0) ? 0.0 : ((volatile double*)scal)[S_RZ + c] / rzp;
+        }
         const T bx = (T)beta[0], by = (T)beta[1], bz = (T)beta[2];
         const vec4_t<T>* pold = (it & 1) ? a.p1 : a.p0;
         vec4_t<T>* pnew = (it & 1) ? a.p0 : a.p1;

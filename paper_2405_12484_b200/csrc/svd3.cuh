@@ -53,7 +53,9 @@ VK_HD void givens_rows(T (&B)[3][3], T (&Qt)[3][3], int i, int j) {
     const T a = B[i][i], b = B[j][i];
     const T rr = a * a + b * b;
     T c = T(1), s = T(0);
-    if (rr > T(0)) {
+    if (b == T(0)) {
+        c = a < T(0) ? T(-1) : T(1);      // exact: keeps already-triangular (e.g. diagonal) F exact
+    } else if (rr > T(0)) {
         const T inv = rsqrt_(rr);
         c = a * inv;
         s = b * inv;

@@ -193,7 +193,8 @@ def test_non_finite_abort_reports_iteration(c1):
 
 def test_device_step_non_finite_abort_keeps_state(c1):
     f = c1.forces.copy()
-    f[5, 1] = np.nan
+    node = int(np.setdiff1d(np.arange(c1.n_nodes), c1.pins)[-1])     # a free node
+    f[node, 1] = np.nan
     st = pdsolver.SimState(x=c1.mesh.nodes, v=np.zeros_like(c1.mesh.nodes), dt=c1.dt, pins=c1.pins)
     with pytest.raises(RuntimeError, match="iteration 0"):
         pdsolver.pd_step(st, c1.mesh, c1.gammas, iterations=3, forces=f)
