@@ -5,8 +5,9 @@
 // projection of the singular values (material.py:343-392, float64), then
 //   P = gs R + gv V = U diag(gs + gv s) W^T                    (pdsolver.py:67)
 // and the per-corner contributions 2 V P g_n                  (pdsolver.py:68)
-// written to a corner-major buffer `corner[a * nE + e]`; a deterministic
-// node-centric gather (no float atomics) sums them later in tet order.
+// written into each node's incidence run (`corner[slot4[e].a]`); a
+// deterministic node-centric gather (no float atomics) sums the run later, in
+// tet order, like `np.add.at` (pdsolver.py:69-70).
 //
 // MODE_RESID writes 2V (P - (gs+gv) F) g_n instead: summed over a node and
 // added to (m/dt^2)(xhat - x) it is exactly b - K x, the global-step residual
@@ -66,7 +67,8 @@ struct LocalArgs {
     const T* G;                  // 9 planes of nE: rows 1..3 of the shape gradient (= Dm^-1 rows)
     const T* w;                  // 2 planes of nE: 2 V gs, 2 V gv
     const vec4_t<T>* x;          // positions, internal order
-    vec4_t<T>* corner;           // 4 planes of nE
+    const int4* slot4;           // position of (e, corner a) in its node's incidence run
+    vec4_t<T>* corner;           // per-incidence contributions, node-sorted (tet order within a node)
     ProjStats* stats;
     double* F_out;               // optional (nE,3,3) (RHS mode only)
     double* R_out;
@@ -132,11 +134,14 @@ __global__ void __launch_bounds__(128) k_local(LocalArgs<T> a) {
     for (int n = 0; n < 3; ++n)
 #pragma unroll
         for (int i = 0; i < 3; ++i) f[n][i] = P[i][0] * g[n][0] + P[i][1] * g[n][1] + P[i][2] * g[n][2];
-    st4(&a.corner[e], make4<T>(-(f[0][0] + f[1][0] + f[2][0]), -(f[0][1] + f[1][1] + f[2][1]),
-                               -(f[0][2] + f[1][2] + f[2][2]), T(0)));
-#pragma unroll
-    for (int n = 0; n < 3; ++n)
-        st4(&a.corner[(size_t)(n + 1) * nE + e], make4<T>(f[n][0], f[n][1], f[n][2], T(0)));
+    // scatter into each node's incidence run (slot precomputed): writes are
+    // fire-and-forget, and the later per-node gather reads a contiguous run
+    const int4 sl = __ldg(&a.slot4[e]);
+    st4(&a.corner[sl.x], make4<T>(-(f[0][0] + f[1][0] + f[2][0]), -(f[0][1] + f[1][1] + f[2][1]),
+                                  -(f[0][2] + f[1][2] + f[2][2]), T(0)));
+    st4(&a.corner[sl.y], make4<T>(f[0][0], f[0][1], f[0][2], T(0)));
+    st4(&a.corner[sl.z], make4<T>(f[1][0], f[1][1], f[1][2], T(0)));
+    st4(&a.corner[sl.w], make4<T>(f[2][0], f[2][1], f[2][2], T(0)));
 }
 
 // Stateless projections of a batch of F (material.py:395-407): (R, V).

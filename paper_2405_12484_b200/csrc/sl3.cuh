@@ -90,14 +90,35 @@ VK_HD bool kkt_newton(const double (&sig)[3], double (&s)[3], double& lam) {
         double rn = 0.0;
         for (int i = 0; i < 4; ++i) rn = nanmax(rn, fabs(r[i]));
         if (rn < kTol) break;
-        double J[4][4] = {{1.0, lam * s[2], lam * s[1], p[0]},
-                          {lam * s[2], 1.0, lam * s[0], p[1]},
-                          {lam * s[1], lam * s[0], 1.0, p[2]},
-                          {p[0], p[1], p[2], 0.0}};
-        double d[4] = {-r[0], -r[1], -r[2], -r[3]};
-        if (!gesv4(J, d)) return false;
-        s[0] += d[0]; s[1] += d[1]; s[2] += d[2];
-        lam += d[3];
+        // Bordered solve of [[A, p], [p^T, 0]] [ds; dl] = -[r; r4] with
+        // A = I + lam * offdiag(s2, s1, s0) through the adjugate of A; the
+        // pivoted 4x4 elimination takes over when A is near singular.
+        const double a = lam * s[2], b = lam * s[1], c = lam * s[0];
+        const double c00 = 1.0 - c * c, c11 = 1.0 - b * b, c22 = 1.0 - a * a;
+        const double c01 = b * c - a, c02 = a * c - b, c12 = a * b - c;
+        const double det = c00 + a * c01 + b * c02;
+        const double ar0 = c00 * r[0] + c01 * r[1] + c02 * r[2];
+        const double ar1 = c01 * r[0] + c11 * r[1] + c12 * r[2];
+        const double ar2 = c02 * r[0] + c12 * r[1] + c22 * r[2];
+        const double ap0 = c00 * p[0] + c01 * p[1] + c02 * p[2];
+        const double ap1 = c01 * p[0] + c11 * p[1] + c12 * p[2];
+        const double ap2 = c02 * p[0] + c12 * p[1] + c22 * p[2];
+        const double pap = p[0] * ap0 + p[1] * ap1 + p[2] * ap2;
+        const double par = p[0] * ar0 + p[1] * ar1 + p[2] * ar2;
+        if (fabs(det) > 1e-6 && fabs(pap) > 1e-12 * fabs(det) * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2])) {
+            const double dl = (r[3] * det - par) / pap;
+            const double idet = 1.0 / det;
+            s[0] -= (ar0 + ap0 * dl) * idet;
+            s[1] -= (ar1 + ap1 * dl) * idet;
+            s[2] -= (ar2 + ap2 * dl) * idet;
+            lam += dl;
+        } else {
+            double J[4][4] = {{1.0, a, b, p[0]}, {a, 1.0, c, p[1]}, {b, c, 1.0, p[2]}, {p[0], p[1], p[2], 0.0}};
+            double d[4] = {-r[0], -r[1], -r[2], -r[3]};
+            if (!gesv4(J, d)) return false;
+            s[0] += d[0]; s[1] += d[1]; s[2] += d[2];
+            lam += d[3];
+        }
     }
     pairprod(s, p);
     double r3 = 0.0;

@@ -8,7 +8,11 @@
 // are eliminated exactly as GlobalSolver does (pdsolver.py:210-229).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "vk_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace vk {
 
@@ -23,7 +27,8 @@ struct AssembleArgs {
     const double* G;             // (nE,4,3) float64 shape gradients (host layout)
     const double* wsum;          // (nE) 2 V (gs + gv)
     const double* m_dt2;         // (n) m / dt^2, internal order
-    const int* ell_col;          // [s * nF + i]
+    const int* ell_col;          // [s * nF + i], padded with the row's own index
+    const int* ell_len;          // real entries per row
     T* ell_val;
     T* inv_diag;                 // (nF)
     double* diag64;              // (nF) float64 diagonal (A-Jacobi / reference-compat paths)
@@ -40,10 +45,11 @@ __global__ void k_assemble(AssembleArgs<T> a) {
     if (i >= a.nF) return;
     const int b0 = a.inc_ptr[i], b1 = a.inc_ptr[i + 1];
     double diag = a.m_dt2[i];
+    const int len = a.ell_len[i];
     for (int s = 0; s < a.ell_w; ++s) {
         const int col = a.ell_col[(size_t)s * a.nF + i];
         double v = 0.0;
-        if (col >= 0) {
+        if (s < len) {
             for (int k = b0; k < b1; ++k) {
                 const int code = a.inc_code[k];
                 const int e = code % a.nE, an = code / a.nE;
@@ -127,13 +133,13 @@ __global__ void k_restore(int n, vec4_t<T>* x, vec4_t<T>* v, const vec4_t<T>* x_
 // rhs_i = sum over incidences of corner contributions (tet order) -- the
 // `np.add.at` of pdsolver.py:69-70, without atomics.  All n nodes.
 template <typename T>
-__global__ void k_gather(int n, const int* __restrict__ inc_ptr, const int* __restrict__ inc_code,
-                         const vec4_t<T>* __restrict__ corner, vec4_t<T>* out) {
+__global__ void k_gather(int n, const int* __restrict__ inc_ptr, const vec4_t<T>* __restrict__ corner,
+                         vec4_t<T>* out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     T sx = 0, sy = 0, sz = 0;
     for (int k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
-        const vec4_t<T> c = ldg4(&corner[inc_code[k]]);
+        const vec4_t<T> c = ldg4(&corner[k]);
         sx += c.x; sy += c.y; sz += c.z;
     }
     out[i] = make4<T>(sx, sy, sz, T(0));
@@ -152,6 +158,7 @@ __global__ void k_gather(int n, const int* __restrict__ inc_ptr, const int* __re
 // Stops when sum_c |r_c|^2 <= tol^2 * scale^2 (scale^2 = |M/dt^2 xhat|^2 for
 // INIT_PD, |r0|^2 for INIT_RHS) or after max_iters.
 enum PcgInit { INIT_PD = 0, INIT_RHS = 1 };
+constexpr int kEllUnroll = 16;     // voxel meshes: <= 15 entries per row
 
 template <typename T>
 struct PcgArgs {
@@ -183,108 +190,121 @@ struct PcgArgs {
     int init;
 };
 
-// scal layout
-enum { S_RZ = 0, S_RZP = 3, S_PQ = 6, S_RR = 9, S_BB = 10 };
 
+// Every CTA sums the per-CTA partials of the last phase in the same fixed
+// order after the grid barrier, so all CTAs hold bit-identical scalars (no
+// serial "last CTA" step, deterministic across runs).
 template <int NV>
-__device__ __forceinline__ void reduce_partials(const double* partials, double* out, double* smem) {
-    // deterministic: fixed strided assignment + fixed-order block sum
-    double v[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
-#pragma unroll
-        for (int k = 0; k < NV; ++k) v[k] += partials[b * 8 + k];
-    block_sum<NV>(v, smem);
+__device__ __forceinline__ void pcg_allreduce(cg::grid_group& grid, double* partials, int& parity, double (&acc)[NV],
+                                              double* red, double* smem) {
+    block_sum<NV>(acc, smem);
+    double* P = partials + (size_t)parity * gridDim.x * 8;
     if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k < NV; ++k) out[k] = v[k];
+        for (int k = 0; k < NV; ++k) P[blockIdx.x * 8 + k] = acc[k];
+    grid.sync();
+    reduce_partials_all<NV>(P, red, smem);
+    parity ^= 1;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
+__global__ void __launch_bounds__(256) k_pcg(PcgArgs<T> a) {
+    cg::grid_group grid = cg::this_grid();
     __shared__ double smem[32 * 8];
-    __shared__ double s_out[8];
+    __shared__ double red[8];
     const int nF = a.nF;
     const int chunk = (nF + gridDim.x - 1) / gridDim.x;
     const int row0 = blockIdx.x * chunk;
     const int row1 = min(nF, row0 + chunk);
-    double* scal = a.scal;
+    int parity = 0;
+    double rz[3], rzp[3] = {1.0, 1.0, 1.0}, rr, bb;
 
     // ---- init: residual, z = D^-1 r, p0 = 0, dx = 0
     {
         double acc[5] = {0, 0, 0, 0, 0};     // rz x3, rr, bb
         for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
-            T rx, ry, rz;
+            T rx, ry, rzv;
             if (a.init == INIT_PD) {
-                rx = 0; ry = 0; rz = 0;
-                for (int k = a.inc_ptr[i]; k < a.inc_ptr[i + 1]; ++k) {
-                    const vec4_t<T> c = ld4(&a.corner[a.inc_code[k]]);
-                    rx += c.x; ry += c.y; rz += c.z;
+                rx = 0; ry = 0; rzv = 0;
+                const int k0 = a.inc_ptr[i], k1 = a.inc_ptr[i + 1];
+#pragma unroll 4
+                for (int k = k0; k < k1; ++k) {
+                    const vec4_t<T> c = ldg4(&a.corner[k]);
+                    rx += c.x; ry += c.y; rzv += c.z;
                 }
                 const T m = a.m_dt2[i];
                 const vec4_t<T> xh = a.xhat[i], xi = a.x[i];
                 rx += m * (xh.x - xi.x);
                 ry += m * (xh.y - xi.y);
-                rz += m * (xh.z - xi.z);
+                rzv += m * (xh.z - xi.z);
                 const double bx = (double)m * xh.x, by = (double)m * xh.y, bz = (double)m * xh.z;
                 acc[4] += bx * bx + by * by + bz * bz;
             } else {
                 const vec4_t<T> b = a.rhs[i];
-                rx = b.x; ry = b.y; rz = b.z;
-                acc[4] += (double)rx * rx + (double)ry * ry + (double)rz * rz;
+                rx = b.x; ry = b.y; rzv = b.z;
+                acc[4] += (double)rx * rx + (double)ry * ry + (double)rzv * rzv;
             }
             const T d = a.inv_diag[i];
-            const vec4_t<T> zi = make4<T>(d * rx, d * ry, d * rz, T(0));
-            a.r[i] = make4<T>(rx, ry, rz, T(0));
+            const vec4_t<T> zi = make4<T>(d * rx, d * ry, d * rzv, T(0));
+            a.r[i] = make4<T>(rx, ry, rzv, T(0));
             a.z[i] = zi;
             a.p0[i] = make4<T>(T(0), T(0), T(0), T(0));
             a.dx[i] = make4<T>(T(0), T(0), T(0), T(0));
             acc[0] += (double)rx * zi.x;
             acc[1] += (double)ry * zi.y;
-            acc[2] += (double)rz * zi.z;
-            acc[3] += (double)rx * rx + (double)ry * ry + (double)rz * rz;
+            acc[2] += (double)rzv * zi.z;
+            acc[3] += (double)rx * rx + (double)ry * ry + (double)rzv * rzv;
         }
-        block_sum<5>(acc, smem);
-        if (threadIdx.x == 0)
-            for (int k = 0; k < 5; ++k) a.partials[blockIdx.x * 8 + k] = acc[k];
-        grid_sync(a.bar, [&]() {
-            reduce_partials<5>(a.partials, s_out, smem);
-            if (threadIdx.x == 0) {
-                for (int c = 0; c < 3; ++c) { scal[S_RZ + c] = s_out[c]; scal[S_RZP + c] = 1.0; }
-                scal[S_RR] = s_out[3];
-                scal[S_BB] = s_out[4];
-            }
-        });
+        pcg_allreduce<5>(grid, a.partials, parity, acc, red, smem);
+        for (int c = 0; c < 3; ++c) rz[c] = red[c];
+        rr = red[3];
+        bb = red[4];
     }
 
     int it = 0;
     for (;; ++it) {
-        const double rr = ((volatile double*)scal)[S_RR];
-        const double bb = ((volatile double*)scal)[S_BB];
         if (!(rr > a.tol * a.tol * bb) || it >= a.max_iters) break;   // also stops on NaN
         double beta[3];
-        for (int c = 0; c < 3; ++c) {
-            const double rzp = ((volatile double*)scal)[S_RZP + c];
-            beta[c] = (it == 0 || rzp == 0.0) ? 0.0 : ((volatile double*)scal)[S_RZ + c] / rzp;
-        }
+        for (int c = 0; c < 3; ++c) beta[c] = (it == 0 || rzp[c] == 0.0) ? 0.0 : rz[c] / rzp[c];
         const T bx = (T)beta[0], by = (T)beta[1], bz = (T)beta[2];
         const vec4_t<T>* pold = (it & 1) ? a.p1 : a.p0;
         vec4_t<T>* pnew = (it & 1) ? a.p0 : a.p1;
+        double pq[3];
         // ---- phase A: p_new = z + beta p_old; q = K_ff p_new
         {
             double acc[3] = {0, 0, 0};
             for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
                 T qx = 0, qy = 0, qz = 0;
-                for (int s = 0; s < a.ell_w; ++s) {
-                    const int col = __ldg(&a.ell_col[(size_t)s * nF + i]);
-                    if (col < 0) break;
-                    const T kv = __ldg(&a.ell_val[(size_t)s * nF + i]);
-                    const vec4_t<T> zc = ld4(&a.z[col]);
-                    const vec4_t<T> pc = ld4(&pold[col]);
-                    qx += kv * (zc.x + bx * pc.x);
-                    qy += kv * (zc.y + by * pc.y);
-                    qz += kv * (zc.z + bz * pc.z);
+                // padded ELL (pad = own column, value 0): fixed trip count, all
+                // column/value loads issued before the gathers
+                if (a.ell_w <= kEllUnroll) {
+                    int cols[kEllUnroll];
+                    T vals[kEllUnroll];
+#pragma unroll
+                    for (int s = 0; s < kEllUnroll; ++s) {
+                        cols[s] = s < a.ell_w ? __ldg(&a.ell_col[(size_t)s * nF + i]) : i;
+                        vals[s] = s < a.ell_w ? __ldg(&a.ell_val[(size_t)s * nF + i]) : T(0);
+                    }
+#pragma unroll
+                    for (int s = 0; s < kEllUnroll; ++s) {
+                        if (s < a.ell_w) {
+                            const vec4_t<T> zc = ld4(&a.z[cols[s]]);
+                            const vec4_t<T> pc = ld4(&pold[cols[s]]);
+                            qx += vals[s] * (zc.x + bx * pc.x);
+                            qy += vals[s] * (zc.y + by * pc.y);
+                            qz += vals[s] * (zc.z + bz * pc.z);
+                        }
+                    }
+                } else {
+                    for (int s = 0; s < a.ell_w; ++s) {
+                        const int col = __ldg(&a.ell_col[(size_t)s * nF + i]);
+                        const T kv = __ldg(&a.ell_val[(size_t)s * nF + i]);
+                        const vec4_t<T> zc = ld4(&a.z[col]);
+                        const vec4_t<T> pc = ld4(&pold[col]);
+                        qx += kv * (zc.x + bx * pc.x);
+                        qy += kv * (zc.y + by * pc.y);
+                        qz += kv * (zc.z + bz * pc.z);
+                    }
                 }
                 const vec4_t<T> zi = ld4(&a.z[i]);
                 const vec4_t<T> pi = ld4(&pold[i]);
@@ -295,22 +315,13 @@ __global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
                 acc[1] += (double)pn.y * qy;
                 acc[2] += (double)pn.z * qz;
             }
-            block_sum<3>(acc, smem);
-            if (threadIdx.x == 0)
-                for (int k = 0; k < 3; ++k) a.partials[blockIdx.x * 8 + k] = acc[k];
-            grid_sync(a.bar, [&]() {
-                reduce_partials<3>(a.partials, s_out, smem);
-                if (threadIdx.x == 0)
-                    for (int c = 0; c < 3; ++c) scal[S_PQ + c] = s_out[c];
-            });
+            pcg_allreduce<3>(grid, a.partials, parity, acc, red, smem);
+            for (int c = 0; c < 3; ++c) pq[c] = red[c];
         }
         // ---- phase B: dx += alpha p; r -= alpha q; z = D^-1 r
         {
             double alpha[3];
-            for (int c = 0; c < 3; ++c) {
-                const double pq = ((volatile double*)scal)[S_PQ + c];
-                alpha[c] = pq != 0.0 ? ((volatile double*)scal)[S_RZ + c] / pq : 0.0;
-            }
+            for (int c = 0; c < 3; ++c) alpha[c] = pq[c] != 0.0 ? rz[c] / pq[c] : 0.0;
             const T ax = (T)alpha[0], ay = (T)alpha[1], az = (T)alpha[2];
             double acc[4] = {0, 0, 0, 0};
             for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
@@ -330,40 +341,25 @@ __global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
                 acc[2] += (double)ri.z * zi.z;
                 acc[3] += (double)ri.x * ri.x + (double)ri.y * ri.y + (double)ri.z * ri.z;
             }
-            block_sum<4>(acc, smem);
-            if (threadIdx.x == 0)
-                for (int k = 0; k < 4; ++k) a.partials[blockIdx.x * 8 + k] = acc[k];
-            grid_sync(a.bar, [&]() {
-                reduce_partials<4>(a.partials, s_out, smem);
-                if (threadIdx.x == 0) {
-                    for (int c = 0; c < 3; ++c) {
-                        scal[S_RZP + c] = scal[S_RZ + c];
-                        scal[S_RZ + c] = s_out[c];
-                    }
-                    scal[S_RR] = s_out[3];
-                }
-            });
+            pcg_allreduce<4>(grid, a.partials, parity, acc, red, smem);
+            for (int c = 0; c < 3; ++c) { rzp[c] = rz[c]; rz[c] = red[c]; }
+            rr = red[3];
         }
     }
     // ---- finish: x += dx (PD mode), finite check
-    if (a.init == INIT_PD) {
-        bool bad = false;
-        for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
-            const vec4_t<T> d = ld4(&a.dx[i]);
+    bool bad = false;
+    for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+        const vec4_t<T> d = ld4(&a.dx[i]);
+        if (a.init == INIT_PD) {
             vec4_t<T> xi = a.x[i];
             xi.x += d.x; xi.y += d.y; xi.z += d.z;
             a.x[i] = xi;
             bad |= !(isfinite(xi.x) && isfinite(xi.y) && isfinite(xi.z));
-        }
-        if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, a.pd_iter);
-    } else {
-        bool bad = false;
-        for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
-            const vec4_t<T> d = ld4(&a.dx[i]);
+        } else {
             bad |= !(isfinite(d.x) && isfinite(d.y) && isfinite(d.z));
         }
-        if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, a.pd_iter);
     }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, a.pd_iter);
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.iters_out = it;
 }
 

@@ -116,6 +116,42 @@ __device__ __forceinline__ void grid_sync(GridBar* bar, OnLast on_last) {
 
 struct NoOp { __device__ void operator()() const {} };
 
+// Lean grid barrier: one release-add per CTA, tight acquire-poll on the
+// generation word (no sleep), no serial reduction step.  Callers that need
+// grid-wide sums write per-CTA partials before the barrier and every CTA
+// reduces them afterwards in the same fixed order (identical results).
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned int atom_add_acqrel_gpu(unsigned int* p, unsigned int v) {
+    unsigned int old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void grid_sync_lean(GridBar* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int g = ld_acquire_gpu(&bar->gen);
+        const unsigned int arrived = atom_add_acqrel_gpu(&bar->count, 1u);
+        if (arrived == gridDim.x - 1) {
+            bar->count = 0;                      // ordered before the release below
+            st_release_gpu(&bar->gen, g + 1u);
+        } else {
+            unsigned long long spins = 0;
+            while (ld_acquire_gpu(&bar->gen) == g) {
+                if (++spins > (1ull << 33)) __trap();
+            }
+        }
+    }
+    __syncthreads();
+}
+
 // Block-wide sum of NV doubles per thread; result valid in thread 0.
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* >= 32*NV */) {
@@ -137,6 +173,84 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* >= 32
             v[k] = a;
         }
     }
+    __syncthreads();
+}
+
+// After grid_sync_lean: sum NV per-CTA partials (stride 8 doubles) in fixed
+// order; every CTA gets the same bits.  Result broadcast through `out` (smem).
+template <int NV>
+__device__ __forceinline__ void reduce_partials_all(const double* partials, double* out, double* smem) {
+    double v[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] += __ldcg(&partials[b * 8 + k]);
+    }
+    block_sum<NV>(v, smem);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) out[k] = v[k];
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// All-to-all flag barrier with a fused, deterministic all-reduce.
+//
+// Every CTA owns one 64-byte slot {7 doubles, epoch}.  To cross a barrier a
+// CTA publishes its partial sums and the new epoch (release store after a
+// __syncthreads, so all of the CTA's earlier global writes are ordered before
+// it); then thread t polls slot t with acquire loads until its epoch arrives
+// and the CTA sums the slots in index order.  No atomics, no serial "last
+// CTA" step, and the reduction rides on the barrier's own traffic.  Every CTA
+// adds the same values in the same order, so all get identical bits.
+// Requires gridDim.x <= blockDim.x.  Epochs increase monotonically across
+// launches (the caller persists the base), so slots never need resetting.
+struct alignas(64) FlagSlot {
+    double v[7];
+    unsigned long long epoch;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+// `part` holds this CTA's NV partials in thread 0 (e.g. from block_sum); on
+// return `out[0..NV)` (shared memory) holds the grid-wide sums in every CTA.
+template <int NV>
+__device__ __forceinline__ void grid_allreduce(FlagSlot* slots, unsigned long long epoch, const double (&part)[NV],
+                                               double* out, double* smem) {
+    static_assert(NV <= 7, "at most 7 values per slot");
+    // two slot banks by epoch parity: a CTA can only reuse a bank after every
+    // CTA has published the next epoch, i.e. finished reading this one
+    slots += (epoch & 1ull) * gridDim.x;
+    if (threadIdx.x == 0) {
+        FlagSlot* me = &slots[blockIdx.x];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) me->v[k] = part[k];
+        st_release_u64(&me->epoch, epoch);
+    }
+    double v[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = 0.0;
+    if (threadIdx.x < gridDim.x) {
+        const FlagSlot* sl = &slots[threadIdx.x];
+        unsigned long long spins = 0;
+        while (ld_acquire_u64(&sl->epoch) < epoch) {
+            if (++spins > (1ull << 33)) __trap();
+        }
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] = __ldcg(&sl->v[k]);
+    }
+    block_sum<NV>(v, smem);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) out[k] = v[k];
     __syncthreads();
 }
 

@@ -51,6 +51,7 @@ struct DBuf {
 };
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+constexpr int kPcgThreads = 256;
 
 // ---------------------------------------------------------------------------
 // layout conversion kernels: host (nV,3) float64 in caller order <-> device vec4 internal order
@@ -95,16 +96,16 @@ __global__ void k_rhs_minus_fp(int nF, const vk::vec4_t<T>* __restrict__ Bint, c
 }
 // Y_f = K_ff X_f + K_fp X_p (free rows), Y_p = 0
 template <typename T>
-__global__ void k_apply_K(int n, int nF, int ell_w, const int* __restrict__ ell_col, const T* __restrict__ ell_val,
+__global__ void k_apply_K(int n, int nF, const int* __restrict__ ell_len, const int* __restrict__ ell_col,
+                          const T* __restrict__ ell_val,
                           const int* __restrict__ fp_ptr, const int* __restrict__ fp_col, const T* __restrict__ fp_val,
                           const vk::vec4_t<T>* __restrict__ X, vk::vec4_t<T>* Y) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     if (i >= nF) { Y[i] = vk::make4<T>(T(0), T(0), T(0), T(0)); return; }
     T a = 0, b = 0, c = 0;
-    for (int s = 0; s < ell_w; ++s) {
+    for (int s = 0; s < ell_len[i]; ++s) {
         const int col = ell_col[(size_t)s * nF + i];
-        if (col < 0) break;
         const T v = ell_val[(size_t)s * nF + i];
         const vk::vec4_t<T> x = X[col];
         a += v * x.x; b += v * x.y; c += v * x.z;
@@ -155,7 +156,8 @@ struct Ctx : CtxBase {
     // topology / material
     DBuf<int4> tets;
     DBuf<T> G, w, inv_diag, ell_val, fp_val, m_dt2, dt2_inv_m;
-    DBuf<int> ell_col, fp_ptr, fp_col, inc_ptr, inc_code, int_of_orig;
+    DBuf<int> ell_col, ell_len, fp_ptr, fp_col, inc_ptr, inc_code, int_of_orig;
+    DBuf<int4> slot4;
     DBuf<double> diag64;
     // state
     DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
@@ -226,9 +228,14 @@ struct Ctx : CtxBase {
         }
         for (int i = 0; i < n; ++i) iptr[i + 1] += iptr[i];
         std::vector<int> icode(iptr[n]), fillp(iptr.begin(), iptr.end() - 1);
+        std::vector<int4> slot_h(nE);
         for (int e = 0; e < nE; ++e) {
             const int* t = &tets_h[e].x;
-            for (int a = 0; a < 4; ++a) icode[fillp[t[a]]++] = a * nE + e;
+            int* sl = &slot_h[e].x;
+            for (int a = 0; a < 4; ++a) {
+                sl[a] = fillp[t[a]];
+                icode[fillp[t[a]]++] = a * nE + e;
+            }
         }
         // neighbour sets of free rows -> ELL (free cols) + K_fp CSR (pin slots)
         std::vector<std::vector<int>> nb(nF);
@@ -252,11 +259,13 @@ struct Ctx : CtxBase {
             fptr[i + 1] = (int)fcol.size();
             ell_w = std::max(ell_w, nfree);
         }
-        std::vector<int> ecol((size_t)ell_w * nF, -1);
+        std::vector<int> ecol((size_t)ell_w * nF), elen(nF);
         for (int i = 0; i < nF; ++i) {
             int s = 0;
             for (int col : nb[i])
                 if (col < nF) ecol[(size_t)s++ * nF + i] = col;
+            elen[i] = s;
+            for (; s < ell_w; ++s) ecol[(size_t)s * nF + i] = i;     // pad: own column, value 0
         }
         // per-node arrays in internal order
         std::vector<double> mdt2(n);
@@ -285,6 +294,8 @@ struct Ctx : CtxBase {
         stream = own_stream;
         cudaStream_t s = stream;
         CK(tets.alloc(nE)); CK(tets.upload(tets_h.data(), nE, s));
+        CK(slot4.alloc(nE)); CK(slot4.upload(slot_h.data(), nE, s));
+        CK(ell_len.alloc(nF)); CK(ell_len.upload(elen.data(), nF, s));
         CK(G.alloc((size_t)9 * nE)); CK(G.upload(Gp.data(), Gp.size(), s));
         CK(w.alloc((size_t)2 * nE)); CK(w.upload(wp.data(), wp.size(), s));
         CK(inc_ptr.alloc(n + 1)); CK(inc_ptr.upload(iptr.data(), n + 1, s));
@@ -309,7 +320,8 @@ struct Ctx : CtxBase {
             vk::AssembleArgs<T> aa;
             aa.nF = nF; aa.nE = nE; aa.ell_w = ell_w;
             aa.inc_ptr = inc_ptr.p; aa.inc_code = inc_code.p; aa.tets = tets.p; aa.G = G64.p; aa.wsum = ws64.p;
-            aa.m_dt2 = md64.p; aa.ell_col = ell_col.p; aa.ell_val = ell_val.p; aa.inv_diag = inv_diag.p;
+            aa.m_dt2 = md64.p; aa.ell_col = ell_col.p; aa.ell_len = ell_len.p; aa.ell_val = ell_val.p;
+            aa.inv_diag = inv_diag.p;
             aa.diag64 = diag64.p; aa.fp_ptr = fp_ptr.p; aa.fp_col = fp_col.p; aa.fp_val = fp_val.p;
             aa.n_free_cols_base = nF;
             if (nF > 0) vk::k_assemble<T><<<cdiv(nF, 128), 128, 0, s>>>(aa);
@@ -335,12 +347,12 @@ struct Ctx : CtxBase {
             CK(cudaMemsetAsync(b->p, 0, std::max(1, nF) * sizeof(V4), s));
         }
         int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_pcg<T>, 512, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_pcg<T>, kPcgThreads, 0));
         if (occ < 1) return fail(VKPD_ECUDA, "persistent solver kernel cannot be resident");
-        pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : n_sms;
-        pcg_blocks = std::min(pcg_blocks, occ * n_sms);
-        pcg_blocks = std::max(1, std::min(pcg_blocks, cdiv(std::max(1, nF), 32)));
-        CK(partials.alloc((size_t)8 * pcg_blocks));
+        // default: one row per thread, capped by co-residency
+        pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : cdiv(std::max(1, nF), kPcgThreads);
+        pcg_blocks = std::max(1, std::min(pcg_blocks, occ * n_sms));
+        CK(partials.alloc((size_t)16 * pcg_blocks));      // two parity banks x 8 doubles per CTA
         CK(scal.alloc(16));
         CK(bar.alloc(1));
         CK(cudaMemsetAsync(bar.p, 0, sizeof(vk::GridBar), s));
@@ -401,13 +413,15 @@ struct Ctx : CtxBase {
             ell_w = std::max(ell_w, (int)rows[i].size());
             if (!(dg[i] > 0.0)) return fail(VKPD_EINVAL, "matrix diagonal must be positive");
         }
-        std::vector<int> ecol((size_t)ell_w * nF, -1);
+        std::vector<int> ecol((size_t)ell_w * nF), elen(nF);
         std::vector<T> evals((size_t)ell_w * nF, T(0)), idg(nF);
         for (int i = 0; i < nF; ++i) {
-            for (size_t s2 = 0; s2 < rows[i].size(); ++s2) {
-                ecol[s2 * nF + i] = rows[i][s2].first;
-                evals[s2 * nF + i] = (T)rows[i][s2].second;
+            for (size_t s2 = 0; s2 < (size_t)ell_w; ++s2) {
+                const bool real = s2 < rows[i].size();
+                ecol[s2 * nF + i] = real ? rows[i][s2].first : i;
+                evals[s2 * nF + i] = real ? (T)rows[i][s2].second : T(0);
             }
+            elen[i] = (int)rows[i].size();
             idg[i] = (T)(1.0 / dg[i]);
         }
         CK(cudaSetDevice(device));
@@ -418,6 +432,7 @@ struct Ctx : CtxBase {
         CK(int_of_orig.alloc(n)); CK(int_of_orig.upload(ioo.data(), n, s));
         CK(ell_col.alloc(ecol.size())); CK(ell_col.upload(ecol.data(), ecol.size(), s));
         CK(ell_val.alloc(evals.size())); CK(ell_val.upload(evals.data(), evals.size(), s));
+        CK(ell_len.alloc(nF)); CK(ell_len.upload(elen.data(), nF, s));
         CK(fp_ptr.alloc(nF + 1)); CK(fp_ptr.upload(fptr.data(), nF + 1, s));
         CK(fp_col.alloc(std::max<size_t>(1, fcol.size())));
         CK(fp_val.alloc(std::max<size_t>(1, fcol.size())));
@@ -436,7 +451,9 @@ struct Ctx : CtxBase {
         std::vector<int> ecol((size_t)ell_w * nF), fptr(nF + 1), fcol(fp_col.n);
         std::vector<T> evals((size_t)ell_w * nF), fval(fp_val.n);
         CK(cudaStreamSynchronize(stream));
+        std::vector<int> elen(nF);
         if (nF) {
+            CK(cudaMemcpy(elen.data(), ell_len.p, nF * sizeof(int), cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(ecol.data(), ell_col.p, ecol.size() * sizeof(int), cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(evals.data(), ell_val.p, evals.size() * sizeof(T), cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(fptr.data(), fp_ptr.p, fptr.size() * sizeof(int), cudaMemcpyDeviceToHost));
@@ -450,9 +467,8 @@ struct Ctx : CtxBase {
         std::vector<std::vector<std::pair<int64_t, double>>> rows(n);
         for (int i = 0; i < nF; ++i) {
             auto& r = rows[orig_of_int[i]];
-            for (int s2 = 0; s2 < ell_w; ++s2) {
+            for (int s2 = 0; s2 < elen[i]; ++s2) {
                 const int col = ecol[(size_t)s2 * nF + i];
-                if (col < 0) break;
                 r.push_back({orig_of_int[col], (double)evals[(size_t)s2 * nF + i]});
             }
             for (int k = fptr[i]; k < fptr[i + 1]; ++k) r.push_back({orig_of_int[nF + fcol[k]], (double)fval[k]});
@@ -514,6 +530,7 @@ struct Ctx : CtxBase {
     vk::LocalArgs<T> local_args(const V4* xin) {
         vk::LocalArgs<T> la;
         la.nE = nE; la.tets = tets.p; la.G = G.p; la.w = w.p; la.x = xin; la.corner = corner.p;
+        la.slot4 = slot4.p;
         la.stats = pstats.p; la.F_out = la.R_out = la.V_out = nullptr;
         return la;
     }
@@ -530,7 +547,7 @@ struct Ctx : CtxBase {
     cudaError_t launch_pcg(const vk::PcgArgs<T>& pa) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(pcg_blocks);
-        cfg.blockDim = dim3(512);
+        cfg.blockDim = dim3(kPcgThreads);
         cfg.dynamicSmemBytes = 0;
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
@@ -660,7 +677,7 @@ struct Ctx : CtxBase {
             vk::k_local<T, vk::MODE_RHS, false><<<cdiv(nE, 128), 128, 0, stream>>>(la);
         }
         CK(cudaGetLastError());
-        vk::k_gather<T><<<cdiv(n, 256), 256, 0, stream>>>(n, inc_ptr.p, inc_code.p, corner.p, tmp4b.p);
+        vk::k_gather<T><<<cdiv(n, 256), 256, 0, stream>>>(n, inc_ptr.p, corner.p, tmp4b.p);
         CK(cudaGetLastError());
         rc = download_nodes(tmp4b.p, hrhs);
         if (rc) return rc;
@@ -715,7 +732,7 @@ struct Ctx : CtxBase {
     int apply_K(const double* hX, double* hY) override {
         int rc = upload_nodes(hX, tmp4a.p);
         if (rc) return rc;
-        k_apply_K<T><<<cdiv(n, 256), 256, 0, stream>>>(n, nF, ell_w, ell_col.p, ell_val.p, fp_ptr.p, fp_col.p,
+        k_apply_K<T><<<cdiv(n, 256), 256, 0, stream>>>(n, nF, ell_len.p, ell_col.p, ell_val.p, fp_ptr.p, fp_col.p,
                                                        fp_val.p, tmp4a.p, tmp4b.p);
         CK(cudaGetLastError());
         return download_nodes(tmp4b.p, hY);
