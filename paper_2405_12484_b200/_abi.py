@@ -58,9 +58,10 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"vkpd CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
-    lib = C.CDLL(LIB_PATH)
+    path = os.environ.get("VKPD_LIB", LIB_PATH)      # experiment builds live next to the default
+    if not os.path.exists(path):
+        raise ImportError(f"vkpd CUDA library not built: {path} (run __graft_entry__.build())")
+    lib = C.CDLL(path)
     P = C.c_void_p
     I = C.c_int
     sig = {

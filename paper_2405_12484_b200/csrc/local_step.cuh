@@ -24,6 +24,11 @@ namespace vk {
 
 enum LocalMode { MODE_RHS = 0, MODE_RESID = 1 };
 
+#ifndef VK_LOCAL_MINB
+#define VK_LOCAL_MINB 8        // resident 128-thread CTAs per SM the register budget targets
+                               // (64 regs; measured faster than 4/6 despite small spills)
+#endif
+
 struct ProjStats {
     unsigned int robust;     // elements re-solved on the scalar path
     unsigned int fallback;   // robust path fell back to uniform scaling
@@ -76,7 +81,7 @@ struct LocalArgs {
 };
 
 template <typename T, int MODE, bool WITH_FRV>
-__global__ void __launch_bounds__(128) k_local(LocalArgs<T> a) {
+__global__ void __launch_bounds__(128, VK_LOCAL_MINB) k_local(LocalArgs<T> a) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= a.nE) return;
     const int nE = a.nE;

@@ -281,7 +281,21 @@ VK_HD int project(const double (&sig)[3], double (&s)[3]) {
     bool feas = ok && (nanmin3(s) >= kFloor - 1e-12);
     double obj = feas ? sq3(s, sig) : INFINITY;
     const double prod = sig[0] * sig[1] * sig[2];
-    if (prod > 1.0) {
+    // The second start can only be taken if it lands on a strictly better
+    // stationary point.  Any stationary point that uses the smaller root of
+    // s_j^2 - sigma_j s_j + lam = 0 for some j has (s_j - sigma_j)^2 >=
+    // sigma_j^2 / 4; so when the first start found the all-larger-root point
+    // with an objective below min_j sigma_j^2 / 4 it is the global stationary
+    // minimum and the reference's second Newton cannot replace it (it would
+    // reproduce it or land higher).  Skipping it is exact.
+    bool need_second = prod > 1.0;
+    if (need_second && feas) {
+        const double mn = fmin(fmin(sig[0], sig[1]), sig[2]);
+        const bool plus_root = s[0] >= 0.5 * sig[0] && s[1] >= 0.5 * sig[1] && s[2] >= 0.5 * sig[2];
+        // margin 1e-8 covers the 1e-10 KKT residual the reference accepts as "ok"
+        if (plus_root && mn > 0.0 && obj < 0.25 * mn * mn - 1e-8) need_second = false;
+    }
+    if (need_second) {
         const int j = argmin3(sig);
         const double others = prod / fmax(sig[j], 1e-300);
         double s2[3];

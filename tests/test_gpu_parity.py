@@ -260,3 +260,16 @@ def test_c3_frame_matches_reference_fp32():
     ref = sc.mesh.nodes + g["frame1"].astype(np.float64)
     assert rel_l2(fr[0], ref) < 1e-5
     assert rel_l2(fr[0] - sc.mesh.nodes, g["frame1"]) < 1e-2
+
+
+@pytest.mark.parametrize("prec,tols", [("fp32", {1: 1e-5, 10: 1e-4, 100: 1e-3}),
+                                       ("fp64", {1: 1e-10, 10: 1e-10, 100: 1e-10})])
+def test_c2_hundred_frames_match_reference(prec, tols):
+    """BASELINE configs[1]: 30K-tet rib scarf hanging from one edge, 100 frames."""
+    g = golden("c2.npz")
+    sc = scenes.c2_scarf()
+    assert scene_digest(sc) == str(g["digest"])
+    fr = pdsolver.simulate_mesh(sc.mesh, sc.gammas, 100, sc.dt, forces=sc.forces, pins=sc.pins,
+                                pin_targets=sc.pin_targets, iterations=30, precision=prec)
+    for k, tol in tols.items():
+        assert rel_l2(fr[k - 1], g[f"frame{k}"]) < tol, (k, rel_l2(fr[k - 1], g[f"frame{k}"]))
