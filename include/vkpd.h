@@ -120,6 +120,22 @@ int vkpd_global_solve(vkpd_ctx* ctx, const double* B, const double* pin_vals, do
 int vkpd_apply_K(vkpd_ctx* ctx, const double* X, double* Y);
 int vkpd_get_stats(vkpd_ctx* ctx, vkpd_stats* st);
 
+/* a_jacobi_refine (pdsolver.py:632-703) on K_ff over free-node vectors (n_free, k), k <= 3:
+ * aggregated weighted-Jacobi sweeps (or the Chebyshev variant with spectral radius rho),
+ * best-iterate tracking and divergence stop.  hist: (k, steps+1) residual norms, row-major,
+ * steps = sweeps (plain) or sweeps*aggregation (Chebyshev); n_hist/diverged: (k,). */
+int vkpd_a_jacobi_refine(vkpd_ctx* ctx, const double* Bf, const double* X0f, int k, int sweeps, int aggregation,
+                         double omega, int chebyshev, double rho, double* Xf, double* hist, int* n_hist,
+                         int* diverged);
+/* _power_rho (pdsolver.py:616-629): 30-ish power iterations of I - omega D^-1 K_ff from v0 (n_free) */
+int vkpd_power_rho(vkpd_ctx* ctx, double omega, int iters, const double* v0, double* rho);
+/* CmsSubspace (pdsolver.py:512-593): dense basis T (n_free x m, column-major) and K_red^-1 (m x m) */
+int vkpd_cms_set_basis(vkpd_ctx* ctx, int m, const double* T, const double* Kred_inv);
+/* GlobalSolver.solve in "cms" mode (pdsolver.py:225-246): x0 = T K_red^-1 T^T (B_f - K_fp P), then
+ * sweeps of a_jacobi_refine per column; B (nV,k), P (n_pins,k), X (nV,k) */
+int vkpd_cms_solve(vkpd_ctx* ctx, const double* B, const double* P, int k, int sweeps, int aggregation, double omega,
+                   int chebyshev, double rho, double* X);
+
 int vkpd_batch_projections(int precision, int64_t n, const double* F, double* R, double* V,
                            unsigned int* n_robust, unsigned int* n_fallback);
 

@@ -22,7 +22,8 @@ EXPORTS = (
     "vkpd_get_stream", "vkpd_set_state", "vkpd_get_state", "vkpd_set_pin_targets",
     "vkpd_set_forces", "vkpd_step", "vkpd_step_async", "vkpd_sync", "vkpd_profile_step",
     "vkpd_elastic_rhs", "vkpd_global_solve", "vkpd_apply_K", "vkpd_get_stats",
-    "vkpd_batch_projections", "vkpd_create_matrix", "vkpd_get_matrix_csr",
+    "vkpd_batch_projections", "vkpd_create_matrix", "vkpd_get_matrix_csr", "vkpd_a_jacobi_refine",
+    "vkpd_power_rho", "vkpd_cms_set_basis", "vkpd_cms_solve",
 )
 
 
@@ -87,6 +88,10 @@ def load():
         "vkpd_batch_projections": (I, [I, C.c_int64, P, P, P, C.POINTER(C.c_uint), C.POINTER(C.c_uint)]),
         "vkpd_create_matrix": (I, [C.c_int64, P, P, P, P, C.c_int64, C.POINTER(Config), C.POINTER(P)]),
         "vkpd_get_matrix_csr": (I, [P, P, P, P, C.POINTER(C.c_int64)]),
+        "vkpd_a_jacobi_refine": (I, [P, P, P, I, I, I, C.c_double, I, C.c_double, P, P, P, P]),
+        "vkpd_power_rho": (I, [P, C.c_double, I, P, C.POINTER(C.c_double)]),
+        "vkpd_cms_set_basis": (I, [P, I, P, P]),
+        "vkpd_cms_solve": (I, [P, P, P, I, I, I, C.c_double, I, C.c_double, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -251,6 +256,46 @@ class Context:
         Y = np.empty_like(X)
         check(self.lib.vkpd_apply_K(self.h, ptr(X), ptr(Y)))
         return Y
+
+    def a_jacobi_refine(self, Bf, X0f, sweeps, aggregation, omega, chebyshev, rho):
+        """Columns of Bf (n_free, k<=3) refined from X0f; returns (X, hist list per column, diverged)."""
+        Bf = f64(Bf)
+        X0f = f64(X0f)
+        if Bf.ndim == 1:
+            Bf, X0f = Bf[:, None], X0f[:, None]
+        k = Bf.shape[1]
+        steps = sweeps * aggregation if chebyshev else sweeps
+        X = np.empty_like(Bf)
+        hist = np.zeros((k, steps + 1))
+        nh = np.zeros(k, dtype=np.int32)
+        dv = np.zeros(k, dtype=np.int32)
+        check(self.lib.vkpd_a_jacobi_refine(self.h, ptr(np.ascontiguousarray(Bf)), ptr(np.ascontiguousarray(X0f)),
+                                            k, int(sweeps), int(aggregation), float(omega), int(bool(chebyshev)),
+                                            float(rho), ptr(X), ptr(hist), ptr(nh), ptr(dv)))
+        return X, [hist[c, :nh[c]].tolist() for c in range(k)], [bool(d) for d in dv]
+
+    def power_rho(self, omega, v0, iters=30):
+        rho = C.c_double(0.0)
+        check(self.lib.vkpd_power_rho(self.h, float(omega), int(iters), ptr(f64(v0).reshape(-1)), C.byref(rho)))
+        return rho.value
+
+    def cms_set_basis(self, T, Kred_inv):
+        T = np.asfortranarray(T, dtype=np.float64)
+        Ki = np.asfortranarray(Kred_inv, dtype=np.float64)
+        self._keep["cmsT"], self._keep["cmsKi"] = T, Ki
+        check(self.lib.vkpd_cms_set_basis(self.h, T.shape[1], T.ctypes.data_as(C.c_void_p),
+                                          Ki.ctypes.data_as(C.c_void_p)))
+
+    def cms_solve(self, B, pin_vals, sweeps, aggregation, omega, chebyshev, rho):
+        B = f64(B)
+        if B.ndim == 1:
+            B = B[:, None]
+        k = B.shape[1]
+        P = f64(pin_vals).reshape(self.n_pins, k) if self.n_pins else np.zeros((0, k))
+        X = np.empty_like(B)
+        check(self.lib.vkpd_cms_solve(self.h, ptr(B), ptr(P), k, int(sweeps), int(aggregation), float(omega),
+                                      int(bool(chebyshev)), float(rho), ptr(X)))
+        return X
 
     def matrix_csr(self):
         nnz = C.c_int64(0)

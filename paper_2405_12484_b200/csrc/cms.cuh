@@ -1,0 +1,365 @@
+// Reference-compatible domain-decomposed global solve:
+// the component-mode-synthesis subspace apply x = T K_red^-1 T^T b and the
+// aggregated / Chebyshev weighted-Jacobi refinement `a_jacobi_refine`
+// (pdsolver.py:632-703), with the reference's control flow: recursive
+// residual, per-column residual history, best-iterate tracking, divergence
+// stop at 10x the best residual.  Up to three right-hand-side columns run in
+// lockstep inside one persistent cooperative kernel; a diverged column freezes
+// (the reference solves columns one by one and breaks that column's loop).
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "vk_common.cuh"
+
+namespace vk {
+
+namespace cgr = cooperative_groups;
+
+template <typename T>
+struct AJArgs {
+    int nF, ell_w;
+    const int* ell_col;
+    const T* ell_val;
+    const double* diag;          // float64 diagonal of K_ff
+    const vec4_t<T>* b;          // rhs (3 columns)
+    vec4_t<T>* x;                // in: x0, out: result
+    vec4_t<T>* r;                // residual (plain) / b - K x (Chebyshev)
+    vec4_t<T>* s;
+    vec4_t<T>* e;                // e (plain) / x_prev (Chebyshev)
+    vec4_t<T>* cs0;
+    vec4_t<T>* cs1;
+    vec4_t<T>* best;
+    double* partials;            // 2 * grid * 8
+    double* hist;                // [(steps + 1) x 3] residual norms per column
+    int* n_hist;                 // [3]
+    int* diverged;               // [3]
+    int sweeps, aggregation;
+    double omega, rho;
+    int ncols;                   // active columns (1..3)
+};
+
+template <typename T>
+__device__ __forceinline__ vec4_t<T> spmv_row(const AJArgs<T>& a, const vec4_t<T>* v, int i) {
+    T qx = 0, qy = 0, qz = 0;
+    for (int sl = 0; sl < a.ell_w; ++sl) {
+        const int col = __ldg(&a.ell_col[(size_t)sl * a.nF + i]);
+        const T kv = __ldg(&a.ell_val[(size_t)sl * a.nF + i]);
+        const vec4_t<T> c = ld4(&v[col]);
+        qx += kv * c.x; qy += kv * c.y; qz += kv * c.z;
+    }
+    return make4<T>(qx, qy, qz, T(0));
+}
+
+template <int NV>
+__device__ __forceinline__ void aj_allreduce(cgr::grid_group& grid, double* partials, int& parity, double (&acc)[NV],
+                                             double* red, double* smem) {
+    block_sum<NV>(acc, smem);
+    double* P = partials + (size_t)parity * gridDim.x * 8;
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) P[blockIdx.x * 8 + k] = acc[k];
+    grid.sync();
+    reduce_partials_all<NV>(P, red, smem);
+    parity ^= 1;
+}
+
+// Per-column bookkeeping, identical in every thread of the grid.
+struct AJState {
+    double best[3], last[3];
+    int nh[3];
+    bool act[3], div[3];
+};
+
+__device__ __forceinline__ void aj_record(AJState& st, const double* red, double* hist, bool (&improve)[3],
+                                          bool writer) {
+    for (int c = 0; c < 3; ++c) {
+        improve[c] = false;
+        if (!st.act[c]) continue;
+        const double rn = sqrt(red[c]);
+        if (writer) hist[st.nh[c] * 3 + c] = rn;
+        st.nh[c]++;
+        st.last[c] = rn;
+        if (rn < st.best[c]) { st.best[c] = rn; improve[c] = true; }
+        if (rn > 10.0 * st.best[c]) { st.div[c] = true; st.act[c] = false; }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void aj_save_best(const AJArgs<T>& a, const bool (&improve)[3], int tid, int stride) {
+    if (!(improve[0] || improve[1] || improve[2])) return;
+    for (int i = tid; i < a.nF; i += stride) {
+        const vec4_t<T> xi = a.x[i];
+        vec4_t<T> bi = a.best[i];
+        if (improve[0]) bi.x = xi.x;
+        if (improve[1]) bi.y = xi.y;
+        if (improve[2]) bi.z = xi.z;
+        a.best[i] = bi;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void aj_finish(const AJArgs<T>& a, const AJState& st, int tid, int stride) {
+    bool pick[3];
+    for (int c = 0; c < 3; ++c) pick[c] = st.div[c] || st.last[c] > st.best[c];
+    for (int i = tid; i < a.nF; i += stride) {
+        vec4_t<T> xi = a.x[i];
+        const vec4_t<T> bi = a.best[i];
+        if (pick[0]) xi.x = bi.x;
+        if (pick[1]) xi.y = bi.y;
+        if (pick[2]) xi.z = bi.z;
+        a.x[i] = xi;
+    }
+    if (tid == 0)
+        for (int c = 0; c < 3; ++c) {
+            a.diverged[c] = st.div[c] ? 1 : 0;
+            a.n_hist[c] = st.nh[c];
+        }
+}
+
+// r = b - K x, best = x, history[0]
+template <typename T>
+__device__ __forceinline__ void aj_start(const AJArgs<T>& a, AJState& st, cgr::grid_group& grid, int& parity,
+                                         double* red, double* smem, int tid, int stride) {
+    double acc[3] = {0, 0, 0};
+    for (int i = tid; i < a.nF; i += stride) {
+        const vec4_t<T> kx = spmv_row(a, a.x, i);
+        const vec4_t<T> bi = a.b[i];
+        const vec4_t<T> ri = make4<T>(bi.x - kx.x, bi.y - kx.y, bi.z - kx.z, T(0));
+        a.r[i] = ri;
+        a.best[i] = a.x[i];
+        acc[0] += (double)ri.x * ri.x; acc[1] += (double)ri.y * ri.y; acc[2] += (double)ri.z * ri.z;
+    }
+    aj_allreduce<3>(grid, a.partials, parity, acc, red, smem);
+    for (int c = 0; c < 3; ++c) {
+        st.best[c] = sqrt(red[c]);
+        st.last[c] = st.best[c];
+        st.nh[c] = 1;
+        st.act[c] = c < a.ncols;
+        st.div[c] = false;
+        if (tid == 0) a.hist[c] = st.best[c];
+    }
+}
+
+// Plain aggregated sweeps (pdsolver.py:683-703).
+template <typename T>
+__global__ void __launch_bounds__(256) k_ajacobi(AJArgs<T> a) {
+    cgr::grid_group grid = cgr::this_grid();
+    __shared__ double smem[32 * 8];
+    __shared__ double red[8];
+    const int nF = a.nF;
+    const int stride = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    int parity = 0;
+    AJState st;
+    aj_start(a, st, grid, parity, red, smem, tid, stride);
+    for (int sw = 0; sw < a.sweeps; ++sw) {
+        if (!(st.act[0] || st.act[1] || st.act[2])) break;
+        const T w0 = st.act[0] ? (T)a.omega : T(0), w1 = st.act[1] ? (T)a.omega : T(0),
+                w2 = st.act[2] ? (T)a.omega : T(0);
+        // s = r; cs = omega D^-1 s; e = cs
+        for (int i = tid; i < nF; i += stride) {
+            const vec4_t<T> ri = a.r[i];
+            const T di = (T)(1.0 / a.diag[i]);
+            const vec4_t<T> c = make4<T>(w0 * (di * ri.x), w1 * (di * ri.y), w2 * (di * ri.z), T(0));
+            a.s[i] = ri;
+            a.e[i] = c;
+            a.cs0[i] = c;
+        }
+        grid.sync();
+        for (int ag = 0; ag < a.aggregation; ++ag) {
+            const vec4_t<T>* cur = (ag & 1) ? a.cs1 : a.cs0;
+            vec4_t<T>* nxt = (ag & 1) ? a.cs0 : a.cs1;
+            const bool more = ag + 1 < a.aggregation;
+            for (int i = tid; i < nF; i += stride) {
+                const vec4_t<T> kc = spmv_row(a, cur, i);
+                vec4_t<T> si = a.s[i];
+                si.x -= kc.x; si.y -= kc.y; si.z -= kc.z;
+                a.s[i] = si;
+                if (more) {
+                    const T di = (T)(1.0 / a.diag[i]);
+                    const vec4_t<T> c = make4<T>(w0 * (di * si.x), w1 * (di * si.y), w2 * (di * si.z), T(0));
+                    nxt[i] = c;
+                    vec4_t<T> ei = a.e[i];
+                    ei.x += c.x; ei.y += c.y; ei.z += c.z;
+                    a.e[i] = ei;
+                }
+            }
+            if (more) grid.sync();
+        }
+        // x += e; r = s; |r|
+        double acc[3] = {0, 0, 0};
+        for (int i = tid; i < nF; i += stride) {
+            vec4_t<T> xi = a.x[i];
+            const vec4_t<T> ei = a.e[i];
+            xi.x += ei.x; xi.y += ei.y; xi.z += ei.z;
+            a.x[i] = xi;
+            const vec4_t<T> si = a.s[i];
+            a.r[i] = si;
+            acc[0] += (double)si.x * si.x; acc[1] += (double)si.y * si.y; acc[2] += (double)si.z * si.z;
+        }
+        aj_allreduce<3>(grid, a.partials, parity, acc, red, smem);
+        bool improve[3];
+        aj_record(st, red, a.hist, improve, tid == 0);
+        aj_save_best(a, improve, tid, stride);
+    }
+    aj_finish(a, st, tid, stride);
+}
+
+// Chebyshev semi-iterative variant (pdsolver.py:657-681): sweeps * aggregation
+// steps y = x + omega D^-1 (b - K x), x_new = w (y - x_prev) + x_prev; the
+// residual b - K x_new of each step is reused by the next one (one SpMV/step).
+template <typename T>
+__global__ void __launch_bounds__(256) k_chebyshev(AJArgs<T> a) {
+    cgr::grid_group grid = cgr::this_grid();
+    __shared__ double smem[32 * 8];
+    __shared__ double red[8];
+    const int nF = a.nF;
+    const int stride = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    int parity = 0;
+    AJState st;
+    aj_start(a, st, grid, parity, red, smem, tid, stride);     // a.r = b - K x0
+    for (int i = tid; i < nF; i += stride) a.e[i] = a.x[i];    // x_prev
+    const double rho2 = a.rho * a.rho;
+    double w = 1.0;
+    const int total = a.sweeps * a.aggregation;
+    for (int k = 0; k < total; ++k) {
+        if (!(st.act[0] || st.act[1] || st.act[2])) break;
+        const T om = (T)a.omega;
+        const T ww = (T)(k == 0 ? 1.0 : w);
+        // new iterate (own rows)
+        for (int i = tid; i < nF; i += stride) {
+            const vec4_t<T> xi = a.x[i], xp = a.e[i], ri = a.r[i];
+            const T di = (T)(1.0 / a.diag[i]);
+            vec4_t<T> xn;
+            const T yx = xi.x + om * (di * ri.x), yy = xi.y + om * (di * ri.y), yz = xi.z + om * (di * ri.z);
+            if (k == 0) {
+                xn = make4<T>(yx, yy, yz, T(0));
+            } else {
+                xn = make4<T>(ww * (yx - xp.x) + xp.x, ww * (yy - xp.y) + xp.y, ww * (yz - xp.z) + xp.z, T(0));
+            }
+            xn.x = st.act[0] ? xn.x : xi.x;
+            xn.y = st.act[1] ? xn.y : xi.y;
+            xn.z = st.act[2] ? xn.z : xi.z;
+            a.e[i] = xi;
+            a.s[i] = xn;
+        }
+        grid.sync();
+        double acc[3] = {0, 0, 0};
+        for (int i = tid; i < nF; i += stride) {
+            const vec4_t<T> kx = spmv_row(a, a.s, i);
+            const vec4_t<T> bi = a.b[i];
+            const vec4_t<T> ri = make4<T>(bi.x - kx.x, bi.y - kx.y, bi.z - kx.z, T(0));
+            a.r[i] = ri;
+            acc[0] += (double)ri.x * ri.x; acc[1] += (double)ri.y * ri.y; acc[2] += (double)ri.z * ri.z;
+        }
+        aj_allreduce<3>(grid, a.partials, parity, acc, red, smem);
+        for (int i = tid; i < nF; i += stride) a.x[i] = a.s[i];
+        w = (k == 0) ? 2.0 / (2.0 - rho2) : 4.0 / (4.0 - rho2 * w);
+        bool improve[3];
+        aj_record(st, red, a.hist, improve, tid == 0);
+        aj_save_best(a, improve, tid, stride);
+    }
+    aj_finish(a, st, tid, stride);
+}
+
+// Power iteration for the spectral radius of I - omega D^-1 K (pdsolver.py:616-629),
+// 3 independent columns (column 0 is the reference's); v is the start vector.
+template <typename T>
+__global__ void __launch_bounds__(256) k_power_rho(AJArgs<T> a, int iters, double* rho_out) {
+    cgr::grid_group grid = cgr::this_grid();
+    __shared__ double smem[32 * 8];
+    __shared__ double red[8];
+    const int nF = a.nF;
+    const int stride = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    int parity = 0;
+    // normalise v (held in a.x)
+    double acc[3] = {0, 0, 0};
+    for (int i = tid; i < nF; i += stride) {
+        const vec4_t<T> v = a.x[i];
+        acc[0] += (double)v.x * v.x; acc[1] += (double)v.y * v.y; acc[2] += (double)v.z * v.z;
+    }
+    aj_allreduce<3>(grid, a.partials, parity, acc, red, smem);
+    double nrm[3] = {sqrt(red[0]), sqrt(red[1]), sqrt(red[2])};
+    for (int i = tid; i < nF; i += stride) {
+        const vec4_t<T> v = a.x[i];
+        a.s[i] = make4<T>((T)(v.x / nrm[0]), (T)(v.y / nrm[1]), (T)(v.z / nrm[2]), T(0));
+    }
+    double rho[3] = {0, 0, 0};
+    bool stop[3] = {false, false, false};
+    for (int k = 0; k < iters; ++k) {
+        grid.sync();
+        double ac2[3] = {0, 0, 0};
+        for (int i = tid; i < nF; i += stride) {
+            const vec4_t<T> kv = spmv_row(a, a.s, i);
+            const vec4_t<T> v = a.s[i];
+            const T di = (T)(1.0 / a.diag[i]);
+            const T om = (T)a.omega;
+            const vec4_t<T> u = make4<T>(v.x - om * (di * kv.x), v.y - om * (di * kv.y), v.z - om * (di * kv.z), T(0));
+            a.r[i] = u;
+            ac2[0] += (double)u.x * u.x; ac2[1] += (double)u.y * u.y; ac2[2] += (double)u.z * u.z;
+        }
+        aj_allreduce<3>(grid, a.partials, parity, ac2, red, smem);
+        for (int c = 0; c < 3; ++c) {
+            const double nv = sqrt(red[c]);
+            if (stop[c]) continue;
+            if (nv < 1e-300) { rho[c] = 0.0; stop[c] = true; continue; }
+            rho[c] = nv;
+            nrm[c] = nv;
+        }
+        for (int i = tid; i < nF; i += stride) {
+            const vec4_t<T> u = a.r[i];
+            a.s[i] = make4<T>((T)(u.x / nrm[0]), (T)(u.y / nrm[1]), (T)(u.z / nrm[2]), T(0));
+        }
+    }
+    if (tid == 0)
+        for (int c = 0; c < 3; ++c) rho_out[c] = fmin(rho[c], 0.9999);
+}
+
+// CMS subspace apply with a dense basis (column-major T: n x m) and a dense
+// symmetric K_red^-1 (m x m):  y = T^T b  (one warp per basis column),
+// z = K_red^-1 y, x = T z (one thread per row).
+template <typename T>
+__global__ void k_tmv(int n, int m, const double* __restrict__ Tb, const vec4_t<T>* __restrict__ b, double* y) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= m) return;
+    const double* col = Tb + (size_t)warp * n;
+    double s0 = 0, s1 = 0, s2 = 0;
+    for (int i = lane; i < n; i += 32) {
+        const double t = col[i];
+        const vec4_t<T> v = b[i];
+        s0 += t * v.x; s1 += t * v.y; s2 += t * v.z;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) { y[3 * warp] = s0; y[3 * warp + 1] = s1; y[3 * warp + 2] = s2; }
+}
+__global__ void k_symv3(int m, const double* __restrict__ A, const double* __restrict__ y, double* z) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double s0 = 0, s1 = 0, s2 = 0;
+    for (int j = 0; j < m; ++j) {
+        const double a = A[(size_t)j * m + i];
+        s0 += a * y[3 * j]; s1 += a * y[3 * j + 1]; s2 += a * y[3 * j + 2];
+    }
+    z[3 * i] = s0; z[3 * i + 1] = s1; z[3 * i + 2] = s2;
+}
+template <typename T>
+__global__ void k_tv(int n, int m, const double* __restrict__ Tb, const double* __restrict__ z, vec4_t<T>* x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s0 = 0, s1 = 0, s2 = 0;
+    for (int j = 0; j < m; ++j) {
+        const double t = Tb[(size_t)j * n + i];
+        s0 += t * z[3 * j]; s1 += t * z[3 * j + 1]; s2 += t * z[3 * j + 2];
+    }
+    x[i] = make4<T>((T)s0, (T)s1, (T)s2, T(0));
+}
+
+}  // namespace vk

@@ -17,6 +17,7 @@
 #include "../../include/vkpd.h"
 #include "local_step.cuh"
 #include "solver.cuh"
+#include "cms.cuh"
 
 namespace {
 
@@ -136,6 +137,12 @@ struct CtxBase {
     virtual int init_matrix(int64_t n, const int64_t* indptr, const int64_t* indices, const double* data,
                             const int64_t* pins, int64_t npins, const vkpd_config* c) = 0;
     virtual int get_csr(int64_t* indptr, int64_t* indices, double* data, int64_t* nnz) = 0;
+    virtual int aj_refine(const double* Bf, const double* X0f, int k, int sweeps, int agg, double omega, int cheb,
+                          double rho, double* Xf, double* hist, int* nhist, int* diverged) = 0;
+    virtual int power_rho(double omega, int iters, const double* v0, double* rho) = 0;
+    virtual int cms_set_basis(int m, const double* T, const double* Kinv) = 0;
+    virtual int cms_solve(const double* B, const double* P, int k, int sweeps, int agg, double omega, int cheb,
+                          double rho, double* X) = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
     int device = 0;
@@ -729,6 +736,174 @@ struct Ctx : CtxBase {
         return VKPD_OK;
     }
 
+    // ---- reference-compatible CMS / A-Jacobi path (cms.cuh) ----------------
+    DBuf<double> cmsT, cmsKinv, cms_y, cms_z, hist_d, rho_d;
+    DBuf<V4> bestv;
+    DBuf<int> nhist_d, div_d;
+    int cms_m = 0;
+
+    // rows [0, m) of a V4 buffer from an (m, k) float64 host array, columns c0..c0+2
+    int upload_rows(const double* h, int m, int k, int c0, V4* dst) {
+        std::vector<double> pk((size_t)3 * std::max(1, m), 0.0);
+        const int kc = std::min(3, k - c0);
+        for (int j = 0; j < m; ++j)
+            for (int c = 0; c < kc; ++c) pk[3 * (size_t)j + c] = h[(size_t)j * k + c0 + c];
+        if (m == 0) return VKPD_OK;
+        CK(cudaMemcpyAsync(stage.p, pk.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, stream));
+        k_rows_in<T><<<cdiv(m, 256), 256, 0, stream>>>(m, stage.p, dst);
+        CK(cudaGetLastError());
+        // the pageable host buffer must outlive the copy
+        CK(cudaStreamSynchronize(stream));
+        return VKPD_OK;
+    }
+    int download_rows(const V4* src, int m, int k, int c0, double* h) {
+        if (m == 0) return VKPD_OK;
+        std::vector<V4> tmp(m);
+        CK(cudaMemcpyAsync(tmp.data(), src, sizeof(V4) * m, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        const int kc = std::min(3, k - c0);
+        for (int j = 0; j < m; ++j) {
+            const double v[3] = {(double)tmp[j].x, (double)tmp[j].y, (double)tmp[j].z};
+            for (int c = 0; c < kc; ++c) h[(size_t)j * k + c0 + c] = v[c];
+        }
+        return VKPD_OK;
+    }
+    int ensure_aj() {
+        if (!bestv.p) CK(bestv.alloc(std::max(1, nF)));
+        if (!nhist_d.p) { CK(nhist_d.alloc(3)); CK(div_d.alloc(3)); CK(rho_d.alloc(3)); }
+        return VKPD_OK;
+    }
+    vk::AJArgs<T> aj_args(int sweeps, int agg, double omega, double rho, int ncols) {
+        vk::AJArgs<T> a;
+        a.nF = nF; a.ell_w = ell_w; a.ell_col = ell_col.p; a.ell_val = ell_val.p; a.diag = diag64.p;
+        a.b = rhs.p; a.x = dx.p; a.r = r.p; a.s = z.p; a.e = p0.p; a.cs0 = p1.p; a.cs1 = q.p; a.best = bestv.p;
+        a.partials = partials.p; a.hist = hist_d.p; a.n_hist = nhist_d.p; a.diverged = div_d.p;
+        a.sweeps = sweeps; a.aggregation = agg; a.omega = omega; a.rho = rho; a.ncols = ncols;
+        return a;
+    }
+    template <typename K>
+    cudaError_t launch_coop(K kernel, void** args) {
+        int occ = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0);
+        if (e != cudaSuccess) return e;
+        const int blocks = std::max(1, std::min(std::min(occ * n_sms, pcg_blocks), cdiv(std::max(1, nF), 256)));
+        return cudaLaunchCooperativeKernel((const void*)kernel, dim3(blocks), dim3(256), args, 0, stream);
+    }
+    // a_jacobi_refine on K_ff over free-node vectors (pdsolver.py:632-703)
+    int run_aj(int ncols, int sweeps, int agg, double omega, int cheb, double rho) {
+        const int steps = cheb ? sweeps * agg : sweeps;
+        CK(hist_d.alloc((size_t)3 * (steps + 1)));
+        CK(cudaMemsetAsync(hist_d.p, 0, sizeof(double) * 3 * (steps + 1), stream));
+        vk::AJArgs<T> a = aj_args(sweeps, agg, omega, rho, ncols);
+        void* args[] = {&a};
+        if (cheb) CK(launch_coop(vk::k_chebyshev<T>, args));
+        else CK(launch_coop(vk::k_ajacobi<T>, args));
+        return VKPD_OK;
+    }
+    int aj_refine(const double* Bf, const double* X0f, int k, int sweeps, int agg, double omega, int cheb,
+                  double rho, double* Xf, double* hist, int* nhist, int* diverged) override {
+        if (agg != 2 && agg != 3) return fail(VKPD_EINVAL, "aggregation must be 2 or 3");
+        if (k < 1 || k > 3) return fail(VKPD_EINVAL, "a_jacobi_refine takes 1 to 3 columns");
+        int rc = ensure_aj();
+        if (rc) return rc;
+        if (cheb && !(rho >= 0.0)) return fail(VKPD_EINVAL, "chebyshev needs rho (vkpd_power_rho)");
+        if ((rc = upload_rows(Bf, nF, k, 0, rhs.p))) return rc;
+        if ((rc = upload_rows(X0f, nF, k, 0, dx.p))) return rc;
+        if ((rc = run_aj(k, sweeps, agg, omega, cheb, rho))) return rc;
+        if ((rc = download_rows(dx.p, nF, k, 0, Xf))) return rc;
+        const int steps = cheb ? sweeps * agg : sweeps;
+        std::vector<double> hh((size_t)3 * (steps + 1));
+        CK(cudaMemcpy(hh.data(), hist_d.p, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost));
+        int nh[3], dv[3];
+        CK(cudaMemcpy(nh, nhist_d.p, sizeof nh, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(dv, div_d.p, sizeof dv, cudaMemcpyDeviceToHost));
+        for (int c = 0; c < k; ++c) {
+            if (nhist) nhist[c] = nh[c];
+            if (diverged) diverged[c] = dv[c];
+            if (hist)
+                for (int j = 0; j < nh[c]; ++j) hist[(size_t)c * (steps + 1) + j] = hh[(size_t)j * 3 + c];
+        }
+        return VKPD_OK;
+    }
+    // reference start vector: default_rng(0).normal(size=n) supplied by the caller (v0, nF)
+    int power_rho(double omega, int iters, const double* v0, double* rho) override {
+        int rc = ensure_aj();
+        if (rc) return rc;
+        if (!v0) return fail(VKPD_EINVAL, "power iteration needs a start vector");
+        {
+            std::vector<double> v3((size_t)3 * nF);
+            for (int j = 0; j < nF; ++j) v3[3 * j] = v3[3 * j + 1] = v3[3 * j + 2] = v0[j];
+            if ((rc = upload_rows(v3.data(), nF, 3, 0, dx.p))) return rc;
+        }
+        vk::AJArgs<T> a = aj_args(0, 2, omega, 0.0, 3);
+        double* out = rho_d.p;
+        void* args[] = {&a, &iters, &out};
+        CK(launch_coop(vk::k_power_rho<T>, args));
+        double hr[3];
+        CK(cudaMemcpy(hr, rho_d.p, sizeof hr, cudaMemcpyDeviceToHost));
+        *rho = hr[0];
+        return VKPD_OK;
+    }
+    int cms_set_basis(int m, const double* Tb, const double* Kinv) override {
+        if (m < 0) return fail(VKPD_EINVAL, "bad subspace size");
+        cms_m = m;
+        CK(cmsT.alloc((size_t)std::max(1, nF) * std::max(1, m)));
+        CK(cmsKinv.alloc((size_t)std::max(1, m) * std::max(1, m)));
+        CK(cms_y.alloc((size_t)3 * std::max(1, m)));
+        CK(cms_z.alloc((size_t)3 * std::max(1, m)));
+        if (m > 0) {
+            CK(cudaMemcpy(cmsT.p, Tb, sizeof(double) * nF * (size_t)m, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(cmsKinv.p, Kinv, sizeof(double) * (size_t)m * m, cudaMemcpyHostToDevice));
+        }
+        return VKPD_OK;
+    }
+    // GlobalSolver.solve in "cms" mode (pdsolver.py:237-246): per column
+    // x0 = T K_red^-1 T^T b_f, then a_jacobi_refine(K_ff, b_f, x0, ...).
+    int cms_solve(const double* B, const double* P, int k, int sweeps, int agg, double omega, int cheb, double rho,
+                  double* X) override {
+        if (sweeps > 0 && agg != 2 && agg != 3) return fail(VKPD_EINVAL, "aggregation must be 2 or 3");
+        int rc = ensure_aj();
+        if (rc) return rc;
+        if (cheb && sweeps > 0 && !(rho >= 0.0)) return fail(VKPD_EINVAL, "chebyshev needs rho (vkpd_power_rho)");
+        std::vector<double> xcol((size_t)nF * k);
+        for (int c0 = 0; c0 < k; c0 += 3) {
+            const int kc = std::min(3, k - c0);
+            // b_f - K_fp P  -> rhs
+            std::vector<double> b3((size_t)3 * n, 0.0), p3((size_t)3 * std::max(1, nP), 0.0);
+            for (int j = 0; j < n; ++j)
+                for (int c = 0; c < kc; ++c) b3[3 * (size_t)j + c] = B[(size_t)j * k + c0 + c];
+            for (int j = 0; j < nP; ++j)
+                for (int c = 0; c < kc; ++c) p3[3 * (size_t)j + c] = P[(size_t)j * k + c0 + c];
+            if ((rc = upload_nodes(b3.data(), tmp4a.p))) return rc;
+            if (nP) {
+                CK(cudaMemcpyAsync(stage.p, p3.data(), sizeof(double) * 3 * nP, cudaMemcpyHostToDevice, stream));
+                k_rows_in<T><<<cdiv(nP, 256), 256, 0, stream>>>(nP, stage.p, tmp4b.p);
+                CK(cudaGetLastError());
+            }
+            if (nF > 0) {
+                k_rhs_minus_fp<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, tmp4a.p, fp_ptr.p, fp_col.p, fp_val.p,
+                                                                    tmp4b.p, rhs.p);
+                CK(cudaGetLastError());
+                if (cms_m > 0) {
+                    vk::k_tmv<T><<<cdiv((size_t)cms_m * 32, 256), 256, 0, stream>>>(nF, cms_m, cmsT.p, rhs.p, cms_y.p);
+                    vk::k_symv3<<<cdiv(cms_m, 128), 128, 0, stream>>>(cms_m, cmsKinv.p, cms_y.p, cms_z.p);
+                    vk::k_tv<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, cms_m, cmsT.p, cms_z.p, dx.p);
+                    CK(cudaGetLastError());
+                } else {
+                    CK(cudaMemsetAsync(dx.p, 0, sizeof(V4) * nF, stream));
+                }
+                if (sweeps > 0 && (rc = run_aj(kc, sweeps, agg, omega, cheb, rho))) return rc;
+                CK(cudaMemcpyAsync(tmp4a.p, dx.p, sizeof(V4) * nF, cudaMemcpyDeviceToDevice, stream));
+            }
+            if (nP) CK(cudaMemcpyAsync(tmp4a.p + nF, tmp4b.p, sizeof(V4) * nP, cudaMemcpyDeviceToDevice, stream));
+            std::vector<double> x3((size_t)3 * n);
+            if ((rc = download_nodes(tmp4a.p, x3.data()))) return rc;
+            for (int j = 0; j < n; ++j)
+                for (int c = 0; c < kc; ++c) X[(size_t)j * k + c0 + c] = x3[3 * (size_t)j + c];
+        }
+        return VKPD_OK;
+    }
+
     int apply_K(const double* hX, double* hY) override {
         int rc = upload_nodes(hX, tmp4a.p);
         if (rc) return rc;
@@ -873,6 +1048,25 @@ int vkpd_global_solve(vkpd_ctx* ctx, const double* B, const double* P, double* X
 int vkpd_apply_K(vkpd_ctx* ctx, const double* X, double* Y) {
     if (!X || !Y) return fail(VKPD_EINVAL, "null buffer");
     CTX_CALL(apply_K(X, Y));
+}
+int vkpd_a_jacobi_refine(vkpd_ctx* ctx, const double* Bf, const double* X0f, int k, int sweeps, int aggregation,
+                         double omega, int chebyshev, double rho, double* Xf, double* hist, int* n_hist,
+                         int* diverged) {
+    if (!Bf || !X0f || !Xf) return fail(VKPD_EINVAL, "null buffer");
+    CTX_CALL(aj_refine(Bf, X0f, k, sweeps, aggregation, omega, chebyshev, rho, Xf, hist, n_hist, diverged));
+}
+int vkpd_power_rho(vkpd_ctx* ctx, double omega, int iters, const double* v0, double* rho) {
+    if (!rho) return fail(VKPD_EINVAL, "null buffer");
+    CTX_CALL(power_rho(omega, iters, v0, rho));
+}
+int vkpd_cms_set_basis(vkpd_ctx* ctx, int m, const double* T, const double* Kred_inv) {
+    if (m > 0 && (!T || !Kred_inv)) return fail(VKPD_EINVAL, "null buffer");
+    CTX_CALL(cms_set_basis(m, T, Kred_inv));
+}
+int vkpd_cms_solve(vkpd_ctx* ctx, const double* B, const double* P, int k, int sweeps, int aggregation, double omega,
+                   int chebyshev, double rho, double* X) {
+    if (!B || !X) return fail(VKPD_EINVAL, "null buffer");
+    CTX_CALL(cms_solve(B, P, k, sweeps, aggregation, omega, chebyshev, rho, X));
 }
 int vkpd_get_stats(vkpd_ctx* ctx, vkpd_stats* st) {
     if (!st) return fail(VKPD_EINVAL, "null stats");

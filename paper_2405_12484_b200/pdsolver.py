@@ -32,6 +32,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _abi
+from .cms import CmsSubspace, a_jacobi_refine, build_cms, classify_nodes, partition_elements  # noqa: F401
 from .material import MaterialField
 
 log = logging.getLogger(__name__)
