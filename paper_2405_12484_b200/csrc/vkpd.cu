@@ -839,6 +839,7 @@ struct Ctx : CtxBase {
         double* out = rho_d.p;
         void* args[] = {&a, &iters, &out};
         CK(launch_coop(vk::k_power_rho<T>, args));
+        CK(cudaStreamSynchronize(stream));            // non-blocking stream: no implicit sync with cudaMemcpy
         double hr[3];
         CK(cudaMemcpy(hr, rho_d.p, sizeof hr, cudaMemcpyDeviceToHost));
         *rho = hr[0];
