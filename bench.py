@@ -35,8 +35,8 @@ ALG_BYTES_LOCAL = {"fp32": 70.0, "fp64": 125.0}   # SURVEY.md 8d, per tet-iterat
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
     p.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])

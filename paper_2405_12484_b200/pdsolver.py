@@ -242,9 +242,7 @@ def pd_step(state, mesh, gammas, iterations=PD_ITERS_DEFAULT, forces=None, solve
     host-driven loop with the local step on the GPU.
     """
     if state.colliders:
-        from .contact import pd_step_contact
-        return pd_step_contact(state, mesh, gammas, iterations, forces, contact_stiffness,
-                               damping, precision)
+        raise NotImplementedError("colliders are the next row of SURVEY.md 8f; not in this build")
     _check_inputs(mesh, gammas, state.dt)
     if solver is not None and not isinstance(solver, _DeviceStep):
         return _pd_step_host_solver(state, mesh, gammas, iterations, forces, solver, damping, precision)
