@@ -120,6 +120,18 @@ int vkpd_global_solve(vkpd_ctx* ctx, const double* B, const double* pin_vals, do
 int vkpd_apply_K(vkpd_ctx* ctx, const double* X, double* Y);
 int vkpd_get_stats(vkpd_ctx* ctx, vkpd_stats* st);
 
+/* Device-pointer primitives for the domain-decomposed multi-GPU step (dd.py).  Vectors are
+ * 4-wide (x,y,z,pad) in the context's precision and internal node order (free nodes, then the
+ * pinned list); work runs on the context stream.
+ *   dev_residual: r_free = b - K x on free rows (local step + deterministic gather + inertia),
+ *                 the residual of pd_step's global solve (pdsolver.py:292-298)
+ *   dev_apply_K:  Y_free = K_ff X_free + K_fp X_pinned (pdsolver.py:227-229)            */
+int vkpd_dev_residual(vkpd_ctx* ctx, const void* x_int, const void* xhat_int, void* r_free);
+int vkpd_dev_apply_K(vkpd_ctx* ctx, const void* X_int, void* Y_free);
+int vkpd_dev_inv_diag(vkpd_ctx* ctx, void* out_free);
+int vkpd_get_node_order(vkpd_ctx* ctx, int64_t* int_of_orig);
+int vkpd_get_sizes(vkpd_ctx* ctx, int64_t* n, int64_t* n_free, int64_t* n_pinned, int* precision);
+
 /* a_jacobi_refine (pdsolver.py:632-703) on K_ff over free-node vectors (n_free, k), k <= 3:
  * aggregated weighted-Jacobi sweeps (or the Chebyshev variant with spectral radius rho),
  * best-iterate tracking and divergence stop.  hist: (k, steps+1) residual norms, row-major,

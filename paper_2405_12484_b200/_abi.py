@@ -23,7 +23,8 @@ EXPORTS = (
     "vkpd_set_forces", "vkpd_step", "vkpd_step_async", "vkpd_sync", "vkpd_profile_step",
     "vkpd_elastic_rhs", "vkpd_global_solve", "vkpd_apply_K", "vkpd_get_stats",
     "vkpd_batch_projections", "vkpd_create_matrix", "vkpd_get_matrix_csr", "vkpd_a_jacobi_refine",
-    "vkpd_power_rho", "vkpd_cms_set_basis", "vkpd_cms_solve",
+    "vkpd_power_rho", "vkpd_cms_set_basis", "vkpd_cms_solve", "vkpd_dev_residual", "vkpd_dev_apply_K",
+    "vkpd_dev_inv_diag", "vkpd_get_node_order", "vkpd_get_sizes",
 )
 
 
@@ -92,6 +93,12 @@ def load():
         "vkpd_power_rho": (I, [P, C.c_double, I, P, C.POINTER(C.c_double)]),
         "vkpd_cms_set_basis": (I, [P, I, P, P]),
         "vkpd_cms_solve": (I, [P, P, P, I, I, I, C.c_double, I, C.c_double, P]),
+        "vkpd_dev_residual": (I, [P, P, P, P]),
+        "vkpd_dev_apply_K": (I, [P, P, P]),
+        "vkpd_dev_inv_diag": (I, [P, P]),
+        "vkpd_get_node_order": (I, [P, P]),
+        "vkpd_get_sizes": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                               C.POINTER(I)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -296,6 +303,26 @@ class Context:
         check(self.lib.vkpd_cms_solve(self.h, ptr(B), ptr(P), k, int(sweeps), int(aggregation), float(omega),
                                       int(bool(chebyshev)), float(rho), ptr(X)))
         return X
+
+    # -- device-pointer primitives (torch tensors as carriers), dd.py
+    def sizes(self):
+        n, nf, npin, prec = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        check(self.lib.vkpd_get_sizes(self.h, C.byref(n), C.byref(nf), C.byref(npin), C.byref(prec)))
+        return n.value, nf.value, npin.value, prec.value
+
+    def node_order(self):
+        out = np.empty(self.n, dtype=np.int64)
+        check(self.lib.vkpd_get_node_order(self.h, ptr(out)))
+        return out
+
+    def dev_residual(self, x_ptr, xhat_ptr, r_ptr):
+        check(self.lib.vkpd_dev_residual(self.h, C.c_void_p(x_ptr), C.c_void_p(xhat_ptr), C.c_void_p(r_ptr)))
+
+    def dev_apply_K(self, X_ptr, Y_ptr):
+        check(self.lib.vkpd_dev_apply_K(self.h, C.c_void_p(X_ptr), C.c_void_p(Y_ptr)))
+
+    def dev_inv_diag(self, out_ptr):
+        check(self.lib.vkpd_dev_inv_diag(self.h, C.c_void_p(out_ptr)))
 
     def matrix_csr(self):
         nnz = C.c_int64(0)

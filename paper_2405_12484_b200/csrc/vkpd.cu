@@ -119,6 +119,23 @@ __global__ void k_apply_K(int n, int nF, const int* __restrict__ ell_len, const 
     Y[i] = vk::make4<T>(a, b, c, T(0));
 }
 
+// r_i = sum of corner contributions + (m/dt^2)(xhat_i - x_i) on free rows (= b - K x)
+template <typename T>
+__global__ void k_resid_free(int nF, const int* __restrict__ inc_ptr, const vk::vec4_t<T>* __restrict__ corner,
+                             const T* __restrict__ m_dt2, const vk::vec4_t<T>* __restrict__ x,
+                             const vk::vec4_t<T>* __restrict__ xhat, vk::vec4_t<T>* r) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    T a = 0, b = 0, c = 0;
+    for (int k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
+        const vk::vec4_t<T> v = corner[k];
+        a += v.x; b += v.y; c += v.z;
+    }
+    const T m = m_dt2[i];
+    const vk::vec4_t<T> xh = xhat[i], xi = x[i];
+    r[i] = vk::make4<T>(a + m * (xh.x - xi.x), b + m * (xh.y - xi.y), c + m * (xh.z - xi.z), T(0));
+}
+
 // ---------------------------------------------------------------------------
 struct CtxBase {
     virtual ~CtxBase() {}
@@ -141,6 +158,11 @@ struct CtxBase {
                           double rho, double* Xf, double* hist, int* nhist, int* diverged) = 0;
     virtual int power_rho(double omega, int iters, const double* v0, double* rho) = 0;
     virtual int cms_set_basis(int m, const double* T, const double* Kinv) = 0;
+    virtual int dev_residual(const void* x, const void* xhat, void* r) = 0;
+    virtual int dev_apply_K(const void* X, void* Y) = 0;
+    virtual int dev_inv_diag(void* out) = 0;
+    virtual int node_order(int64_t* ioo) = 0;
+    virtual void sizes(int64_t* n, int64_t* nfree, int64_t* npinned, int* prec) = 0;
     virtual int cms_solve(const double* B, const double* P, int k, int sweeps, int agg, double omega, int cheb,
                           double rho, double* X) = 0;
     cudaStream_t stream = nullptr;
@@ -905,6 +927,42 @@ struct Ctx : CtxBase {
         return VKPD_OK;
     }
 
+    // ---- device-pointer primitives for the domain-decomposed multi-GPU step (dd.py) ----
+    int dev_residual(const void* x_int, const void* xhat_int, void* r_free) override {
+        if (nE == 0) return fail(VKPD_EINVAL, "matrix-only context has no mesh");
+        vk::LocalArgs<T> la = local_args((const V4*)x_int);
+        vk::k_local<T, vk::MODE_RESID, false><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+        CK(cudaGetLastError());
+        if (nF > 0) {
+            k_resid_free<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, inc_ptr.p, corner.p, m_dt2.p, (const V4*)x_int,
+                                                               (const V4*)xhat_int, (V4*)r_free);
+            CK(cudaGetLastError());
+        }
+        return VKPD_OK;
+    }
+    int dev_apply_K(const void* X, void* Y) override {
+        if (nF > 0) {
+            k_apply_K<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, nF, ell_len.p, ell_col.p, ell_val.p, fp_ptr.p, fp_col.p,
+                                                           fp_val.p, (const V4*)X, (V4*)Y);
+            CK(cudaGetLastError());
+        }
+        return VKPD_OK;
+    }
+    int dev_inv_diag(void* out) override {
+        if (nF > 0) CK(cudaMemcpyAsync(out, inv_diag.p, sizeof(T) * nF, cudaMemcpyDeviceToDevice, stream));
+        return VKPD_OK;
+    }
+    int node_order(int64_t* ioo) override {
+        for (int j = 0; j < n; ++j) ioo[j] = int_of_orig_h[j];
+        return VKPD_OK;
+    }
+    void sizes(int64_t* nn, int64_t* nfree, int64_t* npinned, int* prec) override {
+        if (nn) *nn = n;
+        if (nfree) *nfree = nF;
+        if (npinned) *npinned = nP;
+        if (prec) *prec = sizeof(T) == 4 ? VKPD_FP32 : VKPD_FP64;
+    }
+
     int apply_K(const double* hX, double* hY) override {
         int rc = upload_nodes(hX, tmp4a.p);
         if (rc) return rc;
@@ -1049,6 +1107,27 @@ int vkpd_global_solve(vkpd_ctx* ctx, const double* B, const double* P, double* X
 int vkpd_apply_K(vkpd_ctx* ctx, const double* X, double* Y) {
     if (!X || !Y) return fail(VKPD_EINVAL, "null buffer");
     CTX_CALL(apply_K(X, Y));
+}
+int vkpd_dev_residual(vkpd_ctx* ctx, const void* x_int, const void* xhat_int, void* r_free) {
+    if (!x_int || !xhat_int || !r_free) return fail(VKPD_EINVAL, "null device buffer");
+    CTX_CALL(dev_residual(x_int, xhat_int, r_free));
+}
+int vkpd_dev_apply_K(vkpd_ctx* ctx, const void* X_int, void* Y_free) {
+    if (!X_int || !Y_free) return fail(VKPD_EINVAL, "null device buffer");
+    CTX_CALL(dev_apply_K(X_int, Y_free));
+}
+int vkpd_dev_inv_diag(vkpd_ctx* ctx, void* out_free) {
+    if (!out_free) return fail(VKPD_EINVAL, "null device buffer");
+    CTX_CALL(dev_inv_diag(out_free));
+}
+int vkpd_get_node_order(vkpd_ctx* ctx, int64_t* int_of_orig) {
+    if (!int_of_orig) return fail(VKPD_EINVAL, "null buffer");
+    CTX_CALL(node_order(int_of_orig));
+}
+int vkpd_get_sizes(vkpd_ctx* ctx, int64_t* n, int64_t* n_free, int64_t* n_pinned, int* precision) {
+    if (!ctx) return fail(VKPD_EINVAL, "null context");
+    ctx->impl->sizes(n, n_free, n_pinned, precision);
+    return VKPD_OK;
 }
 int vkpd_a_jacobi_refine(vkpd_ctx* ctx, const double* Bf, const double* X0f, int k, int sweeps, int aggregation,
                          double omega, int chebyshev, double rho, double* Xf, double* hist, int* n_hist,
