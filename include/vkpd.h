@@ -81,6 +81,8 @@ typedef struct {
     int pcg_blocks;
     int ell_width;
     int64_t n_free;
+    double local_ms[256];      /* per-PD-iteration event times of the last vkpd_profile_step */
+    double global_ms[256];
 } vkpd_stats;
 
 const char* vkpd_last_error(void);

@@ -50,9 +50,19 @@ __device__ __forceinline__ void count_path(ProjStats* st, int path) {
 template <typename T>
 __device__ __forceinline__ int project_element(const T (&F)[3][3], T (&U)[3][3], T (&W)[3][3],
                                                T (&sig)[3], double (&s)[3]) {
+#ifdef VK_EXP_NO_SVD          // cost-attribution experiments only (never in the product build)
+    for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) { U[i][j] = W[i][j] = (i == j); }
+    sig[0] = F[0][0]; sig[1] = F[1][1]; sig[2] = F[2][2];
+#else
     svd3_rv(F, U, sig, W);
+#endif
     const double sd[3] = {(double)sig[0], (double)sig[1], (double)sig[2]};
+#ifdef VK_EXP_NO_SL3
+    s[0] = sd[0]; s[1] = sd[1]; s[2] = sd[2];
+    return 0;
+#else
     return sl3::project(sd, s);
+#endif
 }
 
 // out = U diag(d) W^T

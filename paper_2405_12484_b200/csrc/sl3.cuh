@@ -75,44 +75,57 @@ VK_HD bool gesv4(double (&A)[4][4], double (&b)[4]) {
     return true;
 }
 
-// One element of `_sl3_batch_newton` (material.py:309-340): unclamped KKT
-// Newton on (s, lam) from start s; returns ok.
-VK_HD bool kkt_newton(const double (&sig)[3], double (&s)[3], double& lam) {
-    double p[3];
-    pairprod(s, p);
-    const double denom = fmax(p[0] * p[0] + p[1] * p[1] + p[2] * p[2], 1e-300);
-    lam = (s[0] * s[1] * s[2] - 1.0) / denom;
-    for (int it = 0; it < kIters; ++it) {
-        pairprod(s, p);
-        double r[4];
-        for (int i = 0; i < 3; ++i) r[i] = s[i] - sig[i] + lam * p[i];
-        r[3] = s[0] * s[1] * s[2] - 1.0;
-        double rn = 0.0;
-        for (int i = 0; i < 4; ++i) rn = nanmax(rn, fabs(r[i]));
+// One KKT Newton update on (s, lam) in precision R (material.py:322-335):
+// bordered solve of [[A, p], [p^T, 0]] [ds; dl] = -[r; r4] with
+// A = I + lam * offdiag(s2, s1, s0) through the adjugate of A.  Returns
+// false when A is near singular (the caller then uses the pivoted 4x4
+// elimination in float64, or gives the step to the float64 phase).
+template <typename R>
+VK_HD bool kkt_bordered_step(const R (&r)[4], const R (&p)[3], R (&s)[3], R& lam) {
+    const R a = lam * s[2], b = lam * s[1], c = lam * s[0];
+    const R c00 = R(1) - c * c, c11 = R(1) - b * b, c22 = R(1) - a * a;
+    const R c01 = b * c - a, c02 = a * c - b, c12 = a * b - c;
+    const R det = c00 + a * c01 + b * c02;
+    const R ar0 = c00 * r[0] + c01 * r[1] + c02 * r[2];
+    const R ar1 = c01 * r[0] + c11 * r[1] + c12 * r[2];
+    const R ar2 = c02 * r[0] + c12 * r[1] + c22 * r[2];
+    const R ap0 = c00 * p[0] + c01 * p[1] + c02 * p[2];
+    const R ap1 = c01 * p[0] + c11 * p[1] + c12 * p[2];
+    const R ap2 = c02 * p[0] + c12 * p[1] + c22 * p[2];
+    const R pap = p[0] * ap0 + p[1] * ap1 + p[2] * ap2;
+    const R par = p[0] * ar0 + p[1] * ar1 + p[2] * ar2;
+    if (!(fabs(det) > R(1e-6) && fabs(pap) > R(1e-12) * fabs(det) * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2])))
+        return false;
+    const R dl = (r[3] * det - par) / pap;
+    const R idet = R(1) / det;
+    s[0] -= (ar0 + ap0 * dl) * idet;
+    s[1] -= (ar1 + ap1 * dl) * idet;
+    s[2] -= (ar2 + ap2 * dl) * idet;
+    lam += dl;
+    return true;
+}
+
+template <typename R>
+VK_HD R kkt_residual(const R (&sig)[3], const R (&s)[3], R lam, R (&r)[4], R (&p)[3]) {
+    p[0] = s[1] * s[2];
+    p[1] = s[0] * s[2];
+    p[2] = s[0] * s[1];
+    for (int i = 0; i < 3; ++i) r[i] = s[i] - sig[i] + lam * p[i];
+    r[3] = s[0] * s[1] * s[2] - R(1);
+    R rn = R(0);
+    for (int i = 0; i < 4; ++i) rn = (fabs(r[i]) > rn || r[i] != r[i]) ? fabs(r[i]) : rn;
+    return rn;
+}
+
+// float64 Newton loop of `_sl3_batch_newton` from (s, lam) with an iteration
+// budget; returns the reference's ok flag (material.py:336-340).
+VK_HD bool kkt_newton_f64(const double (&sig)[3], double (&s)[3], double& lam, int budget) {
+    double r[4], p[3];
+    for (int it = 0; it < budget; ++it) {
+        const double rn = kkt_residual(sig, s, lam, r, p);
         if (rn < kTol) break;
-        // Bordered solve of [[A, p], [p^T, 0]] [ds; dl] = -[r; r4] with
-        // A = I + lam * offdiag(s2, s1, s0) through the adjugate of A; the
-        // pivoted 4x4 elimination takes over when A is near singular.
-        const double a = lam * s[2], b = lam * s[1], c = lam * s[0];
-        const double c00 = 1.0 - c * c, c11 = 1.0 - b * b, c22 = 1.0 - a * a;
-        const double c01 = b * c - a, c02 = a * c - b, c12 = a * b - c;
-        const double det = c00 + a * c01 + b * c02;
-        const double ar0 = c00 * r[0] + c01 * r[1] + c02 * r[2];
-        const double ar1 = c01 * r[0] + c11 * r[1] + c12 * r[2];
-        const double ar2 = c02 * r[0] + c12 * r[1] + c22 * r[2];
-        const double ap0 = c00 * p[0] + c01 * p[1] + c02 * p[2];
-        const double ap1 = c01 * p[0] + c11 * p[1] + c12 * p[2];
-        const double ap2 = c02 * p[0] + c12 * p[1] + c22 * p[2];
-        const double pap = p[0] * ap0 + p[1] * ap1 + p[2] * ap2;
-        const double par = p[0] * ar0 + p[1] * ar1 + p[2] * ar2;
-        if (fabs(det) > 1e-6 && fabs(pap) > 1e-12 * fabs(det) * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2])) {
-            const double dl = (r[3] * det - par) / pap;
-            const double idet = 1.0 / det;
-            s[0] -= (ar0 + ap0 * dl) * idet;
-            s[1] -= (ar1 + ap1 * dl) * idet;
-            s[2] -= (ar2 + ap2 * dl) * idet;
-            lam += dl;
-        } else {
+        if (!kkt_bordered_step(r, p, s, lam)) {
+            const double a = lam * s[2], b = lam * s[1], c = lam * s[0];
             double J[4][4] = {{1.0, a, b, p[0]}, {a, 1.0, c, p[1]}, {b, c, 1.0, p[2]}, {p[0], p[1], p[2], 0.0}};
             double d[4] = {-r[0], -r[1], -r[2], -r[3]};
             if (!gesv4(J, d)) return false;
@@ -126,6 +139,17 @@ VK_HD bool kkt_newton(const double (&sig)[3], double (&s)[3], double& lam) {
     const double rc = fabs(s[0] * s[1] * s[2] - 1.0);
     const bool fin = isfinite(s[0]) && isfinite(s[1]) && isfinite(s[2]);
     return (nanmax(r3, rc) < 1e-10) && fin;
+}
+
+// One element of `_sl3_batch_newton` (material.py:309-340): unclamped KKT
+// Newton on (s, lam) from start s (lam0 = (prod s - 1)/|p|^2); returns ok.
+// (A float32-first variant was measured: no gain, the loop is latency-bound.)
+VK_HD bool kkt_newton(const double (&sig)[3], double (&s)[3], double& lam) {
+    double p[3];
+    pairprod(s, p);
+    const double denom = fmax(p[0] * p[0] + p[1] * p[1] + p[2] * p[2], 1e-300);
+    lam = (s[0] * s[1] * s[2] - 1.0) / denom;
+    return kkt_newton_f64(sig, s, lam, kIters);
 }
 
 VK_HD double sq3(const double (&a)[3], const double (&b)[3]) {

@@ -52,7 +52,7 @@ struct DBuf {
 };
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
-constexpr int kPcgThreads = 256;
+int kPcgThreads = 512;          // CTA size of the persistent solver (env VKPD_PCG_THREADS; 512 measured best)
 
 // ---------------------------------------------------------------------------
 // layout conversion kernels: host (nV,3) float64 in caller order <-> device vec4 internal order
@@ -190,12 +190,15 @@ struct Ctx : CtxBase {
     DBuf<double> diag64;
     // state
     DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
+    DBuf<V4> m1, qq, ss, pp;             // pipelined-CG recurrences
+    bool pcg_classic = false;
     DBuf<double> partials, scal, stage;
     DBuf<vk::GridBar> bar;
     DBuf<int> iters, fail_iter;
     DBuf<vk::ProjStats> pstats;
     int* h_fail = nullptr;
     int last_iterations = 0;
+    std::vector<double> prof_local, prof_global;
 
     // graph cache
     cudaGraphExec_t graph_exec = nullptr;
@@ -371,12 +374,17 @@ struct Ctx : CtxBase {
         CK(pin_tgt.alloc(std::max(1, nP)));
         CK(cudaMemsetAsync(pin_tgt.p, 0, std::max(1, nP) * sizeof(V4), s));
         CK(corner.alloc((size_t)4 * nE));
-        for (DBuf<V4>* b : {&r, &z, &p0, &p1, &q, &dx, &rhs}) {
+        for (DBuf<V4>* b : {&r, &z, &p0, &p1, &q, &dx, &rhs, &m1, &qq, &ss, &pp}) {
             CK(b->alloc(std::max(1, nF)));
             CK(cudaMemsetAsync(b->p, 0, std::max(1, nF) * sizeof(V4), s));
         }
-        int occ = 0;
+        if (const char* pt = getenv("VKPD_PCG_THREADS")) kPcgThreads = std::max(64, std::min(1024, atoi(pt)));
+        const char* pv = getenv("VKPD_PCG");
+        pcg_classic = !(pv && std::string(pv) == "pipe");   // classic measured faster at C3
+        int occ = 0, occ2 = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_pcg<T>, kPcgThreads, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, vk::k_pcg_classic<T>, kPcgThreads, 0));
+        occ = std::min(occ, occ2);
         if (occ < 1) return fail(VKPD_ECUDA, "persistent solver kernel cannot be resident");
         // default: one row per thread, capped by co-residency
         pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : cdiv(std::max(1, nF), kPcgThreads);
@@ -569,6 +577,7 @@ struct Ctx : CtxBase {
         pa.inc_ptr = inc_ptr.p; pa.inc_code = inc_code.p; pa.corner = corner.p; pa.m_dt2 = m_dt2.p;
         pa.xhat = xhat.p; pa.rhs = rhs.p; pa.x = x.p; pa.r = r.p; pa.z = z.p; pa.p0 = p0.p; pa.p1 = p1.p;
         pa.q = q.p; pa.dx = dx.p; pa.partials = partials.p; pa.scal = scal.p; pa.bar = bar.p;
+        pa.m1 = m1.p; pa.qq = qq.p; pa.ss = ss.p; pa.pp = pp.p;
         pa.iters_out = iters_slot; pa.fail_iter = fail_iter.p; pa.pd_iter = pd_iter; pa.tol = tol;
         pa.max_iters = max_iters; pa.init = init;
         return pa;
@@ -584,6 +593,7 @@ struct Ctx : CtxBase {
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        if (pcg_classic) return cudaLaunchKernelEx(&cfg, vk::k_pcg_classic<T>, pa);
         return cudaLaunchKernelEx(&cfg, vk::k_pcg<T>, pa);
     }
 
@@ -675,11 +685,15 @@ struct Ctx : CtxBase {
         CK(cudaEventRecord(ev[3 * iterations + 1], stream));
         CK(cudaStreamSynchronize(stream));
         double lsum = 0, gsum = 0;
+        prof_local.assign(iterations, 0.0);
+        prof_global.assign(iterations, 0.0);
         for (int it = 0; it < iterations; ++it) {
             float a = 0, b = 0;
             CK(cudaEventElapsedTime(&a, ev[3 * it], ev[3 * it + 1]));
             CK(cudaEventElapsedTime(&b, ev[3 * it + 1], ev[3 * it + 2]));
             lsum += a; gsum += b;
+            prof_local[it] = a;
+            prof_global[it] = b;
         }
         float fr = 0;
         CK(cudaEventElapsedTime(&fr, ev[3 * iterations], ev[3 * iterations + 1]));
@@ -986,6 +1000,10 @@ struct Ctx : CtxBase {
         st->pcg_blocks = pcg_blocks;
         st->ell_width = ell_w;
         st->n_free = nF;
+        for (size_t i = 0; i < prof_local.size() && i < 256; ++i) {
+            st->local_ms[i] = prof_local[i];
+            st->global_ms[i] = prof_global[i];
+        }
         return VKPD_OK;
     }
 };
