@@ -47,9 +47,11 @@ __device__ __forceinline__ void count_path(ProjStats* st, int path) {
 }
 
 // F -> (U, d, W) with P = U diag(d_i) W^T for d_i = a + b * s_i.  Returns path id.
+// pass: 0 = full per-element logic inline, 1 = defer suspicious elements
+// (returns 3), 2 = robust scalar path only (for elements known suspicious).
 template <typename T>
 __device__ __forceinline__ int project_element(const T (&F)[3][3], T (&U)[3][3], T (&W)[3][3],
-                                               T (&sig)[3], double (&s)[3]) {
+                                               T (&sig)[3], double (&s)[3], int pass = 0) {
 #ifdef VK_EXP_NO_SVD          // cost-attribution experiments only (never in the product build)
     for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) { U[i][j] = W[i][j] = (i == j); }
     sig[0] = F[0][0]; sig[1] = F[1][1]; sig[2] = F[2][2];
@@ -61,7 +63,8 @@ __device__ __forceinline__ int project_element(const T (&F)[3][3], T (&U)[3][3],
     s[0] = sd[0]; s[1] = sd[1]; s[2] = sd[2];
     return 0;
 #else
-    return sl3::project(sd, s);
+    if (pass == 2) return sl3::project_robust(sd, s) ? 1 : 2;
+    return sl3::project(sd, s, pass == 1);
 #endif
 }
 
@@ -85,41 +88,75 @@ struct LocalArgs {
     const int4* slot4;           // position of (e, corner a) in its node's incidence run
     vec4_t<T>* corner;           // per-incidence contributions, node-sorted (tet order within a node)
     ProjStats* stats;
+    int* robust_list;            // optional: suspicious elements are queued here (k_robust finishes them)
+    int* robust_count;
     double* F_out;               // optional (nE,3,3) (RHS mode only)
     double* R_out;
     double* V_out;
 };
 
-template <typename T, int MODE, bool WITH_FRV>
-__global__ void __launch_bounds__(128, VK_LOCAL_MINB) k_local(LocalArgs<T> a) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= a.nE) return;
+// One tet of the local step.  COH selects coherent loads of x: required when
+// x was written earlier in the same launch (the fused frame kernel).
+// Load one tet: shape-gradient rows g, weights (2V gs, 2V gv) and F = Ds Dm^-1.
+template <typename T, bool COH>
+__device__ __forceinline__ void load_tet(const LocalArgs<T>& a, int e, T (&g)[3][3], T& ws, T& wv, T (&F)[3][3]) {
     const int nE = a.nE;
     const int4 t = __ldg(&a.tets[e]);
-    T g[3][3];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) g[k / 3][k % 3] = a.G[(size_t)k * nE + e];
-    const T ws = a.w[e], wv = a.w[(size_t)nE + e];
-    const vec4_t<T> x0 = ldg4(&a.x[t.x]);
-    const vec4_t<T> x1 = ldg4(&a.x[t.y]);
-    const vec4_t<T> x2 = ldg4(&a.x[t.z]);
-    const vec4_t<T> x3 = ldg4(&a.x[t.w]);
+    for (int k = 0; k < 9; ++k) g[k / 3][k % 3] = __ldg(&a.G[(size_t)k * nE + e]);
+    ws = __ldg(&a.w[e]);
+    wv = __ldg(&a.w[(size_t)nE + e]);
+    const vec4_t<T> x0 = COH ? ld4(&a.x[t.x]) : ldg4(&a.x[t.x]);
+    const vec4_t<T> x1 = COH ? ld4(&a.x[t.y]) : ldg4(&a.x[t.y]);
+    const vec4_t<T> x2 = COH ? ld4(&a.x[t.z]) : ldg4(&a.x[t.z]);
+    const vec4_t<T> x3 = COH ? ld4(&a.x[t.w]) : ldg4(&a.x[t.w]);
     // edges x_n - x_0 (n = 1..3) as rows e[n-1][:]
     const T ed[3][3] = {{x1.x - x0.x, x1.y - x0.y, x1.z - x0.z},
                         {x2.x - x0.x, x2.y - x0.y, x2.z - x0.z},
                         {x3.x - x0.x, x3.y - x0.y, x3.z - x0.z}};
-    T F[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
             F[i][j] = ed[0][i] * g[0][j] + ed[1][i] * g[1][j] + ed[2][i] * g[2][j];
+}
 
+template <typename T, int MODE, bool WITH_FRV>
+__device__ __forceinline__ void finish_tet(const LocalArgs<T>& a, int e, const T (&g)[3][3], T ws, T wv,
+                                           const T (&F)[3][3], const T (&U)[3][3], const T (&W)[3][3],
+                                           const double (&s)[3]);
+
+template <typename T, int MODE, bool WITH_FRV, bool COH, int PASS = 0>
+__device__ __forceinline__ void local_tet(const LocalArgs<T>& a, int e) {
+    T g[3][3], F[3][3], ws, wv;
+    load_tet<T, COH>(a, e, g, ws, wv, F);
     T U[3][3], W[3][3], sig[3];
     double s[3];
-    const int path = project_element(F, U, W, sig, s);
-    count_path(a.stats, path);
+    const int path = project_element(F, U, W, sig, s, PASS);
+    if (PASS == 1) {
+        // queue suspicious elements (warp-aggregated); their corners are written by k_robust
+        const unsigned int am = __activemask();
+        const unsigned int m3 = __ballot_sync(am, path == 3);
+        if (m3) {
+            const int lane = threadIdx.x & 31;
+            const int lead = __ffs(m3) - 1;
+            int base = 0;
+            if (lane == lead) base = atomicAdd(a.robust_count, __popc(m3));
+            base = __shfl_sync(m3, base, lead);
+            if (path == 3) a.robust_list[base + __popc(m3 & ((1u << lane) - 1u))] = e;
+        }
+        if (path == 3) return;
+    }
+    if (PASS != 1) count_path(a.stats, path);
+    finish_tet<T, MODE, WITH_FRV>(a, e, g, ws, wv, F, U, W, s);
+}
 
+// P = U diag(ws + wv s) W^T (minus (ws+wv) F in residual mode), optional
+// (F, R, V) outputs, and the four corner contributions 2V P g_n.
+template <typename T, int MODE, bool WITH_FRV>
+__device__ __forceinline__ void finish_tet(const LocalArgs<T>& a, int e, const T (&g)[3][3], T ws, T wv,
+                                           const T (&F)[3][3], const T (&U)[3][3], const T (&W)[3][3],
+                                           const double (&s)[3]) {
     const T d[3] = {ws + wv * (T)s[0], ws + wv * (T)s[1], ws + wv * (T)s[2]};
     T P[3][3];
     udw(U, d, W, P);
@@ -157,6 +194,72 @@ __global__ void __launch_bounds__(128, VK_LOCAL_MINB) k_local(LocalArgs<T> a) {
     st4(&a.corner[sl.y], make4<T>(f[0][0], f[0][1], f[0][2], T(0)));
     st4(&a.corner[sl.z], make4<T>(f[1][0], f[1][1], f[1][2], T(0)));
     st4(&a.corner[sl.w], make4<T>(f[2][0], f[2][1], f[2][2], T(0)));
+}
+
+template <typename T, int MODE, bool WITH_FRV, int PASS = 0>
+__global__ void __launch_bounds__(128, VK_LOCAL_MINB) k_local(LocalArgs<T> a) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= a.nE) return;
+    local_tet<T, MODE, WITH_FRV, false, PASS>(a, e);
+}
+
+// Dense second pass over the queued suspicious elements: the robust
+// multi-start scalar projection (material.py:242-287) for each, then the same
+// corner contributions.  Queue order does not matter (each element writes
+// only its own corner slots), so results are deterministic.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128) k_robust(LocalArgs<T> a) {
+    const int cnt = *a.robust_count;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+        local_tet<T, MODE, false, false, 2>(a, a.robust_list[i]);
+}
+
+// Same pass, but the (up to four) Newton starts of each element's robust
+// projection run on the four lanes of a quad in parallel -- the scalar path
+// is a long serial chain (starts x clamp rounds x Newton x line search), so
+// this cuts the pass latency ~4x.  The quad leader then selects the winner
+// exactly as the reference's sequential loop does (material.py:264-280: in
+// start order, replace only when strictly better by 1e-15).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128) k_robust4(LocalArgs<T> a) {
+    const int cnt = *a.robust_count;
+    const int lane = threadIdx.x & 31, q = lane & 3;
+    const unsigned int qmask = 0xFu << (lane & ~3);
+    const int gq = (blockIdx.x * blockDim.x + threadIdx.x) >> 2;
+    const int nq = (gridDim.x * blockDim.x) >> 2;
+    for (int i = gq; i < cnt; i += nq) {
+        const int e = a.robust_list[i];
+        T g[3][3], F[3][3], ws, wv, U[3][3], W[3][3], sig[3];
+        load_tet<T, false>(a, e, g, ws, wv, F);
+        svd3_rv(F, U, sig, W);
+        const double sd[3] = {(double)sig[0], (double)sig[1], (double)sig[2]};
+        double st[3], sk[3] = {0, 0, 0}, obj = 0.0;
+        const bool use = sl3::robust_start(sd, q, st);
+        const bool ok = use && sl3::robust_try(sd, st, sk, obj);
+        bool have = false;
+        double best = 0.0, s[3] = {0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int src = (lane & ~3) + k;
+            const bool okk = __shfl_sync(qmask, ok, src);
+            const double ob = __shfl_sync(qmask, obj, src);
+            const double s0 = __shfl_sync(qmask, sk[0], src);
+            const double s1 = __shfl_sync(qmask, sk[1], src);
+            const double s2 = __shfl_sync(qmask, sk[2], src);
+            if (okk && (!have || ob < best - 1e-15)) {
+                have = true;
+                best = ob;
+                s[0] = s0; s[1] = s1; s[2] = s2;
+            }
+        }
+        if (q != 0) continue;
+        if (!have) sl3::robust_fallback(sd, s);
+        if (a.stats) {
+            atomicAdd(&a.stats->robust, 1u);
+            if (!have) atomicAdd(&a.stats->fallback, 1u);
+        }
+        finish_tet<T, MODE, false>(a, e, g, ws, wv, F, U, W, s);
+    }
 }
 
 // Stateless projections of a batch of F (material.py:395-407): (R, V).

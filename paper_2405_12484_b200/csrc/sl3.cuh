@@ -182,7 +182,7 @@ VK_HD double free_resnorm(const double (&sig)[3], const double (&s)[3], double l
 // `_sl3_newton_free` (material.py:171-214).  The reduced (nf+1) system is
 // solved embedded in the 4x4 one: frozen entries get an identity row/column
 // and a zero right-hand side, so their update is exactly zero.
-VK_HDNI bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, const bool (&fr)[3]) {
+VK_HD bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, const bool (&fr)[3]) {
     const int nf = (int)fr[0] + (int)fr[1] + (int)fr[2];
     if (nf == 0) return false;
     for (int it = 0; it < kIters; ++it) {
@@ -190,21 +190,58 @@ VK_HDNI bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, co
         if (rn < kTol) return true;
         double p[3];
         pairprod(s, p);
-        double J[4][4], d[4];
+        double d[4];
+        {
+            // masked bordered system: frozen entries get identity rows/cols, zero p and rhs;
+            // solved through the adjugate (kkt_bordered_step), pivoted elimination if A is near singular
+            double rr[4], pm[3], sd[3] = {0.0, 0.0, 0.0}, ld = 0.0;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const double v = (i == j) ? 1.0 : lam * s[3 - i - j];
-                J[i][j] = (fr[i] && fr[j]) ? v : (i == j ? 1.0 : 0.0);
+            for (int i = 0; i < 3; ++i) {
+                pm[i] = fr[i] ? p[i] : 0.0;
+                rr[i] = fr[i] ? (s[i] - sig[i] + lam * p[i]) : 0.0;
             }
-            J[i][3] = fr[i] ? p[i] : 0.0;
-            J[3][i] = fr[i] ? p[i] : 0.0;
-            d[i] = fr[i] ? -(s[i] - sig[i] + lam * p[i]) : 0.0;
+            rr[3] = s[0] * s[1] * s[2] - 1.0;
+            const double a = (fr[0] && fr[1]) ? lam * s[2] : 0.0;
+            const double b = (fr[0] && fr[2]) ? lam * s[1] : 0.0;
+            const double c = (fr[1] && fr[2]) ? lam * s[0] : 0.0;
+            const double c00 = 1.0 - c * c, c11 = 1.0 - b * b, c22 = 1.0 - a * a;
+            const double c01 = b * c - a, c02 = a * c - b, c12 = a * b - c;
+            const double det = c00 + a * c01 + b * c02;
+            const double ar0 = c00 * rr[0] + c01 * rr[1] + c02 * rr[2];
+            const double ar1 = c01 * rr[0] + c11 * rr[1] + c12 * rr[2];
+            const double ar2 = c02 * rr[0] + c12 * rr[1] + c22 * rr[2];
+            const double ap0 = c00 * pm[0] + c01 * pm[1] + c02 * pm[2];
+            const double ap1 = c01 * pm[0] + c11 * pm[1] + c12 * pm[2];
+            const double ap2 = c02 * pm[0] + c12 * pm[1] + c22 * pm[2];
+            const double pap = pm[0] * ap0 + pm[1] * ap1 + pm[2] * ap2;
+            const double par = pm[0] * ar0 + pm[1] * ar1 + pm[2] * ar2;
+            const double pp = pm[0] * pm[0] + pm[1] * pm[1] + pm[2] * pm[2];
+            if (fabs(det) > 1e-6 && fabs(pap) > 1e-12 * fabs(det) * pp) {
+                ld = (rr[3] * det - par) / pap;
+                const double idet = 1.0 / det;
+                sd[0] = -(ar0 + ap0 * ld) * idet;
+                sd[1] = -(ar1 + ap1 * ld) * idet;
+                sd[2] = -(ar2 + ap2 * ld) * idet;
+                d[0] = fr[0] ? sd[0] : 0.0; d[1] = fr[1] ? sd[1] : 0.0; d[2] = fr[2] ? sd[2] : 0.0;
+                d[3] = ld;
+            } else {
+                double J[4][4];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        const double v = (i == j) ? 1.0 : lam * s[3 - i - j];
+                        J[i][j] = (fr[i] && fr[j]) ? v : (i == j ? 1.0 : 0.0);
+                    }
+                    J[i][3] = pm[i];
+                    J[3][i] = pm[i];
+                    d[i] = -rr[i];
+                }
+                J[3][3] = 0.0;
+                d[3] = -rr[3];
+                if (!gesv4(J, d)) return false;
+            }
         }
-        J[3][3] = 0.0;
-        d[3] = -(s[0] * s[1] * s[2] - 1.0);
-        if (!gesv4(J, d)) return false;
         double step = 1.0;
         double sn[3] = {s[0], s[1], s[2]}, ln = lam;
         for (int t = 0; t < 6; ++t) {
@@ -222,7 +259,7 @@ VK_HDNI bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, co
 }
 
 // `_sl3_solve_clamping` (material.py:217-239); returns false for "None"
-VK_HDNI bool solve_clamping(const double (&sig)[3], double (&s)[3], double& lam) {
+VK_HD bool solve_clamping(const double (&sig)[3], double (&s)[3], double& lam) {
     bool fr[3] = {true, true, true};
     for (int round = 0; round < 3; ++round) {
         for (int i = 0; i < 3; ++i) if (!fr[i]) s[i] = kFloor;
@@ -245,7 +282,59 @@ VK_HDNI bool solve_clamping(const double (&sig)[3], double (&s)[3], double& lam)
 }
 
 // `sl3_sigma_project` (material.py:242-287); returns ok (false = uniform-scaling fallback)
-VK_HDNI bool project_robust(const double (&sig)[3], double (&out)[3]) {
+// Start k (0..3) of the multi-start list (material.py:251-263); false if the
+// reference would not use start k for this sigma.
+VK_HD bool robust_start(const double (&sig)[3], int k, double (&st)[3]) {
+    const double prod = sig[0] * sig[1] * sig[2];
+    int idx = 0;
+    for (int i = 0; i < 3; ++i) st[i] = fmax(sig[i], kFloor);
+    if (k == idx++) return true;
+    st[0] = st[1] = st[2] = 1.0;
+    if (k == idx++) return true;
+    if (prod > 1e-12) {
+        const double c = cbrt(prod);
+        for (int i = 0; i < 3; ++i) st[i] = fmax(sig[i] / c, kFloor);
+        if (k == idx++) return true;
+    }
+    if (prod > 1.0) {
+        const int j = argmin3(sig);
+        double others = 1.0;
+        for (int i = 0; i < 3; ++i) if (i != j) others *= sig[i];
+        if (others > 1e-12) {
+            for (int i = 0; i < 3; ++i) st[i] = fmax(sig[i], kFloor);
+            st[j] = fmax(1.0 / others, kFloor);
+            if (k == idx++) return true;
+        }
+    }
+    return false;
+}
+
+// One start of `sl3_sigma_project` (material.py:265-277): clamped Newton and the
+// acceptance test; returns true with (s, obj) when the start is admissible.
+VK_HD bool robust_try(const double (&sig)[3], const double (&st)[3], double (&s)[3], double& obj) {
+    s[0] = st[0]; s[1] = st[1]; s[2] = st[2];
+    double p[3];
+    pairprod(s, p);
+    const double den = p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
+    double lam = den > 1e-300 ? (s[0] * s[1] * s[2] - 1.0) / den : 0.0;
+    if (!solve_clamping(sig, s, lam)) return false;
+    if (nanmin3(s) < kFloor - 1e-9 || fabs(s[0] * s[1] * s[2] - 1.0) > 1e-8) return false;
+    obj = sq3(s, sig);
+    return true;
+}
+
+// Uniform-scaling fallback with its warning (material.py:281-287).
+VK_HD void robust_fallback(const double (&sig)[3], double (&out)[3]) {
+    double s[3];
+    for (int i = 0; i < 3; ++i) s[i] = fmax(fabs(sig[i]), kFloor);
+    for (int r = 0; r < 3; ++r) {
+        const double c = cbrt(s[0] * s[1] * s[2]);
+        for (int i = 0; i < 3; ++i) s[i] = fmax(s[i] / c, kFloor);
+    }
+    out[0] = s[0]; out[1] = s[1]; out[2] = s[2];
+}
+
+VK_HD bool project_robust(const double (&sig)[3], double (&out)[3]) {
     double starts[4][3];
     int ns = 0;
     for (int i = 0; i < 3; ++i) starts[0][i] = fmax(sig[i], kFloor);
@@ -298,7 +387,21 @@ VK_HDNI bool project_robust(const double (&sig)[3], double (&out)[3]) {
 // Per-element `sl3_sigma_project_batch` (material.py:343-392).
 // Returns 0 = batch Newton result, 1 = robust path, 2 = robust path fell back
 // to uniform scaling (the reference logs a warning).
-VK_HD int project(const double (&sig)[3], double (&s)[3]) {
+// defer = true: a "suspicious" element returns 3 without running the robust
+// scalar path; the caller queues it for a separate dense pass (no warp
+// divergence between the cheap batch path and the expensive robust one).
+VK_HD int project(const double (&sig)[3], double (&s)[3], bool defer = false) {
+    // Elements outside [0.2, 5] are "suspicious" whatever the batch Newton
+    // returns, and the reference overwrites their batch result with the robust
+    // scalar solve (material.py:377-391) -- so the batch solves are skipped.
+    {
+        const double mn = nanmin3(sig);
+        const double mx = fmax(fmax(fabs(sig[0]), fabs(sig[1])), fabs(sig[2]));
+        if (mn < 0.2 || mx > 5.0) {
+            if (defer) return 3;
+            return project_robust(sig, s) ? 1 : 2;
+        }
+    }
     for (int i = 0; i < 3; ++i) s[i] = fmax(sig[i], kFloor);
     double lam;
     const bool ok = kkt_newton(sig, s, lam);
@@ -347,6 +450,7 @@ VK_HD int project(const double (&sig)[3], double (&s)[3]) {
         }
     }
     if (!odd) return 0;
+    if (defer) return 3;
     return project_robust(sig, s) ? 1 : 2;
 }
 

@@ -198,24 +198,42 @@ struct PcgArgs {
 // Every CTA sums the per-CTA partials of the last phase in the same fixed
 // order after the grid barrier, so all CTAs hold bit-identical scalars (no
 // serial "last CTA" step, deterministic across runs).
+#ifdef VK_PCG_TRACE               // phase-timing experiment build only
+__device__ unsigned long long g_pcg_trace[8192];
+__device__ int g_pcg_trace_n;
+__device__ __forceinline__ void pcg_mark(int tag) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const int k = g_pcg_trace_n;
+        if (k < 8190) { g_pcg_trace[k] = ((unsigned long long)tag << 56) | (t & 0xffffffffffffffull); g_pcg_trace_n = k + 1; }
+    }
+}
+#else
+__device__ __forceinline__ void pcg_mark(int) {}
+#endif
+
 template <int NV>
 __device__ __forceinline__ void pcg_allreduce(cg::grid_group& grid, double* partials, int& parity, double (&acc)[NV],
                                               double* red, double* smem) {
+    pcg_mark(1);
     block_sum<NV>(acc, smem);
     double* P = partials + (size_t)parity * gridDim.x * 8;
     if (threadIdx.x == 0)
 #pragma unroll
         for (int k = 0; k < NV; ++k) P[blockIdx.x * 8 + k] = acc[k];
+    pcg_mark(2);
     grid.sync();
+    pcg_mark(3);
     reduce_partials_all<NV>(P, red, smem);
+    pcg_mark(4);
     parity ^= 1;
 }
 
 template <typename T>
-__global__ void __launch_bounds__(1024) k_pcg_classic(PcgArgs<T> a) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double smem[32 * 8];
-    __shared__ double red[8];
+__device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_group& grid, double* smem,
+                                                 double* red, bool coherent_corners) {
+    pcg_mark(0);
     const int nF = a.nF;
     const int chunk = (nF + gridDim.x - 1) / gridDim.x;
     const int row0 = blockIdx.x * chunk;
@@ -233,7 +251,7 @@ __global__ void __launch_bounds__(1024) k_pcg_classic(PcgArgs<T> a) {
                 const int k0 = a.inc_ptr[i], k1 = a.inc_ptr[i + 1];
 #pragma unroll 4
                 for (int k = k0; k < k1; ++k) {
-                    const vec4_t<T> c = ldg4(&a.corner[k]);
+                    const vec4_t<T> c = coherent_corners ? ld4(&a.corner[k]) : ldg4(&a.corner[k]);
                     rx += c.x; ry += c.y; rzv += c.z;
                 }
                 const T m = a.m_dt2[i];
@@ -364,7 +382,16 @@ __global__ void __launch_bounds__(1024) k_pcg_classic(PcgArgs<T> a) {
         }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, a.pd_iter);
+    pcg_mark(5);
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.iters_out = it;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_pcg_classic(PcgArgs<T> a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double smem[32 * 8];
+    __shared__ double red[8];
+    pcg_classic_body(a, grid, smem, red, false);
 }
 
 // ---------------------------------------------------------------------------
@@ -418,7 +445,8 @@ __device__ __forceinline__ void pipe_dots(double (&acc)[8], const vec4_t<T>& r, 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(1024) k_pcg(PcgArgs<T> a) {
+__global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
+    pcg_mark(0);
     cg::grid_group grid = cg::this_grid();
     __shared__ double smem[32 * 8];
     __shared__ double red[8];

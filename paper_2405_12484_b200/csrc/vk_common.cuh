@@ -166,10 +166,14 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem /* >= 32
         for (int k = 0; k < NV; ++k) smem[warp * NV + k] = v[k];
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // second level: warp 0 combines the per-warp sums with a shuffle tree
+    // (a serial loop over warps in thread 0 cost ~1 us at 16 warps)
+    if (warp == 0) {
+#pragma unroll
         for (int k = 0; k < NV; ++k) {
-            double a = 0.0;
-            for (int w = 0; w < nw; ++w) a += smem[w * NV + k];
+            double a = lane < nw ? smem[lane * NV + k] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
             v[k] = a;
         }
     }

@@ -18,6 +18,7 @@
 #include "local_step.cuh"
 #include "solver.cuh"
 #include "cms.cuh"
+#include "frame.cuh"
 
 namespace {
 
@@ -53,6 +54,7 @@ struct DBuf {
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 int kPcgThreads = 512;          // CTA size of the persistent solver (env VKPD_PCG_THREADS; 512 measured best)
+constexpr int kFrameThreads = 512;   // CTA size of the fused frame kernel
 
 // ---------------------------------------------------------------------------
 // layout conversion kernels: host (nV,3) float64 in caller order <-> device vec4 internal order
@@ -192,9 +194,12 @@ struct Ctx : CtxBase {
     DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
     DBuf<V4> m1, qq, ss, pp;             // pipelined-CG recurrences
     bool pcg_classic = false;
+    bool fused = false;                  // whole frame in one cooperative kernel (env VKPD_FUSED=1); measured
+                                         // slower than per-phase kernels in a graph (register spills)
+    int frame_blocks = 0;
     DBuf<double> partials, scal, stage;
     DBuf<vk::GridBar> bar;
-    DBuf<int> iters, fail_iter;
+    DBuf<int> iters, fail_iter, robust_list, robust_count;
     DBuf<vk::ProjStats> pstats;
     int* h_fail = nullptr;
     int last_iterations = 0;
@@ -378,7 +383,7 @@ struct Ctx : CtxBase {
             CK(b->alloc(std::max(1, nF)));
             CK(cudaMemsetAsync(b->p, 0, std::max(1, nF) * sizeof(V4), s));
         }
-        if (const char* pt = getenv("VKPD_PCG_THREADS")) kPcgThreads = std::max(64, std::min(1024, atoi(pt)));
+        if (const char* pt = getenv("VKPD_PCG_THREADS")) kPcgThreads = std::max(64, std::min(512, atoi(pt)));
         const char* pv = getenv("VKPD_PCG");
         pcg_classic = !(pv && std::string(pv) == "pipe");   // classic measured faster at C3
         int occ = 0, occ2 = 0;
@@ -389,13 +394,24 @@ struct Ctx : CtxBase {
         // default: one row per thread, capped by co-residency
         pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : cdiv(std::max(1, nF), kPcgThreads);
         pcg_blocks = std::max(1, std::min(pcg_blocks, occ * n_sms));
-        CK(partials.alloc((size_t)16 * pcg_blocks));      // two parity banks x 8 doubles per CTA
+        {
+            const char* fz = getenv("VKPD_FUSED");
+            fused = fz && std::string(fz) == "1";
+            int occf = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, vk::k_frame<T>, kFrameThreads, 0));
+            frame_blocks = std::max(1, std::min(occf * n_sms, cdiv(std::max(std::max(nE, nF), 1), kFrameThreads)));
+            if (occf < 1) fused = false;
+        }
+        CK(partials.alloc((size_t)16 * std::max(pcg_blocks, frame_blocks)));   // 2 parity banks x 8 doubles/CTA
         CK(scal.alloc(16));
         CK(bar.alloc(1));
         CK(cudaMemsetAsync(bar.p, 0, sizeof(vk::GridBar), s));
         CK(iters.alloc(1024));
         CK(cudaMemsetAsync(iters.p, 0, 1024 * sizeof(int), s));
         CK(fail_iter.alloc(1));
+        CK(robust_list.alloc(std::max(1, nE)));
+        CK(robust_count.alloc(1));
+        CK(cudaMemsetAsync(robust_count.p, 0, sizeof(int), s));
         CK(pstats.alloc(1));
         CK(cudaMemsetAsync(pstats.p, 0, sizeof(vk::ProjStats), s));
         CK(stage.alloc((size_t)3 * n));
@@ -569,7 +585,17 @@ struct Ctx : CtxBase {
         la.nE = nE; la.tets = tets.p; la.G = G.p; la.w = w.p; la.x = xin; la.corner = corner.p;
         la.slot4 = slot4.p;
         la.stats = pstats.p; la.F_out = la.R_out = la.V_out = nullptr;
+        la.robust_list = robust_list.p; la.robust_count = robust_count.p;
         return la;
+    }
+    // local step in residual form, suspicious elements compacted into a dense second pass
+    int launch_local_resid(const vk::LocalArgs<T>& la) {
+        CK(cudaMemsetAsync(robust_count.p, 0, sizeof(int), stream));
+        vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+        CK(cudaGetLastError());
+        vk::k_robust4<T, vk::MODE_RESID><<<8 * n_sms, 128, 0, stream>>>(la);
+        CK(cudaGetLastError());
+        return VKPD_OK;
     }
     vk::PcgArgs<T> pcg_args(int init, int pd_iter, int* iters_slot) {
         vk::PcgArgs<T> pa;
@@ -599,6 +625,28 @@ struct Ctx : CtxBase {
 
     // enqueue one frame on `stream`; events (optional) bracket local / global launches
     int enqueue_frame(int iterations, double damping, std::vector<cudaEvent_t>* ev) {
+        if (fused && ev == nullptr && nE > 0 && nF > 0) {
+            vk::FrameArgs<T> fa;
+            fa.la = local_args(x.p);
+            fa.pa = pcg_args(vk::INIT_PD, 0, iters.p);
+            fa.n = n; fa.nF = nF; fa.iterations = iterations;
+            fa.dt = (T)dt; fa.damp_over_dt = (T)(damping / dt);
+            fa.dt2_inv_m = dt2_inv_m.p; fa.f = has_forces ? f.p : nullptr; fa.pin_tgt = pin_tgt.p;
+            fa.x = x.p; fa.v = v.p; fa.x_start = x_start.p; fa.v_start = v_start.p; fa.xhat = xhat.p;
+            fa.fail_iter = fail_iter.p; fa.iters = iters.p;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(frame_blocks);
+            cfg.blockDim = dim3(kFrameThreads);
+            cfg.stream = stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&cfg, vk::k_frame<T>, fa));
+            CK(cudaMemcpyAsync(h_fail, fail_iter.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+            return VKPD_OK;
+        }
         const int nb = cdiv(n, 256);
         vk::k_prologue<T><<<nb, 256, 0, stream>>>(n, nF, (T)dt, dt2_inv_m.p, has_forces ? f.p : nullptr,
                                                   pin_tgt.p, x.p, v.p, x_start.p, v_start.p, xhat.p,
@@ -607,8 +655,7 @@ struct Ctx : CtxBase {
         const vk::LocalArgs<T> la = local_args(x.p);
         for (int it = 0; it < iterations; ++it) {
             if (ev) CK(cudaEventRecord((*ev)[3 * it], stream));
-            vk::k_local<T, vk::MODE_RESID, false><<<cdiv(nE, 128), 128, 0, stream>>>(la);
-            CK(cudaGetLastError());
+            if (int rc = launch_local_resid(la)) return rc;
             if (ev) CK(cudaEventRecord((*ev)[3 * it + 1], stream));
             if (nF > 0) CK(launch_pcg(pcg_args(vk::INIT_PD, it, iters.p + it)));
             if (ev) CK(cudaEventRecord((*ev)[3 * it + 2], stream));
@@ -945,8 +992,7 @@ struct Ctx : CtxBase {
     int dev_residual(const void* x_int, const void* xhat_int, void* r_free) override {
         if (nE == 0) return fail(VKPD_EINVAL, "matrix-only context has no mesh");
         vk::LocalArgs<T> la = local_args((const V4*)x_int);
-        vk::k_local<T, vk::MODE_RESID, false><<<cdiv(nE, 128), 128, 0, stream>>>(la);
-        CK(cudaGetLastError());
+        if (int rc = launch_local_resid(la)) return rc;
         if (nF > 0) {
             k_resid_free<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, inc_ptr.p, corner.p, m_dt2.p, (const V4*)x_int,
                                                                (const V4*)xhat_int, (V4*)r_free);
@@ -1126,6 +1172,18 @@ int vkpd_apply_K(vkpd_ctx* ctx, const double* X, double* Y) {
     if (!X || !Y) return fail(VKPD_EINVAL, "null buffer");
     CTX_CALL(apply_K(X, Y));
 }
+#ifdef VK_PCG_TRACE
+int vkpd_debug_pcg_trace(unsigned long long* out, int max) {
+    int n = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&n, vk::g_pcg_trace_n, sizeof(int));
+    n = std::min(n, max);
+    if (n) cudaMemcpyFromSymbol(out, vk::g_pcg_trace, sizeof(unsigned long long) * n);
+    int zero = 0;
+    cudaMemcpyToSymbol(vk::g_pcg_trace_n, &zero, sizeof(int));
+    return n;
+}
+#endif
 int vkpd_dev_residual(vkpd_ctx* ctx, const void* x_int, const void* xhat_int, void* r_free) {
     if (!x_int || !xhat_int || !r_free) return fail(VKPD_EINVAL, "null device buffer");
     CTX_CALL(dev_residual(x_int, xhat_int, r_free));
