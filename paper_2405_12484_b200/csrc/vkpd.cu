@@ -389,10 +389,12 @@ struct Ctx : CtxBase {
         int occ = 0, occ2 = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_pcg<T>, kPcgThreads, 0));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, vk::k_pcg_classic<T>, kPcgThreads, 0));
-        occ = std::min(occ, occ2);
+        occ = pcg_classic ? occ2 : occ;          // co-residency of the kernel actually launched
         if (occ < 1) return fail(VKPD_ECUDA, "persistent solver kernel cannot be resident");
         // default: one row per thread, capped by co-residency
-        pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : cdiv(std::max(1, nF), kPcgThreads);
+        // default: at most one CTA per SM (fewer arrivals per grid barrier measured faster
+        // than 2 CTAs/SM at C3), at least one row per thread
+        pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : std::min(cdiv(std::max(1, nF), kPcgThreads), n_sms);
         pcg_blocks = std::max(1, std::min(pcg_blocks, occ * n_sms));
         {
             const char* fz = getenv("VKPD_FUSED");
