@@ -595,7 +595,8 @@ struct Ctx : CtxBase {
         CK(cudaMemsetAsync(robust_count.p, 0, sizeof(int), stream));
         vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
         CK(cudaGetLastError());
-        vk::k_robust4<T, vk::MODE_RESID><<<8 * n_sms, 128, 0, stream>>>(la);
+        // 4 CTAs/SM: enough lanes for the heavy frames, cheap when the queue is empty
+        vk::k_robust4<T, vk::MODE_RESID><<<4 * n_sms, 128, 0, stream>>>(la);
         CK(cudaGetLastError());
         return VKPD_OK;
     }
