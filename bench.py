@@ -323,10 +323,11 @@ def run_ours(args):
                    "l2": "flushed between frames" if flush is not None else "not flushed"},
         "e2e": {"value": e2e_val, "unit": "tet-iters/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3 / args.steps},
-        "gpu_launches": args.steps * (2 * its + 2),
+        "gpu_launches": args.steps * (3 * its + 2),      # prologue, its x (local, robust pass, CG), epilogue
         "roofline": {"bound": "hbm", "kernel": "k_local (PD local step)", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "alg_bytes_per_launch": alg,
+                     "traffic": ncu_traffic(args.precision), "traffic_source": "profiles/r01_launches_steady_summary.json (ncu dram read+write, cold L2)",
+                     "alg_bytes_per_launch": alg,
                      "local_ms_per_launch": local_ms, "global_ms_per_launch": global_ms,
                      "profiled_frame_ms": prof_frame_ms},
         "clocks": clocks,
@@ -339,6 +340,21 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def ncu_traffic(precision):
+    """dram__bytes_read+write per k_local launch from the committed ncu capture (fp32 only)."""
+    if precision != "fp32":
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_launches_steady_summary.json")) as f:
+            d = json.load(f)
+        for k, v in d.items():
+            if k.startswith("void k_local"):
+                return v["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
 
 
 def ctx_tol(args):
