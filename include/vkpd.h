@@ -105,6 +105,10 @@ int vkpd_set_state(vkpd_ctx* ctx, const double* x, const double* v);      /* (nV
 int vkpd_get_state(vkpd_ctx* ctx, double* x, double* v);                  /* either may be NULL */
 int vkpd_set_pin_targets(vkpd_ctx* ctx, const double* targets);           /* (n_pins,3) */
 int vkpd_set_forces(vkpd_ctx* ctx, const double* forces);                 /* (nV,3) or NULL = none */
+/* colliders of the following steps (SimState.colliders, pdsolver.py:125-173, 271-297):
+ * kinds[c] = 0 plane (params: point xyz, normal xyz) or 1 sphere (centre xyz, radius, -, -);
+ * params (n,6); nodes penetrating at the prediction get weight k * K_ii (n = 0: none) */
+int vkpd_set_colliders(vkpd_ctx* ctx, int n, const int* kinds, const double* params, double contact_stiffness);
 
 /* one implicit-Euler step by `iterations` local/global rounds; blocks until done.
  * On VKPD_ENONFINITE the state is left as it was before the step. */

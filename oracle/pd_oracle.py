@@ -362,6 +362,75 @@ def predicted(x, v, dt, mass, forces):
     return x + dt * v + dt ** 2 * inv_m[:, None] * f
 
 
+def collider_targets(x, colliders):
+    """Penetrating nodes and their closest surface points (`pdsolver.py:125-155`)."""
+    x = np.asarray(x, dtype=float)
+    idx, tgt = [], []
+    for kind, *args in colliders:
+        if kind == "plane":
+            p0 = np.asarray(args[0], dtype=float)
+            nrm = np.asarray(args[1], dtype=float)
+            nrm = nrm / np.linalg.norm(nrm)
+            depth = (x - p0) @ nrm
+            pen = np.flatnonzero(depth < 0.0)
+            idx.append(pen)
+            tgt.append(x[pen] - depth[pen, None] * nrm)
+        elif kind == "sphere":
+            c = np.asarray(args[0], dtype=float)
+            r = float(args[1])
+            rel = x - c
+            dist = np.linalg.norm(rel, axis=1)
+            pen = np.flatnonzero(dist < r)
+            idx.append(pen)
+            tgt.append(c + rel[pen] * (r / np.maximum(dist[pen], 1e-12))[:, None])
+        else:
+            raise ValueError(f"unknown collider kind {kind!r}")
+    if not idx:
+        return np.empty(0, dtype=int), np.empty((0, 3))
+    return np.concatenate(idx), np.concatenate(tgt)
+
+
+def surface_targets(points, colliders):
+    """Points projected out of any collider they penetrate (`pdsolver.py:158-163`)."""
+    out = np.asarray(points, dtype=float).copy()
+    i, t = collider_targets(out, colliders)
+    out[i] = t
+    return out
+
+
+def pd_step_contact(x, v, dt, tets, G, vol, gs, gv, mass, pins, pin_targets, forces, colliders,
+                    iterations=PD_ITERS, damping=1.0, contact_stiffness=1e4):
+    """pd_step with colliders (`pdsolver.py:271-281, 294-297`): contact weight
+    cw = k * diag(K) at the nodes penetrating at the prediction, folded into K
+    (duplicates summed) and into b once per node; direct solve every step."""
+    n = len(mass)
+    pins = np.asarray(pins, dtype=np.int64)
+    free = np.setdiff1d(np.arange(n), pins)
+    xhat = predicted(x, v, dt, mass, forces)
+    cidx, _ = collider_targets(xhat, colliders)
+    K = assemble_K(tets, G, vol, gs, gv, mass, dt, n)
+    cw = None
+    if len(cidx):
+        cw = contact_stiffness * K.diagonal()[cidx]
+        K = (K + sp.csr_matrix((cw, (cidx, cidx)), shape=(n, n))).tocsc()
+    solver = GlobalSolver(K, free, pins)
+    x_start = x.copy()
+    xi = xhat.copy()
+    pin_vals = np.empty((0, 3))
+    if len(pins):
+        pin_vals = pin_targets
+        xi[pins] = pin_vals
+    inertia = (mass[:, None] / dt ** 2) * xhat
+    for it in range(iterations):
+        b = inertia + elastic_rhs(xi, tets, G, vol, gs, gv, n)[0]
+        if len(cidx):
+            b[cidx] += cw[:, None] * surface_targets(xi[cidx], colliders)
+        xi = solver.solve(b, pin_vals)
+        if not np.all(np.isfinite(xi)):
+            raise RuntimeError(f"projective step produced non-finite positions at iteration {it}")
+    return xi, damping * (xi - x_start) / dt
+
+
 def pd_step(x, v, dt, tets, G, vol, gs, gv, mass, solver, pins=(), pin_targets=None,
             forces=None, iterations=PD_ITERS, damping=1.0, timers=None):
     """One implicit-Euler step by local/global rounds (`pdsolver.py:257-304`, no colliders).

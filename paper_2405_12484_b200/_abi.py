@@ -24,7 +24,7 @@ EXPORTS = (
     "vkpd_elastic_rhs", "vkpd_global_solve", "vkpd_apply_K", "vkpd_get_stats",
     "vkpd_batch_projections", "vkpd_create_matrix", "vkpd_get_matrix_csr", "vkpd_a_jacobi_refine",
     "vkpd_power_rho", "vkpd_cms_set_basis", "vkpd_cms_solve", "vkpd_dev_residual", "vkpd_dev_apply_K",
-    "vkpd_dev_inv_diag", "vkpd_get_node_order", "vkpd_get_sizes",
+    "vkpd_dev_inv_diag", "vkpd_get_node_order", "vkpd_get_sizes", "vkpd_set_colliders",
 )
 
 
@@ -95,6 +95,7 @@ def load():
         "vkpd_cms_set_basis": (I, [P, I, P, P]),
         "vkpd_cms_solve": (I, [P, P, P, I, I, I, C.c_double, I, C.c_double, P]),
         "vkpd_dev_residual": (I, [P, P, P, P]),
+        "vkpd_set_colliders": (I, [P, I, P, P, C.c_double]),
         "vkpd_dev_apply_K": (I, [P, P, P]),
         "vkpd_dev_inv_diag": (I, [P, P]),
         "vkpd_get_node_order": (I, [P, P]),
@@ -220,6 +221,23 @@ class Context:
 
     def set_forces(self, f):
         check(self.lib.vkpd_set_forces(self.h, None if f is None else ptr(f64(f, (self.n, 3)))))
+
+    def set_colliders(self, colliders, contact_stiffness=1e4):
+        """colliders: sequence of ("plane", point, normal) / ("sphere", centre, radius)."""
+        kinds, params = [], []
+        for kind, *args in colliders:
+            if kind == "plane":
+                kinds.append(0)
+                params.append(list(np.asarray(args[0], dtype=float)) + list(np.asarray(args[1], dtype=float)))
+            elif kind == "sphere":
+                kinds.append(1)
+                params.append(list(np.asarray(args[0], dtype=float)) + [float(args[1]), 0.0, 0.0])
+            else:
+                raise ValueError(f"unknown collider kind {kind!r}")
+        k = np.asarray(kinds, dtype=np.int32)
+        p = np.asarray(params, dtype=np.float64).reshape(-1, 6)
+        check(self.lib.vkpd_set_colliders(self.h, len(k), ptr(k) if len(k) else None, ptr(p) if len(k) else None,
+                                          float(contact_stiffness)))
 
     def step(self, iterations, damping=1.0):
         fi = C.c_int(-1)

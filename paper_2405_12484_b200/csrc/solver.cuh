@@ -192,7 +192,67 @@ struct PcgArgs {
     double tol;
     int max_iters;
     int init;
+    // colliders (pdsolver.py:271-297): extra diagonal m_i * k * K_ii and rhs weight k * K_ii
+    const T* cdiag;              // null without colliders
+    const T* cb;
+    const double* coll;          // kCollStride doubles per collider
+    int ncoll;
 };
+
+// ---------------------------------------------------------------------------
+// Colliders: plane {0, p0, n_hat} and sphere {1, c, r} (pdsolver.py:125-163).
+constexpr int kCollStride = 8;
+constexpr int kMaxColliders = 16;
+
+// Number of colliders x penetrates (the multiplicity of x in `collider_targets`).
+__device__ __forceinline__ int collider_hits(const double* coll, int ncoll, double x, double y, double z) {
+    int m = 0;
+    for (int c = 0; c < ncoll; ++c) {
+        const double* q = coll + c * kCollStride;
+        if (q[0] == 0.0) {
+            if ((x - q[1]) * q[4] + (y - q[2]) * q[5] + (z - q[3]) * q[6] < 0.0) ++m;
+        } else {
+            const double dx = x - q[1], dy = y - q[2], dz = z - q[3];
+            if (sqrt(dx * dx + dy * dy + dz * dz) < q[4]) ++m;
+        }
+    }
+    return m;
+}
+
+// `surface_targets` for one point: every collider is tested on the original
+// point and a later penetrated collider overrides an earlier one.
+__device__ __forceinline__ void collider_target(const double* coll, int ncoll, double x, double y, double z,
+                                                double& tx, double& ty, double& tz) {
+    tx = x; ty = y; tz = z;
+    for (int c = 0; c < ncoll; ++c) {
+        const double* q = coll + c * kCollStride;
+        if (q[0] == 0.0) {
+            const double depth = (x - q[1]) * q[4] + (y - q[2]) * q[5] + (z - q[3]) * q[6];
+            if (depth < 0.0) { tx = x - depth * q[4]; ty = y - depth * q[5]; tz = z - depth * q[6]; }
+        } else {
+            const double dx = x - q[1], dy = y - q[2], dz = z - q[3];
+            const double d = sqrt(dx * dx + dy * dy + dz * dz);
+            if (d < q[4]) {
+                const double f = q[4] / fmax(d, 1e-12);
+                tx = q[1] + dx * f; ty = q[2] + dy * f; tz = q[3] + dz * f;
+            }
+        }
+    }
+}
+
+// Per step: contact set from the prediction xhat (pdsolver.py:271, 277-280).
+template <typename T>
+__global__ void k_contact_setup(int nF, const vec4_t<T>* __restrict__ xhat, const double* __restrict__ diag64,
+                                const double* __restrict__ coll, int ncoll, double kc, T* inv_diag_c, T* cdiag, T* cb) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    const vec4_t<T> xh = xhat[i];
+    const int m = collider_hits(coll, ncoll, (double)xh.x, (double)xh.y, (double)xh.z);
+    const double w = kc * diag64[i];
+    cdiag[i] = (T)(m * w);
+    cb[i] = (T)(m > 0 ? w : 0.0);
+    inv_diag_c[i] = (T)(1.0 / (diag64[i] + m * w));
+}
 
 
 // Every CTA sums the per-CTA partials of the last phase in the same fixed
@@ -259,6 +319,18 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
                 rx += m * (xh.x - xi.x);
                 ry += m * (xh.y - xi.y);
                 rzv += m * (xh.z - xi.z);
+                if (a.ncoll > 0) {
+                    // contact rows: b += cw * surface_target(x), K x += m cw x (pdsolver.py:294-297)
+                    const T w = a.cb[i];
+                    if (w != T(0)) {
+                        double tx, ty, tz;
+                        collider_target(a.coll, a.ncoll, (double)xi.x, (double)xi.y, (double)xi.z, tx, ty, tz);
+                        const T cd = a.cdiag[i];
+                        rx += w * (T)tx - cd * xi.x;
+                        ry += w * (T)ty - cd * xi.y;
+                        rzv += w * (T)tz - cd * xi.z;
+                    }
+                }
                 const double bx = (double)m * xh.x, by = (double)m * xh.y, bz = (double)m * xh.z;
                 acc[4] += bx * bx + by * by + bz * bz;
             } else {
@@ -331,6 +403,10 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
                 const vec4_t<T> zi = ld4(&a.z[i]);
                 const vec4_t<T> pi = ld4(&pold[i]);
                 const vec4_t<T> pn = make4<T>(zi.x + bx * pi.x, zi.y + by * pi.y, zi.z + bz * pi.z, T(0));
+                if (a.cdiag != nullptr) {
+                    const T cd = a.cdiag[i];
+                    qx += cd * pn.x; qy += cd * pn.y; qz += cd * pn.z;
+                }
                 pnew[i] = pn;
                 a.q[i] = make4<T>(qx, qy, qz, T(0));
                 acc[0] += (double)pn.x * qx;

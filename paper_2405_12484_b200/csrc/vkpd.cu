@@ -146,6 +146,7 @@ struct CtxBase {
     virtual int get_state(double* x, double* v) = 0;
     virtual int set_pin_targets(const double* t) = 0;
     virtual int set_forces(const double* f) = 0;
+    virtual int set_colliders(int n, const int* kinds, const double* params, double kc) = 0;
     virtual int step_async(int iterations, double damping) = 0;
     virtual int sync(int* failed) = 0;
     virtual int profile(int iterations, double damping, double* lms, double* gms, double* fms) = 0;
@@ -211,6 +212,12 @@ struct Ctx : CtxBase {
     double graph_damp = 0;
     bool graph_forces = false;
     bool graph_broken = false;
+    int graph_ncoll = 0;
+    // colliders (pdsolver.py:125-173, 271-297)
+    int ncoll = 0;
+    double contact_k = 1e4;
+    DBuf<double> coll_d;
+    DBuf<T> inv_diag_c, cdiag, cb;
 
     ~Ctx() override {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
@@ -576,6 +583,35 @@ struct Ctx : CtxBase {
         CK(cudaGetLastError());
         return VKPD_OK;
     }
+    int set_colliders(int nc, const int* kinds, const double* params, double kc) override {
+        if (nc < 0 || nc > vk::kMaxColliders) return fail(VKPD_EINVAL, "at most 16 colliders");
+        std::vector<double> h((size_t)vk::kCollStride * std::max(1, nc), 0.0);
+        for (int c = 0; c < nc; ++c) {
+            const double* p = params + 6 * c;
+            double* q = h.data() + vk::kCollStride * c;
+            if (kinds[c] == 0) {                      // plane: point, normal (normalised here)
+                const double nn = std::sqrt(p[3] * p[3] + p[4] * p[4] + p[5] * p[5]);
+                if (!(nn > 0.0)) return fail(VKPD_EINVAL, "plane normal must be non-zero");
+                q[0] = 0.0; q[1] = p[0]; q[2] = p[1]; q[3] = p[2];
+                q[4] = p[3] / nn; q[5] = p[4] / nn; q[6] = p[5] / nn;
+            } else if (kinds[c] == 1) {               // sphere: centre, radius
+                q[0] = 1.0; q[1] = p[0]; q[2] = p[1]; q[3] = p[2]; q[4] = p[3];
+            } else {
+                return fail(VKPD_EINVAL, "unknown collider kind");
+            }
+        }
+        if (!coll_d.p) {
+            CK(coll_d.alloc((size_t)vk::kCollStride * vk::kMaxColliders));
+            CK(inv_diag_c.alloc(std::max(1, nF)));
+            CK(cdiag.alloc(std::max(1, nF)));
+            CK(cb.alloc(std::max(1, nF)));
+        }
+        if (nc > 0) CK(cudaMemcpyAsync(coll_d.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
+        ncoll = nc;
+        contact_k = kc;
+        return VKPD_OK;
+    }
     int set_forces(const double* hf) override {
         if (hf == nullptr) { has_forces = false; return VKPD_OK; }
         has_forces = true;
@@ -609,6 +645,10 @@ struct Ctx : CtxBase {
         pa.m1 = m1.p; pa.qq = qq.p; pa.ss = ss.p; pa.pp = pp.p;
         pa.iters_out = iters_slot; pa.fail_iter = fail_iter.p; pa.pd_iter = pd_iter; pa.tol = tol;
         pa.max_iters = max_iters; pa.init = init;
+        pa.cdiag = nullptr; pa.cb = nullptr; pa.coll = nullptr; pa.ncoll = 0;
+        if (init == vk::INIT_PD && ncoll > 0) {
+            pa.inv_diag = inv_diag_c.p; pa.cdiag = cdiag.p; pa.cb = cb.p; pa.coll = coll_d.p; pa.ncoll = ncoll;
+        }
         return pa;
     }
     cudaError_t launch_pcg(const vk::PcgArgs<T>& pa) {
@@ -622,13 +662,13 @@ struct Ctx : CtxBase {
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (pcg_classic) return cudaLaunchKernelEx(&cfg, vk::k_pcg_classic<T>, pa);
+        if (pcg_classic || pa.ncoll > 0) return cudaLaunchKernelEx(&cfg, vk::k_pcg_classic<T>, pa);
         return cudaLaunchKernelEx(&cfg, vk::k_pcg<T>, pa);
     }
 
     // enqueue one frame on `stream`; events (optional) bracket local / global launches
     int enqueue_frame(int iterations, double damping, std::vector<cudaEvent_t>* ev) {
-        if (fused && ev == nullptr && nE > 0 && nF > 0) {
+        if (fused && ev == nullptr && nE > 0 && nF > 0 && ncoll == 0) {
             vk::FrameArgs<T> fa;
             fa.la = local_args(x.p);
             fa.pa = pcg_args(vk::INIT_PD, 0, iters.p);
@@ -655,6 +695,11 @@ struct Ctx : CtxBase {
                                                   pin_tgt.p, x.p, v.p, x_start.p, v_start.p, xhat.p,
                                                   fail_iter.p);
         CK(cudaGetLastError());
+        if (ncoll > 0 && nF > 0) {
+            vk::k_contact_setup<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, xhat.p, diag64.p, coll_d.p, ncoll,
+                                                                      contact_k, inv_diag_c.p, cdiag.p, cb.p);
+            CK(cudaGetLastError());
+        }
         const vk::LocalArgs<T> la = local_args(x.p);
         for (int it = 0; it < iterations; ++it) {
             if (ev) CK(cudaEventRecord((*ev)[3 * it], stream));
@@ -692,6 +737,7 @@ struct Ctx : CtxBase {
         graph_iters = iterations;
         graph_damp = damping;
         graph_forces = has_forces;
+        graph_ncoll = ncoll;
         return VKPD_OK;
     }
 
@@ -699,7 +745,8 @@ struct Ctx : CtxBase {
         if (iterations < 0 || iterations > 1024) return fail(VKPD_EINVAL, "iterations must be in [0, 1024]");
         last_iterations = iterations;
         if (use_graph && !graph_broken) {
-            if (!graph_exec || graph_iters != iterations || graph_damp != damping || graph_forces != has_forces) {
+            if (!graph_exec || graph_iters != iterations || graph_damp != damping || graph_forces != has_forces ||
+                graph_ncoll != ncoll) {
                 int rc = build_graph(iterations, damping);
                 if (rc) return rc;
             }
@@ -1152,6 +1199,10 @@ int vkpd_set_pin_targets(vkpd_ctx* ctx, const double* t) {
     CTX_CALL(set_pin_targets(t));
 }
 int vkpd_set_forces(vkpd_ctx* ctx, const double* f) { CTX_CALL(set_forces(f)); }
+int vkpd_set_colliders(vkpd_ctx* ctx, int n, const int* kinds, const double* params, double contact_stiffness) {
+    if (n > 0 && (!kinds || !params)) return fail(VKPD_EINVAL, "null collider arrays");
+    CTX_CALL(set_colliders(n, kinds, params, contact_stiffness));
+}
 int vkpd_step_async(vkpd_ctx* ctx, int iterations, double damping) { CTX_CALL(step_async(iterations, damping)); }
 int vkpd_sync(vkpd_ctx* ctx, int* failed_iter) { CTX_CALL(sync(failed_iter)); }
 int vkpd_step(vkpd_ctx* ctx, int iterations, double damping, int* failed_iter) {

@@ -241,16 +241,19 @@ def pd_step(state, mesh, gammas, iterations=PD_ITERS_DEFAULT, forces=None, solve
     `solver` (anything with `.solve(B, pin_vals)`) keeps the reference's
     host-driven loop with the local step on the GPU.
     """
-    if state.colliders:
-        raise NotImplementedError("colliders are the next row of SURVEY.md 8f; not in this build")
     _check_inputs(mesh, gammas, state.dt)
-    if solver is not None and not isinstance(solver, _DeviceStep):
+    if state.colliders:
+        _validate_colliders(state.colliders)
+    elif solver is not None and not isinstance(solver, _DeviceStep):
         return _pd_step_host_solver(state, mesh, gammas, iterations, forces, solver, damping, precision)
+    # with colliders the reference re-assembles K with the contact diagonal and ignores
+    # `solver` (pdsolver.py:273-281); the device step adds the contact terms per step
     ctx = device_context(mesh, gammas, state.dt, state.pins, precision, tol, max_iters)
     ctx.set_state(state.x, state.v)
     if len(state.pins):
         ctx.set_pin_targets(state.pin_targets)
     ctx.set_forces(forces)
+    ctx.set_colliders(state.colliders, contact_stiffness)
     try:
         ctx.step(iterations, damping)
     except _abi.NonFiniteError as exc:
@@ -262,6 +265,63 @@ def pd_step(state, mesh, gammas, iterations=PD_ITERS_DEFAULT, forces=None, solve
 
 class _DeviceStep:
     """Marker base for solvers that run inside the device-resident step."""
+
+
+# ---------------------------------------------------------------------------
+# colliders (pdsolver.py:125-173).  Host helpers for callers; inside the step the
+# contact set, weights and surface targets are computed on the device.
+
+
+def _validate_colliders(colliders):
+    for kind, *_ in colliders:
+        if kind not in ("plane", "sphere"):
+            raise ValueError(f"unknown collider kind {kind!r}")
+
+
+def collider_targets(x, colliders):
+    """Nodes penetrating a collider and their closest surface points (`pdsolver.py:125-155`)."""
+    x = np.asarray(x, dtype=float)
+    idx, tgt = [], []
+    for kind, *args in colliders:
+        if kind == "plane":
+            p0 = np.asarray(args[0], dtype=float)
+            nrm = np.asarray(args[1], dtype=float)
+            nrm = nrm / np.linalg.norm(nrm)
+            depth = (x - p0) @ nrm
+            pen = np.flatnonzero(depth < 0.0)
+            idx.append(pen)
+            tgt.append(x[pen] - depth[pen, None] * nrm)
+        elif kind == "sphere":
+            c = np.asarray(args[0], dtype=float)
+            r = float(args[1])
+            rel = x - c
+            dist = np.linalg.norm(rel, axis=1)
+            pen = np.flatnonzero(dist < r)
+            idx.append(pen)
+            tgt.append(c + rel[pen] * (r / np.maximum(dist[pen], 1e-12))[:, None])
+        else:
+            raise ValueError(f"unknown collider kind {kind!r}")
+    if not idx:
+        return np.empty(0, dtype=int), np.empty((0, 3))
+    return np.concatenate(idx), np.concatenate(tgt)
+
+
+def surface_targets(points, colliders):
+    """Project points out of any collider they penetrate; identity otherwise (`pdsolver.py:158-163`)."""
+    out = np.asarray(points, dtype=float).copy()
+    idx, tgt = collider_targets(out, colliders)
+    out[idx] = tgt
+    return out
+
+
+def collide_project(state, colliders=None):
+    """Snap penetrating nodes of a state to the collider surfaces (`pdsolver.py:166-173`)."""
+    colliders = state.colliders if colliders is None else colliders
+    idx, tgt = collider_targets(state.x, colliders)
+    if len(idx):
+        state.x = state.x.copy()
+        state.x[idx] = tgt
+    return state
 
 
 def _pd_step_host_solver(state, mesh, gammas, iterations, forces, solver, damping, precision):
@@ -315,13 +375,9 @@ def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=Non
             forces = np.broadcast_to(forces, (steps,) + forces.shape)
     frames = np.empty((steps, mesh.n_nodes, 3))
     if state.colliders:
-        for i in range(steps):
-            if pin_path is not None:
-                state.pin_targets = pin_path[i]
-            pd_step(state, mesh, gammas, iterations, None if forces is None else forces[i],
-                    damping=damping, precision=precision)
-            frames[i] = state.x
-        return frames
+        # the reference drops the prefactored solver when colliders exist (pdsolver.py:753)
+        _validate_colliders(state.colliders)
+        solver_mode = "direct"
     if solver_mode == "cms":
         from .cms import simulate_cms
         return simulate_cms(mesh, gammas, steps, dt, forces, state, pin_path, iterations,
@@ -333,6 +389,7 @@ def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=Non
         ctx.set_pin_targets(state.pin_targets)
     const_forces = forces is not None and forces.strides[0] == 0      # broadcast (nV,3) input
     ctx.set_forces(None if forces is None else forces[0])
+    ctx.set_colliders(state.colliders)
     for i in range(steps):
         if pin_path is not None:
             ctx.set_pin_targets(pin_path[i])

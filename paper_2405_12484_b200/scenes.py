@@ -153,6 +153,17 @@ def c5_garment(seed=SEED):
                          name=None)
 
 
+def contact_scene():
+    """Small box dropped onto a tilted plane and a sphere (collider parity scene)."""
+    sc = box_scene(8, 6, 3, name="contact-box")
+    m = sc.mesh
+    lo = m.nodes.min(axis=0)
+    hi = m.nodes.max(axis=0)
+    colliders = [("plane", (0.0, 0.0, lo[2] - 0.002), (0.1, 0.0, 1.0)),
+                 ("sphere", (hi[0] - 0.006, 0.5 * (lo[1] + hi[1]), lo[2] - 0.02), 0.0195)]
+    return sc, colliders
+
+
 SCENES = {
     "C1": c1_swatch,
     "C2": c2_scarf,

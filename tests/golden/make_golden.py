@@ -18,6 +18,7 @@ the reference saw.  Per-fixture contents:
                    start, `build_cms(...).solve`, and `simulate_mesh(cms)` 1 frame.
   c2.npz           C2 scarf: `simulate_mesh(direct)` frames 1, 10, 100 (f64).
   c3.npz           C3 sweater: `simulate_mesh(direct)` frame 1, displacement as f32.
+  contact.npz      box dropped on a plane + sphere collider: `simulate_mesh(colliders=...)`, 20 frames.
 """
 
 from __future__ import annotations
@@ -153,6 +154,20 @@ def make_solvers():
     print("solvers")
 
 
+def contact_scene():
+    return scenes.contact_scene()
+
+
+def make_contact():
+    sc, colliders = contact_scene()
+    rm = ref_mesh(sc)
+    gam = ref_mat.MaterialField(sc.gammas.gamma_s, sc.gammas.gamma_v)
+    fr = ref_pd.simulate_mesh(rm, gam, 20, sc.dt, forces=sc.forces, colliders=colliders, iterations=10,
+                              damping=0.9)
+    np.savez_compressed(os.path.join(HERE, "contact.npz"), digest=scene_digest(sc), frames=fr)
+    print("contact", fr.shape)
+
+
 def make_big(key, frames_keep, steps, f32_disp):
     sc = scenes.make_scene(key)
     rm = ref_mesh(sc)
@@ -174,6 +189,8 @@ if __name__ == "__main__":
         make_projections()
         make_c1()
         make_solvers()
+    if what in ("contact", "all"):
+        make_contact()
     if what in ("c2", "all"):
         make_big("C2", (1, 10, 100), 100, False)
     if what in ("c3", "all"):

@@ -273,3 +273,59 @@ def test_c2_hundred_frames_match_reference(prec, tols):
                                 pin_targets=sc.pin_targets, iterations=30, precision=prec)
     for k, tol in tols.items():
         assert rel_l2(fr[k - 1], g[f"frame{k}"]) < tol, (k, rel_l2(fr[k - 1], g[f"frame{k}"]))
+
+
+# ---------------------------------------------------------------------------
+# colliders (pdsolver.py:125-173, 271-297)
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 2e-4)])
+def test_contact_frames_match_reference(prec, tol):
+    g = golden("contact.npz")
+    sc, colliders = scenes.contact_scene()
+    assert scene_digest(sc) == str(g["digest"])
+    fr = pdsolver.simulate_mesh(sc.mesh, sc.gammas, 20, sc.dt, forces=sc.forces, colliders=colliders,
+                                iterations=10, damping=0.9, precision=prec)
+    x0 = sc.mesh.nodes
+    for k in (0, 9, 19):
+        assert rel_l2(fr[k] - x0, g["frames"][k] - x0) < tol, (k, rel_l2(fr[k] - x0, g["frames"][k] - x0))
+
+
+def _settle(colliders, steps=250):
+    sc = scenes.box_scene(10, 4, 3)
+    mesh = sc.mesh
+    mesh.node_mass = np.full(mesh.n_nodes, 2e-4)
+    gam = MaterialField.uniform(mesh.n_elements, 50.0, 25.0)
+    st = pdsolver.SimState(x=mesh.nodes, v=np.zeros_like(mesh.nodes), dt=2e-3, colliders=colliders)
+    f = mesh.node_mass[:, None] * np.array([0.0, -9.8, 0.0])
+    for _ in range(steps):
+        pdsolver.pd_step(st, mesh, gam, iterations=10, forces=f, damping=0.9, precision="fp64")
+    return mesh, st
+
+
+def test_plane_resting_contact_depth():
+    mesh0 = scenes.box_scene(10, 4, 3).mesh
+    floor_y = mesh0.nodes[:, 1].min() + 0.002
+    mesh, st = _settle((("plane", (0.0, floor_y, 0.0), (0.0, 1.0, 0.0)),))
+    assert floor_y - st.x[:, 1].min() < 1e-4 * mesh.cell_size
+
+
+def test_sphere_resting_contact_depth():
+    mesh0 = scenes.box_scene(10, 4, 3).mesh
+    c = mesh0.nodes.mean(axis=0) + np.array([0.0, -0.2, 0.0])
+    r = 0.2 - 0.006
+    mesh, st = _settle((("sphere", c, r),))
+    assert r - np.linalg.norm(st.x - c, axis=1).min() < 1e-4 * mesh.cell_size
+
+
+def test_collide_project_and_bad_kind():
+    x = np.array([[0.0, -0.5, 0.0], [0.0, 0.5, 0.0]])
+    st = pdsolver.SimState(x=x, v=np.zeros_like(x), dt=1e-3, colliders=(("plane", (0, 0, 0), (0, 1, 0)),))
+    pdsolver.collide_project(st)
+    assert np.allclose(st.x[0], [0.0, 0.0, 0.0]) and np.allclose(st.x[1], [0.0, 0.5, 0.0])
+    with pytest.raises(ValueError):
+        pdsolver.collider_targets(np.zeros((1, 3)), [("torus", 0, 1)])
+    sc = scenes.box_scene(4, 3, 2)
+    st = pdsolver.SimState(x=sc.mesh.nodes, v=np.zeros_like(sc.mesh.nodes), dt=1e-3, colliders=(("torus", 0, 1),))
+    with pytest.raises(ValueError):
+        pdsolver.pd_step(st, sc.mesh, sc.gammas, iterations=2)

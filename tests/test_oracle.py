@@ -107,3 +107,15 @@ def test_cms_mode_frame_matches_reference():
 def test_aggregation_rejects_bad_value():
     with pytest.raises(ValueError):
         orc.a_jacobi_refine(sp.eye(4).tocsc(), np.ones(4), np.zeros(4), aggregation=4)
+
+
+def test_contact_oracle_matches_reference():
+    g = golden("contact.npz")
+    sc, colliders = scenes.contact_scene()
+    assert scene_digest(sc) == str(g["digest"])
+    m = sc.mesh
+    x, v = m.nodes.copy(), np.zeros_like(m.nodes)
+    for k in range(20):
+        x, v = orc.pd_step_contact(x, v, sc.dt, m.tets, m.shape_grad, m.volume, sc.gammas.gamma_s,
+                                   sc.gammas.gamma_v, m.node_mass, [], None, sc.forces, colliders, 10, 0.9)
+        assert np.abs(x - g["frames"][k]).max() < 1e-12
