@@ -325,10 +325,12 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
                     if (w != T(0)) {
                         double tx, ty, tz;
                         collider_target(a.coll, a.ncoll, (double)xi.x, (double)xi.y, (double)xi.z, tx, ty, tz);
-                        const T cd = a.cdiag[i];
-                        rx += w * (T)tx - cd * xi.x;
-                        ry += w * (T)ty - cd * xi.y;
-                        rzv += w * (T)tz - cd * xi.z;
+                        // cw (target - x) - (m - 1) cw x: the penetration vector is formed
+                        // before scaling by the (1e4 K_ii) weight, which keeps float32 exact enough
+                        const T extra = a.cdiag[i] - w;
+                        rx += w * (T)(tx - (double)xi.x) - extra * xi.x;
+                        ry += w * (T)(ty - (double)xi.y) - extra * xi.y;
+                        rzv += w * (T)(tz - (double)xi.z) - extra * xi.z;
                     }
                 }
                 const double bx = (double)m * xh.x, by = (double)m * xh.y, bz = (double)m * xh.z;
