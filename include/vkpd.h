@@ -13,7 +13,8 @@
  *   vkpd_get_state
  *   vkpd_set_pin_targets  SimState.pin_targets / per-step pin path (pdsolver.py:750-751)
  *   vkpd_set_forces       per-step external forces (pdsolver.py:744-752)
- *   vkpd_step             pd_step (pdsolver.py:257-304), no colliders
+ *   vkpd_step             pd_step (pdsolver.py:257-304)
+ *   vkpd_set_colliders    SimState.colliders (pdsolver.py:125-173, 271-297)
  *   vkpd_elastic_rhs      elastic_rhs (pdsolver.py:59-71)
  *   vkpd_global_solve     GlobalSolver.solve (pdsolver.py:225-246)
  *   vkpd_apply_K          the assembled K (pdsolver.py:42-56) applied to a vector

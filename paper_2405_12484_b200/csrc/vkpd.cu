@@ -230,7 +230,7 @@ struct Ctx : CtxBase {
         nE = (int)d->n_tets;
         nP = (int)d->n_pins;
         dt = d->dt;
-        tol = c->tol > 0 ? c->tol : (sizeof(T) == 4 ? 1e-6 : 1e-12);
+        tol = c->tol > 0 ? c->tol : (sizeof(T) == 4 ? 2e-6 : 1e-12);
         max_iters = c->max_iters > 0 ? c->max_iters : 1000;
         use_graph = c->use_graph != 0;
         if (n <= 0 || nE <= 0) return fail(VKPD_EINVAL, "empty mesh");
@@ -438,7 +438,7 @@ struct Ctx : CtxBase {
         nE = 0;
         nP = (int)npins;
         dt = 1.0;
-        tol = c->tol > 0 ? c->tol : (sizeof(T) == 4 ? 1e-6 : 1e-12);
+        tol = c->tol > 0 ? c->tol : (sizeof(T) == 4 ? 2e-6 : 1e-12);
         max_iters = c->max_iters > 0 ? c->max_iters : 1000;
         use_graph = false;
         if (n <= 0) return fail(VKPD_EINVAL, "empty matrix");

@@ -174,7 +174,7 @@ class CudaOps:
 class DistributedStepper:
     """One rank of the domain-decomposed PD step (`pd_step` semantics, no colliders)."""
 
-    def __init__(self, plan, rank, mesh, gammas, dt, ops, comm, pin_targets=None, tol=1e-6, max_iters=1000):
+    def __init__(self, plan, rank, mesh, gammas, dt, ops, comm, pin_targets=None, tol=2e-6, max_iters=1000):
         import torch
         self.torch = torch
         self.plan, self.rank, self.dt, self.ops, self.comm = plan, rank, float(dt), ops, comm
