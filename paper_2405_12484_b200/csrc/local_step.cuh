@@ -89,7 +89,7 @@ struct LocalArgs {
     vec4_t<T>* corner;           // per-incidence contributions, node-sorted (tet order within a node)
     ProjStats* stats;
     int* robust_list;            // optional: suspicious elements are queued here (k_robust finishes them)
-    int* robust_count;
+    int* robust_count;           // [0] queued elements, [1] chunk cursor of the robust pass
     double* F_out;               // optional (nE,3,3) (RHS mode only)
     double* R_out;
     double* V_out;
@@ -142,7 +142,7 @@ __device__ __forceinline__ void local_tet(const LocalArgs<T>& a, int e) {
             const int lead = __ffs(m3) - 1;
             int base = 0;
             if (lane == lead) base = atomicAdd(a.robust_count, __popc(m3));
-            base = __shfl_sync(m3, base, lead);
+            base = __shfl_sync(am, base, lead);
             if (path == 3) a.robust_list[base + __popc(m3 & ((1u << lane) - 1u))] = e;
         }
         if (path == 3) return;
@@ -259,6 +259,80 @@ __global__ void __launch_bounds__(128) k_robust4(LocalArgs<T> a) {
             if (!have) atomicAdd(&a.stats->fallback, 1u);
         }
         finish_tet<T, MODE, false>(a, e, g, ws, wv, F, U, W, s);
+    }
+}
+
+// Same pass with a warp-per-start layout: a CTA takes 32 queued elements, warp
+// w runs start w of all 32 (lane = element).  Lanes of a warp then follow the
+// same start, whose trip counts are alike across elements (e.g. the sigma/cbrt
+// start usually stalls for all 20 Newton iterations), so a warp costs about
+// its slowest lane instead of the serialised union of four different starts
+// of eight elements, and the four starts still run concurrently on four warps.
+// Warp 0 loads the tet, shares sigma through shared memory, then selects the
+// winner in start order (material.py:264-280) and writes the corners.
+#ifndef VK_ROBUST_MINB
+#define VK_ROBUST_MINB 4
+#endif
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128, VK_ROBUST_MINB) k_robust_ws(LocalArgs<T> a) {
+    __shared__ double s_sig[32][3];
+    __shared__ double s_res[4][32][4];
+    __shared__ int s_ok[4][32];
+    __shared__ int s_chunk;
+    const int cnt = *a.robust_count;
+    if (cnt == 0) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (;;) {
+        // chunks of 32 queued elements handed out dynamically (robust_count[1] is the cursor):
+        // per-chunk cost varies with how many Newton starts stall
+        if (threadIdx.x == 0) s_chunk = atomicAdd(a.robust_count + 1, 1);
+        __syncthreads();
+        const int base = s_chunk * 32;
+        if (base >= cnt) break;
+        const int i = base + lane;
+        const bool act = i < cnt;
+        const int e = act ? a.robust_list[i] : 0;
+        T g[3][3], F[3][3], ws, wv, U[3][3], W[3][3], sig[3];
+        if (w == 0 && act) {
+            load_tet<T, false>(a, e, g, ws, wv, F);
+            svd3_rv(F, U, sig, W);
+            s_sig[lane][0] = (double)sig[0];
+            s_sig[lane][1] = (double)sig[1];
+            s_sig[lane][2] = (double)sig[2];
+        }
+        __syncthreads();
+        if (act) {
+            const double sd[3] = {s_sig[lane][0], s_sig[lane][1], s_sig[lane][2]};
+            double st[3], sk[3] = {0, 0, 0}, obj = 0.0;
+            const bool ok = sl3::robust_start(sd, w, st) && sl3::robust_try(sd, st, sk, obj);
+            s_ok[w][lane] = ok;
+            s_res[w][lane][0] = sk[0];
+            s_res[w][lane][1] = sk[1];
+            s_res[w][lane][2] = sk[2];
+            s_res[w][lane][3] = obj;
+        }
+        __syncthreads();
+        if (w == 0 && act) {
+            bool have = false;
+            double best = 0.0, s[3] = {0, 0, 0};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double ob = s_res[k][lane][3];
+                if (s_ok[k][lane] && (!have || ob < best - 1e-15)) {
+                    have = true;
+                    best = ob;
+                    s[0] = s_res[k][lane][0]; s[1] = s_res[k][lane][1]; s[2] = s_res[k][lane][2];
+                }
+            }
+            const double sd[3] = {s_sig[lane][0], s_sig[lane][1], s_sig[lane][2]};
+            if (!have) sl3::robust_fallback(sd, s);
+            if (a.stats) {
+                atomicAdd(&a.stats->robust, 1u);
+                if (!have) atomicAdd(&a.stats->fallback, 1u);
+            }
+            finish_tet<T, MODE, false>(a, e, g, ws, wv, F, U, W, s);
+        }
+        __syncthreads();
     }
 }
 

@@ -28,6 +28,11 @@ constexpr double kFloor = 0.01;     // material.py:25
 constexpr double kTol = 1e-12;      // material.py:30
 constexpr int kIters = 20;          // material.py:29
 
+// instrumentation hook for tests/native probes (iteration / line-search / round counters)
+#ifndef VK_SL3_PROBE
+#define VK_SL3_PROBE(k)
+#endif
+
 VK_HD double nanmax(double m, double a) { return (a > m || a != a) ? a : m; }
 
 VK_HD void pairprod(const double (&s)[3], double (&p)[3]) {
@@ -96,8 +101,10 @@ VK_HD bool kkt_bordered_step(const R (&r)[4], const R (&p)[3], R (&s)[3], R& lam
     const R par = p[0] * ar0 + p[1] * ar1 + p[2] * ar2;
     if (!(fabs(det) > R(1e-6) && fabs(pap) > R(1e-12) * fabs(det) * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2])))
         return false;
-    const R dl = (r[3] * det - par) / pap;
-    const R idet = R(1) / det;
+    // one reciprocal for both divisions: 1/pap = det q, 1/det = pap q
+    const R q = R(1) / (det * pap);
+    const R dl = (r[3] * det - par) * (det * q);
+    const R idet = pap * q;
     s[0] -= (ar0 + ap0 * dl) * idet;
     s[1] -= (ar1 + ap1 * dl) * idet;
     s[2] -= (ar2 + ap2 * dl) * idet;
@@ -124,6 +131,7 @@ VK_HD bool kkt_newton_f64(const double (&sig)[3], double (&s)[3], double& lam, i
     for (int it = 0; it < budget; ++it) {
         const double rn = kkt_residual(sig, s, lam, r, p);
         if (rn < kTol) break;
+        VK_SL3_PROBE(3);
         if (!kkt_bordered_step(r, p, s, lam)) {
             const double a = lam * s[2], b = lam * s[1], c = lam * s[0];
             double J[4][4] = {{1.0, a, b, p[0]}, {a, 1.0, c, p[1]}, {b, c, 1.0, p[2]}, {p[0], p[1], p[2], 0.0}};
@@ -179,28 +187,49 @@ VK_HD double free_resnorm(const double (&sig)[3], const double (&s)[3], double l
     return rn;
 }
 
+// same residual, also returning the masked residual vector and the pair products
+VK_HD double free_res(const double (&sig)[3], const double (&s)[3], double lam, const bool (&fr)[3],
+                      double (&rr)[4], double (&p)[3]) {
+    pairprod(s, p);
+    rr[3] = s[0] * s[1] * s[2] - 1.0;
+    double rn = fabs(rr[3]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        rr[i] = fr[i] ? (s[i] - sig[i] + lam * p[i]) : 0.0;
+        if (fr[i]) rn = nanmax(rn, fabs(rr[i]));
+    }
+    return rn;
+}
+
 // `_sl3_newton_free` (material.py:171-214).  The reduced (nf+1) system is
 // solved embedded in the 4x4 one: frozen entries get an identity row/column
 // and a zero right-hand side, so their update is exactly zero.
+//
+// Same iterates as the reference loop, shorter dependency chain:
+//  - the residual of the accepted line-search point is the next iteration's
+//    residual (the reference recomputes the same value);
+//  - the damped line search (step 1, 1/2, ..., 1/32; first step whose residual
+//    drops, else the last) tries the full step first and, when that fails,
+//    evaluates the five shorter steps independently (steps are exact powers of
+//    two, so every candidate is the value the sequential halving produces) and
+//    takes the first acceptable one.  A stalled start (the usual fate of the
+//    sigma/cbrt start on strongly stretched tets) then costs two residual
+//    latencies per iteration instead of up to six.
 VK_HD bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, const bool (&fr)[3]) {
     const int nf = (int)fr[0] + (int)fr[1] + (int)fr[2];
     if (nf == 0) return false;
+    double rr[4], p[3];
+    double rn = free_res(sig, s, lam, fr, rr, p);
     for (int it = 0; it < kIters; ++it) {
-        const double rn = free_resnorm(sig, s, lam, fr);
         if (rn < kTol) return true;
-        double p[3];
-        pairprod(s, p);
+        VK_SL3_PROBE(0);
         double d[4];
         {
             // masked bordered system: frozen entries get identity rows/cols, zero p and rhs;
             // solved through the adjugate (kkt_bordered_step), pivoted elimination if A is near singular
-            double rr[4], pm[3], sd[3] = {0.0, 0.0, 0.0}, ld = 0.0;
+            double pm[3], sd[3] = {0.0, 0.0, 0.0}, ld = 0.0;
 #pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                pm[i] = fr[i] ? p[i] : 0.0;
-                rr[i] = fr[i] ? (s[i] - sig[i] + lam * p[i]) : 0.0;
-            }
-            rr[3] = s[0] * s[1] * s[2] - 1.0;
+            for (int i = 0; i < 3; ++i) pm[i] = fr[i] ? p[i] : 0.0;
             const double a = (fr[0] && fr[1]) ? lam * s[2] : 0.0;
             const double b = (fr[0] && fr[2]) ? lam * s[1] : 0.0;
             const double c = (fr[1] && fr[2]) ? lam * s[0] : 0.0;
@@ -217,8 +246,9 @@ VK_HD bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, cons
             const double par = pm[0] * ar0 + pm[1] * ar1 + pm[2] * ar2;
             const double pp = pm[0] * pm[0] + pm[1] * pm[1] + pm[2] * pm[2];
             if (fabs(det) > 1e-6 && fabs(pap) > 1e-12 * fabs(det) * pp) {
-                ld = (rr[3] * det - par) / pap;
-                const double idet = 1.0 / det;
+                const double q = 1.0 / (det * pap);
+                ld = (rr[3] * det - par) * (det * q);
+                const double idet = pap * q;
                 sd[0] = -(ar0 + ap0 * ld) * idet;
                 sd[1] = -(ar1 + ap1 * ld) * idet;
                 sd[2] = -(ar2 + ap2 * ld) * idet;
@@ -242,26 +272,46 @@ VK_HD bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, cons
                 if (!gesv4(J, d)) return false;
             }
         }
-        double step = 1.0;
-        double sn[3] = {s[0], s[1], s[2]}, ln = lam;
-        for (int t = 0; t < 6; ++t) {
+        double sn[3], ln, rrn[4], pn[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) sn[i] = fr[i] ? s[i] + d[i] : s[i];
+        ln = lam + d[3];
+        VK_SL3_PROBE(1);
+        double rn_new = free_res(sig, sn, ln, fr, rrn, pn);
+        if (!(rn_new < rn || rn_new < kTol)) {
+            // steps 1/2 .. 1/32 (material.py:203-211), evaluated independently
+            double step = 0.5;
+            int take = 5;
+#pragma unroll
+            for (int t = 1; t < 6; ++t) {
+                double st[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) st[i] = fr[i] ? s[i] + step * d[i] : s[i];
+                const double rt = free_resnorm(sig, st, lam + step * d[3], fr);
+                if (take == 5 && (rt < rn || rt < kTol)) take = t;
+                step *= 0.5;
+            }
+            step = ldexp(1.0, -take);
 #pragma unroll
             for (int i = 0; i < 3; ++i) sn[i] = fr[i] ? s[i] + step * d[i] : s[i];
             ln = lam + step * d[3];
-            const double rn_new = free_resnorm(sig, sn, ln, fr);
-            if (rn_new < rn || rn_new < kTol) break;
-            step *= 0.5;
+            VK_SL3_PROBE(1);
+            rn_new = free_res(sig, sn, ln, fr, rrn, pn);
         }
         s[0] = sn[0]; s[1] = sn[1]; s[2] = sn[2];
         lam = ln;
+        rr[0] = rrn[0]; rr[1] = rrn[1]; rr[2] = rrn[2]; rr[3] = rrn[3];
+        p[0] = pn[0]; p[1] = pn[1]; p[2] = pn[2];
+        rn = rn_new;
     }
-    return free_resnorm(sig, s, lam, fr) < 1e-10;
+    return rn < 1e-10;
 }
 
 // `_sl3_solve_clamping` (material.py:217-239); returns false for "None"
 VK_HD bool solve_clamping(const double (&sig)[3], double (&s)[3], double& lam) {
     bool fr[3] = {true, true, true};
     for (int round = 0; round < 3; ++round) {
+        VK_SL3_PROBE(2);
         for (int i = 0; i < 3; ++i) if (!fr[i]) s[i] = kFloor;
         if (!newton_free(sig, s, lam, fr)) return false;
         bool viol[3], any = false;
@@ -429,6 +479,7 @@ VK_HD int project(const double (&sig)[3], double (&s)[3], bool defer = false) {
         for (int i = 0; i < 3; ++i) s2[i] = fmax(sig[i], kFloor);
         s2[j] = fmax(1.0 / fmax(others, 1e-12), kFloor);
         double lam2;
+        VK_SL3_PROBE(2);
         const bool ok2 = kkt_newton(sig, s2, lam2);
         const double obj2 = sq3(s2, sig);
         if (ok2 && nanmin3(s2) >= kFloor - 1e-12 && obj2 < obj - 1e-15) {

@@ -195,6 +195,8 @@ struct Ctx : CtxBase {
     DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
     DBuf<V4> m1, qq, ss, pp;             // pipelined-CG recurrences
     bool pcg_classic = false;
+    bool robust_quad = false;            // env VKPD_ROBUST=quad: quad-per-element robust pass (A/B only)
+    int robust_blocks = 4;               // k_robust_ws CTAs per SM (its co-residency)
     bool fused = false;                  // whole frame in one cooperative kernel (env VKPD_FUSED=1); measured
                                          // slower than per-phase kernels in a graph (register spills)
     int frame_blocks = 0;
@@ -393,6 +395,10 @@ struct Ctx : CtxBase {
         if (const char* pt = getenv("VKPD_PCG_THREADS")) kPcgThreads = std::max(64, std::min(512, atoi(pt)));
         const char* pv = getenv("VKPD_PCG");
         pcg_classic = !(pv && std::string(pv) == "pipe");   // classic measured faster at C3
+        const char* rb = getenv("VKPD_ROBUST");
+        robust_quad = rb && std::string(rb) == "quad";
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&robust_blocks, vk::k_robust_ws<T, vk::MODE_RESID>, 128, 0));
+        robust_blocks = std::max(1, robust_blocks);   // chunks are handed out dynamically: one resident wave
         int occ = 0, occ2 = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_pcg<T>, kPcgThreads, 0));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, vk::k_pcg_classic<T>, kPcgThreads, 0));
@@ -419,8 +425,8 @@ struct Ctx : CtxBase {
         CK(cudaMemsetAsync(iters.p, 0, 1024 * sizeof(int), s));
         CK(fail_iter.alloc(1));
         CK(robust_list.alloc(std::max(1, nE)));
-        CK(robust_count.alloc(1));
-        CK(cudaMemsetAsync(robust_count.p, 0, sizeof(int), s));
+        CK(robust_count.alloc(2));   // [0] queued elements, [1] k_robust_ws chunk cursor
+        CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), s));
         CK(pstats.alloc(1));
         CK(cudaMemsetAsync(pstats.p, 0, sizeof(vk::ProjStats), s));
         CK(stage.alloc((size_t)3 * n));
@@ -628,11 +634,14 @@ struct Ctx : CtxBase {
     }
     // local step in residual form, suspicious elements compacted into a dense second pass
     int launch_local_resid(const vk::LocalArgs<T>& la) {
-        CK(cudaMemsetAsync(robust_count.p, 0, sizeof(int), stream));
+        CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
         vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
         CK(cudaGetLastError());
         // 4 CTAs/SM: enough lanes for the heavy frames, cheap when the queue is empty
-        vk::k_robust4<T, vk::MODE_RESID><<<4 * n_sms, 128, 0, stream>>>(la);
+        if (robust_quad)
+            vk::k_robust4<T, vk::MODE_RESID><<<4 * n_sms, 128, 0, stream>>>(la);
+        else
+            vk::k_robust_ws<T, vk::MODE_RESID><<<robust_blocks * n_sms, 128, 0, stream>>>(la);
         CK(cudaGetLastError());
         return VKPD_OK;
     }
