@@ -198,6 +198,7 @@ __device__ __forceinline__ void finish_tet(const LocalArgs<T>& a, int e, const T
 
 template <typename T, int MODE, bool WITH_FRV, int PASS = 0>
 __global__ void __launch_bounds__(128, VK_LOCAL_MINB) k_local(LocalArgs<T> a) {
+    if (PASS == 1) pcg_mark(8);
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= a.nE) return;
     local_tet<T, MODE, WITH_FRV, false, PASS>(a, e);
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(128, VK_ROBUST_MINB) k_robust_ws(LocalArgs<T> 
     __shared__ double s_res[4][32][4];
     __shared__ int s_ok[4][32];
     __shared__ int s_chunk;
+    pcg_mark(9);
     const int cnt = *a.robust_count;
     if (cnt == 0) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -96,6 +96,7 @@ template <typename T>
 __global__ void k_prologue(int n, int nF, T dt, const T* __restrict__ dt2_inv_m, const vec4_t<T>* __restrict__ f,
                            const vec4_t<T>* __restrict__ pin_tgt, vec4_t<T>* x, vec4_t<T>* v,
                            vec4_t<T>* x_start, vec4_t<T>* v_start, vec4_t<T>* xhat, int* fail_iter) {
+    pcg_mark(10);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) *fail_iter = 0x7fffffff;
     if (i >= n) return;
@@ -115,6 +116,7 @@ __global__ void k_prologue(int n, int nF, T dt, const T* __restrict__ dt2_inv_m,
 template <typename T>
 __global__ void k_epilogue(int n, T damp_over_dt, const vec4_t<T>* __restrict__ x,
                            const vec4_t<T>* __restrict__ x_start, vec4_t<T>* v) {
+    pcg_mark(11);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const vec4_t<T> a = x[i], b = x_start[i];
@@ -128,6 +130,20 @@ __global__ void k_restore(int n, vec4_t<T>* x, vec4_t<T>* v, const vec4_t<T>* x_
     if (i >= n) return;
     x[i] = x_start[i];
     v[i] = v_start[i];
+}
+
+// Gershgorin bound of D^-1 K_ff: max_i sum_{j != i} |K_ij| / K_ii (the caller adds 1).
+// Non-negative doubles order like their bit patterns, so an integer atomicMax works.
+template <typename T>
+__global__ void k_gershgorin(int nF, int ell_w, const int* __restrict__ ell_col, const T* __restrict__ ell_val,
+                             const double* __restrict__ diag64, unsigned long long* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    double off = 0.0;
+    for (int s = 0; s < ell_w; ++s)
+        if (ell_col[(size_t)s * nF + i] != i) off += fabs((double)ell_val[(size_t)s * nF + i]);
+    const double g = off / diag64[i];
+    atomicMax(out, (unsigned long long)__double_as_longlong(g >= 0.0 ? g : 0.0));
 }
 
 // rhs_i = sum over incidences of corner contributions (tet order) -- the
@@ -197,7 +213,19 @@ struct PcgArgs {
     const T* cb;
     const double* coll;          // kCollStride doubles per collider
     int ncoll;
+    int* reset_count;            // optional: the local step's suspicious-tet queue, zeroed on entry
+    vec4_t<T>* h;                // POLY: h = K D^-1 r, updated with r
+    double omega;                // POLY: polynomial preconditioner weight
+    const T* ell_kd;             // POLY: ELL values of K_ff D^-1 (no contact diagonal), or null
 };
+
+template <typename T>
+__device__ __forceinline__ void pcg_entry(const PcgArgs<T>& a) {
+    if (a.reset_count != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+        a.reset_count[0] = 0;
+        a.reset_count[1] = 0;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // Colliders: plane {0, p0, n_hat} and sphere {1, c, r} (pdsolver.py:125-163).
@@ -258,20 +286,6 @@ __global__ void k_contact_setup(int nF, const vec4_t<T>* __restrict__ xhat, cons
 // Every CTA sums the per-CTA partials of the last phase in the same fixed
 // order after the grid barrier, so all CTAs hold bit-identical scalars (no
 // serial "last CTA" step, deterministic across runs).
-#ifdef VK_PCG_TRACE               // phase-timing experiment build only
-__device__ unsigned long long g_pcg_trace[8192];
-__device__ int g_pcg_trace_n;
-__device__ __forceinline__ void pcg_mark(int tag) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        const int k = g_pcg_trace_n;
-        if (k < 8190) { g_pcg_trace[k] = ((unsigned long long)tag << 56) | (t & 0xffffffffffffffull); g_pcg_trace_n = k + 1; }
-    }
-}
-#else
-__device__ __forceinline__ void pcg_mark(int) {}
-#endif
 
 template <int NV>
 __device__ __forceinline__ void pcg_allreduce(cg::grid_group& grid, double* partials, int& parity, double (&acc)[NV],
@@ -290,10 +304,110 @@ __device__ __forceinline__ void pcg_allreduce(cg::grid_group& grid, double* part
     parity ^= 1;
 }
 
+// Right-hand side of row i of the global solve: the PD residual b - K x
+// (deterministic gather of the node's corner run + inertia + contact terms,
+// pdsolver.py:292-298) or the given rhs; adds |b|^2 of the reference rhs to bb.
 template <typename T>
+__device__ __forceinline__ void init_residual_row(const PcgArgs<T>& a, int i, bool coherent_corners, T& rx, T& ry,
+                                                  T& rzv, double& bb) {
+    if (a.init == INIT_PD) {
+        rx = 0; ry = 0; rzv = 0;
+        const int k0 = a.inc_ptr[i], k1 = a.inc_ptr[i + 1];
+#pragma unroll 4
+        for (int k = k0; k < k1; ++k) {
+            const vec4_t<T> c = coherent_corners ? ld4(&a.corner[k]) : ldg4(&a.corner[k]);
+            rx += c.x; ry += c.y; rzv += c.z;
+        }
+        const T m = a.m_dt2[i];
+        const vec4_t<T> xh = a.xhat[i], xi = a.x[i];
+        rx += m * (xh.x - xi.x);
+        ry += m * (xh.y - xi.y);
+        rzv += m * (xh.z - xi.z);
+        if (a.ncoll > 0) {
+            // contact rows: b += cw * surface_target(x), K x += m cw x (pdsolver.py:294-297)
+            const T w = a.cb[i];
+            if (w != T(0)) {
+                double tx, ty, tz;
+                collider_target(a.coll, a.ncoll, (double)xi.x, (double)xi.y, (double)xi.z, tx, ty, tz);
+                // cw (target - x) - (m - 1) cw x: the penetration vector is formed
+                // before scaling by the (1e4 K_ii) weight, which keeps float32 exact enough
+                const T extra = a.cdiag[i] - w;
+                rx += w * (T)(tx - (double)xi.x) - extra * xi.x;
+                ry += w * (T)(ty - (double)xi.y) - extra * xi.y;
+                rzv += w * (T)(tz - (double)xi.z) - extra * xi.z;
+            }
+        }
+        const double bx = (double)m * xh.x, by = (double)m * xh.y, bz = (double)m * xh.z;
+        bb += bx * bx + by * by + bz * bz;
+    } else {
+        const vec4_t<T> b = a.rhs[i];
+        rx = b.x; ry = b.y; rzv = b.z;
+        bb += (double)rx * rx + (double)ry * ry + (double)rzv * rzv;
+    }
+}
+
+// (K_ff D^-1 v)_i, contact diagonal included: one ELL row against D^-1 v
+template <typename T>
+__device__ __forceinline__ vec4_t<T> kdinv_row(const PcgArgs<T>& a, const vec4_t<T>* v, int i) {
+    const int nF = a.nF;
+    T hx = 0, hy = 0, hz = 0;
+    if (a.ell_kd != nullptr && a.ell_w <= kEllUnroll) {
+        // prescaled values K_ij / K_jj: same load pattern as the p-update SpMV
+        int cols[kEllUnroll];
+        T vals[kEllUnroll];
+#pragma unroll
+        for (int s = 0; s < kEllUnroll; ++s) {
+            cols[s] = s < a.ell_w ? __ldg(&a.ell_col[(size_t)s * nF + i]) : i;
+            vals[s] = s < a.ell_w ? __ldg(&a.ell_kd[(size_t)s * nF + i]) : T(0);
+        }
+#pragma unroll
+        for (int s = 0; s < kEllUnroll; ++s) {
+            if (s < a.ell_w) {
+                const vec4_t<T> vc = ld4(&v[cols[s]]);
+                hx += vals[s] * vc.x; hy += vals[s] * vc.y; hz += vals[s] * vc.z;
+            }
+        }
+    } else {
+        for (int s = 0; s < a.ell_w; ++s) {
+            const int c = __ldg(&a.ell_col[(size_t)s * nF + i]);
+            const T kd = __ldg(&a.ell_val[(size_t)s * nF + i]) * a.inv_diag[c];
+            const vec4_t<T> vc = ld4(&v[c]);
+            hx += kd * vc.x; hy += kd * vc.y; hz += kd * vc.z;
+        }
+    }
+    if (a.cdiag != nullptr) {
+        const vec4_t<T> vi = ld4(&v[i]);
+        const T kd = a.cdiag[i] * a.inv_diag[i];
+        hx += kd * vi.x; hy += kd * vi.y; hz += kd * vi.z;
+    }
+    return make4<T>(hx, hy, hz, T(0));
+}
+
+// K_ff D^-1 in ELL: kd[s][i] = K[s][i] / K_{col,col}
+template <typename T>
+__global__ void k_scale_ell(int nF, int ell_w, const int* __restrict__ ell_col, const T* __restrict__ ell_val,
+                            const T* __restrict__ inv_diag, T* kd) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    for (int s = 0; s < ell_w; ++s) {
+        const size_t k = (size_t)s * nF + i;
+        kd[k] = ell_val[k] * inv_diag[ell_col[k]];
+    }
+}
+
+// POLY = true: preconditioner M^-1 = w D^-1 (2 I - w K D^-1) (one Neumann step
+// on weighted Jacobi; SPD while w lambda_max(D^-1 K) < 2, w set from the
+// Gershgorin bound at assembly).  It roughly halves the CG iterations at C3.
+// h = K D^-1 r is carried alongside r (h -= alpha K D^-1 q, with q read at
+// the neighbour rows after the alpha barrier), so applying M^-1 costs one
+// SpMV inside the existing update phase and no extra grid barrier; only the
+// first application (h0 from r0) needs one more barrier, taken only when the
+// initial residual is above tolerance.
+template <typename T, bool POLY = false>
 __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_group& grid, double* smem,
                                                  double* red, bool coherent_corners) {
     pcg_mark(0);
+    pcg_entry(a);
     const int nF = a.nF;
     const int chunk = (nF + gridDim.x - 1) / gridDim.x;
     const int row0 = blockIdx.x * chunk;
@@ -302,44 +416,11 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
     double rz[3], rzp[3] = {1.0, 1.0, 1.0}, rr, bb;
 
     // ---- init: residual, z = D^-1 r, p0 = 0, dx = 0
-    {
+    if (!POLY) {
         double acc[5] = {0, 0, 0, 0, 0};     // rz x3, rr, bb
         for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
             T rx, ry, rzv;
-            if (a.init == INIT_PD) {
-                rx = 0; ry = 0; rzv = 0;
-                const int k0 = a.inc_ptr[i], k1 = a.inc_ptr[i + 1];
-#pragma unroll 4
-                for (int k = k0; k < k1; ++k) {
-                    const vec4_t<T> c = coherent_corners ? ld4(&a.corner[k]) : ldg4(&a.corner[k]);
-                    rx += c.x; ry += c.y; rzv += c.z;
-                }
-                const T m = a.m_dt2[i];
-                const vec4_t<T> xh = a.xhat[i], xi = a.x[i];
-                rx += m * (xh.x - xi.x);
-                ry += m * (xh.y - xi.y);
-                rzv += m * (xh.z - xi.z);
-                if (a.ncoll > 0) {
-                    // contact rows: b += cw * surface_target(x), K x += m cw x (pdsolver.py:294-297)
-                    const T w = a.cb[i];
-                    if (w != T(0)) {
-                        double tx, ty, tz;
-                        collider_target(a.coll, a.ncoll, (double)xi.x, (double)xi.y, (double)xi.z, tx, ty, tz);
-                        // cw (target - x) - (m - 1) cw x: the penetration vector is formed
-                        // before scaling by the (1e4 K_ii) weight, which keeps float32 exact enough
-                        const T extra = a.cdiag[i] - w;
-                        rx += w * (T)(tx - (double)xi.x) - extra * xi.x;
-                        ry += w * (T)(ty - (double)xi.y) - extra * xi.y;
-                        rzv += w * (T)(tz - (double)xi.z) - extra * xi.z;
-                    }
-                }
-                const double bx = (double)m * xh.x, by = (double)m * xh.y, bz = (double)m * xh.z;
-                acc[4] += bx * bx + by * by + bz * bz;
-            } else {
-                const vec4_t<T> b = a.rhs[i];
-                rx = b.x; ry = b.y; rzv = b.z;
-                acc[4] += (double)rx * rx + (double)ry * ry + (double)rzv * rzv;
-            }
+            init_residual_row(a, i, coherent_corners, rx, ry, rzv, acc[4]);
             const T d = a.inv_diag[i];
             const vec4_t<T> zi = make4<T>(d * rx, d * ry, d * rzv, T(0));
             a.r[i] = make4<T>(rx, ry, rzv, T(0));
@@ -355,6 +436,40 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
         for (int c = 0; c < 3; ++c) rz[c] = red[c];
         rr = red[3];
         bb = red[4];
+    } else {
+        {
+            double acc[2] = {0, 0};          // rr, bb
+            for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+                T rx, ry, rzv;
+                init_residual_row(a, i, coherent_corners, rx, ry, rzv, acc[1]);
+                a.r[i] = make4<T>(rx, ry, rzv, T(0));
+                a.p0[i] = make4<T>(T(0), T(0), T(0), T(0));
+                a.dx[i] = make4<T>(T(0), T(0), T(0), T(0));
+                acc[0] += (double)rx * rx + (double)ry * ry + (double)rzv * rzv;
+            }
+            pcg_allreduce<2>(grid, a.partials, parity, acc, red, smem);
+            rr = red[0];
+            bb = red[1];
+        }
+        rz[0] = rz[1] = rz[2] = 0.0;
+        if (rr > a.tol * a.tol * bb && a.max_iters > 0) {
+            const T w = (T)a.omega;
+            double acc[3] = {0, 0, 0};
+            for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+                const vec4_t<T> hi = kdinv_row(a, a.r, i);
+                const vec4_t<T> ri = ld4(&a.r[i]);
+                const T wd = w * a.inv_diag[i];
+                const vec4_t<T> zi = make4<T>(wd * (T(2) * ri.x - w * hi.x), wd * (T(2) * ri.y - w * hi.y),
+                                              wd * (T(2) * ri.z - w * hi.z), T(0));
+                a.h[i] = hi;
+                a.z[i] = zi;
+                acc[0] += (double)ri.x * zi.x;
+                acc[1] += (double)ri.y * zi.y;
+                acc[2] += (double)ri.z * zi.z;
+            }
+            pcg_allreduce<3>(grid, a.partials, parity, acc, red, smem);
+            for (int c = 0; c < 3; ++c) rz[c] = red[c];
+        }
     }
 
     int it = 0;
@@ -432,7 +547,19 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
                 d.x += ax * pn.x; d.y += ay * pn.y; d.z += az * pn.z;
                 ri.x -= ax * qi.x; ri.y -= ay * qi.y; ri.z -= az * qi.z;
                 const T dg = a.inv_diag[i];
-                const vec4_t<T> zi = make4<T>(dg * ri.x, dg * ri.y, dg * ri.z, T(0));
+                vec4_t<T> zi;
+                if (POLY) {
+                    // h -= alpha K D^-1 q (q of the neighbour rows is complete after the alpha barrier)
+                    const vec4_t<T> kq = kdinv_row(a, a.q, i);
+                    vec4_t<T> hi = ld4(&a.h[i]);
+                    hi.x -= ax * kq.x; hi.y -= ay * kq.y; hi.z -= az * kq.z;
+                    a.h[i] = hi;
+                    const T w = (T)a.omega, wd = w * dg;
+                    zi = make4<T>(wd * (T(2) * ri.x - w * hi.x), wd * (T(2) * ri.y - w * hi.y),
+                                  wd * (T(2) * ri.z - w * hi.z), T(0));
+                } else {
+                    zi = make4<T>(dg * ri.x, dg * ri.y, dg * ri.z, T(0));
+                }
                 a.dx[i] = d;
                 a.r[i] = ri;
                 a.z[i] = zi;
@@ -446,8 +573,10 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
             rr = red[3];
         }
     }
-    // ---- finish: x += dx (PD mode), finite check
-    bool bad = false;
+    // ---- finish: x += dx (PD mode), finite check.  Nothing to add after zero
+    // iterations; a non-finite iterate then shows up as a non-finite residual.
+    bool bad = a.init == INIT_PD && !(rr == rr && rr < INFINITY);
+    if (it > 0 || bad)
     for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
         const vec4_t<T> d = ld4(&a.dx[i]);
         if (a.init == INIT_PD) {
@@ -464,12 +593,26 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.iters_out = it;
 }
 
+#ifndef VK_PCG_LB
+#define VK_PCG_LB 768
+#endif
 template <typename T>
-__global__ void __launch_bounds__(512) k_pcg_classic(PcgArgs<T> a) {
+__global__ void __launch_bounds__(VK_PCG_LB) k_pcg_classic(PcgArgs<T> a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double smem[32 * 8];
     __shared__ double red[8];
-    pcg_classic_body(a, grid, smem, red, false);
+    pcg_classic_body<T, false>(a, grid, smem, red, false);
+}
+
+#ifndef VK_POLY_MAXNREG
+#define VK_POLY_MAXNREG 80     // 768 threads x 80 registers: one CTA per SM
+#endif
+template <typename T>
+__global__ void __maxnreg__(VK_POLY_MAXNREG) k_pcg_poly(PcgArgs<T> a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double smem[32 * 8];
+    __shared__ double red[8];
+    pcg_classic_body<T, true>(a, grid, smem, red, false);
 }
 
 // ---------------------------------------------------------------------------
@@ -525,6 +668,7 @@ __device__ __forceinline__ void pipe_dots(double (&acc)[8], const vec4_t<T>& r, 
 template <typename T>
 __global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
     pcg_mark(0);
+    pcg_entry(a);
     cg::grid_group grid = cg::this_grid();
     __shared__ double smem[32 * 8];
     __shared__ double red[8];
@@ -634,8 +778,10 @@ __global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
         for (int c = 0; c < 3; ++c) { g[c] = red[c]; dd[c] = red[3 + c]; }
         rr = red[6];
     }
-    // ---- finish: x += dx (PD mode), finite check
-    bool bad = false;
+    // ---- finish: x += dx (PD mode), finite check.  Nothing to add after zero
+    // iterations; a non-finite iterate then shows up as a non-finite residual.
+    bool bad = a.init == INIT_PD && !(rr == rr && rr < INFINITY);
+    if (it > 0 || bad)
     for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
         const vec4_t<T> d = ld4(&DX[i]);
         if (a.init == INIT_PD) {

@@ -258,4 +258,20 @@ __device__ __forceinline__ void grid_allreduce(FlagSlot* slots, unsigned long lo
     __syncthreads();
 }
 
+// Phase timeline (globaltimer marks of block 0, thread 0): experiment build only.
+#ifdef VK_PCG_TRACE               // phase-timing experiment build only
+__device__ unsigned long long g_pcg_trace[8192];
+__device__ int g_pcg_trace_n;
+__device__ __forceinline__ void pcg_mark(int tag) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const int k = g_pcg_trace_n;
+        if (k < 8190) { g_pcg_trace[k] = ((unsigned long long)tag << 56) | (t & 0xffffffffffffffull); g_pcg_trace_n = k + 1; }
+    }
+}
+#else
+__device__ __forceinline__ void pcg_mark(int) {}
+#endif
+
 }  // namespace vk

@@ -53,7 +53,6 @@ struct DBuf {
 };
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
-int kPcgThreads = 512;          // CTA size of the persistent solver (env VKPD_PCG_THREADS; 512 measured best)
 constexpr int kFrameThreads = 512;   // CTA size of the fused frame kernel
 
 // ---------------------------------------------------------------------------
@@ -191,10 +190,14 @@ struct Ctx : CtxBase {
     DBuf<int> ell_col, ell_len, fp_ptr, fp_col, inc_ptr, inc_code, int_of_orig;
     DBuf<int4> slot4;
     DBuf<double> diag64;
+    DBuf<T> ell_kd;                      // K_ff D^-1 (polynomial preconditioner)
     // state
     DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
     DBuf<V4> m1, qq, ss, pp;             // pipelined-CG recurrences
     bool pcg_classic = false;
+    int pcg_threads = 512;               // CTA size of the persistent solver
+    bool pcg_poly = true;                // Neumann-1 polynomial preconditioner (env VKPD_PCG=jacobi: plain Jacobi)
+    double poly_omega = 1.0;             // min(1, 1.9 / Gershgorin bound of D^-1 K_ff)
     bool robust_quad = false;            // env VKPD_ROBUST=quad: quad-per-element robust pass (A/B only)
     int robust_blocks = 4;               // k_robust_ws CTAs per SM (its co-residency)
     bool fused = false;                  // whole frame in one cooperative kernel (env VKPD_FUSED=1); measured
@@ -392,22 +395,48 @@ struct Ctx : CtxBase {
             CK(b->alloc(std::max(1, nF)));
             CK(cudaMemsetAsync(b->p, 0, std::max(1, nF) * sizeof(V4), s));
         }
-        if (const char* pt = getenv("VKPD_PCG_THREADS")) kPcgThreads = std::max(64, std::min(512, atoi(pt)));
+        // one row per thread where possible (each extra row per thread adds a full memory round
+        // trip to every solver phase): CTA size = rows per SM rounded up to a warp, <= 768
+        pcg_threads = std::max(128, std::min(768, 32 * cdiv(cdiv(std::max(1, nF), n_sms), 32)));
+        if (const char* pt = getenv("VKPD_PCG_THREADS")) pcg_threads = std::max(64, std::min(768, atoi(pt)));
         const char* pv = getenv("VKPD_PCG");
         pcg_classic = !(pv && std::string(pv) == "pipe");   // classic measured faster at C3
+        pcg_poly = !(pv && (std::string(pv) == "jacobi" || std::string(pv) == "pipe"));
+        if (!pcg_classic) pcg_threads = std::min(pcg_threads, 512);   // the pipelined kernel's bound
         const char* rb = getenv("VKPD_ROBUST");
         robust_quad = rb && std::string(rb) == "quad";
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&robust_blocks, vk::k_robust_ws<T, vk::MODE_RESID>, 128, 0));
         robust_blocks = std::max(1, robust_blocks);   // chunks are handed out dynamically: one resident wave
-        int occ = 0, occ2 = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_pcg<T>, kPcgThreads, 0));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, vk::k_pcg_classic<T>, kPcgThreads, 0));
-        occ = pcg_classic ? occ2 : occ;          // co-residency of the kernel actually launched
+        int occ = 0, occ2 = 0, occ3 = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_pcg<T>, pcg_threads, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, vk::k_pcg_classic<T>, pcg_threads, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, vk::k_pcg_poly<T>, pcg_threads, 0));
+        // co-residency of every kernel that may be launched (classic also serves contact frames)
+        occ = pcg_poly ? std::min(occ2, occ3) : pcg_classic ? occ2 : std::min(occ, occ2);
+        if (nF > 0) {
+            // Gershgorin bound G >= lambda_max(D^-1 K_ff); w = min(1, 1.9 / G) keeps
+            // w D^-1 (2 - w K D^-1) SPD with margin
+            DBuf<unsigned long long> gmax;
+            CK(gmax.alloc(1));
+            CK(cudaMemsetAsync(gmax.p, 0, sizeof(unsigned long long), s));
+            vk::k_gershgorin<T><<<cdiv(nF, 256), 256, 0, s>>>(nF, ell_w, ell_col.p, ell_val.p, diag64.p, gmax.p);
+            CK(cudaGetLastError());
+            unsigned long long gb = 0;
+            CK(cudaMemcpyAsync(&gb, gmax.p, sizeof gb, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            double g = 1.0;
+            std::memcpy(&g, &gb, sizeof g);
+            g += 1.0;
+            poly_omega = (g > 0.0 && std::isfinite(g)) ? std::min(1.0, 1.9 / g) : 0.5;
+            CK(ell_kd.alloc((size_t)std::max(1, ell_w) * nF));
+            vk::k_scale_ell<T><<<cdiv(nF, 256), 256, 0, s>>>(nF, ell_w, ell_col.p, ell_val.p, inv_diag.p, ell_kd.p);
+            CK(cudaGetLastError());
+        }
         if (occ < 1) return fail(VKPD_ECUDA, "persistent solver kernel cannot be resident");
         // default: one row per thread, capped by co-residency
         // default: at most one CTA per SM (fewer arrivals per grid barrier measured faster
         // than 2 CTAs/SM at C3), at least one row per thread
-        pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : std::min(cdiv(std::max(1, nF), kPcgThreads), n_sms);
+        pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : std::min(cdiv(std::max(1, nF), pcg_threads), n_sms);
         pcg_blocks = std::max(1, std::min(pcg_blocks, occ * n_sms));
         {
             const char* fz = getenv("VKPD_FUSED");
@@ -633,8 +662,9 @@ struct Ctx : CtxBase {
         return la;
     }
     // local step in residual form, suspicious elements compacted into a dense second pass
-    int launch_local_resid(const vk::LocalArgs<T>& la) {
-        CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
+    // reset = false inside a frame: the previous PD iteration's solver kernel zeroed the queue
+    int launch_local_resid(const vk::LocalArgs<T>& la, bool reset = true) {
+        if (reset) CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
         vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
         CK(cudaGetLastError());
         // 4 CTAs/SM: enough lanes for the heavy frames, cheap when the queue is empty
@@ -655,15 +685,18 @@ struct Ctx : CtxBase {
         pa.iters_out = iters_slot; pa.fail_iter = fail_iter.p; pa.pd_iter = pd_iter; pa.tol = tol;
         pa.max_iters = max_iters; pa.init = init;
         pa.cdiag = nullptr; pa.cb = nullptr; pa.coll = nullptr; pa.ncoll = 0;
+        pa.reset_count = nullptr;
+        pa.h = ss.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
         if (init == vk::INIT_PD && ncoll > 0) {
             pa.inv_diag = inv_diag_c.p; pa.cdiag = cdiag.p; pa.cb = cb.p; pa.coll = coll_d.p; pa.ncoll = ncoll;
+            pa.ell_kd = nullptr;                  // D changes with the contact set: scale on the fly
         }
         return pa;
     }
     cudaError_t launch_pcg(const vk::PcgArgs<T>& pa) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(pcg_blocks);
-        cfg.blockDim = dim3(kPcgThreads);
+        cfg.blockDim = dim3(pcg_threads);
         cfg.dynamicSmemBytes = 0;
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
@@ -671,6 +704,7 @@ struct Ctx : CtxBase {
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        if (pcg_poly) return cudaLaunchKernelEx(&cfg, vk::k_pcg_poly<T>, pa);
         if (pcg_classic || pa.ncoll > 0) return cudaLaunchKernelEx(&cfg, vk::k_pcg_classic<T>, pa);
         return cudaLaunchKernelEx(&cfg, vk::k_pcg<T>, pa);
     }
@@ -712,9 +746,13 @@ struct Ctx : CtxBase {
         const vk::LocalArgs<T> la = local_args(x.p);
         for (int it = 0; it < iterations; ++it) {
             if (ev) CK(cudaEventRecord((*ev)[3 * it], stream));
-            if (int rc = launch_local_resid(la)) return rc;
+            if (int rc = launch_local_resid(la, it == 0 || nF == 0)) return rc;
             if (ev) CK(cudaEventRecord((*ev)[3 * it + 1], stream));
-            if (nF > 0) CK(launch_pcg(pcg_args(vk::INIT_PD, it, iters.p + it)));
+            if (nF > 0) {
+                vk::PcgArgs<T> pa = pcg_args(vk::INIT_PD, it, iters.p + it);
+                pa.reset_count = robust_count.p;      // zero the suspicious-tet queue for the next local step
+                CK(launch_pcg(pa));
+            }
             if (ev) CK(cudaEventRecord((*ev)[3 * it + 2], stream));
         }
         vk::k_epilogue<T><<<nb, 256, 0, stream>>>(n, (T)(damping / dt), x.p, x_start.p, v.p);
