@@ -95,10 +95,15 @@ __global__ void k_assemble(AssembleArgs<T> a) {
 template <typename T>
 __global__ void k_prologue(int n, int nF, T dt, const T* __restrict__ dt2_inv_m, const vec4_t<T>* __restrict__ f,
                            const vec4_t<T>* __restrict__ pin_tgt, vec4_t<T>* x, vec4_t<T>* v,
-                           vec4_t<T>* x_start, vec4_t<T>* v_start, vec4_t<T>* xhat, int* fail_iter) {
+                           vec4_t<T>* x_start, vec4_t<T>* v_start, vec4_t<T>* xhat, int* fail_iter,
+                           int* zero2 = nullptr, int* zero1 = nullptr) {
     pcg_mark(10);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) *fail_iter = 0x7fffffff;
+    if (i == 0) {
+        *fail_iter = 0x7fffffff;
+        if (zero2) { zero2[0] = 0; zero2[1] = 0; }     // suspicious-tet queue of the first local step
+        if (zero1) *zero1 = 0;                          // PD-iteration counter of the loop node
+    }
     if (i >= n) return;
     const vec4_t<T> xi = x[i], vi = v[i];
     x_start[i] = xi;
@@ -217,7 +222,33 @@ struct PcgArgs {
     vec4_t<T>* h;                // POLY: h = K D^-1 r, updated with r
     double omega;                // POLY: polynomial preconditioner weight
     const T* ell_kd;             // POLY: ELL values of K_ff D^-1 (no contact diagonal), or null
+    int* pd_iter_dev;            // optional: PD iteration index read on the device (graph loop body);
+                                 // then fail_iter gets *pd_iter_dev and the count goes to iters_out[*pd_iter_dev]
+    unsigned long long loop_handle;   // nonzero: conditional handle of the PD-iteration loop node
+    int loop_iterations;
 };
+
+template <typename T>
+__device__ __forceinline__ void pcg_exit(const PcgArgs<T>& a, bool bad, int it) {
+    const int pdi = a.pd_iter_dev != nullptr ? *a.pd_iter_dev : a.pd_iter;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, pdi);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *(a.pd_iter_dev != nullptr ? a.iters_out + pdi : a.iters_out) = it;
+        if (a.loop_handle != 0) {
+            // PD-iteration loop node (graph WHILE): continue unless this was the last
+            // round, or the solve took zero CG iterations -- x did not change, so every
+            // remaining local step and solve would reproduce exactly this state (bit for
+            // bit) -- or a round has failed (a failure in this very launch may only be
+            // seen one round later; fail_iter keeps the earliest round either way).
+            // Skipped rounds are recorded with 0 CG iterations.
+            const bool stop = pdi + 1 >= a.loop_iterations || it == 0 || *(volatile int*)a.fail_iter != 0x7fffffff;
+            if (stop)
+                for (int j = pdi + 1; j < a.loop_iterations; ++j) a.iters_out[j] = 0;
+            *a.pd_iter_dev = pdi + 1;
+            cudaGraphSetConditional((cudaGraphConditionalHandle)a.loop_handle, stop ? 0u : 1u);
+        }
+    }
+}
 
 template <typename T>
 __device__ __forceinline__ void pcg_entry(const PcgArgs<T>& a) {
@@ -588,9 +619,8 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
             bad |= !(isfinite(d.x) && isfinite(d.y) && isfinite(d.z));
         }
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, a.pd_iter);
     pcg_mark(5);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *a.iters_out = it;
+    pcg_exit(a, bad, it);
 }
 
 #ifndef VK_PCG_LB
@@ -793,8 +823,7 @@ __global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
             bad |= !(isfinite(d.x) && isfinite(d.y) && isfinite(d.z));
         }
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, a.pd_iter);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *a.iters_out = it;
+    pcg_exit(a, bad, it);
 }
 
 }  // namespace vk

@@ -217,6 +217,9 @@ struct Ctx : CtxBase {
     double graph_damp = 0;
     bool graph_forces = false;
     bool graph_broken = false;
+    bool pd_early_exit = true;           // loop node with the zero-CG-iteration exit (env VKPD_PD_EXIT=0: off)
+    cudaStream_t body_stream = nullptr;  // captures the loop body
+    DBuf<int> pd_it;                     // device PD-iteration counter of the loop node
     int graph_ncoll = 0;
     // colliders (pdsolver.py:125-173, 271-297)
     int ncoll = 0;
@@ -228,6 +231,7 @@ struct Ctx : CtxBase {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (h_fail) cudaFreeHost(h_fail);
         if (own_stream) cudaStreamDestroy(own_stream);
+        if (body_stream) cudaStreamDestroy(body_stream);
     }
 
     int init(const vkpd_mesh_desc* d, const vkpd_config* c) override {
@@ -455,6 +459,11 @@ struct Ctx : CtxBase {
         CK(fail_iter.alloc(1));
         CK(robust_list.alloc(std::max(1, nE)));
         CK(robust_count.alloc(2));   // [0] queued elements, [1] k_robust_ws chunk cursor
+        CK(pd_it.alloc(1));
+        {
+            const char* pe = getenv("VKPD_PD_EXIT");
+            pd_early_exit = !(pe && std::string(pe) == "0");
+        }
         CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), s));
         CK(pstats.alloc(1));
         CK(cudaMemsetAsync(pstats.p, 0, sizeof(vk::ProjStats), s));
@@ -686,6 +695,7 @@ struct Ctx : CtxBase {
         pa.max_iters = max_iters; pa.init = init;
         pa.cdiag = nullptr; pa.cb = nullptr; pa.coll = nullptr; pa.ncoll = 0;
         pa.reset_count = nullptr;
+        pa.pd_iter_dev = nullptr; pa.loop_handle = 0; pa.loop_iterations = 0;
         pa.h = ss.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
         if (init == vk::INIT_PD && ncoll > 0) {
             pa.inv_diag = inv_diag_c.p; pa.cdiag = cdiag.p; pa.cb = cb.p; pa.coll = coll_d.p; pa.ncoll = ncoll;
@@ -761,15 +771,78 @@ struct Ctx : CtxBase {
         return VKPD_OK;
     }
 
+    // One frame for graph capture with the PD iterations in a conditional WHILE node:
+    // body = local step, robust pass, solver (which sets the loop condition).  The body stops after
+    // `iterations` rounds, on a non-finite solve, or as soon as a solve needs zero CG
+    // iterations (x unchanged: the remaining rounds would be exact repeats).
+    int enqueue_frame_loop(int iterations, double damping) {
+        const int nb = cdiv(n, 256);
+        vk::k_prologue<T><<<nb, 256, 0, stream>>>(n, nF, (T)dt, dt2_inv_m.p, has_forces ? f.p : nullptr,
+                                                  pin_tgt.p, x.p, v.p, x_start.p, v_start.p, xhat.p,
+                                                  fail_iter.p, robust_count.p, pd_it.p);
+        CK(cudaGetLastError());
+        if (ncoll > 0) {
+            vk::k_contact_setup<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, xhat.p, diag64.p, coll_d.p, ncoll,
+                                                                      contact_k, inv_diag_c.p, cdiag.p, cb.p);
+            CK(cudaGetLastError());
+        }
+        // conditional node after the captured prologue
+        cudaStreamCaptureStatus st;
+        cudaGraph_t g = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        CK(cudaStreamGetCaptureInfo(stream, &st, nullptr, &g, &deps, &ndeps));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        CK(cudaGraphAddNode(&cnode, g, deps, ndeps, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        if (!body_stream) CK(cudaStreamCreateWithFlags(&body_stream, cudaStreamNonBlocking));
+        CK(cudaStreamBeginCaptureToGraph(body_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        cudaStream_t outer = stream;
+        stream = body_stream;
+        int rc = VKPD_OK;
+        {
+            const vk::LocalArgs<T> la = local_args(x.p);
+            rc = launch_local_resid(la, false);
+            if (rc == VKPD_OK) {
+                vk::PcgArgs<T> pa = pcg_args(vk::INIT_PD, 0, iters.p);
+                pa.reset_count = robust_count.p;
+                pa.pd_iter_dev = pd_it.p;
+                pa.loop_handle = (unsigned long long)h;
+                pa.loop_iterations = iterations;
+                cudaError_t e = launch_pcg(pa);
+                if (e != cudaSuccess) rc = fail(VKPD_ECUDA, cudaGetErrorString(e));
+            }
+        }
+        stream = outer;
+        cudaGraph_t body_out = nullptr;
+        cudaError_t e = cudaStreamEndCapture(body_stream, &body_out);
+        if (rc) return rc;
+        CK(e);
+        CK(cudaStreamUpdateCaptureDependencies(stream, &cnode, 1, cudaStreamSetCaptureDependencies));
+        vk::k_epilogue<T><<<nb, 256, 0, stream>>>(n, (T)(damping / dt), x.p, x_start.p, v.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h_fail, fail_iter.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        return VKPD_OK;
+    }
+
     int build_graph(int iterations, double damping) {
         if (graph_exec) { cudaGraphExecDestroy(graph_exec); graph_exec = nullptr; }
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-        int rc = enqueue_frame(iterations, damping, nullptr);
+        const bool loop = pd_early_exit && iterations >= 2 && nF > 0 && !(fused && ncoll == 0);
+        int rc = loop ? enqueue_frame_loop(iterations, damping) : enqueue_frame(iterations, damping, nullptr);
         cudaError_t e = cudaStreamEndCapture(stream, &g);
         if (rc != VKPD_OK || e != cudaSuccess) {
             if (g) cudaGraphDestroy(g);
             cudaGetLastError();
+            if (loop) { pd_early_exit = false; return build_graph(iterations, damping); }   // plain unrolled frame
             graph_broken = true;
             return VKPD_OK;     // fall back to direct launches
         }
@@ -778,6 +851,7 @@ struct Ctx : CtxBase {
         if (e != cudaSuccess) {
             cudaGetLastError();
             graph_exec = nullptr;
+            if (loop) { pd_early_exit = false; return build_graph(iterations, damping); }
             graph_broken = true;
             return VKPD_OK;
         }

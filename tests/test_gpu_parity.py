@@ -233,6 +233,41 @@ def test_bit_identical_reruns(c1):
     assert np.array_equal(a, b)
 
 
+def _run_frames(sc, frames, precision, collect_every=1):
+    from paper_2405_12484_b200 import _abi
+    m = sc.mesh
+    ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s,
+                       sc.gammas.gamma_v, sc.pins, sc.dt, precision=precision,
+                       tol=pdsolver.DEFAULT_TOL[precision])
+    ctx.set_state(m.nodes)
+    ctx.set_pin_targets(sc.pin_targets)
+    ctx.set_forces(sc.forces)
+    xs, its = [], []
+    for k in range(frames):
+        ctx.step(30)
+        its.append(list(ctx.stats()["cg_iters"][:30]))
+        if (k + 1) % collect_every == 0:
+            xs.append(ctx.get_state()[0])
+    return np.stack(xs), its
+
+
+@pytest.mark.parametrize("config,frames,precision", [("C2", 40, "fp32"), ("C2", 10, "fp64"), ("C3", 100, "fp32")])
+def test_pd_loop_early_exit_is_exact(monkeypatch, config, frames, precision):
+    """The graph's PD-iteration loop stops at the first solve that needs zero CG
+    iterations (x unchanged, so the remaining rounds are exact repeats).  Same
+    bits as running every round; C3 to frame 100 crosses into the frames with
+    robust-path tets."""
+    sc = scenes.make_scene(config)
+    monkeypatch.setenv("VKPD_PD_EXIT", "0")
+    a, ia = _run_frames(sc, frames, precision, collect_every=5)
+    monkeypatch.delenv("VKPD_PD_EXIT")
+    b, ib = _run_frames(sc, frames, precision, collect_every=5)
+    assert np.array_equal(a, b)
+    assert ia == ib
+    if precision == "fp32":
+        assert any(0 in it for it in ib)     # the exit was actually taken (fp64 at 1e-12 rarely exits)
+
+
 def test_pin_path_and_per_step_forces(c1):
     steps = 3
     path = np.stack([c1.pin_targets + np.array([0.0, 0.0, 1e-3 * k]) for k in range(steps)])
