@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--tol", type=float, default=None)
     p.add_argument("--no-flush", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-all-rounds", action="store_true", help="skip the every-PD-round comparison run")
     p.add_argument("--cpu-sample-iters", type=int, default=3)
     return p.parse_args()
 
@@ -236,6 +237,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         ctx.step_async(its)
     ctx.sync()
+    rounds0 = ctx.stats()["pd_rounds_total"]
 
     def barrier():
         if world > 1:
@@ -262,6 +264,36 @@ def run_ours(args):
     frame_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     tot_ms = sum(frame_ms)
     st = ctx.stats()
+    rounds = st["pd_rounds_total"] - rounds0
+
+    # ---- the same frames with every PD round executed (no early loop exit): the rounds the
+    # default path skips are exact repeats (tests/test_gpu_parity.py::test_pd_loop_early_exit_is_exact)
+    all_rounds_ms = None
+    if not args.no_all_rounds:
+        import os as _os
+        _os.environ["VKPD_PD_EXIT"] = "0"
+        ctx2 = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s,
+                            sc.gammas.gamma_v, sc.pins, sc.dt, precision=args.precision, tol=ctx_tol(args),
+                            device=local)
+        del _os.environ["VKPD_PD_EXIT"]
+        ctx2.set_stream(stream.cuda_stream)
+        ctx2.set_state(m.nodes)
+        ctx2.set_pin_targets(sc.pin_targets)
+        ctx2.set_forces(sc.forces)
+        for _ in range(args.warmup):
+            ctx2.step_async(its)
+        ctx2.sync()
+        barrier()
+        for k in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            starts[k].record(stream)
+            ctx2.step_async(its)
+            ends[k].record(stream)
+        ctx2.sync()
+        barrier()
+        all_rounds_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+        del ctx2
 
     # ---- end to end through the public API with host buffers (pinned), copies inside
     hf = torch.empty((m.n_nodes, 3), dtype=torch.float64, pin_memory=True).numpy()
@@ -320,10 +352,15 @@ def run_ours(args):
         "config": {"workload": sc.name, "n_tets": nE, "n_nodes": m.n_nodes, "pd_iterations": its,
                    "dt": sc.dt, "solver": "direct-equivalent (device CG to tol)",
                    "tol": ctx_tol(args), "parallelism": f"replicas x{world}",
+                   "pd_loop": "graph WHILE node; stops at the first solve needing 0 CG iterations "
+                              "(later rounds repeat it bit for bit); value counts all 30 rounds",
                    "l2": "flushed between frames" if flush is not None else "not flushed"},
         "e2e": {"value": e2e_val, "unit": "tet-iters/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3 / args.steps},
-        "gpu_launches": args.steps * (3 * its + 2),      # prologue, its x (local, robust pass, CG), epilogue
+        # prologue + epilogue per frame; local step, robust pass, solver per executed PD round
+        "gpu_launches": int(args.steps * 2 + 3 * rounds),
+        "pd_rounds_executed_per_frame": rounds / args.steps,
+        "ms_per_step_every_round": all_rounds_ms,
         "roofline": {"bound": "hbm", "kernel": "k_local (PD local step)", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.precision), "traffic_source": "profiles/r01_launches_steady_summary.json (ncu dram read+write, cold L2)",

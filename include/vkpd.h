@@ -84,6 +84,8 @@ typedef struct {
     int64_t n_free;
     double local_ms[256];      /* per-PD-iteration event times of the last vkpd_profile_step */
     double global_ms[256];
+    unsigned long long pd_rounds_total; /* PD rounds executed since creation: a frame stops early once a
+                                           solve needs zero CG iterations (the rest would repeat it exactly) */
 } vkpd_stats;
 
 const char* vkpd_last_error(void);

@@ -32,6 +32,7 @@ enum LocalMode { MODE_RHS = 0, MODE_RESID = 1 };
 struct ProjStats {
     unsigned int robust;     // elements re-solved on the scalar path
     unsigned int fallback;   // robust path fell back to uniform scaling
+    unsigned long long pd_rounds;   // PD rounds executed (solver launches in the PD loop)
 };
 
 __device__ __forceinline__ void count_path(ProjStats* st, int path) {

@@ -226,6 +226,7 @@ struct PcgArgs {
                                  // then fail_iter gets *pd_iter_dev and the count goes to iters_out[*pd_iter_dev]
     unsigned long long loop_handle;   // nonzero: conditional handle of the PD-iteration loop node
     int loop_iterations;
+    unsigned long long* rounds;  // optional: executed-PD-round counter
 };
 
 template <typename T>
@@ -234,6 +235,7 @@ __device__ __forceinline__ void pcg_exit(const PcgArgs<T>& a, bool bad, int it) 
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, pdi);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *(a.pd_iter_dev != nullptr ? a.iters_out + pdi : a.iters_out) = it;
+        if (a.rounds != nullptr) *a.rounds += 1ull;
         if (a.loop_handle != 0) {
             // PD-iteration loop node (graph WHILE): continue unless this was the last
             // round, or the solve took zero CG iterations -- x did not change, so every

@@ -696,6 +696,7 @@ struct Ctx : CtxBase {
         pa.cdiag = nullptr; pa.cb = nullptr; pa.coll = nullptr; pa.ncoll = 0;
         pa.reset_count = nullptr;
         pa.pd_iter_dev = nullptr; pa.loop_handle = 0; pa.loop_iterations = 0;
+        pa.rounds = init == vk::INIT_PD ? &pstats.p->pd_rounds : nullptr;
         pa.h = ss.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
         if (init == vk::INIT_PD && ncoll > 0) {
             pa.inv_diag = inv_diag_c.p; pa.cdiag = cdiag.p; pa.cb = cb.p; pa.coll = coll_d.p; pa.ncoll = ncoll;
@@ -1214,6 +1215,7 @@ struct Ctx : CtxBase {
         CK(cudaMemcpy(&ps, pstats.p, sizeof(ps), cudaMemcpyDeviceToHost));
         st->robust = ps.robust;
         st->fallback = ps.fallback;
+        st->pd_rounds_total = ps.pd_rounds;
         st->pcg_blocks = pcg_blocks;
         st->ell_width = ell_w;
         st->n_free = nF;
