@@ -218,6 +218,7 @@ struct Ctx : CtxBase {
     bool graph_forces = false;
     bool graph_broken = false;
     bool pd_early_exit = true;           // loop node with the zero-CG-iteration exit (env VKPD_PD_EXIT=0: off)
+    int last_exec_rounds = 0;            // PD rounds of the last directly launched frame
     cudaStream_t body_stream = nullptr;  // captures the loop body
     DBuf<int> pd_it;                     // device PD-iteration counter of the loop node
     int graph_ncoll = 0;
@@ -755,6 +756,10 @@ struct Ctx : CtxBase {
             CK(cudaGetLastError());
         }
         const vk::LocalArgs<T> la = local_args(x.p);
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        CK(cudaStreamIsCapturing(stream, &cap));
+        const bool host_exit = pd_early_exit && nF > 0 && cap == cudaStreamCaptureStatusNone;
+        last_exec_rounds = iterations;
         for (int it = 0; it < iterations; ++it) {
             if (ev) CK(cudaEventRecord((*ev)[3 * it], stream));
             if (int rc = launch_local_resid(la, it == 0 || nF == 0)) return rc;
@@ -765,6 +770,17 @@ struct Ctx : CtxBase {
                 CK(launch_pcg(pa));
             }
             if (ev) CK(cudaEventRecord((*ev)[3 * it + 2], stream));
+            if (host_exit && it + 1 < iterations) {
+                // same early exit as the graph's loop node, decided on the host (direct launches)
+                int cgi = -1;
+                CK(cudaMemcpyAsync(&cgi, iters.p + it, sizeof(int), cudaMemcpyDeviceToHost, stream));
+                CK(cudaStreamSynchronize(stream));
+                if (cgi == 0) {
+                    CK(cudaMemsetAsync(iters.p + it + 1, 0, sizeof(int) * (iterations - it - 1), stream));
+                    last_exec_rounds = it + 1;
+                    break;
+                }
+            }
         }
         vk::k_epilogue<T><<<nb, 256, 0, stream>>>(n, (T)(damping / dt), x.p, x_start.p, v.p);
         CK(cudaGetLastError());
@@ -906,7 +922,8 @@ struct Ctx : CtxBase {
         double lsum = 0, gsum = 0;
         prof_local.assign(iterations, 0.0);
         prof_global.assign(iterations, 0.0);
-        for (int it = 0; it < iterations; ++it) {
+        const int nex = rc ? 0 : std::min(iterations, last_exec_rounds);   // rounds actually launched
+        for (int it = 0; it < nex; ++it) {
             float a = 0, b = 0;
             CK(cudaEventElapsedTime(&a, ev[3 * it], ev[3 * it + 1]));
             CK(cudaEventElapsedTime(&b, ev[3 * it + 1], ev[3 * it + 2]));
@@ -917,8 +934,8 @@ struct Ctx : CtxBase {
         float fr = 0;
         CK(cudaEventElapsedTime(&fr, ev[3 * iterations], ev[3 * iterations + 1]));
         for (auto& e : ev) cudaEventDestroy(e);
-        if (lms) *lms = iterations ? lsum / iterations : 0;
-        if (gms) *gms = iterations ? gsum / iterations : 0;
+        if (lms) *lms = nex ? lsum / nex : 0;
+        if (gms) *gms = nex ? gsum / nex : 0;
         if (fms) *fms = fr;
         if (rc) return rc;
         int failed = -1;
