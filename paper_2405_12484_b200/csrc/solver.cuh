@@ -227,10 +227,12 @@ struct PcgArgs {
     unsigned long long loop_handle;   // nonzero: conditional handle of the PD-iteration loop node
     int loop_iterations;
     unsigned long long* rounds;  // optional: executed-PD-round counter
+    vec4_t<T>* warm;             // POLY, optional: warm_rounds banks of nF; PD round k < warm_rounds starts
+    int warm_rounds;             // from the previous frame's round-k correction and stores its own
 };
 
 template <typename T>
-__device__ __forceinline__ void pcg_exit(const PcgArgs<T>& a, bool bad, int it) {
+__device__ __forceinline__ void pcg_exit(const PcgArgs<T>& a, bool bad, int it, bool moved = false) {
     const int pdi = a.pd_iter_dev != nullptr ? *a.pd_iter_dev : a.pd_iter;
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(a.fail_iter, pdi);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -243,7 +245,8 @@ __device__ __forceinline__ void pcg_exit(const PcgArgs<T>& a, bool bad, int it) 
             // bit) -- or a round has failed (a failure in this very launch may only be
             // seen one round later; fail_iter keeps the earliest round either way).
             // Skipped rounds are recorded with 0 CG iterations.
-            const bool stop = pdi + 1 >= a.loop_iterations || it == 0 || *(volatile int*)a.fail_iter != 0x7fffffff;
+            const bool stop = pdi + 1 >= a.loop_iterations || (it == 0 && !moved) ||
+                              *(volatile int*)a.fail_iter != 0x7fffffff;
             if (stop)
                 for (int j = pdi + 1; j < a.loop_iterations; ++j) a.iters_out[j] = 0;
             *a.pd_iter_dev = pdi + 1;
@@ -379,6 +382,25 @@ __device__ __forceinline__ void init_residual_row(const PcgArgs<T>& a, int i, bo
     }
 }
 
+// (K_ff v)_i, contact diagonal included
+template <typename T>
+__device__ __forceinline__ vec4_t<T> k_row(const PcgArgs<T>& a, const vec4_t<T>* v, int i) {
+    const int nF = a.nF;
+    T hx = 0, hy = 0, hz = 0;
+    for (int s = 0; s < a.ell_w; ++s) {
+        const int c = __ldg(&a.ell_col[(size_t)s * nF + i]);
+        const T kv = __ldg(&a.ell_val[(size_t)s * nF + i]);
+        const vec4_t<T> vc = ld4(&v[c]);
+        hx += kv * vc.x; hy += kv * vc.y; hz += kv * vc.z;
+    }
+    if (a.cdiag != nullptr) {
+        const vec4_t<T> vi = ld4(&v[i]);
+        const T cd = a.cdiag[i];
+        hx += cd * vi.x; hy += cd * vi.y; hz += cd * vi.z;
+    }
+    return make4<T>(hx, hy, hz, T(0));
+}
+
 // (K_ff D^-1 v)_i, contact diagonal included: one ELL row against D^-1 v
 template <typename T>
 __device__ __forceinline__ vec4_t<T> kdinv_row(const PcgArgs<T>& a, const vec4_t<T>* v, int i) {
@@ -447,6 +469,11 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
     const int row1 = min(nF, row0 + chunk);
     int parity = 0;
     double rz[3], rzp[3] = {1.0, 1.0, 1.0}, rr, bb;
+    // warm start: PD round k of a frame begins from the previous frame's round-k
+    // correction (same solution to the tolerance, fewer CG iterations)
+    const int pdi_w = a.pd_iter_dev != nullptr ? *a.pd_iter_dev : a.pd_iter;
+    const bool warm = POLY && a.warm != nullptr && a.init == INIT_PD && pdi_w < a.warm_rounds;
+    vec4_t<T>* const wb = warm ? a.warm + (size_t)pdi_w * nF : nullptr;
 
     // ---- init: residual, z = D^-1 r, p0 = 0, dx = 0
     if (!POLY) {
@@ -475,9 +502,16 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
             for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
                 T rx, ry, rzv;
                 init_residual_row(a, i, coherent_corners, rx, ry, rzv, acc[1]);
+                vec4_t<T> d0 = make4<T>(T(0), T(0), T(0), T(0));
+                if (warm) {
+                    // start from the previous frame's first correction: r -= K dx0
+                    d0 = ld4(&wb[i]);
+                    const vec4_t<T> kw = k_row(a, wb, i);
+                    rx -= kw.x; ry -= kw.y; rzv -= kw.z;
+                }
                 a.r[i] = make4<T>(rx, ry, rzv, T(0));
                 a.p0[i] = make4<T>(T(0), T(0), T(0), T(0));
-                a.dx[i] = make4<T>(T(0), T(0), T(0), T(0));
+                a.dx[i] = d0;
                 acc[0] += (double)rx * rx + (double)ry * ry + (double)rzv * rzv;
             }
             pcg_allreduce<2>(grid, a.partials, parity, acc, red, smem);
@@ -609,20 +643,21 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
     // ---- finish: x += dx (PD mode), finite check.  Nothing to add after zero
     // iterations; a non-finite iterate then shows up as a non-finite residual.
     bool bad = a.init == INIT_PD && !(rr == rr && rr < INFINITY);
-    if (it > 0 || bad)
+    if (it > 0 || bad || warm)
     for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
         const vec4_t<T> d = ld4(&a.dx[i]);
         if (a.init == INIT_PD) {
             vec4_t<T> xi = a.x[i];
             xi.x += d.x; xi.y += d.y; xi.z += d.z;
             a.x[i] = xi;
+            if (warm) wb[i] = d;
             bad |= !(isfinite(xi.x) && isfinite(xi.y) && isfinite(xi.z));
         } else {
             bad |= !(isfinite(d.x) && isfinite(d.y) && isfinite(d.z));
         }
     }
     pcg_mark(5);
-    pcg_exit(a, bad, it);
+    pcg_exit(a, bad, it, warm);
 }
 
 #ifndef VK_PCG_LB

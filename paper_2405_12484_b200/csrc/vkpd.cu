@@ -191,6 +191,9 @@ struct Ctx : CtxBase {
     DBuf<int4> slot4;
     DBuf<double> diag64;
     DBuf<T> ell_kd;                      // K_ff D^-1 (polynomial preconditioner)
+    DBuf<V4> warm0;                      // per-round corrections of the previous frame (solver warm start)
+    bool warm_start = true;              // env VKPD_WARM=0: off
+    int warm_rounds = 3;                 // env VKPD_WARM=<rounds>
     // state
     DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
     DBuf<V4> m1, qq, ss, pp;             // pipelined-CG recurrences
@@ -462,6 +465,13 @@ struct Ctx : CtxBase {
         CK(robust_count.alloc(2));   // [0] queued elements, [1] k_robust_ws chunk cursor
         CK(pd_it.alloc(1));
         {
+            const char* pw = getenv("VKPD_WARM");
+            if (pw) warm_rounds = std::max(0, std::min(8, atoi(pw)));
+            warm_start = warm_rounds > 0;
+        }
+        CK(warm0.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
+        CK(cudaMemsetAsync(warm0.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
+        {
             const char* pe = getenv("VKPD_PD_EXIT");
             pd_early_exit = !(pe && std::string(pe) == "0");
         }
@@ -613,6 +623,8 @@ struct Ctx : CtxBase {
         if (hv) rc = upload_nodes(hv, v.p);
         else CK(cudaMemsetAsync(v.p, 0, n * sizeof(V4), stream));
         if (rc) return rc;
+        // a new trajectory: no warm start from the previous one (results depend on the state only)
+        if (warm0.p) CK(cudaMemsetAsync(warm0.p, 0, warm0.n * sizeof(V4), stream));
         CK(cudaStreamSynchronize(stream));
         return VKPD_OK;
     }
@@ -698,6 +710,8 @@ struct Ctx : CtxBase {
         pa.reset_count = nullptr;
         pa.pd_iter_dev = nullptr; pa.loop_handle = 0; pa.loop_iterations = 0;
         pa.rounds = init == vk::INIT_PD ? &pstats.p->pd_rounds : nullptr;
+        pa.warm = (init == vk::INIT_PD && pcg_poly && warm_start) ? warm0.p : nullptr;
+        pa.warm_rounds = warm_rounds;
         pa.h = ss.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
         if (init == vk::INIT_PD && ncoll > 0) {
             pa.inv_diag = inv_diag_c.p; pa.cdiag = cdiag.p; pa.cb = cb.p; pa.coll = coll_d.p; pa.ncoll = ncoll;
@@ -775,7 +789,7 @@ struct Ctx : CtxBase {
                 int cgi = -1;
                 CK(cudaMemcpyAsync(&cgi, iters.p + it, sizeof(int), cudaMemcpyDeviceToHost, stream));
                 CK(cudaStreamSynchronize(stream));
-                if (cgi == 0) {
+                if (cgi == 0 && !(it < warm_rounds && warm_start && pcg_poly)) {   // a warm round moves x
                     CK(cudaMemsetAsync(iters.p + it + 1, 0, sizeof(int) * (iterations - it - 1), stream));
                     last_exec_rounds = it + 1;
                     break;
