@@ -13,6 +13,7 @@
  *   vkpd_get_state
  *   vkpd_set_pin_targets  SimState.pin_targets / per-step pin path (pdsolver.py:750-751)
  *   vkpd_set_forces       per-step external forces (pdsolver.py:744-752)
+ *   vkpd_set_gammas       MaterialField refresh + assemble_global (material.py:563-590, pdsolver.py:42-56)
  *   vkpd_step             pd_step (pdsolver.py:257-304)
  *   vkpd_set_colliders    SimState.colliders (pdsolver.py:125-173, 271-297)
  *   vkpd_elastic_rhs      elastic_rhs (pdsolver.py:59-71)
@@ -108,6 +109,10 @@ int vkpd_set_state(vkpd_ctx* ctx, const double* x, const double* v);      /* (nV
 int vkpd_get_state(vkpd_ctx* ctx, double* x, double* v);                  /* either may be NULL */
 int vkpd_set_pin_targets(vkpd_ctx* ctx, const double* targets);           /* (n_pins,3) */
 int vkpd_set_forces(vkpd_ctx* ctx, const double* forces);                 /* (nV,3) or NULL = none */
+/* new per-tet material (MaterialField, material.py:563-590) for the same mesh, pins and dt:
+ * the local-step weights and K (assemble_global, pdsolver.py:42-56) are rebuilt on the device
+ * (the fitting loop changes gamma every line-search trial, fitting.py:429-432) */
+int vkpd_set_gammas(vkpd_ctx* ctx, const double* gamma_s, const double* gamma_v);   /* (n_tets,) each */
 /* colliders of the following steps (SimState.colliders, pdsolver.py:125-173, 271-297):
  * kinds[c] = 0 plane (params: point xyz, normal xyz) or 1 sphere (centre xyz, radius, -, -);
  * params (n,6); nodes penetrating at the prediction get weight k * K_ii (n = 0: none) */

@@ -25,6 +25,7 @@ EXPORTS = (
     "vkpd_batch_projections", "vkpd_create_matrix", "vkpd_get_matrix_csr", "vkpd_a_jacobi_refine",
     "vkpd_power_rho", "vkpd_cms_set_basis", "vkpd_cms_solve", "vkpd_dev_residual", "vkpd_dev_apply_K",
     "vkpd_dev_inv_diag", "vkpd_get_node_order", "vkpd_get_sizes", "vkpd_set_colliders",
+    "vkpd_set_gammas",
 )
 
 
@@ -221,6 +222,11 @@ class Context:
 
     def set_forces(self, f):
         check(self.lib.vkpd_set_forces(self.h, None if f is None else ptr(f64(f, (self.n, 3)))))
+
+    def set_gammas(self, gamma_s, gamma_v):
+        """New per-tet material for the same mesh/pins/dt; K is re-assembled on the device."""
+        ne = self.n_tets
+        check(self.lib.vkpd_set_gammas(self.h, ptr(f64(gamma_s, (ne,))), ptr(f64(gamma_v, (ne,)))))
 
     def set_colliders(self, colliders, contact_stiffness=1e4):
         """colliders: sequence of ("plane", point, normal) / ("sphere", centre, radius)."""

@@ -145,6 +145,7 @@ struct CtxBase {
     virtual int get_state(double* x, double* v) = 0;
     virtual int set_pin_targets(const double* t) = 0;
     virtual int set_forces(const double* f) = 0;
+    virtual int set_gammas(const double* gs, const double* gv) = 0;
     virtual int set_colliders(int n, const int* kinds, const double* params, double kc) = 0;
     virtual int step_async(int iterations, double damping) = 0;
     virtual int sync(int* failed) = 0;
@@ -190,6 +191,8 @@ struct Ctx : CtxBase {
     DBuf<int> ell_col, ell_len, fp_ptr, fp_col, inc_ptr, inc_code, int_of_orig;
     DBuf<int4> slot4;
     DBuf<double> diag64;
+    DBuf<double> G64k, md64k;            // float64 shape gradients and m/dt^2 (re-assembly)
+    std::vector<double> vol2_h;          // 2 V per tet (host)
     DBuf<T> ell_kd;                      // K_ff D^-1 (polynomial preconditioner)
     DBuf<V4> warm0;                      // per-round corrections of the previous frame (solver warm start)
     bool warm_start = true;              // env VKPD_WARM=0: off
@@ -368,24 +371,74 @@ struct Ctx : CtxBase {
         CK(diag64.alloc(nF));
         CK(m_dt2.alloc(n)); CK(m_dt2.upload(mdt2_t.data(), n, s));
         CK(dt2_inv_m.alloc(n)); CK(dt2_inv_m.upload(dt2im.data(), n, s));
-        // assembly inputs (float64, freed after)
-        {
-            DBuf<double> G64, ws64, md64;
-            CK(G64.alloc((size_t)12 * nE)); CK(G64.upload(d->shape_grad, (size_t)12 * nE, s));
-            CK(ws64.alloc(nE)); CK(ws64.upload(wsum.data(), nE, s));
-            CK(md64.alloc(n)); CK(md64.upload(mdt2.data(), n, s));
-            vk::AssembleArgs<T> aa;
-            aa.nF = nF; aa.nE = nE; aa.ell_w = ell_w;
-            aa.inc_ptr = inc_ptr.p; aa.inc_code = inc_code.p; aa.tets = tets.p; aa.G = G64.p; aa.wsum = ws64.p;
-            aa.m_dt2 = md64.p; aa.ell_col = ell_col.p; aa.ell_len = ell_len.p; aa.ell_val = ell_val.p;
-            aa.inv_diag = inv_diag.p;
-            aa.diag64 = diag64.p; aa.fp_ptr = fp_ptr.p; aa.fp_col = fp_col.p; aa.fp_val = fp_val.p;
-            aa.n_free_cols_base = nF;
-            if (nF > 0) vk::k_assemble<T><<<cdiv(nF, 128), 128, 0, s>>>(aa);
-            CK(cudaGetLastError());
-            CK(cudaStreamSynchronize(s));
-        }
+        // assembly inputs (float64), kept for re-assembly when the material changes
+        CK(G64k.alloc((size_t)12 * nE)); CK(G64k.upload(d->shape_grad, (size_t)12 * nE, s));
+        CK(md64k.alloc(n)); CK(md64k.upload(mdt2.data(), n, s));
+        vol2_h.resize(nE);
+        for (int e = 0; e < nE; ++e) vol2_h[e] = 2.0 * d->volume[e];
+        if (int rc = assemble(wsum)) return rc;
         return alloc_work(c);
+    }
+
+    // K_ff / K_fp from the per-tet weights 2V(gs+gv) (pdsolver.py:42-56), deterministic
+    int assemble(const std::vector<double>& wsum) {
+        cudaStream_t s = stream;
+        DBuf<double> ws64;
+        CK(ws64.alloc(nE)); CK(ws64.upload(wsum.data(), nE, s));
+        vk::AssembleArgs<T> aa;
+        aa.nF = nF; aa.nE = nE; aa.ell_w = ell_w;
+        aa.inc_ptr = inc_ptr.p; aa.inc_code = inc_code.p; aa.tets = tets.p; aa.G = G64k.p; aa.wsum = ws64.p;
+        aa.m_dt2 = md64k.p; aa.ell_col = ell_col.p; aa.ell_len = ell_len.p; aa.ell_val = ell_val.p;
+        aa.inv_diag = inv_diag.p;
+        aa.diag64 = diag64.p; aa.fp_ptr = fp_ptr.p; aa.fp_col = fp_col.p; aa.fp_val = fp_val.p;
+        aa.n_free_cols_base = nF;
+        if (nF > 0) vk::k_assemble<T><<<cdiv(nF, 128), 128, 0, s>>>(aa);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+        return VKPD_OK;
+    }
+    // polynomial preconditioner: Gershgorin weight and the prescaled K D^-1
+    int refresh_precond() {
+        if (nF <= 0) return VKPD_OK;
+        cudaStream_t s = stream;
+        // Gershgorin bound G >= lambda_max(D^-1 K_ff); w = min(1, 1.9 / G) keeps
+        // w D^-1 (2 - w K D^-1) SPD with margin
+        DBuf<unsigned long long> gmax;
+        CK(gmax.alloc(1));
+        CK(cudaMemsetAsync(gmax.p, 0, sizeof(unsigned long long), s));
+        vk::k_gershgorin<T><<<cdiv(nF, 256), 256, 0, s>>>(nF, ell_w, ell_col.p, ell_val.p, diag64.p, gmax.p);
+        CK(cudaGetLastError());
+        unsigned long long gb = 0;
+        CK(cudaMemcpyAsync(&gb, gmax.p, sizeof gb, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double g = 1.0;
+        std::memcpy(&g, &gb, sizeof g);
+        g += 1.0;
+        poly_omega = (g > 0.0 && std::isfinite(g)) ? std::min(1.0, 1.9 / g) : 0.5;
+        if (ell_kd.n != (size_t)std::max(1, ell_w) * nF) CK(ell_kd.alloc((size_t)std::max(1, ell_w) * nF));
+        vk::k_scale_ell<T><<<cdiv(nF, 256), 256, 0, s>>>(nF, ell_w, ell_col.p, ell_val.p, inv_diag.p, ell_kd.p);
+        CK(cudaGetLastError());
+        return VKPD_OK;
+    }
+    // new per-tet material (MaterialField): weights of the local step, K re-assembled on the
+    // device; the frame graph is rebuilt (its solver weight may change), warm starts dropped
+    int set_gammas(const double* gs, const double* gv) override {
+        if (!G64k.p) return fail(VKPD_EINVAL, "set_gammas needs a mesh context");
+        std::vector<T> wp((size_t)2 * nE);
+        std::vector<double> wsum(nE);
+        for (int e = 0; e < nE; ++e) {
+            if (!(gs[e] >= 0.0) || !(gv[e] >= 0.0)) return fail(VKPD_EINVAL, "gamma must be non-negative");
+            wp[e] = (T)(vol2_h[e] * gs[e]);
+            wp[(size_t)nE + e] = (T)(vol2_h[e] * gv[e]);
+            wsum[e] = vol2_h[e] * (gs[e] + gv[e]);
+        }
+        CK(w.upload(wp.data(), wp.size(), stream));
+        if (int rc = assemble(wsum)) return rc;
+        if (int rc = refresh_precond()) return rc;
+        if (warm0.p) CK(cudaMemsetAsync(warm0.p, 0, warm0.n * sizeof(V4), stream));
+        if (graph_exec) { cudaGraphExecDestroy(graph_exec); graph_exec = nullptr; }
+        CK(cudaStreamSynchronize(stream));
+        return VKPD_OK;
     }
 
     int alloc_work(const vkpd_config* c) {
@@ -421,25 +474,7 @@ struct Ctx : CtxBase {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, vk::k_pcg_poly<T>, pcg_threads, 0));
         // co-residency of every kernel that may be launched (classic also serves contact frames)
         occ = pcg_poly ? std::min(occ2, occ3) : pcg_classic ? occ2 : std::min(occ, occ2);
-        if (nF > 0) {
-            // Gershgorin bound G >= lambda_max(D^-1 K_ff); w = min(1, 1.9 / G) keeps
-            // w D^-1 (2 - w K D^-1) SPD with margin
-            DBuf<unsigned long long> gmax;
-            CK(gmax.alloc(1));
-            CK(cudaMemsetAsync(gmax.p, 0, sizeof(unsigned long long), s));
-            vk::k_gershgorin<T><<<cdiv(nF, 256), 256, 0, s>>>(nF, ell_w, ell_col.p, ell_val.p, diag64.p, gmax.p);
-            CK(cudaGetLastError());
-            unsigned long long gb = 0;
-            CK(cudaMemcpyAsync(&gb, gmax.p, sizeof gb, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            double g = 1.0;
-            std::memcpy(&g, &gb, sizeof g);
-            g += 1.0;
-            poly_omega = (g > 0.0 && std::isfinite(g)) ? std::min(1.0, 1.9 / g) : 0.5;
-            CK(ell_kd.alloc((size_t)std::max(1, ell_w) * nF));
-            vk::k_scale_ell<T><<<cdiv(nF, 256), 256, 0, s>>>(nF, ell_w, ell_col.p, ell_val.p, inv_diag.p, ell_kd.p);
-            CK(cudaGetLastError());
-        }
+        if (int rc = refresh_precond()) return rc;
         if (occ < 1) return fail(VKPD_ECUDA, "persistent solver kernel cannot be resident");
         // default: one row per thread, capped by co-residency
         // default: at most one CTA per SM (fewer arrivals per grid barrier measured faster
@@ -1353,6 +1388,10 @@ int vkpd_set_pin_targets(vkpd_ctx* ctx, const double* t) {
     CTX_CALL(set_pin_targets(t));
 }
 int vkpd_set_forces(vkpd_ctx* ctx, const double* f) { CTX_CALL(set_forces(f)); }
+int vkpd_set_gammas(vkpd_ctx* ctx, const double* gamma_s, const double* gamma_v) {
+    if (!gamma_s || !gamma_v) return fail(VKPD_EINVAL, "null gamma arrays");
+    CTX_CALL(set_gammas(gamma_s, gamma_v));
+}
 int vkpd_set_colliders(vkpd_ctx* ctx, int n, const int* kinds, const double* params, double contact_stiffness) {
     if (n > 0 && (!kinds || !params)) return fail(VKPD_EINVAL, "null collider arrays");
     CTX_CALL(set_colliders(n, kinds, params, contact_stiffness));

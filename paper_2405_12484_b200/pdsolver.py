@@ -81,9 +81,13 @@ _CACHE = {}
 _CACHE_MAX = 8
 
 
+def _ident(arrs):
+    return tuple((id(a), a.__array_interface__["data"][0], a.shape) for a in map(np.asarray, arrs))
+
+
 def _key(mesh, gammas, dt, pins, precision, tol, max_iters):
-    arrs = (mesh.tets, mesh.shape_grad, mesh.volume, mesh.node_mass, gammas.gamma_s, gammas.gamma_v)
-    ident = tuple((id(a), a.__array_interface__["data"][0], a.shape) for a in map(np.asarray, arrs))
+    """Cache key of the mesh part of a device scene (the material is refreshed in place)."""
+    ident = _ident((mesh.tets, mesh.shape_grad, mesh.volume, mesh.node_mass))
     pins = np.asarray(pins, dtype=np.int64)
     return (ident, float(dt), pins.tobytes(), precision, tol, max_iters)
 
@@ -94,20 +98,29 @@ def invalidate_cache():
 
 
 def device_context(mesh, gammas, dt, pins=(), precision="fp32", tol=None, max_iters=0):
-    """Device-resident scene for (mesh, gammas, dt, pins); created once and cached."""
+    """Device-resident scene for (mesh, gammas, dt, pins); created once and cached.
+
+    A new MaterialField for a cached mesh (the fitting loop's case, `fitting.py:429-432`)
+    refreshes the context's weights and re-assembles K on the device instead of rebuilding it.
+    """
     _check_inputs(mesh, gammas, dt)
     tol = DEFAULT_TOL[precision] if tol is None else float(tol)
     k = _key(mesh, gammas, dt, pins, precision, tol, max_iters)
-    ctx = _CACHE.get(k)
-    if ctx is None:
+    gid = _ident((gammas.gamma_s, gammas.gamma_v))
+    hit = _CACHE.get(k)
+    if hit is None:
         if len(_CACHE) >= _CACHE_MAX:
             _CACHE.pop(next(iter(_CACHE)))
         ctx = _abi.Context(mesh.n_nodes if hasattr(mesh, "n_nodes") else len(mesh.nodes), mesh.tets,
                            mesh.shape_grad, mesh.volume, mesh.node_mass, gammas.gamma_s,
                            gammas.gamma_v, pins, dt, precision=precision, tol=tol,
                            max_iters=max_iters)
-        _CACHE[k] = ctx
-    return ctx
+        _CACHE[k] = [gid, ctx]
+        return ctx
+    if hit[0] != gid:
+        hit[1].set_gammas(gammas.gamma_s, gammas.gamma_v)
+        hit[0] = gid
+    return hit[1]
 
 
 # ---------------------------------------------------------------------------

@@ -368,3 +368,51 @@ def test_collide_project_and_bad_kind():
     st = pdsolver.SimState(x=sc.mesh.nodes, v=np.zeros_like(sc.mesh.nodes), dt=1e-3, colliders=(("torus", 0, 1),))
     with pytest.raises(ValueError):
         pdsolver.pd_step(st, sc.mesh, sc.gammas, iterations=2)
+
+
+# ---------------------------------------------------------------------------
+# material refresh: new gamma on a cached device mesh
+
+
+def test_set_gammas_matches_fresh_context(c1):
+    from paper_2405_12484_b200 import _abi
+    m = c1.mesh
+    rng = np.random.default_rng(7)
+    gs2 = c1.gammas.gamma_s * rng.uniform(0.5, 2.0, c1.n_tets)
+    gv2 = c1.gammas.gamma_v * rng.uniform(0.5, 2.0, c1.n_tets)
+
+    def run(ctx):
+        ctx.set_state(m.nodes)
+        ctx.set_pin_targets(c1.pin_targets)
+        ctx.set_forces(c1.forces)
+        out = []
+        for _ in range(3):
+            ctx.step(30)
+            out.append(ctx.get_state()[0])
+        return np.stack(out)
+
+    for prec in ("fp32", "fp64"):
+        mk = lambda gs, gv: _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, gs, gv,
+                                          c1.pins, c1.dt, precision=prec, tol=pdsolver.DEFAULT_TOL[prec])
+        a = mk(c1.gammas.gamma_s, c1.gammas.gamma_v)
+        run(a)                                   # some history on the old material
+        a.set_gammas(gs2, gv2)
+        fa = run(a)
+        fb = run(mk(gs2, gv2))
+        assert np.array_equal(fa, fb), prec
+        with pytest.raises(ValueError):
+            a.set_gammas(-gs2, gv2)
+
+
+def test_simulate_mesh_reuses_mesh_for_new_material(c1):
+    kw = dict(forces=c1.forces, pins=c1.pins, pin_targets=c1.pin_targets, iterations=30, precision="fp64")
+    g2 = MaterialField(c1.gammas.gamma_s * 1.7, c1.gammas.gamma_v * 0.6)
+    pdsolver.invalidate_cache()
+    pdsolver.simulate_mesh(c1.mesh, c1.gammas, 1, c1.dt, **kw)
+    n0 = len(pdsolver._CACHE)
+    a = pdsolver.simulate_mesh(c1.mesh, g2, 2, c1.dt, **kw)
+    assert len(pdsolver._CACHE) == n0            # refreshed in place, not rebuilt
+    m = c1.mesh
+    ref = orc.simulate(m.nodes, m.tets, m.shape_grad, m.volume, g2.gamma_s, g2.gamma_v, m.node_mass, 2, c1.dt,
+                       forces=c1.forces, pins=c1.pins, pin_targets=c1.pin_targets, iterations=30)
+    assert rel_l2(a, ref) < 1e-10
