@@ -14,6 +14,8 @@ Any object exposing `nodes`, `tets`, `volume`, `shape_grad` and `node_mass`
 from __future__ import annotations
 
 import itertools
+import json
+import warnings
 
 import numpy as np
 
@@ -131,3 +133,134 @@ def lump_mass_density(mesh, rho):
     np.add.at(m, mesh.tets.reshape(-1), np.repeat(rho * mesh.volume / 4.0, 4))
     mesh.node_mass = m
     return m
+
+
+# ---------------------------------------------------------------------------
+# mesh and material files: the reference's text formats,
+# parsed with numpy's C reader instead of a Python loop per line
+
+
+class ConfigError(ValueError):
+    """Unreadable input file (the reference CLI's `ConfigError`, `cli.py:225-240`)."""
+
+
+def _header_rows(path):
+    """(number of leading comment/blank lines, first data row as tokens)."""
+    skip = 0
+    with open(path) as fh:
+        for line in fh:
+            s = line.strip()
+            if s and not s.startswith("#"):
+                return skip, s.split()
+            skip += 1
+    raise ConfigError(f"{path}: no data rows")
+
+
+def _table(path, skip, cols, dtype):
+    a = np.loadtxt(path, dtype=dtype, comments="#", skiprows=skip + 1, ndmin=2)
+    if a.size == 0:
+        return np.empty((0, cols), dtype=dtype)
+    if a.shape[1] < cols:
+        raise ConfigError(f"{path}: expected {cols} columns, found {a.shape[1]}")
+    return a[:, :cols]
+
+
+def read_mesh(prefix):
+    """Read `<prefix>.node/.ele/.json` as written by the reference `write_mesh` (`volmesh.py:575-611`).
+
+    Rows are placed by their leading index, as in the reference reader.
+    """
+    skip, head = _header_rows(f"{prefix}.node")
+    n = int(head[0])
+    rows = _table(f"{prefix}.node", skip, 4, np.float64)
+    nodes = np.empty((n, 3))
+    nodes[rows[:, 0].astype(np.int64)] = rows[:, 1:4]
+    skip, head = _header_rows(f"{prefix}.ele")
+    m = int(head[0])
+    rows = _table(f"{prefix}.ele", skip, 5, np.int64)
+    tets = np.empty((m, 4), dtype=np.int64)
+    tets[rows[:, 0]] = rows[:, 1:5]
+    with open(f"{prefix}.json") as fh:
+        meta = json.load(fh)
+    origin = np.asarray(meta["origin"], dtype=float)
+    h = float(meta["cell_size"])
+    grid = np.rint((nodes - origin) / h).astype(np.int64)
+    mesh = VolumeMesh(nodes, tets, cell_size=h, origin=origin, node_grid=grid,
+                      voxels=np.asarray(meta["voxels"], dtype=np.int64),
+                      tet_voxel=np.asarray(meta["tet_voxel"], dtype=np.int64))
+    if "node_mass" in meta:
+        mesh.node_mass = np.asarray(meta["node_mass"], dtype=float)
+    return mesh
+
+
+def boundary_faces(mesh):
+    """Faces used by one tet, outward-oriented, sorted (`volmesh.py:505-535`)."""
+    t = mesh.tets
+    faces, opp = [], []
+    for k in range(4):
+        faces.append(np.delete(t, k, axis=1))
+        opp.append(t[:, k])
+    faces = np.concatenate(faces)
+    opp = np.concatenate(opp)
+    key = np.sort(faces, axis=1)
+    _, inv, cnt = np.unique(key, axis=0, return_inverse=True, return_counts=True)
+    one = cnt[inv.reshape(-1)] == 1
+    f, o = faces[one], opp[one]
+    a, b, c = (mesh.nodes[f[:, i]] for i in range(3))
+    nrm = np.cross(b - a, c - a)
+    flip = np.einsum("ij,ij->i", nrm, mesh.nodes[o] - a) > 0.0
+    f[flip] = f[flip][:, [0, 2, 1]]
+    order = np.lexsort(f.T[::-1])
+    return f[order]
+
+
+def write_mesh(mesh, prefix, comment=None):
+    """Write `<prefix>.node/.ele/.json/_boundary.obj` in the reference format (`volmesh.py:538-572`)."""
+    head = f"# {comment}\n" if comment else ""
+    idx = np.arange(mesh.n_nodes)[:, None]
+    with open(f"{prefix}.node", "w") as fh:
+        fh.write(head)
+        fh.write(f"{mesh.n_nodes} 3 0 0\n")
+        np.savetxt(fh, np.hstack([idx, mesh.nodes]), fmt=["%d", "%.17g", "%.17g", "%.17g"])
+    with open(f"{prefix}.ele", "w") as fh:
+        fh.write(head)
+        fh.write(f"{mesh.n_elements} 4 0\n")
+        np.savetxt(fh, np.hstack([np.arange(mesh.n_elements)[:, None], mesh.tets]), fmt="%d")
+    meta = {
+        "cell_size": mesh.cell_size,
+        "origin": [float(v) for v in mesh.origin],
+        "voxels": [[int(v) for v in c] for c in (mesh.voxels if mesh.voxels is not None else [])],
+        "tet_voxel": [int(v) for v in (mesh.tet_voxel if mesh.tet_voxel is not None else [])],
+    }
+    if mesh.node_mass is not None:
+        meta["node_mass"] = [float(v) for v in mesh.node_mass]
+    if comment:
+        meta["comment"] = comment
+    with open(f"{prefix}.json", "w") as fh:
+        json.dump(meta, fh)
+    with open(f"{prefix}_boundary.obj", "w") as fh:
+        fh.write(head)
+        np.savetxt(fh, mesh.nodes, fmt="v %.17g %.17g %.17g")
+        np.savetxt(fh, boundary_faces(mesh) + 1, fmt="f %d %d %d")
+
+
+def read_material(path):
+    """`element,gamma_s,gamma_v` CSV (`cli.py:225-240`) -> MaterialField."""
+    from .material import MaterialField
+    try:
+        skip, head = _header_rows(path)
+    except OSError as exc:
+        raise ConfigError(f"cannot read material file {path}: {exc}") from exc
+    except ConfigError:
+        raise ConfigError(f"material file {path} holds no rows") from None
+    if head[0].startswith("element"):
+        skip += 1
+    try:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)      # "input contained no data"
+            a = np.loadtxt(path, delimiter=",", comments="#", skiprows=skip, ndmin=2)
+    except (OSError, ValueError) as exc:
+        raise ConfigError(f"cannot read material file {path}: {exc}") from exc
+    if a.size == 0:
+        raise ConfigError(f"material file {path} holds no rows")
+    return MaterialField(np.ascontiguousarray(a[:, 1]), np.ascontiguousarray(a[:, 2]))

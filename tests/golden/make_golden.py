@@ -183,12 +183,34 @@ def make_big(key, frames_keep, steps, f32_disp):
     print(key, "seconds", el)
 
 
+def make_io():
+    """Mesh / material files written by the reference writers, and what its readers return."""
+    from volknit import cli as ref_cli
+    sc = scenes.c1_swatch()
+    rm = ref_mesh(sc)
+    d = os.path.join(HERE, "io")
+    os.makedirs(d, exist_ok=True)
+    prefix = os.path.join(d, "c1")
+    ref_vm.write_mesh(rm, prefix, comment="golden c1")
+    gam = ref_mat.MaterialField(sc.gammas.gamma_s, sc.gammas.gamma_v)
+    ref_cli.write_material(os.path.join(d, "c1_material.csv"), gam, "golden")
+    back = ref_vm.read_mesh(prefix)
+    mat = ref_cli.read_material(os.path.join(d, "c1_material.csv"))
+    np.savez_compressed(os.path.join(HERE, "io.npz"), nodes=back.nodes, tets=back.tets,
+                        node_mass=back.node_mass, node_grid=back.node_grid, voxels=back.voxels,
+                        tet_voxel=back.tet_voxel, cell_size=back.cell_size, origin=back.origin,
+                        faces=ref_vm.boundary_faces(back), gamma_s=mat.gamma_s, gamma_v=mat.gamma_v)
+    print("io fixtures written")
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what in ("small", "all"):
         make_projections()
         make_c1()
         make_solvers()
+    if what in ("io", "all"):
+        make_io()
     if what in ("contact", "all"):
         make_contact()
     if what in ("c2", "all"):
