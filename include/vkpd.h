@@ -20,6 +20,9 @@
  *   vkpd_global_solve     GlobalSolver.solve (pdsolver.py:225-246)
  *   vkpd_apply_K          the assembled K (pdsolver.py:42-56) applied to a vector
  *   vkpd_batch_projections material.batch_projections (material.py:395-407)
+ *   vkpd_set_yarn_interp / vkpd_frame_outputs / vkpd_v2y
+ *                         transfer.v2y (transfer.py:26-28) and the det(F) deviation of the
+ *                         simulate loop (cli.py:639-640)
  *
  * Error convention (mirrors the reference's exceptions):
  *   VKPD_OK          0
@@ -164,6 +167,19 @@ int vkpd_cms_solve(vkpd_ctx* ctx, const double* B, const double* P, int k, int s
 
 int vkpd_batch_projections(int precision, int64_t n, const double* F, double* R, double* V,
                            unsigned int* n_robust, unsigned int* n_fallback);
+
+/* Per-frame output step (cli.py:628-656), on the device-resident state:
+ *   vkpd_set_yarn_interp: the yarn embedding's interpolation matrix (transfer.py:26-28,
+ *                         volmesh.py:401-419) in CSR, columns = caller node ids
+ *   vkpd_frame_outputs:   yarn (n_yarn,3) = interp @ x and/or det_deviation =
+ *                         max_e |det F_e - 1| (cli.py:639-640); either may be NULL
+ *   vkpd_v2y:             transfer.v2y on host positions (float64, bit-identical to
+ *                         scipy's CSR product) */
+int vkpd_set_yarn_interp(vkpd_ctx* ctx, int64_t n_yarn, const int64_t* indptr, const int64_t* indices,
+                         const double* data);
+int vkpd_frame_outputs(vkpd_ctx* ctx, double* yarn, double* det_deviation);
+int vkpd_v2y(int64_t n_yarn, const int64_t* indptr, const int64_t* indices, const double* data, int64_t n_nodes,
+             const double* x, double* y);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,7 @@ EXPORTS = (
     "vkpd_batch_projections", "vkpd_create_matrix", "vkpd_get_matrix_csr", "vkpd_a_jacobi_refine",
     "vkpd_power_rho", "vkpd_cms_set_basis", "vkpd_cms_solve", "vkpd_dev_residual", "vkpd_dev_apply_K",
     "vkpd_dev_inv_diag", "vkpd_get_node_order", "vkpd_get_sizes", "vkpd_set_colliders",
-    "vkpd_set_gammas",
+    "vkpd_set_gammas", "vkpd_set_yarn_interp", "vkpd_frame_outputs", "vkpd_v2y",
 )
 
 
@@ -223,6 +223,25 @@ class Context:
     def set_forces(self, f):
         check(self.lib.vkpd_set_forces(self.h, None if f is None else ptr(f64(f, (self.n, 3)))))
 
+    def set_yarn_interp(self, interp):
+        """Yarn embedding interpolation matrix (n_yarn x n_nodes, CSR) for frame_outputs."""
+        import scipy.sparse as sp
+        A = sp.csr_matrix(interp)
+        if A.shape[1] != self.n:
+            raise ValueError("interpolation matrix has the wrong number of columns")
+        ip = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(A.indices, dtype=np.int64)
+        dv = np.ascontiguousarray(A.data, dtype=np.float64)
+        check(self.lib.vkpd_set_yarn_interp(self.h, C.c_int64(A.shape[0]), ptr(ip), ptr(ix), ptr(dv)))
+        self.n_yarn = A.shape[0]
+
+    def frame_outputs(self, yarn=True, det=True):
+        """(yarn positions interp @ x or None, max |det F - 1| or None) of the device state."""
+        y = np.empty((getattr(self, "n_yarn", 0), 3)) if yarn else None
+        d = C.c_double(0.0)
+        check(self.lib.vkpd_frame_outputs(self.h, ptr(y), C.byref(d) if det else None))
+        return y, (d.value if det else None)
+
     def set_gammas(self, gamma_s, gamma_v):
         """New per-tet material for the same mesh/pins/dt; K is re-assembled on the device."""
         ne = self.n_tets
@@ -366,6 +385,19 @@ class Context:
                     robust=st.robust, fallback=st.fallback, pcg_blocks=st.pcg_blocks,
                     ell_width=st.ell_width, n_free=st.n_free, local_ms=list(st.local_ms[:n]),
                     global_ms=list(st.global_ms[:n]), pd_rounds_total=st.pd_rounds_total)
+
+
+def v2y(interp, x):
+    """interp @ x on the device (float64, CSR order, no fused multiply-add)."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix(interp)
+    x = f64(x, (A.shape[1], 3))
+    y = np.empty((A.shape[0], 3))
+    ip = np.ascontiguousarray(A.indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(A.indices, dtype=np.int64)
+    dv = np.ascontiguousarray(A.data, dtype=np.float64)
+    check(load().vkpd_v2y(C.c_int64(A.shape[0]), ptr(ip), ptr(ix), ptr(dv), C.c_int64(A.shape[1]), ptr(x), ptr(y)))
+    return y
 
 
 class MatrixContext(Context):

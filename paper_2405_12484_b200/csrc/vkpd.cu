@@ -19,6 +19,7 @@
 #include "solver.cuh"
 #include "cms.cuh"
 #include "frame.cuh"
+#include "output.cuh"
 
 namespace {
 
@@ -146,6 +147,8 @@ struct CtxBase {
     virtual int set_pin_targets(const double* t) = 0;
     virtual int set_forces(const double* f) = 0;
     virtual int set_gammas(const double* gs, const double* gv) = 0;
+    virtual int set_yarn_interp(int64_t n_yarn, const int64_t* indptr, const int64_t* indices, const double* data) = 0;
+    virtual int frame_outputs(double* yarn, double* det_dev) = 0;
     virtual int set_colliders(int n, const int* kinds, const double* params, double kc) = 0;
     virtual int step_async(int iterations, double damping) = 0;
     virtual int sync(int* failed) = 0;
@@ -378,6 +381,59 @@ struct Ctx : CtxBase {
         for (int e = 0; e < nE; ++e) vol2_h[e] = 2.0 * d->volume[e];
         if (int rc = assemble(wsum)) return rc;
         return alloc_work(c);
+    }
+
+    // per-frame output step (transfer.py:26-28, cli.py:639-640)
+    DBuf<long long> y_ptr;
+    DBuf<int> y_col;
+    DBuf<double> y_w, y_out;
+    int64_t n_yarn = 0;
+    int set_yarn_interp(int64_t ny, const int64_t* indptr, const int64_t* indices, const double* data) override {
+        if (ny < 0 || (ny > 0 && (!indptr || !indices || !data))) return fail(VKPD_EINVAL, "bad interpolation matrix");
+        if (int_of_orig_h.empty()) return fail(VKPD_EINVAL, "no mesh in this context");
+        const int64_t nnz = ny > 0 ? indptr[ny] : 0;
+        std::vector<int> ci(std::max<int64_t>(1, nnz));
+        for (int64_t k = 0; k < ny; ++k)
+            if (indptr[k + 1] < indptr[k]) return fail(VKPD_EINVAL, "interpolation indptr not monotone");
+        for (int64_t j = 0; j < nnz; ++j) {
+            if (indices[j] < 0 || indices[j] >= n) return fail(VKPD_EINVAL, "interpolation column out of range");
+            ci[j] = int_of_orig_h[indices[j]];
+        }
+        n_yarn = ny;
+        CK(y_ptr.alloc(ny + 1));
+        CK(y_ptr.upload((const long long*)indptr, ny + 1, stream));
+        CK(y_col.alloc(std::max<int64_t>(1, nnz)));
+        CK(y_w.alloc(std::max<int64_t>(1, nnz)));
+        if (nnz > 0) { CK(y_col.upload(ci.data(), nnz, stream)); CK(y_w.upload(data, nnz, stream)); }
+        CK(y_out.alloc((size_t)3 * std::max<int64_t>(1, ny)));
+        CK(cudaStreamSynchronize(stream));
+        return VKPD_OK;
+    }
+    int frame_outputs(double* yarn, double* det_dev) override {
+        if (yarn) {
+            if (n_yarn <= 0 && !y_ptr.p) return fail(VKPD_EINVAL, "no yarn interpolation set (vkpd_set_yarn_interp)");
+            if (n_yarn > 0) {
+                vk::k_v2y<T><<<cdiv((int)n_yarn, 256), 256, 0, stream>>>((int)n_yarn, y_ptr.p, y_col.p, y_w.p, x.p,
+                                                                          y_out.p);
+                CK(cudaGetLastError());
+                CK(cudaMemcpyAsync(yarn, y_out.p, sizeof(double) * 3 * n_yarn, cudaMemcpyDeviceToHost, stream));
+            }
+        }
+        if (det_dev) {
+            if (!G64k.p) return fail(VKPD_EINVAL, "det deviation needs a mesh context");
+            DBuf<unsigned long long> m;
+            CK(m.alloc(1));
+            CK(cudaMemsetAsync(m.p, 0, sizeof(unsigned long long), stream));
+            if (nE > 0)
+                vk::k_det_deviation<T><<<cdiv(nE, 256), 256, 0, stream>>>(nE, tets.p, G64k.p, x.p, m.p);
+            CK(cudaGetLastError());
+            unsigned long long b = 0;
+            CK(cudaMemcpyAsync(&b, m.p, sizeof b, cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            std::memcpy(det_dev, &b, sizeof b);
+        }
+        CK(cudaStreamSynchronize(stream));
+        return VKPD_OK;
     }
 
     // K_ff / K_fp from the per-tet weights 2V(gs+gv) (pdsolver.py:42-56), deterministic
@@ -1388,6 +1444,39 @@ int vkpd_set_pin_targets(vkpd_ctx* ctx, const double* t) {
     CTX_CALL(set_pin_targets(t));
 }
 int vkpd_set_forces(vkpd_ctx* ctx, const double* f) { CTX_CALL(set_forces(f)); }
+int vkpd_set_yarn_interp(vkpd_ctx* ctx, int64_t n_yarn, const int64_t* indptr, const int64_t* indices,
+                         const double* data) {
+    CTX_CALL(set_yarn_interp(n_yarn, indptr, indices, data));
+}
+int vkpd_frame_outputs(vkpd_ctx* ctx, double* yarn, double* det_deviation) {
+    CTX_CALL(frame_outputs(yarn, det_deviation));
+}
+int vkpd_v2y(int64_t n_yarn, const int64_t* indptr, const int64_t* indices, const double* data, int64_t n_nodes,
+             const double* x, double* y) {
+    if (n_yarn < 0 || n_nodes < 0 || (n_yarn > 0 && (!indptr || !indices || !data || !y)) || (n_nodes > 0 && !x))
+        return fail(VKPD_EINVAL, "bad arguments");
+    int count = 0;
+    if (vkpd_device_count(&count) != VKPD_OK || count == 0)
+        return fail(VKPD_ECUDA, "no CUDA device available (the vkpd library has no CPU path)");
+    if (n_yarn == 0) return VKPD_OK;
+    const int64_t nnz = indptr[n_yarn];
+    for (int64_t j = 0; j < nnz; ++j)
+        if (indices[j] < 0 || indices[j] >= n_nodes) return fail(VKPD_EINVAL, "interpolation column out of range");
+    DBuf<long long> dp, dc;
+    DBuf<double> dw, dx, dy;
+    CK(dp.alloc(n_yarn + 1)); CK(dc.alloc(std::max<int64_t>(1, nnz))); CK(dw.alloc(std::max<int64_t>(1, nnz)));
+    CK(dx.alloc((size_t)3 * std::max<int64_t>(1, n_nodes))); CK(dy.alloc((size_t)3 * n_yarn));
+    CK(cudaMemcpy(dp.p, indptr, sizeof(long long) * (n_yarn + 1), cudaMemcpyHostToDevice));
+    if (nnz > 0) {
+        CK(cudaMemcpy(dc.p, indices, sizeof(long long) * nnz, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dw.p, data, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+    }
+    if (n_nodes > 0) CK(cudaMemcpy(dx.p, x, sizeof(double) * 3 * n_nodes, cudaMemcpyHostToDevice));
+    vk::k_v2y_host_order<<<cdiv((int)n_yarn, 256), 256>>>((int)n_yarn, dp.p, dc.p, dw.p, dx.p, dy.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(y, dy.p, sizeof(double) * 3 * n_yarn, cudaMemcpyDeviceToHost));
+    return VKPD_OK;
+}
 int vkpd_set_gammas(vkpd_ctx* ctx, const double* gamma_s, const double* gamma_v) {
     if (!gamma_s || !gamma_v) return fail(VKPD_EINVAL, "null gamma arrays");
     CTX_CALL(set_gammas(gamma_s, gamma_v));

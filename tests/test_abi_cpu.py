@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "vkpd.h")
 
 def declared_symbols():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(vkpd_[A-Za-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(vkpd_[A-Za-z0-9_]+)\s*\(", txt)))
 
 
 def test_header_declares_the_boundary():

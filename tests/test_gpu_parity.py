@@ -416,3 +416,45 @@ def test_simulate_mesh_reuses_mesh_for_new_material(c1):
     ref = orc.simulate(m.nodes, m.tets, m.shape_grad, m.volume, g2.gamma_s, g2.gamma_v, m.node_mass, 2, c1.dt,
                        forces=c1.forces, pins=c1.pins, pin_targets=c1.pin_targets, iterations=30)
     assert rel_l2(a, ref) < 1e-10
+
+
+# ---------------------------------------------------------------------------
+# per-frame output step: v2y and the det(F) deviation
+
+
+def _embedding(mesh, n_yarn, rng):
+    """An interpolation matrix built the way the reference's embed_yarn does (volmesh.py:401-419)."""
+    host = rng.integers(0, mesh.n_elements, n_yarn)
+    w = rng.uniform(0.0, 1.0, (n_yarn, 4)) ** 2
+    w = np.clip(w, 0.0, 1.0)
+    w /= w.sum(axis=1, keepdims=True)
+    rows = np.repeat(np.arange(n_yarn), 4)
+    cols = mesh.tets[host].reshape(-1)
+    return sp.csr_matrix((w.reshape(-1), (rows, cols)), shape=(n_yarn, mesh.n_nodes))
+
+
+def test_v2y_bit_identical_to_reference_product(c1, rng):
+    from paper_2405_12484_b200 import transfer
+    interp = _embedding(c1.mesh, 5000, rng)
+    x = c1.mesh.nodes + 0.01 * rng.normal(size=c1.mesh.nodes.shape)
+    assert np.array_equal(transfer.v2y(interp, x), interp @ x)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_frame_outputs_on_device_state(c1, rng, prec):
+    from paper_2405_12484_b200 import _abi
+    m = c1.mesh
+    ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, c1.gammas.gamma_s,
+                       c1.gammas.gamma_v, c1.pins, c1.dt, precision=prec, tol=pdsolver.DEFAULT_TOL[prec])
+    interp = _embedding(m, 3000, rng)
+    ctx.set_yarn_interp(interp)
+    ctx.set_state(m.nodes)
+    ctx.set_pin_targets(c1.pin_targets)
+    ctx.set_forces(c1.forces)
+    for _ in range(3):
+        ctx.step(30)
+        y, dev = ctx.frame_outputs()
+        x = ctx.get_state()[0]
+        assert np.array_equal(y, interp @ x)
+        ref = float(np.abs(np.linalg.det(m.deformation_gradients(x)) - 1.0).max())
+        assert abs(dev - ref) <= 1e-12 * max(1.0, ref)
