@@ -20,6 +20,7 @@
  *   vkpd_global_solve     GlobalSolver.solve (pdsolver.py:225-246)
  *   vkpd_apply_K          the assembled K (pdsolver.py:42-56) applied to a vector
  *   vkpd_batch_projections material.batch_projections (material.py:395-407)
+ *   vkpd_equilibrium      pd_equilibrium (pdsolver.py:315-338), the fitting side's forward solve
  *   vkpd_set_yarn_interp / vkpd_frame_outputs / vkpd_v2y
  *                         transfer.v2y (transfer.py:26-28) and the det(F) deviation of the
  *                         simulate loop (cli.py:639-640)
@@ -167,6 +168,13 @@ int vkpd_cms_solve(vkpd_ctx* ctx, const double* B, const double* P, int k, int s
 
 int vkpd_batch_projections(int precision, int64_t n, const double* F, double* R, double* V,
                            unsigned int* n_robust, unsigned int* n_fallback);
+
+/* pd_equilibrium (pdsolver.py:315-338): `iterations` proximal local/global rounds solving
+ * K x = (M/dt^2)(x_cur - a) + rhs from x0 with pinned rows = pin_vals (n_pins,3); the
+ * simulation state is not touched.  VKPD_ENONFINITE with *failed_iter on non-finite x
+ * ("quasi-static projection diverged at iteration {it}"). */
+int vkpd_equilibrium(vkpd_ctx* ctx, const double* inertia_target, const double* x0, const double* pin_vals,
+                     int iterations, double* x_out, int* failed_iter);
 
 /* Per-frame output step (cli.py:628-656), on the device-resident state:
  *   vkpd_set_yarn_interp: the yarn embedding's interpolation matrix (transfer.py:26-28,

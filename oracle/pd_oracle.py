@@ -353,6 +353,31 @@ class GlobalSolver:
         return X
 
 
+def pd_equilibrium(x0, tets, G, vol, gs, gv, mass, inertia_target, pins, pin_vals, dt, iterations=PD_ITERS,
+                   solver=None):
+    """Proximal local/global rounds on E(x) + (1/dt^2) a^T M x (`pdsolver.py:315-338`).
+
+    Each round solves K x = (M/dt^2)(x_cur - a) + elastic rhs; RuntimeError
+    "quasi-static projection diverged at iteration {it}" on non-finite x.
+    """
+    n = len(mass)
+    pins = np.asarray(pins, dtype=np.int64)
+    free = np.setdiff1d(np.arange(n), pins)
+    if solver is None:
+        solver = GlobalSolver(assemble_K(tets, G, vol, gs, gv, mass, dt, n), free, pins)
+    x = np.asarray(x0, dtype=float).reshape(-1, 3).copy()
+    if len(pins):
+        x[pins] = pin_vals
+    m_dt2 = np.asarray(mass)[:, None] / dt ** 2
+    for it in range(iterations):
+        rhs = elastic_rhs(x, tets, G, vol, gs, gv, n)[0]
+        b = m_dt2 * (x - inertia_target) + rhs
+        x = solver.solve(b, pin_vals if len(pins) else np.empty((0, 3)))
+        if not np.all(np.isfinite(x)):
+            raise RuntimeError(f"quasi-static projection diverged at iteration {it}")
+    return x
+
+
 def predicted(x, v, dt, mass, forces):
     """xhat = x + dt v + dt^2 m^-1 f with m^-1 := 0 where m = 0 (`pdsolver.py:249-254`)."""
     inv_m = np.zeros_like(mass)

@@ -25,7 +25,7 @@ EXPORTS = (
     "vkpd_batch_projections", "vkpd_create_matrix", "vkpd_get_matrix_csr", "vkpd_a_jacobi_refine",
     "vkpd_power_rho", "vkpd_cms_set_basis", "vkpd_cms_solve", "vkpd_dev_residual", "vkpd_dev_apply_K",
     "vkpd_dev_inv_diag", "vkpd_get_node_order", "vkpd_get_sizes", "vkpd_set_colliders",
-    "vkpd_set_gammas", "vkpd_set_yarn_interp", "vkpd_frame_outputs", "vkpd_v2y",
+    "vkpd_set_gammas", "vkpd_set_yarn_interp", "vkpd_frame_outputs", "vkpd_v2y", "vkpd_equilibrium",
 )
 
 
@@ -241,6 +241,17 @@ class Context:
         d = C.c_double(0.0)
         check(self.lib.vkpd_frame_outputs(self.h, ptr(y), C.byref(d) if det else None))
         return y, (d.value if det else None)
+
+    def equilibrium(self, inertia_target, x0, pin_vals, iterations):
+        """pd_equilibrium rounds on the device (pdsolver.py:315-338); returns x (nV,3)."""
+        a = f64(inertia_target, (self.n, 3))
+        x0 = f64(x0, (self.n, 3))
+        pv = f64(pin_vals, (self.n_pins, 3)) if self.n_pins else None
+        out = np.empty((self.n, 3))
+        failed = C.c_int(-1)
+        check(self.lib.vkpd_equilibrium(self.h, ptr(a), ptr(x0), ptr(pv), int(iterations), ptr(out),
+                                        C.byref(failed)))
+        return out
 
     def set_gammas(self, gamma_s, gamma_v):
         """New per-tet material for the same mesh/pins/dt; K is re-assembled on the device."""

@@ -128,6 +128,25 @@ __global__ void k_epilogue(int n, T damp_over_dt, const vec4_t<T>* __restrict__ 
     v[i] = make4<T>(damp_over_dt * (a.x - b.x), damp_over_dt * (a.y - b.y), damp_over_dt * (a.z - b.z), T(0));
 }
 
+// pd_equilibrium round setup (pdsolver.py:330-333): xhat = x - a on free rows, so the
+// residual-form solve targets K x = (M/dt^2)(x_cur - a) + rhs
+template <typename T>
+__global__ void k_eq_target(int nF, const vec4_t<T>* __restrict__ x, const vec4_t<T>* __restrict__ a,
+                            vec4_t<T>* xhat) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    const vec4_t<T> xi = x[i], ai = a[i];
+    xhat[i] = make4<T>(xi.x - ai.x, xi.y - ai.y, xi.z - ai.z, T(0));
+}
+
+// pinned rows (internal nF..n-1, pin order) := pin values
+template <typename T>
+__global__ void k_set_pinned(int n, int nF, const vec4_t<T>* __restrict__ pin_vals, vec4_t<T>* x) {
+    const int i = nF + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    x[i] = pin_vals[i - nF];
+}
+
 // Restore the step's input state after a non-finite abort.
 template <typename T>
 __global__ void k_restore(int n, vec4_t<T>* x, vec4_t<T>* v, const vec4_t<T>* x_start, const vec4_t<T>* v_start) {

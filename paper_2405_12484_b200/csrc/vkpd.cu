@@ -149,6 +149,8 @@ struct CtxBase {
     virtual int set_gammas(const double* gs, const double* gv) = 0;
     virtual int set_yarn_interp(int64_t n_yarn, const int64_t* indptr, const int64_t* indices, const double* data) = 0;
     virtual int frame_outputs(double* yarn, double* det_dev) = 0;
+    virtual int equilibrium(const double* a, const double* x0, const double* pin_vals, int iterations, double* x_out,
+                            int* failed) = 0;
     virtual int set_colliders(int n, const int* kinds, const double* params, double kc) = 0;
     virtual int step_async(int iterations, double damping) = 0;
     virtual int sync(int* failed) = 0;
@@ -381,6 +383,53 @@ struct Ctx : CtxBase {
         for (int e = 0; e < nE; ++e) vol2_h[e] = 2.0 * d->volume[e];
         if (int rc = assemble(wsum)) return rc;
         return alloc_work(c);
+    }
+
+    // pd_equilibrium (pdsolver.py:315-338): proximal local/global rounds on the quasi-static
+    // objective; the simulation state is untouched (own iterate buffers).  A round whose
+    // solve needs zero CG iterations leaves x unchanged, so the rest would repeat it: stop.
+    int equilibrium(const double* ha, const double* hx0, const double* hpins, int iterations, double* x_out,
+                    int* failed) override {
+        if (!G64k.p) return fail(VKPD_EINVAL, "pd_equilibrium needs a mesh context");
+        if (iterations < 0 || iterations > 100000) return fail(VKPD_EINVAL, "bad iteration count");
+        if (nP > 0 && !hpins) return fail(VKPD_EINVAL, "pin values required");
+        if (failed) *failed = -1;
+        DBuf<V4> a4;
+        CK(a4.alloc(n));
+        if (int rc = upload_nodes(ha, a4.p)) return rc;
+        if (int rc = upload_nodes(hx0, tmp4a.p)) return rc;
+        DBuf<V4> p4;
+        if (nP > 0) {
+            CK(p4.alloc(nP));
+            CK(cudaMemcpyAsync(stage.p, hpins, sizeof(double) * 3 * nP, cudaMemcpyHostToDevice, stream));
+            k_rows_in<T><<<cdiv(nP, 256), 256, 0, stream>>>(nP, stage.p, p4.p);
+            CK(cudaGetLastError());
+            vk::k_set_pinned<T><<<cdiv(nP, 256), 256, 0, stream>>>(n, nF, p4.p, tmp4a.p);
+            CK(cudaGetLastError());
+        }
+        CK(cudaMemsetAsync(fail_iter.p, 0x7f, sizeof(int), stream));     // 0x7f7f7f7f: no failure
+        const vk::LocalArgs<T> la = local_args(tmp4a.p);
+        for (int it = 0; it < iterations && nF > 0; ++it) {
+            vk::k_eq_target<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, tmp4a.p, a4.p, tmp4b.p);
+            CK(cudaGetLastError());
+            if (int rc = launch_local_resid(la)) return rc;
+            vk::PcgArgs<T> pa = pcg_args(vk::INIT_PD, it, iters.p);
+            pa.x = tmp4a.p; pa.xhat = tmp4b.p;
+            pa.warm = nullptr; pa.rounds = nullptr;
+            pa.inv_diag = inv_diag.p; pa.cdiag = nullptr; pa.cb = nullptr; pa.coll = nullptr; pa.ncoll = 0;
+            pa.ell_kd = ell_kd.p;
+            CK(launch_pcg(pa));
+            int cgi = -1, fi = 0;
+            CK(cudaMemcpyAsync(&cgi, iters.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+            CK(cudaMemcpyAsync(&fi, fail_iter.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            if (fi != 0x7f7f7f7f) {
+                if (failed) *failed = fi;
+                return fail(VKPD_ENONFINITE, "quasi-static projection diverged at iteration " + std::to_string(fi));
+            }
+            if (cgi == 0) break;
+        }
+        return download_nodes(tmp4a.p, x_out);
     }
 
     // per-frame output step (transfer.py:26-28, cli.py:639-640)
@@ -1476,6 +1525,11 @@ int vkpd_v2y(int64_t n_yarn, const int64_t* indptr, const int64_t* indices, cons
     CK(cudaGetLastError());
     CK(cudaMemcpy(y, dy.p, sizeof(double) * 3 * n_yarn, cudaMemcpyDeviceToHost));
     return VKPD_OK;
+}
+int vkpd_equilibrium(vkpd_ctx* ctx, const double* inertia_target, const double* x0, const double* pin_vals,
+                     int iterations, double* x_out, int* failed_iter) {
+    if (!inertia_target || !x0 || !x_out) return fail(VKPD_EINVAL, "null array");
+    CTX_CALL(equilibrium(inertia_target, x0, pin_vals, iterations, x_out, failed_iter));
 }
 int vkpd_set_gammas(vkpd_ctx* ctx, const double* gamma_s, const double* gamma_v) {
     if (!gamma_s || !gamma_v) return fail(VKPD_EINVAL, "null gamma arrays");

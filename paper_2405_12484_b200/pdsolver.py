@@ -359,6 +359,38 @@ def _pd_step_host_solver(state, mesh, gammas, iterations, forces, solver, dampin
     return state
 
 
+def pd_equilibrium(mesh, gammas, inertia_target, x0, pins, pin_vals, dt, iterations=PD_ITERS_DEFAULT,
+                   solver=None, precision="fp64", tol=None):
+    """Proximal local/global rounds on E(x) + (1/dt^2) a^T M x (`pdsolver.py:315-338`).
+
+    Each round solves K x = (M/dt^2)(x_cur - a) + elastic rhs.  Without `solver` the
+    rounds run on the device (`vkpd_equilibrium`, fitting-side default precision float64);
+    any object with `.solve(B, pin_vals)` runs the reference loop with the local step on
+    the device.  RuntimeError "quasi-static projection diverged at iteration {it}".
+    """
+    _check_inputs(mesh, gammas, dt)
+    pins = np.asarray(pins, dtype=np.int64)
+    a = np.asarray(inertia_target, dtype=float).reshape(-1, 3)
+    pv = np.asarray(pin_vals, dtype=float).reshape(-1, 3) if len(pins) else np.empty((0, 3))
+    if solver is None:
+        ctx = device_context(mesh, gammas, dt, pins, precision, tol)
+        try:
+            return ctx.equilibrium(a, x0, pv, iterations)
+        except _abi.NonFiniteError as exc:
+            raise RuntimeError(str(exc)) from None
+    ctx = device_context(mesh, gammas, dt, (), precision)
+    x = np.asarray(x0, dtype=float).reshape(-1, 3).copy()
+    if len(pins):
+        x[pins] = pv
+    m_dt2 = mesh.node_mass[:, None] / dt ** 2
+    for it in range(iterations):
+        rhs = ctx.elastic_rhs(x, with_frv=False)[0]
+        x = np.asarray(solver.solve(m_dt2 * (x - a) + rhs, pv), dtype=float)
+        if not np.all(np.isfinite(x)):
+            raise RuntimeError(f"quasi-static projection diverged at iteration {it}")
+    return x
+
+
 def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=None, colliders=(),
                   iterations=PD_ITERS_DEFAULT, solver_mode="direct", n_domains=2, modes_per_domain=20,
                   refine_sweeps=30, aggregation=2, chebyshev=False, damping=1.0, polish_tol=None,

@@ -174,3 +174,12 @@ SCENES = {
 
 def make_scene(key, **kw):
     return SCENES[key](**kw)
+
+
+def equilibrium_case():
+    """C1 inputs of the pd_equilibrium fixtures: a sagging inertia target, a perturbed start."""
+    sc = c1_swatch()
+    rng = np.random.default_rng(11)
+    a = 0.3 * sc.dt ** 2 * sc.forces / sc.mesh.node_mass[:, None]
+    x0 = sc.mesh.nodes + 0.001 * rng.normal(size=sc.mesh.nodes.shape)
+    return sc, a, x0

@@ -183,6 +183,17 @@ def make_big(key, frames_keep, steps, f32_disp):
     print(key, "seconds", el)
 
 
+def make_equilibrium():
+    sc, a, x0 = scenes.equilibrium_case()
+    rm = ref_mesh(sc)
+    gam = ref_mat.MaterialField(sc.gammas.gamma_s, sc.gammas.gamma_v)
+    out = {}
+    for its in (1, 5, 30):
+        out[f"x{its}"] = ref_pd.pd_equilibrium(rm, gam, a, x0, sc.pins, sc.pin_targets, sc.dt, iterations=its)
+    np.savez_compressed(os.path.join(HERE, "equilibrium.npz"), digest=scene_digest(sc), a=a, x0=x0, **out)
+    print("equilibrium fixtures written")
+
+
 def make_io():
     """Mesh / material files written by the reference writers, and what its readers return."""
     from volknit import cli as ref_cli
@@ -209,6 +220,8 @@ if __name__ == "__main__":
         make_projections()
         make_c1()
         make_solvers()
+    if what in ("eq", "all"):
+        make_equilibrium()
     if what in ("io", "all"):
         make_io()
     if what in ("contact", "all"):

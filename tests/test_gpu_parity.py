@@ -458,3 +458,42 @@ def test_frame_outputs_on_device_state(c1, rng, prec):
         assert np.array_equal(y, interp @ x)
         ref = float(np.abs(np.linalg.det(m.deformation_gradients(x)) - 1.0).max())
         assert abs(dev - ref) <= 1e-12 * max(1.0, ref)
+
+
+# ---------------------------------------------------------------------------
+# pd_equilibrium (fitting-side forward solve)
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-10), ("fp32", 2e-5)])
+def test_pd_equilibrium_matches_reference(prec, tol):
+    g = golden("equilibrium.npz")
+    sc, a, x0 = scenes.equilibrium_case()
+    assert scene_digest(sc) == str(g["digest"])
+    for its in (1, 5, 30):
+        x = pdsolver.pd_equilibrium(sc.mesh, sc.gammas, a, x0, sc.pins, sc.pin_targets, sc.dt,
+                                    iterations=its, precision=prec)
+        assert rel_l2(x, g[f"x{its}"]) < tol, its
+        assert np.abs(x[sc.pins] - sc.pin_targets).max() < (1e-14 if prec == "fp64" else 1e-7)
+
+
+def test_pd_equilibrium_host_solver_and_divergence(c1):
+    sc, a, x0 = scenes.equilibrium_case()
+    g = golden("equilibrium.npz")
+    K = orc.assemble_K(sc.mesh.tets, sc.mesh.shape_grad, sc.mesh.volume, sc.gammas.gamma_s, sc.gammas.gamma_v,
+                       sc.mesh.node_mass, sc.dt, sc.n_nodes)
+    ref_solver = orc.GlobalSolver(K, np.setdiff1d(np.arange(sc.n_nodes), sc.pins), sc.pins)
+    x = pdsolver.pd_equilibrium(sc.mesh, sc.gammas, a, x0, sc.pins, sc.pin_targets, sc.dt, iterations=5,
+                                solver=ref_solver)
+    assert rel_l2(x, g["x5"]) < 1e-10
+
+    class BadSolver:
+        def solve(self, b, pin_vals):
+            return np.full_like(b, np.nan)
+
+    with pytest.raises(RuntimeError, match="diverged at iteration 0"):
+        pdsolver.pd_equilibrium(sc.mesh, sc.gammas, a, x0, sc.pins, sc.pin_targets, sc.dt, iterations=3,
+                                solver=BadSolver())
+    bad = x0.copy()
+    bad[np.setdiff1d(np.arange(sc.n_nodes), sc.pins)[-1]] = np.nan
+    with pytest.raises(RuntimeError, match="diverged at iteration 0"):
+        pdsolver.pd_equilibrium(sc.mesh, sc.gammas, a, bad, sc.pins, sc.pin_targets, sc.dt, iterations=3)

@@ -119,3 +119,15 @@ def test_contact_oracle_matches_reference():
         x, v = orc.pd_step_contact(x, v, sc.dt, m.tets, m.shape_grad, m.volume, sc.gammas.gamma_s,
                                    sc.gammas.gamma_v, m.node_mass, [], None, sc.forces, colliders, 10, 0.9)
         assert np.abs(x - g["frames"][k]).max() < 1e-12
+
+
+def test_pd_equilibrium_oracle_matches_reference():
+    g = golden("equilibrium.npz")
+    sc, a, x0 = scenes.equilibrium_case()
+    assert scene_digest(sc) == str(g["digest"])
+    assert np.array_equal(a, g["a"]) and np.array_equal(x0, g["x0"])
+    m = sc.mesh
+    for its in (1, 5):
+        x = orc.pd_equilibrium(x0, m.tets, m.shape_grad, m.volume, sc.gammas.gamma_s, sc.gammas.gamma_v,
+                               m.node_mass, a, sc.pins, sc.pin_targets, sc.dt, iterations=its)
+        assert rel_l2(x, g[f"x{its}"]) < 1e-12
