@@ -169,6 +169,10 @@ int vkpd_cms_solve(vkpd_ctx* ctx, const double* B, const double* P, int k, int s
 int vkpd_batch_projections(int precision, int64_t n, const double* F, double* R, double* V,
                            unsigned int* n_robust, unsigned int* n_fallback);
 
+/* projection_jacobians_batch (material.py:490-524): d vec(R)/d vec(F) and d vec(V)/d vec(F),
+ * (n, 9, 9) each, row-major vec layout, float64 */
+int vkpd_projection_jacobians(int64_t n, const double* F, double* JR, double* JV);
+
 /* pd_equilibrium (pdsolver.py:315-338): `iterations` proximal local/global rounds solving
  * K x = (M/dt^2)(x_cur - a) + rhs from x0 with pinned rows = pin_vals (n_pins,3); the
  * simulation state is not touched.  VKPD_ENONFINITE with *failed_iter on non-finite x

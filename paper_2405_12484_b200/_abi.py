@@ -26,6 +26,7 @@ EXPORTS = (
     "vkpd_power_rho", "vkpd_cms_set_basis", "vkpd_cms_solve", "vkpd_dev_residual", "vkpd_dev_apply_K",
     "vkpd_dev_inv_diag", "vkpd_get_node_order", "vkpd_get_sizes", "vkpd_set_colliders",
     "vkpd_set_gammas", "vkpd_set_yarn_interp", "vkpd_frame_outputs", "vkpd_v2y", "vkpd_equilibrium",
+    "vkpd_projection_jacobians",
 )
 
 
@@ -396,6 +397,15 @@ class Context:
                     robust=st.robust, fallback=st.fallback, pcg_blocks=st.pcg_blocks,
                     ell_width=st.ell_width, n_free=st.n_free, local_ms=list(st.local_ms[:n]),
                     global_ms=list(st.global_ms[:n]), pd_rounds_total=st.pd_rounds_total)
+
+
+def projection_jacobians(F):
+    """(d vec R / d vec F, d vec V / d vec F), each (n, 9, 9), on the device."""
+    F = f64(F).reshape(-1, 3, 3)
+    n = F.shape[0]
+    JR, JV = np.empty((n, 9, 9)), np.empty((n, 9, 9))
+    check(load().vkpd_projection_jacobians(C.c_int64(n), ptr(F), ptr(JR), ptr(JV)))
+    return JR, JV
 
 
 def v2y(interp, x):

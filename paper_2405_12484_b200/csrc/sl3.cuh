@@ -308,7 +308,8 @@ VK_HD bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, cons
 }
 
 // `_sl3_solve_clamping` (material.py:217-239); returns false for "None"
-VK_HD bool solve_clamping(const double (&sig)[3], double (&s)[3], double& lam) {
+// `clamped` (optional, 3 entries): the frozen pattern of the returned solution (~free).
+VK_HD bool solve_clamping(const double (&sig)[3], double (&s)[3], double& lam, bool* clamped = nullptr) {
     bool fr[3] = {true, true, true};
     for (int round = 0; round < 3; ++round) {
         VK_SL3_PROBE(2);
@@ -316,7 +317,10 @@ VK_HD bool solve_clamping(const double (&sig)[3], double (&s)[3], double& lam) {
         if (!newton_free(sig, s, lam, fr)) return false;
         bool viol[3], any = false;
         for (int i = 0; i < 3; ++i) { viol[i] = fr[i] && (s[i] < kFloor - 1e-12); any |= viol[i]; }
-        if (!any) return true;
+        if (!any) {
+            if (clamped) for (int i = 0; i < 3; ++i) clamped[i] = !fr[i];
+            return true;
+        }
         int nfree = 0, last = -1;
         for (int i = 0; i < 3; ++i) { fr[i] = fr[i] && !viol[i]; if (fr[i]) { ++nfree; last = i; } }
         if (nfree == 1) {
@@ -325,6 +329,7 @@ VK_HD bool solve_clamping(const double (&sig)[3], double (&s)[3], double& lam) {
             double p[3];
             pairprod(s, p);
             lam = (sig[last] - s[last]) / p[last];
+            if (clamped) for (int i = 0; i < 3; ++i) clamped[i] = !fr[i];
             return true;
         }
     }
@@ -384,7 +389,10 @@ VK_HD void robust_fallback(const double (&sig)[3], double (&out)[3]) {
     out[0] = s[0]; out[1] = s[1]; out[2] = s[2];
 }
 
-VK_HD bool project_robust(const double (&sig)[3], double (&out)[3]) {
+// lam_out / cl_out (optional): multiplier and clamp pattern of the returned solution
+// (the fallback reports lam = 0 and clamped = s <= floor, material.py:281-287)
+VK_HD bool project_robust(const double (&sig)[3], double (&out)[3], double* lam_out = nullptr,
+                          bool* cl_out = nullptr) {
     double starts[4][3];
     int ns = 0;
     for (int i = 0; i < 3; ++i) starts[0][i] = fmax(sig[i], kFloor);
@@ -414,13 +422,16 @@ VK_HD bool project_robust(const double (&sig)[3], double (&out)[3]) {
         pairprod(s, p);
         const double den = p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
         double lam = den > 1e-300 ? (s[0] * s[1] * s[2] - 1.0) / den : 0.0;
-        if (!solve_clamping(sig, s, lam)) continue;
+        bool cl[3] = {false, false, false};
+        if (!solve_clamping(sig, s, lam, cl)) continue;
         if (nanmin3(s) < kFloor - 1e-9 || fabs(s[0] * s[1] * s[2] - 1.0) > 1e-8) continue;
         const double obj = sq3(s, sig);
         if (!have || obj < best - 1e-15) {
             have = true;
             best = obj;
             out[0] = s[0]; out[1] = s[1]; out[2] = s[2];
+            if (lam_out) *lam_out = lam;
+            if (cl_out) for (int i = 0; i < 3; ++i) cl_out[i] = cl[i];
         }
     }
     if (have) return true;
@@ -431,6 +442,8 @@ VK_HD bool project_robust(const double (&sig)[3], double (&out)[3]) {
         for (int i = 0; i < 3; ++i) s[i] = fmax(s[i] / c, kFloor);
     }
     out[0] = s[0]; out[1] = s[1]; out[2] = s[2];
+    if (lam_out) *lam_out = 0.0;
+    if (cl_out) for (int i = 0; i < 3; ++i) cl_out[i] = s[i] <= kFloor;
     return false;
 }
 
@@ -440,7 +453,8 @@ VK_HD bool project_robust(const double (&sig)[3], double (&out)[3]) {
 // defer = true: a "suspicious" element returns 3 without running the robust
 // scalar path; the caller queues it for a separate dense pass (no warp
 // divergence between the cheap batch path and the expensive robust one).
-VK_HD int project(const double (&sig)[3], double (&s)[3], bool defer = false) {
+VK_HD int project(const double (&sig)[3], double (&s)[3], bool defer = false, double* lam_out = nullptr,
+                  bool* cl_out = nullptr) {
     // Elements outside [0.2, 5] are "suspicious" whatever the batch Newton
     // returns, and the reference overwrites their batch result with the robust
     // scalar solve (material.py:377-391) -- so the batch solves are skipped.
@@ -449,7 +463,7 @@ VK_HD int project(const double (&sig)[3], double (&s)[3], bool defer = false) {
         const double mx = fmax(fmax(fabs(sig[0]), fabs(sig[1])), fabs(sig[2]));
         if (mn < 0.2 || mx > 5.0) {
             if (defer) return 3;
-            return project_robust(sig, s) ? 1 : 2;
+            return project_robust(sig, s, lam_out, cl_out) ? 1 : 2;
         }
     }
     for (int i = 0; i < 3; ++i) s[i] = fmax(sig[i], kFloor);
@@ -485,6 +499,7 @@ VK_HD int project(const double (&sig)[3], double (&s)[3], bool defer = false) {
         if (ok2 && nanmin3(s2) >= kFloor - 1e-12 && obj2 < obj - 1e-15) {
             s[0] = s2[0]; s[1] = s2[1]; s[2] = s2[2];
             obj = obj2;
+            lam = lam2;
             feas = true;
         }
     }
@@ -500,9 +515,13 @@ VK_HD int project(const double (&sig)[3], double (&s)[3], bool defer = false) {
             odd = obj > oref + 1e-12;
         }
     }
-    if (!odd) return 0;
+    if (!odd) {
+        if (lam_out) *lam_out = lam;
+        if (cl_out) cl_out[0] = cl_out[1] = cl_out[2] = false;
+        return 0;
+    }
     if (defer) return 3;
-    return project_robust(sig, s) ? 1 : 2;
+    return project_robust(sig, s, lam_out, cl_out) ? 1 : 2;
 }
 
 }  // namespace sl3

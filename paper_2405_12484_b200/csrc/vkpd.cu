@@ -20,6 +20,7 @@
 #include "cms.cuh"
 #include "frame.cuh"
 #include "output.cuh"
+#include "jacobian.cuh"
 
 namespace {
 
@@ -1617,6 +1618,24 @@ int vkpd_cms_solve(vkpd_ctx* ctx, const double* B, const double* P, int k, int s
 int vkpd_get_stats(vkpd_ctx* ctx, vkpd_stats* st) {
     if (!st) return fail(VKPD_EINVAL, "null stats");
     CTX_CALL(stats(st));
+}
+
+int vkpd_projection_jacobians(int64_t n, const double* F, double* JR, double* JV) {
+    if (n < 0 || (n > 0 && (!F || !JR || !JV))) return fail(VKPD_EINVAL, "bad arguments");
+    int count = 0;
+    if (vkpd_device_count(&count) != VKPD_OK || count == 0)
+        return fail(VKPD_ECUDA, "no CUDA device available (the vkpd library has no CPU path)");
+    for (int64_t i = 0; i < 9 * n; ++i)
+        if (!std::isfinite(F[i])) return fail(VKPD_EINVAL, "non-finite deformation gradient in batch");
+    if (n == 0) return VKPD_OK;
+    DBuf<double> dF, dR, dV;
+    CK(dF.alloc((size_t)9 * n)); CK(dR.alloc((size_t)81 * n)); CK(dV.alloc((size_t)81 * n));
+    CK(cudaMemcpy(dF.p, F, sizeof(double) * 9 * n, cudaMemcpyHostToDevice));
+    vk::k_proj_jacobians<<<cdiv(n, 128), 128>>>((int)n, dF.p, dR.p, dV.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(JR, dR.p, sizeof(double) * 81 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(JV, dV.p, sizeof(double) * 81 * n, cudaMemcpyDeviceToHost));
+    return VKPD_OK;
 }
 
 int vkpd_batch_projections(int precision, int64_t n, const double* F, double* R, double* V,

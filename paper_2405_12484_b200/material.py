@@ -46,3 +46,15 @@ def batch_projections(F, precision="fp64"):
     if not np.all(np.isfinite(F)):
         raise ValueError("non-finite deformation gradient in batch")
     return _abi.batch_projections(F, precision)
+
+
+def projection_jacobians_batch(F):
+    """Batched (d vec R / d vec F, d vec V / d vec F), each (B, 9, 9) (`material.py:490-524`).
+
+    Row-major vec layout; float64 on the GPU (`vkpd_projection_jacobians`).
+    """
+    from . import _abi
+    F = np.ascontiguousarray(F, dtype=np.float64).reshape(-1, 3, 3)
+    if not np.all(np.isfinite(F)):
+        raise ValueError("non-finite deformation gradient in batch")
+    return _abi.projection_jacobians(F)

@@ -183,6 +183,17 @@ def make_big(key, frames_keep, steps, f32_disp):
     print(key, "seconds", el)
 
 
+def make_jacobians():
+    """Reference projection_jacobians_batch on 600 cases of the projection set."""
+    g = np.load(os.path.join(HERE, "projections.npz"))
+    F = g["F"]
+    idx = np.unique(np.concatenate([np.arange(0, len(F), max(1, len(F) // 500)), np.arange(len(F) - 100, len(F))]))
+    F = F[idx]
+    JR, JV = ref_mat.projection_jacobians_batch(F)
+    np.savez_compressed(os.path.join(HERE, "jacobians.npz"), F=F, JR=JR, JV=JV)
+    print("jacobians", F.shape)
+
+
 def make_equilibrium():
     sc, a, x0 = scenes.equilibrium_case()
     rm = ref_mesh(sc)
@@ -220,6 +231,8 @@ if __name__ == "__main__":
         make_projections()
         make_c1()
         make_solvers()
+    if what in ("jac", "all"):
+        make_jacobians()
     if what in ("eq", "all"):
         make_equilibrium()
     if what in ("io", "all"):

@@ -497,3 +497,30 @@ def test_pd_equilibrium_host_solver_and_divergence(c1):
     bad[np.setdiff1d(np.arange(sc.n_nodes), sc.pins)[-1]] = np.nan
     with pytest.raises(RuntimeError, match="diverged at iteration 0"):
         pdsolver.pd_equilibrium(sc.mesh, sc.gammas, a, bad, sc.pins, sc.pin_targets, sc.dt, iterations=3)
+
+
+# ---------------------------------------------------------------------------
+# projection derivatives (material.py:490-524)
+
+
+def test_projection_jacobians_match_reference():
+    g = golden("jacobians.npz")
+    JR, JV = material.projection_jacobians_batch(g["F"])
+    for J, R in ((JR, g["JR"]), (JV, g["JV"])):
+        scale = np.maximum(np.abs(R).reshape(len(R), -1).max(1), 1.0)
+        err = np.abs(J - R).reshape(len(R), -1).max(1) / scale
+        assert err.max() < 1e-8, (int(err.argmax()), float(err.max()))
+
+
+def test_projection_jacobians_finite_difference(rng):
+    F = np.eye(3) + 0.3 * rng.normal(size=(64, 3, 3))
+    F[np.linalg.det(F) < 0.2] = np.eye(3)
+    JR, JV = material.projection_jacobians_batch(F)
+    h = 1e-6
+    for k in range(9):
+        dF = np.zeros((3, 3))
+        dF.flat[k] = h
+        Rp, Vp = material.batch_projections(F + dF)
+        Rm, Vm = material.batch_projections(F - dF)
+        assert np.abs((Rp - Rm).reshape(-1, 9) / (2 * h) - JR[:, :, k]).max() < 1e-5
+        assert np.abs((Vp - Vm).reshape(-1, 9) / (2 * h) - JV[:, :, k]).max() < 1e-5
