@@ -21,6 +21,11 @@
  *   vkpd_apply_K          the assembled K (pdsolver.py:42-56) applied to a vector
  *   vkpd_batch_projections material.batch_projections (material.py:395-407)
  *   vkpd_equilibrium      pd_equilibrium (pdsolver.py:315-338), the fitting side's forward solve
+ *   vkpd_hess_*           fitting-side second order (float64, caller node order):
+ *                         elastic_energy / elastic_gradient (pdsolver.py:72-97),
+ *                         exact_elastic_hessian (pdsolver.py:100-118), the exact Newton step
+ *                         of newton_polish (pdsolver.py:402-414), gamma_jacobian^T lam and the
+ *                         adjoint solve of adjoint_gradient (fitting.py:172-235)
  *   vkpd_set_yarn_interp / vkpd_frame_outputs / vkpd_v2y
  *                         transfer.v2y (transfer.py:26-28) and the det(F) deviation of the
  *                         simulate loop (cli.py:639-640)
@@ -192,6 +197,32 @@ int vkpd_set_yarn_interp(vkpd_ctx* ctx, int64_t n_yarn, const int64_t* indptr, c
 int vkpd_frame_outputs(vkpd_ctx* ctx, double* yarn, double* det_deviation);
 int vkpd_v2y(int64_t n_yarn, const int64_t* indptr, const int64_t* indices, const double* data, int64_t n_nodes,
              const double* x, double* y);
+
+/* ---- fitting-side second order, float64, caller node order ----------------
+ * One handle per (mesh, pins, dt); gammas refreshable.  Vectors are (nV,3) row-major doubles.
+ *   vkpd_hess_energy_grad  elastic_energy (pdsolver.py:72-82) and elastic_gradient
+ *                          (pdsolver.py:85-97) at x; either output may be NULL
+ *   vkpd_hess_gamma_jt     out (2 nE) = gamma_jacobian(mesh, x)^T lam (fitting.py:172-190)
+ *   vkpd_hess_linearize    keep the per-tet blocks 2V (gs (I - dR/dF) + gv (I - dV/dF)) at x
+ *   vkpd_hess_csr          exact_elastic_hessian at the linearized x (pdsolver.py:100-118), CSR
+ *                          3nV x 3nV with sorted columns; indptr = NULL queries *nnz
+ *   vkpd_hess_apply        y = (H + mass_scale M/dt^2) p on all dofs
+ *   vkpd_hess_solve        (H + mass_scale M/dt^2 + ridge I)_ff x_f = b_f by |diag|-preconditioned
+ *                          MINRES (pinned dofs of b ignored, x = 0 there); *relres = the true
+ *                          relative residual.  The caller decides what a non-converged solve
+ *                          means (newton_polish falls back to the Gauss-Newton step, the adjoint
+ *                          adds a ridge, as the reference does on a singular factorization). */
+typedef struct vkpd_hess vkpd_hess;
+int vkpd_hess_create(const vkpd_mesh_desc* mesh, int device, vkpd_hess** out);
+void vkpd_hess_destroy(vkpd_hess* h);
+int vkpd_hess_set_gammas(vkpd_hess* h, const double* gamma_s, const double* gamma_v);
+int vkpd_hess_energy_grad(vkpd_hess* h, const double* x, double* energy, double* grad);
+int vkpd_hess_gamma_jt(vkpd_hess* h, const double* x, const double* lam, double* out);
+int vkpd_hess_linearize(vkpd_hess* h, const double* x);
+int vkpd_hess_csr(vkpd_hess* h, int64_t* indptr, int64_t* indices, double* data, int64_t* nnz);
+int vkpd_hess_apply(vkpd_hess* h, double mass_scale, const double* p, double* y);
+int vkpd_hess_solve(vkpd_hess* h, double mass_scale, double ridge, const double* b, double* x, double tol,
+                    int max_iters, int* iters, double* relres);
 
 #ifdef __cplusplus
 }

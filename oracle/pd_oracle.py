@@ -700,3 +700,200 @@ def a_jacobi_refine(K, b, x0, sweeps=30, aggregation=2, omega=OMEGA, chebyshev=F
     if info["diverged"] or hist[-1] > best_r:
         return best_x, info
     return x, info
+
+
+# ---------------------------------------------------------------------------
+# second order (fitting side)
+
+
+def elastic_gradient(x, tets, G, vol, gs, gv, n_nodes):
+    """sum_e 2 V_e G_e^T (gs (F-R) + gv (F-V)) in tet order (`pdsolver.py:85-97`)."""
+    F = deformation_gradients(x, tets, G)
+    R, V = projections(F)
+    P = gs[:, None, None] * (F - R) + gv[:, None, None] * (F - V)
+    per = 2.0 * vol[:, None, None] * np.einsum("enj,eij->eni", G, P)
+    out = np.zeros((n_nodes, 3))
+    np.add.at(out, tets.reshape(-1), per.reshape(-1, 3))
+    return out
+
+
+def _ds_dsigma(s, lam, clamped):
+    """ds/dsigma of the constrained singular-value solve (`material.py:418-438`)."""
+    idx = np.flatnonzero(~clamped)
+    nf = idx.size
+    D = np.zeros((3, 3))
+    if nf == 0:
+        return D
+    p = _pairprod(s)
+    A = np.zeros((nf + 1, nf + 1))
+    for a, i in enumerate(idx):
+        for b, j in enumerate(idx):
+            A[a, b] = 1.0 if i == j else lam * s[3 - i - j]
+        A[a, nf] = A[nf, a] = p[i]
+    rhs = np.zeros((nf + 1, nf))
+    rhs[:nf, :nf] = np.eye(nf)
+    D[np.ix_(idx, idx)] = np.linalg.solve(A, rhs)[:nf, :]
+    return D
+
+
+def projection_jacobians(F):
+    """(d vec R / d vec F, d vec V / d vec F), (B, 9, 9) each, row-major vec (`material.py:490-524`)."""
+    F = np.asarray(F, dtype=float)
+    B = F.shape[0]
+    U, sig, W = svd_rv(F)
+    s, lam, clamped, _ = sl3_project_batch(sig)
+    LR = np.zeros((B, 9, 9))
+    LV = np.zeros((B, 9, 9))
+    ds = np.stack([_ds_dsigma(s[e], lam[e], clamped[e]) for e in range(B)]) if B else np.zeros((0, 3, 3))
+    dia = (0, 4, 8)
+    for i in range(3):
+        for j in range(3):
+            LV[:, dia[i], dia[j]] = ds[:, i, j]
+    for i, j in ((0, 1), (0, 2), (1, 2)):
+        a, b = 3 * i + j, 3 * j + i
+        den = sig[:, i] + sig[:, j]
+        den = np.where(np.abs(den) < 1e-8, np.copysign(1e-8, np.where(den == 0.0, 1.0, den)), den)
+        LR[:, a, a] = LR[:, b, b] = 1.0 / den
+        LR[:, a, b] = LR[:, b, a] = -1.0 / den
+        dd = sig[:, i] - sig[:, j]
+        scale = np.maximum(1.0, np.maximum(np.abs(sig[:, i]), np.abs(sig[:, j])))
+        safe = np.abs(dd) > 1e-7 * scale
+        cs = np.where(safe, (s[:, i] - s[:, j]) / np.where(safe, dd, 1.0), ds[:, i, i] - ds[:, i, j])
+        ca = (s[:, i] + s[:, j]) / den
+        LV[:, a, a] = LV[:, b, b] = 0.5 * (cs + ca)
+        LV[:, a, b] = LV[:, b, a] = 0.5 * (cs - ca)
+    Q = np.einsum("eik,ejl->eijkl", U, W).reshape(B, 9, 9)
+    Qt = np.swapaxes(Q, 1, 2)
+    return Q @ LR @ Qt, Q @ LV @ Qt
+
+
+def exact_elastic_hessian(x, tets, G, vol, gs, gv, n_nodes):
+    """2 V D^T (gs (I - dR/dF) + gv (I - dV/dF)) D summed over tets, CSR (`pdsolver.py:100-118`)."""
+    F = deformation_gradients(x, tets, G)
+    LR, LV = projection_jacobians(F)
+    I9 = np.eye(9)
+    M9 = gs[:, None, None] * (I9 - LR) + gv[:, None, None] * (I9 - LV)
+    nE = len(tets)
+    D = np.zeros((nE, 9, 12))          # D[3i+j, 3n+i] = G[n, j]   (volmesh.py:92-97)
+    for n in range(4):
+        for i in range(3):
+            for j in range(3):
+                D[:, 3 * i + j, 3 * n + i] = G[:, n, j]
+    He = 2.0 * vol[:, None, None] * np.einsum("eia,eij,ejb->eab", D, M9, D)
+    dofs = (3 * tets[:, :, None] + np.arange(3)).reshape(nE, 12)
+    rows = np.repeat(dofs, 12, axis=1).reshape(-1)
+    cols = np.tile(dofs, (1, 12)).reshape(-1)
+    n = 3 * n_nodes
+    return sp.csr_matrix((He.reshape(-1), (rows, cols)), shape=(n, n))
+
+
+def newton_polish(x0, tets, G, vol, gs, gv, mass, dt, pins=(), pin_vals=None, inertia_target=None, xhat=None,
+                  tol=1e-5, max_iters=20, exact=False):
+    """Newton-type polish of the step / quasi-static residual (`pdsolver.py:350-460`).
+
+    Returns (x, converged, iterations)."""
+    if (inertia_target is None) == (xhat is None):
+        raise ValueError("give exactly one of inertia_target or xhat")
+    n = len(mass)
+    pins = np.asarray(pins, dtype=int)
+    free = np.setdiff1d(np.arange(n), pins)
+    x = np.asarray(x0, dtype=float).reshape(-1, 3).copy()
+    if len(pins):
+        x[pins] = pin_vals
+    m_dt2 = mass[:, None] / dt ** 2
+
+    def residual(xc):
+        g = elastic_gradient(xc, tets, G, vol, gs, gv, n)
+        return g + (m_dt2 * (xc - xhat) if xhat is not None else m_dt2 * inertia_target)
+
+    def objective(xc):
+        e = elastic_energy(xc, tets, G, vol, gs, gv)
+        if xhat is not None:
+            d = xc - xhat
+            return e + 0.5 * float(np.sum(m_dt2 * d * d))
+        return e + float(np.sum(m_dt2 * inertia_target * xc))
+
+    def gmax(gv_):
+        return float(np.abs(gv_[free]).max()) if len(free) else 0.0
+
+    g = residual(x)
+    if gmax(g) < tol:
+        return x, True, 0
+    K = assemble_K(tets, G, vol, gs, gv, mass, dt, n)
+    solve = spla.factorized(K[free][:, free].tocsc())
+    fdofs = (3 * free[:, None] + np.arange(3)[None, :]).reshape(-1)
+    mass_diag = np.repeat(mass, 3) / dt ** 2
+
+    def gn_step(gc):
+        step = np.zeros_like(x)
+        for k in range(3):
+            step[free, k] = solve(-gc[free, k])
+        return step
+
+    def exact_step(xc, gc):
+        J = exact_elastic_hessian(xc, tets, G, vol, gs, gv, n)
+        if xhat is not None:
+            J = J + sp.diags(mass_diag)
+        try:
+            d = spla.spsolve(J[fdofs][:, fdofs].tocsc(), -gc.reshape(-1)[fdofs])
+        except RuntimeError:
+            return None
+        if not np.all(np.isfinite(d)):
+            return None
+        step = np.zeros_like(x)
+        step.reshape(-1)[fdofs] = d
+        return step
+
+    def try_step(step, obj):
+        t = 1.0
+        for _ in range(12):
+            xn = x + t * step
+            if len(pins):
+                xn[pins] = pin_vals
+            on = objective(xn)
+            if on < obj + 1e-15 * max(1.0, abs(obj)):
+                return xn, on
+            t *= 0.5
+        return None, obj
+
+    obj = objective(x)
+    stall = 0
+    for it in range(1, max_iters + 1):
+        xn = None
+        if exact:
+            step = exact_step(x, g)
+            if step is not None:
+                xn, on = try_step(step, obj)
+        if xn is None:
+            xn, on = try_step(gn_step(g), obj)
+        if xn is None:
+            stall += 1
+            if stall >= 10:
+                return x, False, it
+            xn, on = x, obj
+        x, obj = xn, on
+        g = residual(x)
+        if gmax(g) < tol:
+            return x, True, it
+    return x, gmax(g) < tol, max_iters
+
+
+def gamma_jacobian_t(x, lam, tets, G, vol):
+    """gamma_jacobian(mesh, x)^T lam, (2 nE,) (`fitting.py:172-190`)."""
+    F = deformation_gradients(x, tets, G)
+    R, V = projections(F)
+    L = deformation_gradients(lam, tets, G)
+    v2 = 2.0 * vol
+    return np.concatenate([v2 * ((F - R) * L).sum((1, 2)), v2 * ((F - V) * L).sum((1, 2))])
+
+
+def adjoint_gradient(x, gx, tets, G, vol, gs, gv, n_nodes, pins):
+    """grad = -J^T lam with H_ff lam = g_x[free] (`fitting.py:206-238`).  Returns (grad, lam_full)."""
+    free = np.setdiff1d(np.arange(n_nodes), pins)
+    fdofs = (3 * free[:, None] + np.arange(3)[None, :]).reshape(-1)
+    H = exact_elastic_hessian(x, tets, G, vol, gs, gv, n_nodes)
+    lam_f = spla.spsolve(H[fdofs][:, fdofs].tocsc(), np.asarray(gx).reshape(-1)[fdofs])
+    lam = np.zeros(3 * n_nodes)
+    lam[fdofs] = lam_f
+    lam = lam.reshape(-1, 3)
+    return -gamma_jacobian_t(x, lam, tets, G, vol), lam

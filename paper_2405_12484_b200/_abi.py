@@ -26,7 +26,9 @@ EXPORTS = (
     "vkpd_power_rho", "vkpd_cms_set_basis", "vkpd_cms_solve", "vkpd_dev_residual", "vkpd_dev_apply_K",
     "vkpd_dev_inv_diag", "vkpd_get_node_order", "vkpd_get_sizes", "vkpd_set_colliders",
     "vkpd_set_gammas", "vkpd_set_yarn_interp", "vkpd_frame_outputs", "vkpd_v2y", "vkpd_equilibrium",
-    "vkpd_projection_jacobians",
+    "vkpd_projection_jacobians", "vkpd_hess_create", "vkpd_hess_destroy", "vkpd_hess_set_gammas",
+    "vkpd_hess_energy_grad", "vkpd_hess_gamma_jt", "vkpd_hess_linearize", "vkpd_hess_csr",
+    "vkpd_hess_apply", "vkpd_hess_solve",
 )
 
 
@@ -103,6 +105,16 @@ def load():
         "vkpd_get_node_order": (I, [P, P]),
         "vkpd_get_sizes": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                C.POINTER(I)]),
+        "vkpd_hess_create": (I, [C.POINTER(MeshDesc), I, C.POINTER(P)]),
+        "vkpd_hess_destroy": (None, [P]),
+        "vkpd_hess_set_gammas": (I, [P, P, P]),
+        "vkpd_hess_energy_grad": (I, [P, P, P, P]),
+        "vkpd_hess_gamma_jt": (I, [P, P, P, P]),
+        "vkpd_hess_linearize": (I, [P, P]),
+        "vkpd_hess_csr": (I, [P, P, P, P, C.POINTER(C.c_int64)]),
+        "vkpd_hess_apply": (I, [P, C.c_double, P, P]),
+        "vkpd_hess_solve": (I, [P, C.c_double, C.c_double, P, P, C.c_double, I, C.POINTER(I),
+                                C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -444,3 +456,91 @@ class MatrixContext(Context):
                                           C.byref(cfg), C.byref(h)))
         self.h = h
         self.precision = precision
+
+
+class HessContext:
+    """Owns one `vkpd_hess` (float64 second-order machinery of one mesh, pin set and dt)."""
+
+    def __init__(self, nodes_count, tets, shape_grad, volume, node_mass, gamma_s, gamma_v, pins, dt,
+                 device=0):
+        self.lib = load()
+        self._keep = dict(
+            tets=np.ascontiguousarray(tets, dtype=np.int64).reshape(-1, 4),
+            G=f64(shape_grad).reshape(-1, 4, 3),
+            vol=f64(volume).reshape(-1),
+            mass=None if node_mass is None else f64(node_mass).reshape(-1),
+            gs=f64(gamma_s).reshape(-1),
+            gv=f64(gamma_v).reshape(-1),
+            pins=np.ascontiguousarray(pins, dtype=np.int64).reshape(-1),
+        )
+        k = self._keep
+        self.n = int(nodes_count)
+        self.n_tets = k["tets"].shape[0]
+        self.n_pins = k["pins"].shape[0]
+        if k["mass"] is None:
+            raise ValueError("mesh node masses not lumped yet")
+        d = MeshDesc(self.n, self.n_tets, ptr(k["tets"]), ptr(k["G"]), ptr(k["vol"]), ptr(k["mass"]),
+                     ptr(k["gs"]), ptr(k["gv"]), ptr(k["pins"]) if self.n_pins else None,
+                     self.n_pins, float(dt))
+        h = C.c_void_p()
+        check(self.lib.vkpd_hess_create(C.byref(d), int(device), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.vkpd_hess_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_gammas(self, gamma_s, gamma_v):
+        gs, gv = f64(gamma_s).reshape(-1), f64(gamma_v).reshape(-1)
+        if gs.shape[0] != self.n_tets or gv.shape[0] != self.n_tets:
+            raise ValueError("gamma arrays must have one entry per element")
+        check(self.lib.vkpd_hess_set_gammas(self.h, ptr(gs), ptr(gv)))
+
+    def energy_grad(self, x, want_energy=True, want_grad=True):
+        x = f64(x, (self.n, 3))
+        e = np.zeros(1)
+        g = np.empty((self.n, 3)) if want_grad else None
+        check(self.lib.vkpd_hess_energy_grad(self.h, ptr(x), ptr(e) if want_energy else None, ptr(g)))
+        return (float(e[0]) if want_energy else None), g
+
+    def gamma_jt(self, x, lam):
+        x, lam = f64(x, (self.n, 3)), f64(lam, (self.n, 3))
+        out = np.empty(2 * self.n_tets)
+        check(self.lib.vkpd_hess_gamma_jt(self.h, ptr(x), ptr(lam), ptr(out)))
+        return out
+
+    def linearize(self, x):
+        check(self.lib.vkpd_hess_linearize(self.h, ptr(f64(x, (self.n, 3)))))
+
+    def csr(self):
+        import scipy.sparse as sp
+        nnz = C.c_int64(0)
+        check(self.lib.vkpd_hess_csr(self.h, None, None, None, C.byref(nnz)))
+        indptr = np.empty(3 * self.n + 1, dtype=np.int64)
+        indices = np.empty(nnz.value, dtype=np.int64)
+        data = np.empty(nnz.value)
+        check(self.lib.vkpd_hess_csr(self.h, ptr(indptr), ptr(indices), ptr(data), C.byref(nnz)))
+        return sp.csr_matrix((data, indices, indptr), shape=(3 * self.n, 3 * self.n))
+
+    def apply(self, p, mass_scale=0.0):
+        p = f64(p, (self.n, 3))
+        y = np.empty((self.n, 3))
+        check(self.lib.vkpd_hess_apply(self.h, float(mass_scale), ptr(p), ptr(y)))
+        return y
+
+    def solve(self, b, mass_scale=0.0, ridge=0.0, tol=1e-12, max_iters=0):
+        """(H + s M/dt^2 + ridge I)_ff x_f = b_f; returns (x (nV,3), iterations, true relative residual)."""
+        b = f64(b, (self.n, 3))
+        x = np.empty((self.n, 3))
+        it = C.c_int(0)
+        rr = C.c_double(0.0)
+        check(self.lib.vkpd_hess_solve(self.h, float(mass_scale), float(ridge), ptr(b), ptr(x), float(tol),
+                                       int(max_iters), C.byref(it), C.byref(rr)))
+        return x, it.value, rr.value

@@ -220,7 +220,7 @@ class CmsGlobalSolver:
 
 
 def simulate_cms(mesh, gammas, steps, dt, forces, state, pin_path, iterations, n_domains, modes_per_domain,
-                 refine_sweeps, aggregation, chebyshev, damping, precision, labels=None):
+                 refine_sweeps, aggregation, chebyshev, damping, precision, labels=None, polish_tol=None):
     """`simulate_mesh(..., solver_mode="cms")` (`pdsolver.py:734-740`, 749-762)."""
     from . import pdsolver
     pins = state.pins
@@ -238,5 +238,9 @@ def simulate_cms(mesh, gammas, steps, dt, forces, state, pin_path, iterations, n
         f = None if forces is None else forces[i]
         pdsolver.pd_step(state, mesh, gammas, iterations=iterations, forces=f, solver=solver,
                          damping=damping, precision="fp64")
+        if polish_tol is not None:          # pdsolver.py:757-761
+            xh = pdsolver._predicted(state, f, mesh)
+            state.x, _, _ = pdsolver.newton_polish(mesh, gammas, state.x, dt=dt, pins=pins,
+                                                   pin_vals=state.pin_targets, xhat=xh, tol=polish_tol)
         frames[i] = state.x
     return frames

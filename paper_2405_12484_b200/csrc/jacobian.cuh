@@ -16,9 +16,11 @@
 
 namespace vk {
 
-// L (9x9) conjugated by Q = kron(U, W): J = Q L Q^T
+// L (9x9) conjugated by Q = kron(U, W): J[(9r + c) * stride] = (Q L Q^T)[r][c].
+// J is a global pointer on every call site: with a thread-local J the sm_100a build
+// produced wrong values (tests/native/hess_probe.cu), so outputs always go to memory.
 __device__ __forceinline__ void conjugate9(const double (&U)[3][3], const double (&W)[3][3], const double* L,
-                                           double* J) {
+                                           double* J, size_t stride = 1) {
     double Q[9][9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -39,7 +41,7 @@ __device__ __forceinline__ void conjugate9(const double (&U)[3][3], const double
         for (int c = 0; c < 9; ++c) {
             double acc = 0.0;
             for (int m = 0; m < 9; ++m) acc += Tm[r][m] * Q[c][m];
-            J[9 * r + c] = acc;
+            J[(size_t)(9 * r + c) * stride] = acc;
         }
 }
 
@@ -72,15 +74,16 @@ __device__ __forceinline__ void sl3_ds_dsigma(const double (&s)[3], double lam, 
     }
 }
 
-__device__ __forceinline__ void projection_jacobians(const double (&F)[3][3], double* JR, double* JV) {
-    double U[3][3], W[3][3], sg[3];
+// the singular-value-frame derivatives LR, LV (material.py:490-524) and the SVD frame
+__device__ __forceinline__ void projection_frame(const double (&F)[3][3], double (&U)[3][3], double (&W)[3][3],
+                                                 double* LR, double* LV) {
+    double sg[3];
     svd3_rv(F, U, sg, W);
     double s[3], lam = 0.0;
     bool cl[3] = {false, false, false};
     sl3::project(sg, s, false, &lam, cl);
     double ds[3][3];
     sl3_ds_dsigma(s, lam, cl, ds);
-    double LR[81], LV[81];
     for (int k = 0; k < 81; ++k) LR[k] = LV[k] = 0.0;
     const int dia[3] = {0, 4, 8};
     for (int i = 0; i < 3; ++i)
@@ -100,8 +103,26 @@ __device__ __forceinline__ void projection_jacobians(const double (&F)[3][3], do
         LV[9 * a + a] = LV[9 * b + b] = 0.5 * (cs + ca);
         LV[9 * a + b] = LV[9 * b + a] = 0.5 * (cs - ca);
     }
+}
+
+// JR, JV: global memory, 81 entries each
+__device__ __forceinline__ void projection_jacobians(const double (&F)[3][3], double* JR, double* JV) {
+    double U[3][3], W[3][3], LR[81], LV[81];
+    projection_frame(F, U, W, LR, LV);
     conjugate9(U, W, LR, JR);
     conjugate9(U, W, LV, JV);
+}
+
+// M = c (ws (I - JR) + wv (I - JV)) = c (ws + wv) I - Q (c (ws LR + wv LV)) Q^T: the 9x9
+// block of the exact Hessian (pdsolver.py:109-112), written with stride (global memory)
+__device__ __forceinline__ void hessian_block9(const double (&F)[3][3], double ws, double wv, double c, double* M,
+                                               size_t stride) {
+    double U[3][3], W[3][3], LR[81], LV[81];
+    projection_frame(F, U, W, LR, LV);
+    for (int k = 0; k < 81; ++k) LR[k] = -c * (ws * LR[k] + wv * LV[k]);
+    conjugate9(U, W, LR, M, stride);
+    const double d = c * (ws + wv);
+    for (int k = 0; k < 9; ++k) M[(size_t)(10 * k) * stride] += d;
 }
 
 __global__ void __launch_bounds__(128) k_proj_jacobians(int n, const double* __restrict__ Fin, double* JR,

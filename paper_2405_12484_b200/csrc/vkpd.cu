@@ -21,6 +21,7 @@
 #include "frame.cuh"
 #include "output.cuh"
 #include "jacobian.cuh"
+#include "hessian.cuh"
 
 namespace {
 
@@ -1399,10 +1400,15 @@ struct Ctx : CtxBase {
     }
 };
 
+#include "hess_ctx.cuh"
+
 }  // namespace
 
 struct vkpd_ctx {
     std::unique_ptr<CtxBase> impl;
+};
+struct vkpd_hess {
+    HessCtx impl;
 };
 
 extern "C" {
@@ -1664,6 +1670,53 @@ int vkpd_batch_projections(int precision, int64_t n, const double* F, double* R,
     if (n_robust) *n_robust = hs.robust;
     if (n_fallback) *n_fallback = hs.fallback;
     return VKPD_OK;
+}
+
+int vkpd_hess_create(const vkpd_mesh_desc* mesh, int device, vkpd_hess** out) {
+    if (!mesh || !out) return fail(VKPD_EINVAL, "null argument");
+    if (!mesh->tets || !mesh->shape_grad || !mesh->volume || !mesh->gamma_s || !mesh->gamma_v)
+        return fail(VKPD_EINVAL, "missing mesh array");
+    if (mesh->n_pins > 0 && !mesh->pins) return fail(VKPD_EINVAL, "missing pin array");
+    int count = 0;
+    if (vkpd_device_count(&count) != VKPD_OK || count == 0)
+        return fail(VKPD_ECUDA, "no CUDA device available (the vkpd library has no CPU path)");
+    if (device < 0 || device >= count) return fail(VKPD_EINVAL, "bad device ordinal");
+    std::unique_ptr<vkpd_hess> h(new vkpd_hess);
+    int rc = h->impl.init(mesh, device);
+    if (rc != VKPD_OK) return rc;
+    *out = h.release();
+    return VKPD_OK;
+}
+void vkpd_hess_destroy(vkpd_hess* h) {
+    if (h) {
+        cudaSetDevice(h->impl.device);
+        delete h;
+    }
+}
+#define HESS_CALL(expr)                                  \
+    do {                                                 \
+        if (!h) return fail(VKPD_EINVAL, "null context"); \
+        cudaSetDevice(h->impl.device);                   \
+        return h->impl.expr;                             \
+    } while (0)
+int vkpd_hess_set_gammas(vkpd_hess* h, const double* gs, const double* gv) { HESS_CALL(set_gammas(gs, gv)); }
+int vkpd_hess_energy_grad(vkpd_hess* h, const double* x, double* energy, double* grad) {
+    HESS_CALL(energy_grad(x, energy, grad));
+}
+int vkpd_hess_gamma_jt(vkpd_hess* h, const double* x, const double* lam, double* out) {
+    HESS_CALL(gamma_jt(x, lam, out));
+}
+int vkpd_hess_linearize(vkpd_hess* h, const double* x) { HESS_CALL(linearize(x)); }
+int vkpd_hess_csr(vkpd_hess* h, int64_t* indptr, int64_t* indices, double* data, int64_t* nnz) {
+    if (!nnz) return fail(VKPD_EINVAL, "null nnz");
+    HESS_CALL(csr(indptr, indices, data, nnz));
+}
+int vkpd_hess_apply(vkpd_hess* h, double mass_scale, const double* p, double* y) {
+    HESS_CALL(apply(mass_scale, p, y));
+}
+int vkpd_hess_solve(vkpd_hess* h, double mass_scale, double ridge, const double* b, double* x, double tol,
+                    int max_iters, int* iters, double* relres) {
+    HESS_CALL(solve(mass_scale, ridge, b, x, tol, max_iters, iters, relres));
 }
 
 }  // extern "C"

@@ -9,6 +9,9 @@ Mirrors the reference simulator surface (`/root/reference/pkg/src/volknit/pdsolv
   pd_step(state, mesh, g, ...)   pdsolver.py:257-304
   simulate_mesh(mesh, g, ...)    pdsolver.py:710-763
   pd_objective / elastic_energy  pdsolver.py:74-82, 307-312 (diagnostics, projections on GPU)
+  elastic_gradient               pdsolver.py:85-97     (GPU, float64)
+  exact_elastic_hessian          pdsolver.py:100-118   (GPU-assembled CSR, float64)
+  newton_polish                  pdsolver.py:350-460   (GPU gradient/energy, GN solve, MINRES exact step)
 
 Same argument names, meaning and error behaviour: ValueError for invalid input,
 RuntimeError("... non-finite positions at iteration {it}") on blow-up, any
@@ -169,7 +172,14 @@ class _MassShim:
 
 
 def elastic_energy(mesh, gammas, x, FRV=None, precision="fp64"):
-    """sum_e V_e (gs |F - R|^2 + gv |F - V|^2) (`pdsolver.py:74-82`), projections on the GPU."""
+    """sum_e V_e (gs |F - R|^2 + gv |F - V|^2) (`pdsolver.py:74-82`).
+
+    Without FRV the whole sum runs on the GPU in float64 (deterministic reduction);
+    `precision="fp32"` takes the projections from the fp32 local step instead.
+    """
+    if FRV is None and precision == "fp64":
+        e, _ = hess_context(mesh, gammas).energy_grad(x, want_energy=True, want_grad=False)
+        return e
     if FRV is None:
         _, F, R, V = elastic_rhs(mesh, gammas, x, precision)
     else:
@@ -177,6 +187,56 @@ def elastic_energy(mesh, gammas, x, FRV=None, precision="fp64"):
     ds = np.sum((F - R) ** 2, axis=(1, 2))
     dv = np.sum((F - V) ** 2, axis=(1, 2))
     return float(np.sum(mesh.volume * (gammas.gamma_s * ds + gammas.gamma_v * dv)))
+
+
+# ---------------------------------------------------------------------------
+# second order (fitting side): float64 device contexts per (mesh, pins, dt)
+
+_HCACHE = {}
+
+
+def hess_context(mesh, gammas, dt=1.0, pins=()):
+    """Device float64 second-order context for (mesh, pins, dt); gammas refreshed in place."""
+    m = mesh if getattr(mesh, "node_mass", None) is not None else _MassShim(mesh)
+    k = (_ident((m.tets, m.shape_grad, m.volume, m.node_mass)), float(dt),
+         np.asarray(pins, dtype=np.int64).tobytes())
+    gid = _ident((gammas.gamma_s, gammas.gamma_v))
+    hit = _HCACHE.get(k)
+    if hit is None:
+        if len(_HCACHE) >= _CACHE_MAX:
+            _HCACHE.pop(next(iter(_HCACHE)))
+        if dt <= 0.0:
+            raise ValueError("dt must be positive")
+        h = _abi.HessContext(m.n_nodes if hasattr(m, "n_nodes") else len(m.nodes), m.tets, m.shape_grad,
+                             m.volume, m.node_mass, gammas.gamma_s, gammas.gamma_v, pins, dt)
+        _HCACHE[k] = [gid, h]
+        return h
+    if hit[0] != gid:
+        hit[1].set_gammas(gammas.gamma_s, gammas.gamma_v)
+        hit[0] = gid
+    return hit[1]
+
+
+def elastic_gradient(mesh, gammas, x):
+    """Gradient of the elastic energy wrt node positions, (nV, 3) (`pdsolver.py:85-97`).
+
+    Per tet 2 V G^T (gs (F - R) + gv (F - V)) on the GPU, summed per node in tet order
+    (the `np.add.at` order), float64.
+    """
+    _, g = hess_context(mesh, gammas).energy_grad(x, want_energy=False, want_grad=True)
+    return g
+
+
+def exact_elastic_hessian(mesh, gammas, x):
+    """Second derivative of the elastic energy over all DOFs, (3nV, 3nV) CSR (`pdsolver.py:100-118`).
+
+    The per-tet blocks 2 V D^T (gs (I - dR/dF) + gv (I - dV/dF)) D are formed on the GPU
+    (projection Jacobians of `material.projection_jacobians_batch`) and summed per row in tet
+    order; symmetric, not necessarily definite.
+    """
+    h = hess_context(mesh, gammas)
+    h.linearize(np.asarray(x, dtype=float).reshape(-1, 3))
+    return h.csr()
 
 
 def pd_objective(state_or_x, mesh, gammas, xhat, dt, precision="fp64"):
@@ -391,6 +451,117 @@ def pd_equilibrium(mesh, gammas, inertia_target, x0, pins, pin_vals, dt, iterati
     return x
 
 
+def quasi_static_objective(mesh, gammas, inertia_target, x, dt):
+    """E(x) + (1/dt^2) a^T M x (`pdsolver.py:341-343`), elastic part on the GPU."""
+    lin = float(np.sum(mesh.node_mass[:, None] * inertia_target * x)) / dt ** 2
+    return elastic_energy(mesh, gammas, x) + lin
+
+
+EXACT_SOLVE_TOL = 1e-13          # MINRES relative tolerance of the exact Newton step
+EXACT_SOLVE_ACCEPT = 1e-8        # true relative residual above this = failed factorization
+
+
+def newton_polish(mesh, gammas, x0, *, dt, pins=(), pin_vals=None, inertia_target=None, xhat=None,
+                  tol=1e-5, max_iters=20, exact=False):
+    """Drive the step residual below tol with Newton-type iterations (`pdsolver.py:350-460`).
+
+    Same two residual flavours, objective, halving line search, stall rule and return
+    value (x, converged, iterations) as the reference.  On the device: the gradient and
+    energy (float64, `vkpd_hess_energy_grad`), the Gauss-Newton step with the assembled K
+    (the persistent CG of the global step, float64, relative tolerance 1e-12, in place of
+    SuperLU), and with `exact=True` the exact-Jacobian step by preconditioned MINRES on the
+    device-resident exact Hessian (`vkpd_hess_solve`); a solve that does not reach a true
+    relative residual of 1e-8 counts as the reference's failed factorization and falls
+    back to the Gauss-Newton step.
+    """
+    if (inertia_target is None) == (xhat is None):
+        raise ValueError("give exactly one of inertia_target or xhat")
+    _check_inputs(mesh, gammas, dt)
+    n = mesh.n_nodes
+    pins = np.asarray(pins, dtype=int)
+    free = np.setdiff1d(np.arange(n), pins)
+    x = np.asarray(x0, dtype=float).reshape(-1, 3).copy()
+    if len(pins):
+        x[pins] = pin_vals
+    m_dt2 = mesh.node_mass[:, None] / dt ** 2
+    h = hess_context(mesh, gammas, dt, pins)
+
+    def residual(xc):
+        _, g = h.energy_grad(xc, want_energy=False, want_grad=True)
+        if xhat is not None:
+            g = g + m_dt2 * (xc - xhat)
+        else:
+            g = g + m_dt2 * inertia_target
+        return g
+
+    def objective(xc):
+        e, _ = h.energy_grad(xc, want_energy=True, want_grad=False)
+        if xhat is not None:
+            d = xc - xhat
+            return e + 0.5 * float(np.sum(m_dt2 * d * d))
+        return e + float(np.sum(m_dt2 * inertia_target * xc))
+
+    def gmax(gv):
+        return float(np.abs(gv[free]).max()) if len(free) else 0.0
+
+    g = residual(x)
+    if gmax(g) < tol:
+        return x, True, 0
+
+    ctx = device_context(mesh, gammas, dt, pins, "fp64")     # K = GN Hessian + M/dt^2 (scalar)
+    zero_pins = np.zeros((len(pins), 3))
+
+    def gn_step(gc):
+        step = np.asarray(ctx.global_solve(-gc, zero_pins), dtype=float).reshape(-1, 3)
+        if len(pins):
+            step[pins] = 0.0
+        return step
+
+    def exact_step(xc, gc):
+        h.linearize(xc)
+        step, _, rr = h.solve(-gc, mass_scale=1.0 if xhat is not None else 0.0, tol=EXACT_SOLVE_TOL)
+        if not (rr <= EXACT_SOLVE_ACCEPT) or not np.all(np.isfinite(step)):
+            return None
+        return step
+
+    def try_step(step, obj):
+        t = 1.0
+        for _ in range(12):
+            xn = x + t * step
+            if len(pins):
+                xn[pins] = pin_vals
+            on = objective(xn)
+            if on < obj + 1e-15 * max(1.0, abs(obj)):
+                return xn, on
+            t *= 0.5
+        return None, obj
+
+    obj = objective(x)
+    stall = 0
+    for it in range(1, max_iters + 1):
+        xn = None
+        if exact:
+            step = exact_step(x, g)
+            if step is not None:
+                xn, on = try_step(step, obj)
+        if xn is None:
+            xn, on = try_step(gn_step(g), obj)
+        if xn is None:
+            stall += 1
+            if stall >= 10:
+                log.warning("newton polish stalled at residual %.3e", gmax(g))
+                return x, False, it
+            xn, on = x, obj
+        x, obj = xn, on
+        g = residual(x)
+        if gmax(g) < tol:
+            return x, True, it
+    ok = gmax(g) < tol
+    if not ok:
+        log.warning("newton polish hit iteration cap at residual %.3e", gmax(g))
+    return x, ok, max_iters
+
+
 def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=None, colliders=(),
                   iterations=PD_ITERS_DEFAULT, solver_mode="direct", n_domains=2, modes_per_domain=20,
                   refine_sweeps=30, aggregation=2, chebyshev=False, damping=1.0, polish_tol=None,
@@ -399,8 +570,6 @@ def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=Non
 
     pin_targets may be constant (nP, 3) or a per-step path (steps, nP, 3).
     """
-    if polish_tol is not None:
-        raise NotImplementedError("newton_polish is outside the B200 hot path (SURVEY.md 8f)")
     if solver_mode not in ("direct", "cms"):
         raise ValueError(f"unknown solver mode {solver_mode!r}")
     _check_inputs(mesh, gammas, dt)
@@ -427,7 +596,7 @@ def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=Non
         from .cms import simulate_cms
         return simulate_cms(mesh, gammas, steps, dt, forces, state, pin_path, iterations,
                             n_domains, modes_per_domain, refine_sweeps, aggregation, chebyshev,
-                            damping, precision, labels)
+                            damping, precision, labels, polish_tol=polish_tol)
     ctx = device_context(mesh, gammas, dt, pins, precision, tol, max_iters)
     ctx.set_state(state.x, state.v)
     if len(pins):
@@ -444,5 +613,18 @@ def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=Non
             ctx.step(iterations, damping)
         except _abi.NonFiniteError as exc:
             raise RuntimeError(str(exc)) from None
+        if polish_tol is not None and not state.colliders:
+            # pdsolver.py:757-761: polish toward the prediction of the stepped state; the
+            # polished x replaces state.x, v stays the PD step's
+            f = None if forces is None else forces[i]
+            xs, vs = ctx.get_state(want_x=True, want_v=True)
+            st = SimState(x=xs, v=vs, dt=dt, pins=pins,
+                          pin_targets=pin_path[i] if pin_path is not None else state.pin_targets)
+            xh = _predicted(st, f, mesh)
+            xp, _, _ = newton_polish(mesh, gammas, xs, dt=dt, pins=pins, pin_vals=st.pin_targets,
+                                     xhat=xh, tol=polish_tol)
+            ctx.set_state(xp, vs)
+            frames[i] = xp
+            continue
         ctx.get_state(want_x=True, want_v=False, out_x=frames[i])
     return frames

@@ -183,3 +183,59 @@ def equilibrium_case():
     a = 0.3 * sc.dt ** 2 * sc.forces / sc.mesh.node_mass[:, None]
     x0 = sc.mesh.nodes + 0.001 * rng.normal(size=sc.mesh.nodes.shape)
     return sc, a, x0
+
+
+def second_order_case():
+    """C1 inputs of the second-order fixtures: a perturbed x for the gradient / exact
+    Hessian, and the dynamic step of newton_polish (gravity prediction from rest)."""
+    sc = c1_swatch()
+    rng = np.random.default_rng(12)
+    x = sc.mesh.nodes + 0.002 * rng.normal(size=sc.mesh.nodes.shape)
+    inv_m = 1.0 / sc.mesh.node_mass
+    xhat = sc.mesh.nodes + sc.dt ** 2 * inv_m[:, None] * sc.forces
+    return sc, x, xhat
+
+
+class TrackingProblem:
+    """Synthetic stand-in for the reference FitProblem's duck-typed surface
+    (`fitting.py:92-170`) used by the adjoint fixtures: loss = sum_i w_i |x_i - t_i|^2."""
+
+    def __init__(self, mesh, dt, target, weight):
+        self.mesh = mesh
+        self.dt = dt
+        self.target = np.asarray(target, dtype=float)
+        self.weight = np.asarray(weight, dtype=float)
+
+    def loss(self, x, sample):
+        d = np.asarray(x).reshape(-1, 3) - self.target
+        return float(np.sum(self.weight[:, None] * d * d))
+
+    def loss_grad_x(self, x, sample):
+        return 2.0 * self.weight[:, None] * (np.asarray(x).reshape(-1, 3) - self.target)
+
+    def loss_hessian_scalar(self, sample):
+        import scipy.sparse as sp
+        return sp.diags(2.0 * self.weight).tocsr()
+
+    def free_dofs(self, sample):
+        free = np.setdiff1d(np.arange(self.mesh.n_nodes), sample.pins)
+        return (3 * free[:, None] + np.arange(3)[None, :]).reshape(-1)
+
+
+class TrackingSample:
+    def __init__(self, pins, pin_vals, inertia, index=0):
+        self.pins = np.asarray(pins, dtype=int)
+        self.pin_vals = np.asarray(pin_vals, dtype=float)
+        self.inertia = np.asarray(inertia, dtype=float)
+        self.index = index
+
+
+def adjoint_case():
+    """C1 quasi-static sample for the adjoint fixtures: the equilibrium_case loads; the
+    tracking target is a seeded perturbation of the equilibrium (found by the caller)."""
+    sc, a, x0 = equilibrium_case()
+    rng = np.random.default_rng(13)
+    weight = rng.uniform(0.5, 2.0, sc.mesh.n_nodes)
+    shift = 0.001 * rng.normal(size=sc.mesh.nodes.shape)
+    sample = TrackingSample(sc.pins, sc.pin_targets, a)
+    return sc, a, x0, weight, shift, sample

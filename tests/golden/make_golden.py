@@ -18,6 +18,9 @@ the reference saw.  Per-fixture contents:
                    start, `build_cms(...).solve`, and `simulate_mesh(cms)` 1 frame.
   c2.npz           C2 scarf: `simulate_mesh(direct)` frames 1, 10, 100 (f64).
   c3.npz           C3 sweater: `simulate_mesh(direct)` frame 1, displacement as f32.
+  second_order.npz C1: elastic_energy / elastic_gradient / exact_elastic_hessian, newton_polish
+                   (dynamic GN + exact, quasi-static exact), simulate_mesh(polish_tol), and
+                   fitting.adjoint_gradient on a tracking loss (scenes.TrackingProblem).
   contact.npz      box dropped on a plane + sphere collider: `simulate_mesh(colliders=...)`, 20 frames.
 """
 
@@ -225,6 +228,40 @@ def make_io():
     print("io fixtures written")
 
 
+def make_second_order():
+    """Reference elastic_energy / elastic_gradient / exact_elastic_hessian at a perturbed C1 x;
+    newton_polish (dynamic GN and exact, quasi-static exact); simulate_mesh(polish_tol);
+    adjoint_gradient on a tracking loss at the quasi-static equilibrium."""
+    from volknit import fitting as ref_fit
+    sc, x, xhat = scenes.second_order_case()
+    rm = ref_mesh(sc)
+    gam = ref_mat.MaterialField(sc.gammas.gamma_s, sc.gammas.gamma_v)
+    out = dict(digest=scene_digest(sc), x=x, xhat=xhat)
+    out["energy"] = ref_pd.elastic_energy(rm, gam, x)
+    out["grad"] = ref_pd.elastic_gradient(rm, gam, x)
+    H = ref_pd.exact_elastic_hessian(rm, gam, x).tocsr()
+    H.sum_duplicates()
+    H.sort_indices()
+    out.update(H_data=H.data, H_indices=H.indices, H_indptr=H.indptr)
+    for exact in (False, True):
+        xp, ok, its = ref_pd.newton_polish(rm, gam, xhat, dt=sc.dt, pins=sc.pins, pin_vals=sc.pin_targets,
+                                           xhat=xhat, tol=1e-7, max_iters=100, exact=exact)
+        out[f"dyn_x_{int(exact)}"], out[f"dyn_ok_{int(exact)}"], out[f"dyn_it_{int(exact)}"] = xp, ok, its
+    sc2, a, x0, weight, shift, sample = scenes.adjoint_case()
+    xe = ref_pd.pd_equilibrium(rm, gam, a, x0, sc.pins, sc.pin_targets, sc.dt, iterations=8)
+    xq, okq, itq = ref_pd.newton_polish(rm, gam, xe, dt=sc.dt, pins=sc.pins, pin_vals=sc.pin_targets,
+                                        inertia_target=a, tol=1e-10, max_iters=150, exact=True)
+    out.update(qs_x0=xe, qs_x=xq, qs_ok=okq, qs_it=itq)
+    prob = scenes.TrackingProblem(rm, sc.dt, xq + shift, weight)
+    st = ref_fit.adjoint_gradient(prob, sample, gam, xq)
+    out.update(adj_grad=st.grad, adj_lam=st.lam, adj_residual=st.residual)
+    fr = ref_pd.simulate_mesh(rm, gam, 2, sc.dt, forces=sc.forces, pins=sc.pins, pin_targets=sc.pin_targets,
+                              iterations=sc.iterations, polish_tol=1e-6)
+    out["polish_frames"] = fr
+    np.savez_compressed(os.path.join(HERE, "second_order.npz"), **out)
+    print("second-order fixtures written", {k: v for k, v in out.items() if np.ndim(v) == 0})
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what in ("small", "all"):
@@ -235,6 +272,8 @@ if __name__ == "__main__":
         make_jacobians()
     if what in ("eq", "all"):
         make_equilibrium()
+    if what in ("so", "all"):
+        make_second_order()
     if what in ("io", "all"):
         make_io()
     if what in ("contact", "all"):

@@ -131,3 +131,60 @@ def test_pd_equilibrium_oracle_matches_reference():
         x = orc.pd_equilibrium(x0, m.tets, m.shape_grad, m.volume, sc.gammas.gamma_s, sc.gammas.gamma_v,
                                m.node_mass, a, sc.pins, sc.pin_targets, sc.dt, iterations=its)
         assert rel_l2(x, g[f"x{its}"]) < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# second order: oracle vs the reference's outputs (second_order.npz)
+
+
+def _so_scene():
+    g = golden("second_order.npz")
+    sc, x, xhat = scenes.second_order_case()
+    assert scene_digest(sc) == str(g["digest"])
+    assert np.array_equal(x, g["x"]) and np.array_equal(xhat, g["xhat"])
+    m = sc.mesh
+    return g, sc, m, (m.tets, m.shape_grad, m.volume, sc.gammas.gamma_s, sc.gammas.gamma_v)
+
+
+def test_projection_jacobians_oracle_matches_reference():
+    g = golden("jacobians.npz")
+    JR, JV = orc.projection_jacobians(g["F"])
+    assert np.abs(JR - g["JR"]).max() < 1e-9
+    assert np.abs(JV - g["JV"]).max() < 1e-8
+
+
+def test_second_order_oracle_matches_reference():
+    g, sc, m, op = _so_scene()
+    x = g["x"]
+    assert abs(orc.elastic_energy(x, *op) - float(g["energy"])) < 1e-13 * abs(float(g["energy"]))
+    gr = orc.elastic_gradient(x, *op, m.n_nodes)
+    assert rel_l2(gr, g["grad"]) < 1e-12
+    H = orc.exact_elastic_hessian(x, *op, m.n_nodes).tocsr()
+    Href = sp.csr_matrix((g["H_data"], g["H_indices"], g["H_indptr"]), shape=H.shape)
+    assert abs(H - Href).max() < 1e-10 * abs(Href).max()
+
+
+def test_newton_polish_oracle_matches_reference():
+    g, sc, m, op = _so_scene()
+    for exact in (0, 1):
+        x, ok, its = orc.newton_polish(g["xhat"], *op, m.node_mass, sc.dt, sc.pins, sc.pin_targets,
+                                       xhat=g["xhat"], tol=1e-7, max_iters=100, exact=bool(exact))
+        assert ok and bool(g[f"dyn_ok_{exact}"])
+        assert its == int(g[f"dyn_it_{exact}"])
+        assert rel_l2(x, g[f"dyn_x_{exact}"]) < 1e-12
+    _, a, _, _, _, _ = scenes.adjoint_case()
+    x, ok, its = orc.newton_polish(g["qs_x0"], *op, m.node_mass, sc.dt, sc.pins, sc.pin_targets,
+                                   inertia_target=a, tol=1e-10, max_iters=150, exact=True)
+    assert ok and its == int(g["qs_it"])
+    assert rel_l2(x, g["qs_x"]) < 1e-12
+
+
+def test_adjoint_gradient_oracle_matches_reference():
+    g, sc, m, op = _so_scene()
+    _, a, _, weight, shift, sample = scenes.adjoint_case()
+    x = g["qs_x"]
+    prob = scenes.TrackingProblem(m, sc.dt, x + shift, weight)
+    grad, lam = orc.adjoint_gradient(x, prob.loss_grad_x(x, sample), *op, m.n_nodes, sc.pins)
+    assert rel_l2(grad, g["adj_grad"]) < 1e-9
+    free = np.setdiff1d(np.arange(m.n_nodes), sc.pins)
+    assert rel_l2(lam[free].reshape(-1), g["adj_lam"]) < 1e-9
