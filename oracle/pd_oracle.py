@@ -897,3 +897,14 @@ def adjoint_gradient(x, gx, tets, G, vol, gs, gv, n_nodes, pins):
     lam[fdofs] = lam_f
     lam = lam.reshape(-1, 3)
     return -gamma_jacobian_t(x, lam, tets, G, vol), lam
+
+
+def gauss_newton_direction(H_ff, J_f, G_f, grad, kappa):
+    """(J^T H^-1 G H^-1 J + kappa I) d = -grad by dense normal equations: the reference's own
+    oracle route `dense_gauss_newton_direction` (`fitting.py:316-333`) for `adjoint_gauss_newton`
+    (`fitting.py:251-313`)."""
+    Hlu = spla.splu(sp.csc_matrix(H_ff))
+    Jd = np.asarray(sp.csr_matrix(J_f).todense())
+    S = np.column_stack([Hlu.solve(-Jd[:, j]) for j in range(Jd.shape[1])])
+    P = S.T @ (sp.csr_matrix(G_f) @ S)
+    return np.linalg.solve(P + kappa * np.eye(P.shape[0]), -grad)

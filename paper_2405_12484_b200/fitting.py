@@ -5,7 +5,7 @@ Mirrors `/root/reference/pkg/src/volknit/fitting.py`:
   gamma_jacobian(mesh, x)                           fitting.py:172-190
   AdjointState, EquilibriumGateError                fitting.py:193-243
   adjoint_gradient(problem, sample, gammas, x, ...) fitting.py:206-238
-  adjoint_gauss_newton(problem, sample, state, ...) fitting.py:251-313
+  reduce_columns, adjoint_gauss_newton(...)         fitting.py:245-313
 
 `problem` / `sample` are duck-typed exactly as the reference uses them: `problem.mesh`,
 `problem.dt`, `problem.loss_grad_x(x, sample)`, `problem.loss_hessian_scalar(sample)`,
@@ -127,3 +127,80 @@ def adjoint_gradient(problem, sample, gammas, x, residual=None, logger=None, wit
         H = h.csr()[fdofs][:, fdofs].tocsc()
         J = gamma_jacobian(mesh, x)[fdofs]
     return AdjointState(x=x, residual=residual, fdofs=fdofs, H=H, J=J, lam=lam.reshape(-1)[fdofs], grad=grad)
+
+
+def reduce_columns(J, basis):
+    """Map the coefficient Jacobian onto a rank-r basis per field (`fitting.py:245-248`)."""
+    nE = basis.shape[0]
+    return np.hstack([J[:, :nE] @ basis, J[:, nE:] @ basis])
+
+
+DENSE_GN_MAX = 24000        # largest nf or m of the device dense Gauss-Newton solve
+
+
+def adjoint_gauss_newton(problem, sample, state, kappa=None, basis=None, frozen=None):
+    """Gauss-Newton direction d with (J^T H^-1 G H^-1 J + kappa I) d = -grad (`fitting.py:251-313`).
+
+    The reference eliminates v, u from its sparse symmetric block system
+        [ 0   H   J ] [v]   [ 0    ]
+        [ H  -G   0 ] [u] = [ 0    ]
+        [ J^T 0  -kI] [d]   [ grad ]
+    by one sparse LU.  On the B200 the same direction comes from the equivalent reduced
+    system, dense on the device in float64: S = H^-1 J (LU of the exact equilibrium
+    Jacobian, cuSOLVER through torch), P = S^T G S (DGEMM), then a Cholesky solve of
+    P + kappa I.  Same `basis` / `frozen` reductions, the same default kappa and the same
+    (d, kappa, ok) contract: ok False when the factorization fails, the result is not
+    finite, or d is not a descent direction.  Sizes up to DENSE_GN_MAX rows/columns.
+    """
+    import scipy.sparse as sps
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("adjoint_gauss_newton needs a CUDA device (no CPU path)")
+    G_scalar = problem.loss_hessian_scalar(sample)
+    fdofs = state.fdofs
+    G = sps.kron(G_scalar, sps.eye(3)).tocsr()[fdofs][:, fdofs]
+    if kappa is None:
+        kappa = KAPPA_SCALE * G.diagonal().sum() / G.shape[0]
+    J = state.J
+    grad = state.grad
+    if basis is not None:
+        J = sps.csr_matrix(reduce_columns(J, basis))
+        nE = basis.shape[0]
+        grad = np.concatenate([basis.T @ grad[:nE], basis.T @ grad[nE:]])
+    keep = np.setdiff1d(np.arange(J.shape[1]), frozen) if frozen is not None and len(frozen) else None
+    Jk = J[:, keep] if keep is not None else J
+    gk = grad[keep] if keep is not None else grad
+    nf, m = Jk.shape
+    if nf > DENSE_GN_MAX or m > DENSE_GN_MAX:
+        raise NotImplementedError(f"dense device Gauss-Newton solve limited to {DENSE_GN_MAX} rows/columns")
+    dev = torch.device("cuda")
+    f64 = torch.float64
+    H = torch.as_tensor(state.H.toarray(), dtype=f64, device=dev)
+    Jd = torch.as_tensor(Jk.toarray(), dtype=f64, device=dev)
+    Gd = torch.as_tensor(G.toarray(), dtype=f64, device=dev)
+    g = torch.as_tensor(np.asarray(gk, dtype=float), dtype=f64, device=dev)
+    d = np.zeros(J.shape[1])
+    LU, piv, info = torch.linalg.lu_factor_ex(H)
+    if int(info.item()) != 0:
+        return None, kappa, False
+    S = torch.linalg.lu_solve(LU, piv, Jd)
+    if not bool(torch.isfinite(S).all()):
+        return None, kappa, False
+    P = S.T @ (Gd @ S)
+    P = 0.5 * (P + P.T)
+    P.diagonal().add_(kappa)
+    L, info = torch.linalg.cholesky_ex(P)
+    if int(info.item()) != 0:
+        return None, kappa, False
+    dk = torch.cholesky_solve(-g[:, None], L)[:, 0].cpu().numpy()
+    if not np.all(np.isfinite(dk)):
+        return None, kappa, False
+    if keep is not None:
+        d[keep] = dk
+    else:
+        d = dk
+    # d = 0 at a stationary point is the valid homogeneous solution, not a failed descent direction
+    if len(gk) and np.linalg.norm(gk) > 0.0 and float(d @ grad) >= 0.0:
+        return d, kappa, False
+    return d, kappa, True

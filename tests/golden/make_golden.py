@@ -255,6 +255,14 @@ def make_second_order():
     prob = scenes.TrackingProblem(rm, sc.dt, xq + shift, weight)
     st = ref_fit.adjoint_gradient(prob, sample, gam, xq)
     out.update(adj_grad=st.grad, adj_lam=st.lam, adj_residual=st.residual)
+    rng = np.random.default_rng(14)
+    basis, _ = np.linalg.qr(rng.normal(size=(sc.mesh.n_elements, 10)))
+    frozen = np.array([3, 17, 4000])
+    for tag, kw in (("full", {}), ("basis", dict(basis=basis)), ("frozen", dict(frozen=frozen))):
+        d, kap, ok = ref_fit.adjoint_gauss_newton(prob, sample, st, **kw)
+        out[f"gn_{tag}_d"], out[f"gn_{tag}_kappa"], out[f"gn_{tag}_ok"] = d, kap, ok
+    out["gn_basis"] = basis
+    out["gn_frozen"] = frozen
     fr = ref_pd.simulate_mesh(rm, gam, 2, sc.dt, forces=sc.forces, pins=sc.pins, pin_targets=sc.pin_targets,
                               iterations=sc.iterations, polish_tol=1e-6)
     out["polish_frames"] = fr

@@ -208,3 +208,19 @@ def test_hessian_context_errors(so):
         h2.apply(g["x"])
     with pytest.raises(ValueError, match="negative"):
         h2.set_gammas(-sc.gammas.gamma_s, sc.gammas.gamma_v)
+
+
+@pytest.mark.parametrize("tag", ["full", "basis", "frozen"])
+def test_adjoint_gauss_newton_matches_reference(so, tag):
+    g, sc = so
+    _, a, _, weight, shift, sample = scenes.adjoint_case()
+    x = g["qs_x"]
+    prob = scenes.TrackingProblem(sc.mesh, sc.dt, x + shift, weight)
+    st = fitting.adjoint_gradient(prob, sample, sc.gammas, x)
+    kw = {"full": {}, "basis": dict(basis=g["gn_basis"]), "frozen": dict(frozen=g["gn_frozen"])}[tag]
+    d, kap, ok = fitting.adjoint_gauss_newton(prob, sample, st, **kw)
+    assert ok == bool(g[f"gn_{tag}_ok"])
+    assert abs(kap - float(g[f"gn_{tag}_kappa"])) < 1e-15
+    assert rel_l2(d, g[f"gn_{tag}_d"]) < 1e-6
+    if tag == "frozen":
+        assert np.all(d[g["gn_frozen"]] == 0.0)

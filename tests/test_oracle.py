@@ -188,3 +188,25 @@ def test_adjoint_gradient_oracle_matches_reference():
     assert rel_l2(grad, g["adj_grad"]) < 1e-9
     free = np.setdiff1d(np.arange(m.n_nodes), sc.pins)
     assert rel_l2(lam[free].reshape(-1), g["adj_lam"]) < 1e-9
+
+
+def test_gauss_newton_oracle_matches_reference():
+    g, sc, m, op = _so_scene()
+    _, a, _, weight, shift, sample = scenes.adjoint_case()
+    x = g["qs_x"]
+    free = np.setdiff1d(np.arange(m.n_nodes), sc.pins)
+    fd = (3 * free[:, None] + np.arange(3)).reshape(-1)
+    H = orc.exact_elastic_hessian(x, *op, m.n_nodes).tocsr()[fd][:, fd]
+    F = orc.deformation_gradients(x, m.tets, m.shape_grad)
+    R, V = orc.projections(F)
+    v2 = 2.0 * m.volume[:, None, None]
+    Js = (v2 * np.einsum("enj,eij->eni", m.shape_grad, F - R)).reshape(-1)
+    Jv = (v2 * np.einsum("enj,eij->eni", m.shape_grad, F - V)).reshape(-1)
+    nE = m.n_elements
+    dofs = (3 * m.tets[:, :, None] + np.arange(3)).reshape(-1)
+    J = sp.csr_matrix((np.concatenate([Js, Jv]), (np.concatenate([dofs, dofs]),
+                       np.concatenate([np.repeat(np.arange(nE), 12), np.repeat(np.arange(nE, 2 * nE), 12)]))),
+                      shape=(3 * m.n_nodes, 2 * nE))[fd]
+    G = sp.kron(sp.diags(2.0 * weight), sp.eye(3)).tocsr()[fd][:, fd]
+    d = orc.gauss_newton_direction(H, J, G, g["adj_grad"], float(g["gn_full_kappa"]))
+    assert rel_l2(d, g["gn_full_d"]) < 1e-7
