@@ -150,7 +150,7 @@ def c3_sweater(seed=SEED):
 def c5_garment(seed=SEED):
     """C3 scaled by ~sqrt(10) in both radius and height to ~4.0M tets."""
     return sweater_scene(4_000_000, 0.65 * np.sqrt(4_000_000 / 390_000), seed=seed,
-                         name=None)
+                         name="C5-garment-4M")
 
 
 def contact_scene():
