@@ -91,6 +91,8 @@ struct LocalArgs {
     ProjStats* stats;
     int* robust_list;            // optional: suspicious elements are queued here (k_robust finishes them)
     int* robust_count;           // [0] queued elements, [1] chunk cursor of the robust pass
+    T* robust_aux;               // optional, 24 per queue slot: the queued element's (sigma, U, W) from
+                                 // the first pass, so the robust pass does not redo the SVD
     double* F_out;               // optional (nE,3,3) (RHS mode only)
     double* R_out;
     double* V_out;
@@ -144,7 +146,16 @@ __device__ __forceinline__ void local_tet(const LocalArgs<T>& a, int e) {
             int base = 0;
             if (lane == lead) base = atomicAdd(a.robust_count, __popc(m3));
             base = __shfl_sync(am, base, lead);
-            if (path == 3) a.robust_list[base + __popc(m3 & ((1u << lane) - 1u))] = e;
+            if (path == 3) {
+                const int slot = base + __popc(m3 & ((1u << lane) - 1u));
+                a.robust_list[slot] = e;
+                if (a.robust_aux != nullptr) {
+                    T* ax = a.robust_aux + (size_t)24 * slot;
+                    ax[0] = sig[0]; ax[1] = sig[1]; ax[2] = sig[2];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) { ax[3 + k] = U[k / 3][k % 3]; ax[12 + k] = W[k / 3][k % 3]; }
+                }
+            }
         }
         if (path == 3) return;
     }
@@ -277,65 +288,82 @@ __global__ void __launch_bounds__(128) k_robust4(LocalArgs<T> a) {
 #endif
 template <typename T, int MODE>
 __global__ void __launch_bounds__(128, VK_ROBUST_MINB) k_robust_ws(LocalArgs<T> a) {
-    __shared__ double s_sig[32][3];
-    __shared__ double s_res[4][32][4];
-    __shared__ int s_ok[4][32];
-    __shared__ int s_chunk;
+    // double-buffered per-chunk results: warps 1-3 run the next chunk's starts while warp 0
+    // selects and writes the current one, so each chunk costs one CTA barrier
+    __shared__ double s_sig[2][32][3];
+    __shared__ double s_res[2][4][32][4];
+    __shared__ int s_ok[2][4][32];
+    __shared__ int s_chunk[2];
     pcg_mark(9);
     const int cnt = *a.robust_count;
     if (cnt == 0) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const bool have_aux = a.robust_aux != nullptr;
+    if (threadIdx.x == 0) s_chunk[0] = atomicAdd(a.robust_count + 1, 1);
+    __syncthreads();
+    int buf = 0;
+    // warp 0 keeps the current chunk's element data for the finish (no-aux path: its SVD)
+    T g[3][3], F[3][3], ws, wv, U[3][3], W[3][3], sig[3];
     for (;;) {
-        // chunks of 32 queued elements handed out dynamically (robust_count[1] is the cursor):
-        // per-chunk cost varies with how many Newton starts stall
-        if (threadIdx.x == 0) s_chunk = atomicAdd(a.robust_count + 1, 1);
-        __syncthreads();
-        const int base = s_chunk * 32;
+        const int base = s_chunk[buf] * 32;
         if (base >= cnt) break;
         const int i = base + lane;
         const bool act = i < cnt;
         const int e = act ? a.robust_list[i] : 0;
-        T g[3][3], F[3][3], ws, wv, U[3][3], W[3][3], sig[3];
-        if (w == 0 && act) {
-            load_tet<T, false>(a, e, g, ws, wv, F);
-            svd3_rv(F, U, sig, W);
-            s_sig[lane][0] = (double)sig[0];
-            s_sig[lane][1] = (double)sig[1];
-            s_sig[lane][2] = (double)sig[2];
+        double sd[3] = {0.0, 0.0, 0.0};
+        if (have_aux) {
+            if (act) {
+                const T* ax = a.robust_aux + (size_t)24 * i;
+                sd[0] = (double)ax[0]; sd[1] = (double)ax[1]; sd[2] = (double)ax[2];
+            }
+        } else {
+            if (w == 0 && act) {
+                load_tet<T, false>(a, e, g, ws, wv, F);
+                svd3_rv(F, U, sig, W);
+                s_sig[buf][lane][0] = (double)sig[0];
+                s_sig[buf][lane][1] = (double)sig[1];
+                s_sig[buf][lane][2] = (double)sig[2];
+            }
+            __syncthreads();
+            if (act) { sd[0] = s_sig[buf][lane][0]; sd[1] = s_sig[buf][lane][1]; sd[2] = s_sig[buf][lane][2]; }
         }
-        __syncthreads();
         if (act) {
-            const double sd[3] = {s_sig[lane][0], s_sig[lane][1], s_sig[lane][2]};
             double st[3], sk[3] = {0, 0, 0}, obj = 0.0;
             const bool ok = sl3::robust_start(sd, w, st) && sl3::robust_try(sd, st, sk, obj);
-            s_ok[w][lane] = ok;
-            s_res[w][lane][0] = sk[0];
-            s_res[w][lane][1] = sk[1];
-            s_res[w][lane][2] = sk[2];
-            s_res[w][lane][3] = obj;
+            s_ok[buf][w][lane] = ok;
+            s_res[buf][w][lane][0] = sk[0];
+            s_res[buf][w][lane][1] = sk[1];
+            s_res[buf][w][lane][2] = sk[2];
+            s_res[buf][w][lane][3] = obj;
         }
+        if (threadIdx.x == 0) s_chunk[buf ^ 1] = atomicAdd(a.robust_count + 1, 1);
         __syncthreads();
         if (w == 0 && act) {
             bool have = false;
             double best = 0.0, s[3] = {0, 0, 0};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const double ob = s_res[k][lane][3];
-                if (s_ok[k][lane] && (!have || ob < best - 1e-15)) {
+                const double ob = s_res[buf][k][lane][3];
+                if (s_ok[buf][k][lane] && (!have || ob < best - 1e-15)) {
                     have = true;
                     best = ob;
-                    s[0] = s_res[k][lane][0]; s[1] = s_res[k][lane][1]; s[2] = s_res[k][lane][2];
+                    s[0] = s_res[buf][k][lane][0]; s[1] = s_res[buf][k][lane][1]; s[2] = s_res[buf][k][lane][2];
                 }
             }
-            const double sd[3] = {s_sig[lane][0], s_sig[lane][1], s_sig[lane][2]};
             if (!have) sl3::robust_fallback(sd, s);
             if (a.stats) {
                 atomicAdd(&a.stats->robust, 1u);
                 if (!have) atomicAdd(&a.stats->fallback, 1u);
             }
+            if (have_aux) {
+                load_tet<T, false>(a, e, g, ws, wv, F);
+                const T* ax = a.robust_aux + (size_t)24 * i;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) { U[k / 3][k % 3] = ax[3 + k]; W[k / 3][k % 3] = ax[12 + k]; }
+            }
             finish_tet<T, MODE, false>(a, e, g, ws, wv, F, U, W, s);
         }
-        __syncthreads();
+        buf ^= 1;
     }
 }
 

@@ -219,6 +219,8 @@ struct Ctx : CtxBase {
     DBuf<double> partials, scal, stage;
     DBuf<vk::GridBar> bar;
     DBuf<int> iters, fail_iter, robust_list, robust_count;
+    DBuf<T> robust_aux;                  // (sigma, U, W) of each queued element (24 per slot)
+    bool robust_handoff = true;          // env VKPD_ROBUST_AUX=0: the robust pass recomputes the SVD
     DBuf<vk::ProjStats> pstats;
     int* h_fail = nullptr;
     int last_iterations = 0;
@@ -604,6 +606,8 @@ struct Ctx : CtxBase {
         CK(cudaMemsetAsync(iters.p, 0, 1024 * sizeof(int), s));
         CK(fail_iter.alloc(1));
         CK(robust_list.alloc(std::max(1, nE)));
+        if (const char* ev = getenv("VKPD_ROBUST_AUX")) robust_handoff = atoi(ev) != 0;
+        if (robust_handoff) CK(robust_aux.alloc((size_t)24 * std::max(1, nE)));
         CK(robust_count.alloc(2));   // [0] queued elements, [1] k_robust_ws chunk cursor
         CK(pd_it.alloc(1));
         {
@@ -823,6 +827,7 @@ struct Ctx : CtxBase {
         la.slot4 = slot4.p;
         la.stats = pstats.p; la.F_out = la.R_out = la.V_out = nullptr;
         la.robust_list = robust_list.p; la.robust_count = robust_count.p;
+        la.robust_aux = robust_handoff ? robust_aux.p : nullptr;
         return la;
     }
     // local step in residual form, suspicious elements compacted into a dense second pass
