@@ -390,7 +390,7 @@ def run_ours(args):
                      "achieved": sol_achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (sol_achieved / peak) if sol_achieved else None,
                      "traffic": ncu_traffic(args.precision, "k_pcg_poly"),
-                     "traffic_source": "profiles/r01_launches_steady_summary.json (ncu dram read+write per launch, cold L2)",
+                     "traffic_source": "profiles/r01b_launches_steady_summary.json (ncu dram read+write per launch, cold L2)",
                      "alg_bytes_per_launch": sol_bytes / max(1, n_exec), "launch_ms": sol_ms / max(1, n_exec),
                      "cg_iters_per_launch": pst["cg_iters"][:n_exec],
                      "note": "working set (~80 MB) is L2-resident; in practice bound by grid-barrier latency, "
@@ -419,7 +419,7 @@ def ncu_traffic(precision, kernel):
     if precision != "fp32":
         return None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_launches_steady_summary.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r01b_launches_steady_summary.json")) as f:
             d = json.load(f)
         for k, v in d.get("kernels", d).items():
             if kernel in k:
