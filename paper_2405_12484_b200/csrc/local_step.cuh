@@ -367,6 +367,87 @@ __global__ void __launch_bounds__(128, VK_ROBUST_MINB) k_robust_ws(LocalArgs<T> 
     }
 }
 
+// Robust pass as independent (chunk, start) tasks (needs the first pass's SVD hand-off).
+// A warp takes one task = one Newton start (material.py:251-263) for 32 queued elements and
+// writes (s, obj, ok) per (start, slot); no CTA barrier couples the fast starts to the slow
+// one.  Tasks are handed out start-major with the usually-stalling sigma/cbrt start (2) first,
+// then 3, 0, 1 (longest first).  The warp that completes a chunk's fourth start (per-chunk
+// arrival counter, reset by that warp) picks the winner per element in the reference's start
+// order with its strict comparison (material.py:264-280) and writes the corners.
+// res: 4 doubles per (start, slot), ok: one int per (start, slot); cap = nE.
+template <typename T, int MODE>
+__device__ __forceinline__ void robust_select_one(const LocalArgs<T>& a, const double* __restrict__ res,
+                                                  const int* __restrict__ okf, int cap, int i) {
+    bool have = false;
+    double best = 0.0, s[3] = {0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const size_t r = (size_t)k * cap + i;
+        const double ob = __ldcg(&res[4 * r + 3]);
+        if (__ldcg(&okf[r]) && (!have || ob < best - 1e-15)) {
+            have = true;
+            best = ob;
+            s[0] = __ldcg(&res[4 * r]); s[1] = __ldcg(&res[4 * r + 1]); s[2] = __ldcg(&res[4 * r + 2]);
+        }
+    }
+    const T* ax = a.robust_aux + (size_t)24 * i;
+    if (!have) {
+        const double sd[3] = {(double)ax[0], (double)ax[1], (double)ax[2]};
+        sl3::robust_fallback(sd, s);
+    }
+    if (a.stats) {
+        atomicAdd(&a.stats->robust, 1u);
+        if (!have) atomicAdd(&a.stats->fallback, 1u);
+    }
+    const int e = a.robust_list[i];
+    T g[3][3], F[3][3], ws, wv, U[3][3], W[3][3];
+    load_tet<T, false>(a, e, g, ws, wv, F);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) { U[k / 3][k % 3] = ax[3 + k]; W[k / 3][k % 3] = ax[12 + k]; }
+    finish_tet<T, MODE, false>(a, e, g, ws, wv, F, U, W, s);
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128) k_robust_tasks(LocalArgs<T> a, double* __restrict__ res,
+                                                      int* __restrict__ okf, int* __restrict__ arrivals, int cap) {
+    const int cnt = *a.robust_count;
+    if (cnt == 0) return;
+    const int nch = (cnt + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int order[4] = {2, 3, 0, 1};
+    for (;;) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(a.robust_count + 1, 1);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (task >= 4 * nch) break;
+        const int k = order[task / nch];
+        const int chunk = task % nch;
+        const int i = chunk * 32 + lane;
+        if (i < cnt) {
+            const T* ax = a.robust_aux + (size_t)24 * i;
+            const double sd[3] = {(double)ax[0], (double)ax[1], (double)ax[2]};
+            double st[3], sk[3] = {0, 0, 0}, obj = 0.0;
+            const bool ok = sl3::robust_start(sd, k, st) && sl3::robust_try(sd, st, sk, obj);
+            const size_t r = (size_t)k * cap + i;
+            okf[r] = ok;
+            res[4 * r] = sk[0];
+            res[4 * r + 1] = sk[1];
+            res[4 * r + 2] = sk[2];
+            res[4 * r + 3] = obj;
+        }
+        __threadfence();
+        __syncwarp();
+        int prev = 0;
+        if (lane == 0) prev = atomicAdd(&arrivals[chunk], 1);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == 3) {                       // last start of this chunk: select and finish
+            __threadfence();
+            if (i < cnt) robust_select_one<T, MODE>(a, res, okf, cap, i);
+            if (lane == 0) arrivals[chunk] = 0;
+        }
+    }
+}
+
 // Stateless projections of a batch of F (material.py:395-407): (R, V).
 template <typename T>
 __global__ void __launch_bounds__(128) k_project(int n, const double* __restrict__ Fin, double* R, double* V,

@@ -221,6 +221,11 @@ struct Ctx : CtxBase {
     DBuf<int> iters, fail_iter, robust_list, robust_count;
     DBuf<T> robust_aux;                  // (sigma, U, W) of each queued element (24 per slot)
     bool robust_handoff = true;          // env VKPD_ROBUST_AUX=0: the robust pass recomputes the SVD
+    bool robust_tasks = true;            // (chunk, start) task pass (default; env VKPD_ROBUST=ws: the
+                                         // warp-per-start CTA pass, =quad: quad-per-element)
+    int robust_task_blocks = 4;
+    DBuf<double> robust_res;
+    DBuf<int> robust_ok, robust_arrivals;
     DBuf<vk::ProjStats> pstats;
     int* h_fail = nullptr;
     int last_iterations = 0;
@@ -573,8 +578,19 @@ struct Ctx : CtxBase {
         pcg_classic = !(pv && std::string(pv) == "pipe");   // classic measured faster at C3
         pcg_poly = !(pv && (std::string(pv) == "jacobi" || std::string(pv) == "pipe"));
         if (!pcg_classic) pcg_threads = std::min(pcg_threads, 512);   // the pipelined kernel's bound
+        if (const char* ev = getenv("VKPD_ROBUST_AUX")) robust_handoff = atoi(ev) != 0;
         const char* rb = getenv("VKPD_ROBUST");
         robust_quad = rb && std::string(rb) == "quad";
+        robust_tasks = !(rb && (std::string(rb) == "ws" || std::string(rb) == "quad")) && robust_handoff;
+        if (robust_tasks) {
+            CK(robust_res.alloc((size_t)16 * std::max(1, nE)));
+            CK(robust_ok.alloc((size_t)4 * std::max(1, nE)));
+            CK(robust_arrivals.alloc((size_t)std::max(1, cdiv(nE, 32))));
+            CK(cudaMemsetAsync(robust_arrivals.p, 0, sizeof(int) * std::max(1, cdiv(nE, 32)), stream));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&robust_task_blocks,
+                                                             vk::k_robust_tasks<T, vk::MODE_RESID>, 128, 0));
+            robust_task_blocks = std::max(1, robust_task_blocks);
+        }
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&robust_blocks, vk::k_robust_ws<T, vk::MODE_RESID>, 128, 0));
         robust_blocks = std::max(1, robust_blocks);   // chunks are handed out dynamically: one resident wave
         int occ = 0, occ2 = 0, occ3 = 0;
@@ -606,7 +622,6 @@ struct Ctx : CtxBase {
         CK(cudaMemsetAsync(iters.p, 0, 1024 * sizeof(int), s));
         CK(fail_iter.alloc(1));
         CK(robust_list.alloc(std::max(1, nE)));
-        if (const char* ev = getenv("VKPD_ROBUST_AUX")) robust_handoff = atoi(ev) != 0;
         if (robust_handoff) CK(robust_aux.alloc((size_t)24 * std::max(1, nE)));
         CK(robust_count.alloc(2));   // [0] queued elements, [1] k_robust_ws chunk cursor
         CK(pd_it.alloc(1));
@@ -839,7 +854,10 @@ struct Ctx : CtxBase {
         // 4 CTAs/SM: enough lanes for the heavy frames, cheap when the queue is empty
         if (robust_quad)
             vk::k_robust4<T, vk::MODE_RESID><<<4 * n_sms, 128, 0, stream>>>(la);
-        else
+        else if (robust_tasks) {
+            vk::k_robust_tasks<T, vk::MODE_RESID><<<robust_task_blocks * n_sms, 128, 0, stream>>>(
+                la, robust_res.p, robust_ok.p, robust_arrivals.p, std::max(1, nE));
+        } else
             vk::k_robust_ws<T, vk::MODE_RESID><<<robust_blocks * n_sms, 128, 0, stream>>>(la);
         CK(cudaGetLastError());
         return VKPD_OK;

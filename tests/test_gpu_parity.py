@@ -268,6 +268,20 @@ def test_pd_loop_early_exit_is_exact(monkeypatch, config, frames, precision):
         assert any(0 in it for it in ib)     # the exit was actually taken (fp64 at 1e-12 rarely exits)
 
 
+@pytest.mark.parametrize("variant", ["ws", "quad"])
+def test_robust_pass_variants_bit_identical(monkeypatch, variant):
+    """The default robust pass ((chunk, start) tasks, per-chunk last-arrival select) and the
+    CTA warp-per-start / quad-per-element passes run the same starts and the same selection
+    (material.py:242-287): identical bits through the C3 fold frames (≈88K queued tets per
+    round from frame ~100)."""
+    sc = scenes.c3_sweater()
+    a, ia = _run_frames(sc, 115, "fp32", collect_every=5)
+    monkeypatch.setenv("VKPD_ROBUST", variant)
+    b, ib = _run_frames(sc, 115, "fp32", collect_every=5)
+    assert np.array_equal(a, b)
+    assert ia == ib
+
+
 def test_pin_path_and_per_step_forces(c1):
     steps = 3
     path = np.stack([c1.pin_targets + np.array([0.0, 0.0, 1e-3 * k]) for k in range(steps)])
