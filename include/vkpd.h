@@ -166,6 +166,18 @@ int vkpd_a_jacobi_refine(vkpd_ctx* ctx, const double* Bf, const double* X0f, int
 int vkpd_power_rho(vkpd_ctx* ctx, double omega, int iters, const double* v0, double* rho);
 /* CmsSubspace (pdsolver.py:512-593): dense basis T (n_free x m, column-major) and K_red^-1 (m x m) */
 int vkpd_cms_set_basis(vkpd_ctx* ctx, int m, const double* T, const double* Kred_inv);
+/* The same subspace stored per domain (the zeros of the global T are neither stored nor streamed):
+ * domain d holds A_d = [Phi_d | Psi_d on its adjacent boundary columns], n_d x c_d column-major,
+ * concatenated in domain order in A; rows[row_ptr[d]..row_ptr[d+1]) are its interior free-node
+ * indices and colmap[col_ptr[d]..col_ptr[d+1]) the global basis column of each local column
+ * (modes first, then n_modes + j for boundary node boundary[j]); K_red^-1 is m x m with
+ * m = n_modes + nb.  Replaces a dense basis set with vkpd_cms_set_basis. */
+int vkpd_cms_set_blocks(vkpd_ctx* ctx, int n_dom, const int64_t* row_ptr, const int64_t* rows, const int64_t* col_ptr,
+                        const int64_t* colmap, const double* A, int n_modes, int64_t nb, const int64_t* boundary,
+                        const double* Kred_inv);
+/* device times (CUDA events) of the last vkpd_cms_solve's first column group: the subspace
+ * apply x0 = T K_red^-1 T^T b and the a_jacobi_refine sweeps */
+int vkpd_cms_timing(vkpd_ctx* ctx, double* apply_ms, double* sweeps_ms);
 /* GlobalSolver.solve in "cms" mode (pdsolver.py:225-246): x0 = T K_red^-1 T^T (B_f - K_fp P), then
  * sweeps of a_jacobi_refine per column; B (nV,k), P (n_pins,k), X (nV,k) */
 int vkpd_cms_solve(vkpd_ctx* ctx, const double* B, const double* P, int k, int sweeps, int aggregation, double omega,

@@ -28,7 +28,7 @@ EXPORTS = (
     "vkpd_set_gammas", "vkpd_set_yarn_interp", "vkpd_frame_outputs", "vkpd_v2y", "vkpd_equilibrium",
     "vkpd_projection_jacobians", "vkpd_hess_create", "vkpd_hess_destroy", "vkpd_hess_set_gammas",
     "vkpd_hess_energy_grad", "vkpd_hess_gamma_jt", "vkpd_hess_linearize", "vkpd_hess_csr",
-    "vkpd_hess_apply", "vkpd_hess_solve",
+    "vkpd_hess_apply", "vkpd_hess_solve", "vkpd_cms_set_blocks", "vkpd_cms_timing",
 )
 
 
@@ -105,6 +105,8 @@ def load():
         "vkpd_get_node_order": (I, [P, P]),
         "vkpd_get_sizes": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                C.POINTER(I)]),
+        "vkpd_cms_set_blocks": (I, [P, I, P, P, P, P, P, I, C.c_int64, P, P]),
+        "vkpd_cms_timing": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "vkpd_hess_create": (I, [C.POINTER(MeshDesc), I, C.POINTER(P)]),
         "vkpd_hess_destroy": (None, [P]),
         "vkpd_hess_set_gammas": (I, [P, P, P]),
@@ -360,6 +362,22 @@ class Context:
         self._keep["cmsT"], self._keep["cmsKi"] = T, Ki
         check(self.lib.vkpd_cms_set_basis(self.h, T.shape[1], T.ctypes.data_as(C.c_void_p),
                                           Ki.ctypes.data_as(C.c_void_p)))
+
+    def cms_set_blocks(self, blk):
+        """Per-domain basis blocks (see cms.basis_blocks)."""
+        i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)
+        k = dict(rp=i64(blk["row_ptr"]), rows=i64(blk["rows"]), cp=i64(blk["col_ptr"]), cm=i64(blk["colmap"]),
+                 A=f64(blk["A"]).reshape(-1), bnd=i64(blk["boundary"]), Ki=f64(blk["K_red_inv"]))
+        self._keep["cms_blocks"] = k
+        nd = len(k["rp"]) - 1
+        check(self.lib.vkpd_cms_set_blocks(self.h, int(nd), ptr(k["rp"]), ptr(k["rows"]), ptr(k["cp"]), ptr(k["cm"]),
+                                           ptr(k["A"]), int(blk["n_modes"]), C.c_int64(len(k["bnd"])),
+                                           ptr(k["bnd"]), ptr(k["Ki"])))
+
+    def cms_timing(self):
+        a, b = C.c_double(0.0), C.c_double(0.0)
+        check(self.lib.vkpd_cms_timing(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def cms_solve(self, B, pin_vals, sweeps, aggregation, omega, chebyshev, rho):
         B = f64(B)

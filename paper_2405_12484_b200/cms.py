@@ -135,7 +135,7 @@ class CmsSubspace:
     def _context(self):
         if self._ctx is None:
             self._ctx = _abi.MatrixContext(self._K, np.empty(0, dtype=np.int64), precision="fp64")
-            self._ctx.cms_set_basis(self.T_dense, self.K_red_inv)
+            self._ctx.cms_set_blocks(basis_blocks(self))
         return self._ctx
 
     def solve(self, b):
@@ -144,6 +144,47 @@ class CmsSubspace:
         X = self._context().cms_solve(b[:, None] if one else b, np.zeros((0, 1 if one else b.shape[1])),
                                       0, 2, JACOBI_OMEGA, False, 0.0)
         return X[:, 0] if one else X
+
+
+def basis_blocks(cms):
+    """Per-domain storage of the subspace T = [Phi blocks | I_b + Psi blocks] (`pdsolver.py:560-575`).
+
+    Domain d keeps A_d = [Phi_d | Psi_d on the boundary columns it touches] (column-major):
+    Psi_d = -K_ii^-1 K_ib is exactly zero on the boundary nodes no element of d touches,
+    so the dense T's zeros are dropped.  Works for this module's CmsSubspace and the
+    reference's (both expose `blocks` [(sel, Phi, Psi) | None], `boundary`, `K_red`).
+    """
+    boundary = np.asarray(cms.boundary, dtype=np.int64)
+    nb = len(boundary)
+    blocks = [b for b in cms.blocks if b is not None]
+    n_modes = sum(b[1].shape[1] for b in blocks)
+    row_ptr, col_ptr, rows, colmap, parts = [0], [0], [], [], []
+    c0 = 0
+    for sel, Phi, Psi in blocks:
+        sel = np.asarray(sel, dtype=np.int64)
+        m = Phi.shape[1]
+        cols = list(range(c0, c0 + m))
+        mats = [np.asarray(Phi, dtype=float)]
+        if Psi is not None and nb:
+            Psi = np.asarray(Psi.toarray() if hasattr(Psi, "toarray") else Psi, dtype=float)
+            adj = np.flatnonzero(np.any(Psi != 0.0, axis=0))
+            cols += list(n_modes + adj)
+            mats.append(Psi[:, adj])
+        c0 += m
+        A = np.hstack(mats) if len(mats) > 1 else mats[0]
+        parts.append(np.asfortranarray(A).reshape(-1, order="F"))
+        rows.append(sel)
+        colmap.append(np.asarray(cols, dtype=np.int64))
+        row_ptr.append(row_ptr[-1] + len(sel))
+        col_ptr.append(col_ptr[-1] + len(cols))
+    Ki = getattr(cms, "K_red_inv", None)
+    if Ki is None:
+        Kr = cms.K_red.toarray() if hasattr(cms.K_red, "toarray") else np.asarray(cms.K_red)
+        Ki = np.linalg.inv(Kr) if Kr.size else np.zeros((0, 0))
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dtype=dt)
+    return dict(row_ptr=np.asarray(row_ptr), col_ptr=np.asarray(col_ptr), rows=cat(rows, np.int64),
+                colmap=cat(colmap, np.int64), A=cat(parts, float), n_modes=n_modes, boundary=boundary,
+                K_red_inv=np.ascontiguousarray(Ki, dtype=float))
 
 
 def build_cms(K, mesh=None, n_domains=2, modes_per_domain=20, element_labels=None, free=None,
@@ -206,12 +247,8 @@ class CmsGlobalSolver:
         self.chebyshev = bool(chebyshev)
         if self.sweeps > 0 and self.aggregation not in (2, 3):
             raise ValueError("aggregation must be 2 or 3")
-        # also accepts the reference's own CmsSubspace (sparse T, K_red)
-        T = getattr(cms, "T_dense", None)
-        T = cms.T.toarray() if T is None else T
-        Ki = getattr(cms, "K_red_inv", None)
-        Ki = np.linalg.inv(cms.K_red.toarray()) if Ki is None else Ki
-        ctx.cms_set_basis(T, Ki)
+        # also accepts the reference's own CmsSubspace (same `blocks` / `boundary` / `K_red`)
+        ctx.cms_set_blocks(basis_blocks(cms))
         self.rho = _power_rho(ctx, len(free), omega) if (chebyshev and self.sweeps > 0) else 0.0
 
     def solve(self, B, pin_vals):

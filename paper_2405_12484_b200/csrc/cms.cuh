@@ -362,4 +362,117 @@ __global__ void k_tv(int n, int m, const double* __restrict__ Tb, const double* 
     x[i] = make4<T>((T)s0, (T)s1, (T)s2, T(0));
 }
 
+
+// ---------------------------------------------------------------------------
+// Blocked CMS apply (the same T = [Phi blocks | I_b + Psi blocks], stored per domain).
+// Domain d keeps A_d = [Phi_d | Psi_d restricted to its adjacent boundary columns],
+// n_d x c_d column-major (rows = its interior nodes), so the zeros of the global T
+// (pdsolver.py:560-575 stores them) are neither stored nor streamed:
+//   T^T b: per (domain, 8-column tile) CTA, partial y_d = A_d^T b_d; then per global
+//          column the (<= 2 for slabs) domain contributions plus b on the boundary rows,
+//          summed in domain order (deterministic);
+//   T z:   per (domain, row chunk) CTA with the domain's z entries staged in shared
+//          memory, one thread per interior row; boundary rows copy z.
+struct CmsBlocks {
+    int ndom, nmodes, nb, ntiles;
+    const double* A;             // concatenated blocks
+    const long long* a_off;      // per domain offset into A
+    const int* row_ptr;          // per domain range into rows
+    const int* rows;             // interior free-node rows (internal order)
+    const int* col_ptr;          // per domain range into colmap / y_d
+    const int* colmap;           // global column of each local column
+    const int* tile_dom;         // per tile: domain, first local column
+    const int* tile_c0;
+    const int* bnd;              // boundary free-node rows (global column nmodes + j)
+    const int* ysrc_ptr;         // per global column: contributions in y_d
+    const int* ysrc;
+};
+
+constexpr int kCmsTile = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_cms_tb(CmsBlocks c, const vec4_t<T>* __restrict__ b, double* __restrict__ yd) {
+    __shared__ double smem[32 * 3 * kCmsTile];
+    const int t = blockIdx.x;
+    const int d = c.tile_dom[t], c0 = c.tile_c0[t];
+    const int r0 = c.row_ptr[d], nd = c.row_ptr[d + 1] - r0;
+    const int ncol = c.col_ptr[d + 1] - c.col_ptr[d];
+    const int nc = min(kCmsTile, ncol - c0);
+    const double* A = c.A + c.a_off[d] + (size_t)c0 * nd;
+    double acc[3 * kCmsTile];
+#pragma unroll
+    for (int k = 0; k < 3 * kCmsTile; ++k) acc[k] = 0.0;
+    for (int r = threadIdx.x; r < nd; r += blockDim.x) {
+        const vec4_t<T> bv = b[c.rows[r0 + r]];
+        const double bx = (double)bv.x, by = (double)bv.y, bz = (double)bv.z;
+#pragma unroll
+        for (int k = 0; k < kCmsTile; ++k) {
+            if (k < nc) {
+                const double a = __ldg(&A[(size_t)k * nd + r]);
+                acc[3 * k] += a * bx;
+                acc[3 * k + 1] += a * by;
+                acc[3 * k + 2] += a * bz;
+            }
+        }
+    }
+    block_sum<3 * kCmsTile>(acc, smem);
+    if (threadIdx.x == 0) {
+        const int base = c.col_ptr[d] + c0;
+        for (int k = 0; k < nc; ++k) {
+            yd[3 * (size_t)(base + k)] = acc[3 * k];
+            yd[3 * (size_t)(base + k) + 1] = acc[3 * k + 1];
+            yd[3 * (size_t)(base + k) + 2] = acc[3 * k + 2];
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_cms_y(CmsBlocks c, int m, const vec4_t<T>* __restrict__ b, const double* __restrict__ yd,
+                        double* __restrict__ y) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= m) return;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (g >= c.nmodes) {
+        const vec4_t<T> bv = b[c.bnd[g - c.nmodes]];
+        s0 = (double)bv.x; s1 = (double)bv.y; s2 = (double)bv.z;
+    }
+    for (int k = c.ysrc_ptr[g]; k < c.ysrc_ptr[g + 1]; ++k) {
+        const int q = c.ysrc[k];
+        s0 += yd[3 * (size_t)q]; s1 += yd[3 * (size_t)q + 1]; s2 += yd[3 * (size_t)q + 2];
+    }
+    y[3 * (size_t)g] = s0; y[3 * (size_t)g + 1] = s1; y[3 * (size_t)g + 2] = s2;
+}
+
+// grid: (row chunks, domains); dynamic smem = 3 * max columns per domain doubles
+template <typename T>
+__global__ void __launch_bounds__(256) k_cms_tz(CmsBlocks c, const double* __restrict__ z, vec4_t<T>* __restrict__ x) {
+    extern __shared__ double zs[];
+    const int d = blockIdx.y;
+    const int r0 = c.row_ptr[d], nd = c.row_ptr[d + 1] - r0;
+    const int q0 = c.col_ptr[d], ncol = c.col_ptr[d + 1] - q0;
+    for (int k = threadIdx.x; k < ncol; k += blockDim.x) {
+        const int g = c.colmap[q0 + k];
+        zs[3 * k] = z[3 * (size_t)g]; zs[3 * k + 1] = z[3 * (size_t)g + 1]; zs[3 * k + 2] = z[3 * (size_t)g + 2];
+    }
+    __syncthreads();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nd) return;
+    const double* A = c.A + c.a_off[d] + r;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < ncol; ++k) {
+        const double a = __ldg(&A[(size_t)k * nd]);
+        s0 += a * zs[3 * k]; s1 += a * zs[3 * k + 1]; s2 += a * zs[3 * k + 2];
+    }
+    x[c.rows[r0 + r]] = make4<T>((T)s0, (T)s1, (T)s2, T(0));
+}
+
+template <typename T>
+__global__ void k_cms_xb(CmsBlocks c, const double* __restrict__ z, vec4_t<T>* __restrict__ x) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= c.nb) return;
+    const size_t g = (size_t)(c.nmodes + j);
+    x[c.bnd[j]] = make4<T>((T)z[3 * g], (T)z[3 * g + 1], (T)z[3 * g + 2], T(0));
+}
+
 }  // namespace vk

@@ -168,6 +168,10 @@ struct CtxBase {
                           double rho, double* Xf, double* hist, int* nhist, int* diverged) = 0;
     virtual int power_rho(double omega, int iters, const double* v0, double* rho) = 0;
     virtual int cms_set_basis(int m, const double* T, const double* Kinv) = 0;
+    virtual int cms_set_blocks(int ndom, const int64_t* row_ptr, const int64_t* rows, const int64_t* col_ptr,
+                               const int64_t* colmap, const double* A, int nmodes, int64_t nb, const int64_t* bnd,
+                               const double* Kinv) = 0;
+    virtual int cms_timing(double* apply_ms, double* sweeps_ms) = 0;
     virtual int dev_residual(const void* x, const void* xhat, void* r) = 0;
     virtual int dev_apply_K(const void* X, void* Y) = 0;
     virtual int dev_inv_diag(void* out) = 0;
@@ -253,6 +257,8 @@ struct Ctx : CtxBase {
         if (h_fail) cudaFreeHost(h_fail);
         if (own_stream) cudaStreamDestroy(own_stream);
         if (body_stream) cudaStreamDestroy(body_stream);
+        for (auto& ev : cms_ev)
+            if (ev) cudaEventDestroy(ev);
     }
 
     int init(const vkpd_mesh_desc* d, const vkpd_config* c) override {
@@ -1192,6 +1198,15 @@ struct Ctx : CtxBase {
     DBuf<V4> bestv;
     DBuf<int> nhist_d, div_d;
     int cms_m = 0;
+    // blocked basis (cms.cuh CmsBlocks)
+    bool cms_blocked = false;
+    DBuf<double> cmsA, cms_yd;
+    DBuf<long long> cms_aoff;
+    DBuf<int> cms_rowp, cms_rows, cms_colp, cms_colmap, cms_tdom, cms_tc0, cms_bnd, cms_ysp, cms_ys;
+    vk::CmsBlocks cmsb{};
+    int cms_max_rows = 0, cms_max_cols = 0;
+    cudaEvent_t cms_ev[3] = {nullptr, nullptr, nullptr};
+    float cms_apply_ms = 0.f, cms_sweeps_ms = 0.f;
 
     // rows [0, m) of a V4 buffer from an (m, k) float64 host array, columns c0..c0+2
     int upload_rows(const double* h, int m, int k, int c0, V4* dst) {
@@ -1299,6 +1314,7 @@ struct Ctx : CtxBase {
     int cms_set_basis(int m, const double* Tb, const double* Kinv) override {
         if (m < 0) return fail(VKPD_EINVAL, "bad subspace size");
         cms_m = m;
+        cms_blocked = false;
         CK(cmsT.alloc((size_t)std::max(1, nF) * std::max(1, m)));
         CK(cmsKinv.alloc((size_t)std::max(1, m) * std::max(1, m)));
         CK(cms_y.alloc((size_t)3 * std::max(1, m)));
@@ -1307,6 +1323,108 @@ struct Ctx : CtxBase {
             CK(cudaMemcpy(cmsT.p, Tb, sizeof(double) * nF * (size_t)m, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(cmsKinv.p, Kinv, sizeof(double) * (size_t)m * m, cudaMemcpyHostToDevice));
         }
+        return VKPD_OK;
+    }
+    int cms_set_blocks(int ndom, const int64_t* row_ptr, const int64_t* rows, const int64_t* col_ptr,
+                       const int64_t* colmap, const double* A, int nmodes, int64_t nb, const int64_t* bnd,
+                       const double* Kinv) override {
+        if (ndom < 0 || nmodes < 0 || nb < 0) return fail(VKPD_EINVAL, "bad block structure");
+        const int m = nmodes + (int)nb;
+        std::vector<int> rp(ndom + 1), cp(ndom + 1), rw, cm, tdom, tc0, bd(nb);
+        std::vector<long long> aoff(std::max(1, ndom));
+        long long atot = 0;
+        cms_max_rows = cms_max_cols = 0;
+        for (int d = 0; d <= ndom; ++d) { rp[d] = (int)row_ptr[d]; cp[d] = (int)col_ptr[d]; }
+        for (int d = 0; d < ndom; ++d) {
+            const int nd = rp[d + 1] - rp[d], nc = cp[d + 1] - cp[d];
+            if (nd < 0 || nc < 0) return fail(VKPD_EINVAL, "block pointers not monotone");
+            aoff[d] = atot;
+            atot += (long long)nd * nc;
+            cms_max_rows = std::max(cms_max_rows, nd);
+            cms_max_cols = std::max(cms_max_cols, nc);
+            for (int c0 = 0; c0 < nc; c0 += vk::kCmsTile) { tdom.push_back(d); tc0.push_back(c0); }
+        }
+        rw.resize(std::max(1, rp[ndom]));
+        for (int k = 0; k < rp[ndom]; ++k) {
+            if (rows[k] < 0 || rows[k] >= nF) return fail(VKPD_EINVAL, "block row out of range");
+            rw[k] = (int)rows[k];
+        }
+        cm.resize(std::max(1, cp[ndom]));
+        std::vector<std::vector<int>> src(m);
+        for (int k = 0; k < cp[ndom]; ++k) {
+            if (colmap[k] < 0 || colmap[k] >= m) return fail(VKPD_EINVAL, "block column out of range");
+            cm[k] = (int)colmap[k];
+            src[cm[k]].push_back(k);           // domain order (k increases with d)
+        }
+        for (int64_t j = 0; j < nb; ++j) {
+            if (bnd[j] < 0 || bnd[j] >= nF) return fail(VKPD_EINVAL, "boundary row out of range");
+            bd[j] = (int)bnd[j];
+        }
+        std::vector<int> ysp(m + 1, 0), ys;
+        for (int g = 0; g < m; ++g) { ys.insert(ys.end(), src[g].begin(), src[g].end()); ysp[g + 1] = (int)ys.size(); }
+        cudaStream_t st = stream;
+        CK(cmsA.alloc(std::max<long long>(1, atot)));
+        if (atot) CK(cmsA.upload(A, atot, st));
+        CK(cms_aoff.alloc(aoff.size())); CK(cms_aoff.upload(aoff.data(), aoff.size(), st));
+        CK(cms_rowp.alloc(rp.size())); CK(cms_rowp.upload(rp.data(), rp.size(), st));
+        CK(cms_colp.alloc(cp.size())); CK(cms_colp.upload(cp.data(), cp.size(), st));
+        CK(cms_rows.alloc(rw.size())); CK(cms_rows.upload(rw.data(), rw.size(), st));
+        CK(cms_colmap.alloc(cm.size())); CK(cms_colmap.upload(cm.data(), cm.size(), st));
+        tdom.push_back(0); tc0.push_back(0);      // keep the buffers non-empty
+        CK(cms_tdom.alloc(tdom.size())); CK(cms_tdom.upload(tdom.data(), tdom.size(), st));
+        CK(cms_tc0.alloc(tc0.size())); CK(cms_tc0.upload(tc0.data(), tc0.size(), st));
+        bd.push_back(0);
+        CK(cms_bnd.alloc(bd.size())); CK(cms_bnd.upload(bd.data(), bd.size(), st));
+        CK(cms_ysp.alloc(ysp.size())); CK(cms_ysp.upload(ysp.data(), ysp.size(), st));
+        ys.push_back(0);
+        CK(cms_ys.alloc(ys.size())); CK(cms_ys.upload(ys.data(), ys.size(), st));
+        CK(cms_yd.alloc((size_t)3 * std::max(1, cp[ndom])));
+        CK(cmsKinv.alloc((size_t)std::max(1, m) * std::max(1, m)));
+        if (m > 0) CK(cmsKinv.upload(Kinv, (size_t)m * m, st));
+        CK(cms_y.alloc((size_t)3 * std::max(1, m)));
+        CK(cms_z.alloc((size_t)3 * std::max(1, m)));
+        CK(cudaStreamSynchronize(st));
+        cmsb.ndom = ndom; cmsb.nmodes = nmodes; cmsb.nb = (int)nb; cmsb.ntiles = (int)tdom.size() - 1;
+        cmsb.A = cmsA.p; cmsb.a_off = cms_aoff.p; cmsb.row_ptr = cms_rowp.p; cmsb.rows = cms_rows.p;
+        cmsb.col_ptr = cms_colp.p; cmsb.colmap = cms_colmap.p; cmsb.tile_dom = cms_tdom.p; cmsb.tile_c0 = cms_tc0.p;
+        cmsb.bnd = cms_bnd.p; cmsb.ysrc_ptr = cms_ysp.p; cmsb.ysrc = cms_ys.p;
+        const size_t smem = sizeof(double) * 3 * std::max(1, cms_max_cols);
+        if (smem > 48 * 1024) {
+            if (smem > 200 * 1024) return fail(VKPD_EINVAL, "too many basis columns in one domain");
+            CK(cudaFuncSetAttribute(vk::k_cms_tz<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        }
+        cms_m = m;
+        cms_blocked = true;
+        return VKPD_OK;
+    }
+    int cms_timing(double* apply_ms, double* sweeps_ms) override {
+        if (apply_ms) *apply_ms = cms_apply_ms;
+        if (sweeps_ms) *sweeps_ms = cms_sweeps_ms;
+        return VKPD_OK;
+    }
+    // x0 = T K_red^-1 T^T rhs into dx (blocked or dense basis)
+    int cms_apply() {
+        if (cms_m <= 0) {
+            CK(cudaMemsetAsync(dx.p, 0, sizeof(V4) * nF, stream));
+            return VKPD_OK;
+        }
+        if (cms_blocked) {
+            if (cmsb.ntiles > 0) vk::k_cms_tb<T><<<cmsb.ntiles, 256, 0, stream>>>(cmsb, rhs.p, cms_yd.p);
+            vk::k_cms_y<T><<<cdiv(cms_m, 128), 128, 0, stream>>>(cmsb, cms_m, rhs.p, cms_yd.p, cms_y.p);
+            vk::k_symv3<<<cdiv(cms_m, 128), 128, 0, stream>>>(cms_m, cmsKinv.p, cms_y.p, cms_z.p);
+            CK(cudaMemsetAsync(dx.p, 0, sizeof(V4) * nF, stream));
+            if (cmsb.ndom > 0 && cms_max_rows > 0) {
+                const dim3 grid(cdiv(cms_max_rows, 256), cmsb.ndom);
+                vk::k_cms_tz<T><<<grid, 256, sizeof(double) * 3 * std::max(1, cms_max_cols), stream>>>(cmsb, cms_z.p,
+                                                                                                     dx.p);
+            }
+            if (cmsb.nb > 0) vk::k_cms_xb<T><<<cdiv(cmsb.nb, 256), 256, 0, stream>>>(cmsb, cms_z.p, dx.p);
+        } else {
+            vk::k_tmv<T><<<cdiv((size_t)cms_m * 32, 256), 256, 0, stream>>>(nF, cms_m, cmsT.p, rhs.p, cms_y.p);
+            vk::k_symv3<<<cdiv(cms_m, 128), 128, 0, stream>>>(cms_m, cmsKinv.p, cms_y.p, cms_z.p);
+            vk::k_tv<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, cms_m, cmsT.p, cms_z.p, dx.p);
+        }
+        CK(cudaGetLastError());
         return VKPD_OK;
     }
     // GlobalSolver.solve in "cms" mode (pdsolver.py:237-246): per column
@@ -1336,15 +1454,18 @@ struct Ctx : CtxBase {
                 k_rhs_minus_fp<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, tmp4a.p, fp_ptr.p, fp_col.p, fp_val.p,
                                                                     tmp4b.p, rhs.p);
                 CK(cudaGetLastError());
-                if (cms_m > 0) {
-                    vk::k_tmv<T><<<cdiv((size_t)cms_m * 32, 256), 256, 0, stream>>>(nF, cms_m, cmsT.p, rhs.p, cms_y.p);
-                    vk::k_symv3<<<cdiv(cms_m, 128), 128, 0, stream>>>(cms_m, cmsKinv.p, cms_y.p, cms_z.p);
-                    vk::k_tv<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, cms_m, cmsT.p, cms_z.p, dx.p);
-                    CK(cudaGetLastError());
-                } else {
-                    CK(cudaMemsetAsync(dx.p, 0, sizeof(V4) * nF, stream));
-                }
+                if (!cms_ev[0])
+                    for (auto& ev : cms_ev) CK(cudaEventCreate(&ev));
+                CK(cudaEventRecord(cms_ev[0], stream));
+                if ((rc = cms_apply())) return rc;
+                CK(cudaEventRecord(cms_ev[1], stream));
                 if (sweeps > 0 && (rc = run_aj(kc, sweeps, agg, omega, cheb, rho))) return rc;
+                CK(cudaEventRecord(cms_ev[2], stream));
+                if (c0 == 0) {
+                    CK(cudaEventSynchronize(cms_ev[2]));
+                    CK(cudaEventElapsedTime(&cms_apply_ms, cms_ev[0], cms_ev[1]));
+                    CK(cudaEventElapsedTime(&cms_sweeps_ms, cms_ev[1], cms_ev[2]));
+                }
                 CK(cudaMemcpyAsync(tmp4a.p, dx.p, sizeof(V4) * nF, cudaMemcpyDeviceToDevice, stream));
             }
             if (nP) CK(cudaMemcpyAsync(tmp4a.p + nF, tmp4b.p, sizeof(V4) * nP, cudaMemcpyDeviceToDevice, stream));
@@ -1639,6 +1760,14 @@ int vkpd_cms_set_basis(vkpd_ctx* ctx, int m, const double* T, const double* Kred
     if (m > 0 && (!T || !Kred_inv)) return fail(VKPD_EINVAL, "null buffer");
     CTX_CALL(cms_set_basis(m, T, Kred_inv));
 }
+int vkpd_cms_set_blocks(vkpd_ctx* ctx, int n_dom, const int64_t* row_ptr, const int64_t* rows, const int64_t* col_ptr,
+                        const int64_t* colmap, const double* A, int n_modes, int64_t nb, const int64_t* boundary,
+                        const double* Kred_inv) {
+    if (n_dom < 0 || (n_dom > 0 && (!row_ptr || !col_ptr)) || (nb > 0 && !boundary) || !Kred_inv)
+        return fail(VKPD_EINVAL, "null buffer");
+    CTX_CALL(cms_set_blocks(n_dom, row_ptr, rows, col_ptr, colmap, A, n_modes, nb, boundary, Kred_inv));
+}
+int vkpd_cms_timing(vkpd_ctx* ctx, double* apply_ms, double* sweeps_ms) { CTX_CALL(cms_timing(apply_ms, sweeps_ms)); }
 int vkpd_cms_solve(vkpd_ctx* ctx, const double* B, const double* P, int k, int sweeps, int aggregation, double omega,
                    int chebyshev, double rho, double* X) {
     if (!B || !X) return fail(VKPD_EINVAL, "null buffer");
