@@ -141,7 +141,12 @@ __device__ __forceinline__ void aj_start(const AJArgs<T>& a, AJState& st, cgr::g
     }
 }
 
-// Plain aggregated sweeps (pdsolver.py:683-703).
+// Plain aggregated sweeps (pdsolver.py:683-703).  Same arithmetic as the reference loop;
+// two grid barriers per aggregated sweep at aggregation 2 (instead of three):
+//  - the sweep's first correction cs = omega D^-1 r is formed in the previous sweep's
+//    residual pass, unmasked, and masked per column (x 1 or x 0, exact) where it is read;
+//  - the best-iterate copy of an improving sweep is deferred into the next sweep's first
+//    pass (x is not touched there) or the final pass.
 template <typename T>
 __global__ void __launch_bounds__(256) k_ajacobi(AJArgs<T> a) {
     cgr::grid_group grid = cgr::this_grid();
@@ -152,42 +157,75 @@ __global__ void __launch_bounds__(256) k_ajacobi(AJArgs<T> a) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     int parity = 0;
     AJState st;
-    aj_start(a, st, grid, parity, red, smem, tid, stride);
+    const T om = (T)a.omega;
+    // r = b - K x, best = x, cs0 = omega D^-1 r, |r|
+    {
+        double acc[3] = {0, 0, 0};
+        for (int i = tid; i < nF; i += stride) {
+            const vec4_t<T> kx = spmv_row(a, a.x, i);
+            const vec4_t<T> bi = a.b[i];
+            const vec4_t<T> ri = make4<T>(bi.x - kx.x, bi.y - kx.y, bi.z - kx.z, T(0));
+            a.r[i] = ri;
+            a.best[i] = a.x[i];
+            const T di = (T)(1.0 / a.diag[i]);
+            a.cs0[i] = make4<T>(om * (di * ri.x), om * (di * ri.y), om * (di * ri.z), T(0));
+            acc[0] += (double)ri.x * ri.x; acc[1] += (double)ri.y * ri.y; acc[2] += (double)ri.z * ri.z;
+        }
+        aj_allreduce<3>(grid, a.partials, parity, acc, red, smem);
+        for (int c = 0; c < 3; ++c) {
+            st.best[c] = sqrt(red[c]);
+            st.last[c] = st.best[c];
+            st.nh[c] = 1;
+            st.act[c] = c < a.ncols;
+            st.div[c] = false;
+            if (tid == 0) a.hist[c] = st.best[c];
+        }
+    }
+    bool pend[3] = {false, false, false};           // best = x still owed for these columns
     for (int sw = 0; sw < a.sweeps; ++sw) {
         if (!(st.act[0] || st.act[1] || st.act[2])) break;
-        const T w0 = st.act[0] ? (T)a.omega : T(0), w1 = st.act[1] ? (T)a.omega : T(0),
-                w2 = st.act[2] ? (T)a.omega : T(0);
-        // s = r; cs = omega D^-1 s; e = cs
-        for (int i = tid; i < nF; i += stride) {
-            const vec4_t<T> ri = a.r[i];
-            const T di = (T)(1.0 / a.diag[i]);
-            const vec4_t<T> c = make4<T>(w0 * (di * ri.x), w1 * (di * ri.y), w2 * (di * ri.z), T(0));
-            a.s[i] = ri;
-            a.e[i] = c;
-            a.cs0[i] = c;
-        }
-        grid.sync();
+        const T m0 = st.act[0] ? T(1) : T(0), m1 = st.act[1] ? T(1) : T(0), m2 = st.act[2] ? T(1) : T(0);
+        const T w0 = st.act[0] ? om : T(0), w1 = st.act[1] ? om : T(0), w2 = st.act[2] ? om : T(0);
+        const bool owe = pend[0] || pend[1] || pend[2];
         for (int ag = 0; ag < a.aggregation; ++ag) {
             const vec4_t<T>* cur = (ag & 1) ? a.cs1 : a.cs0;
             vec4_t<T>* nxt = (ag & 1) ? a.cs0 : a.cs1;
             const bool more = ag + 1 < a.aggregation;
             for (int i = tid; i < nF; i += stride) {
-                const vec4_t<T> kc = spmv_row(a, cur, i);
-                vec4_t<T> si = a.s[i];
-                si.x -= kc.x; si.y -= kc.y; si.z -= kc.z;
+                vec4_t<T> kc = spmv_row(a, cur, i);
+                vec4_t<T> si, ei;
+                if (ag == 0) {
+                    // s = r - K (mask cs0); e = mask cs0 (the reference's s = r, cs, e = cs)
+                    kc.x *= m0; kc.y *= m1; kc.z *= m2;
+                    const vec4_t<T> ri = a.r[i], c0 = a.cs0[i];
+                    si = make4<T>(ri.x - kc.x, ri.y - kc.y, ri.z - kc.z, T(0));
+                    ei = make4<T>(m0 * c0.x, m1 * c0.y, m2 * c0.z, T(0));
+                    if (owe) {
+                        const vec4_t<T> xi = a.x[i];
+                        vec4_t<T> bi = a.best[i];
+                        if (pend[0]) bi.x = xi.x;
+                        if (pend[1]) bi.y = xi.y;
+                        if (pend[2]) bi.z = xi.z;
+                        a.best[i] = bi;
+                    }
+                } else {
+                    si = a.s[i];
+                    si.x -= kc.x; si.y -= kc.y; si.z -= kc.z;
+                    ei = a.e[i];
+                }
                 a.s[i] = si;
                 if (more) {
                     const T di = (T)(1.0 / a.diag[i]);
                     const vec4_t<T> c = make4<T>(w0 * (di * si.x), w1 * (di * si.y), w2 * (di * si.z), T(0));
                     nxt[i] = c;
-                    vec4_t<T> ei = a.e[i];
                     ei.x += c.x; ei.y += c.y; ei.z += c.z;
-                    a.e[i] = ei;
                 }
+                a.e[i] = ei;
             }
             if (more) grid.sync();
         }
-        // x += e; r = s; |r|
+        pend[0] = pend[1] = pend[2] = false;
+        // x += e; r = s; |r|; next sweep's cs0 = omega D^-1 r
         double acc[3] = {0, 0, 0};
         for (int i = tid; i < nF; i += stride) {
             vec4_t<T> xi = a.x[i];
@@ -196,13 +234,16 @@ __global__ void __launch_bounds__(256) k_ajacobi(AJArgs<T> a) {
             a.x[i] = xi;
             const vec4_t<T> si = a.s[i];
             a.r[i] = si;
+            const T di = (T)(1.0 / a.diag[i]);
+            a.cs0[i] = make4<T>(om * (di * si.x), om * (di * si.y), om * (di * si.z), T(0));
             acc[0] += (double)si.x * si.x; acc[1] += (double)si.y * si.y; acc[2] += (double)si.z * si.z;
         }
         aj_allreduce<3>(grid, a.partials, parity, acc, red, smem);
         bool improve[3];
         aj_record(st, red, a.hist, improve, tid == 0);
-        aj_save_best(a, improve, tid, stride);
+        for (int c = 0; c < 3; ++c) pend[c] = improve[c];
     }
+    if (pend[0] || pend[1] || pend[2]) aj_save_best(a, pend, tid, stride);
     aj_finish(a, st, tid, stride);
 }
 
@@ -402,17 +443,26 @@ __global__ void __launch_bounds__(256) k_cms_tb(CmsBlocks c, const vec4_t<T>* __
     double acc[3 * kCmsTile];
 #pragma unroll
     for (int k = 0; k < 3 * kCmsTile; ++k) acc[k] = 0.0;
-    for (int r = threadIdx.x; r < nd; r += blockDim.x) {
+    // two rows per thread per step: 16 basis loads in flight (HBM latency)
+    const int bd = blockDim.x;
+    for (int r = threadIdx.x; r < nd; r += 2 * bd) {
+        const int r2 = r + bd;
+        const bool two = r2 < nd;
         const vec4_t<T> bv = b[c.rows[r0 + r]];
-        const double bx = (double)bv.x, by = (double)bv.y, bz = (double)bv.z;
+        const vec4_t<T> bw = two ? b[c.rows[r0 + r2]] : make4<T>(T(0), T(0), T(0), T(0));
+        double av[kCmsTile], aw[kCmsTile];
 #pragma unroll
         for (int k = 0; k < kCmsTile; ++k) {
-            if (k < nc) {
-                const double a = __ldg(&A[(size_t)k * nd + r]);
-                acc[3 * k] += a * bx;
-                acc[3 * k + 1] += a * by;
-                acc[3 * k + 2] += a * bz;
-            }
+            av[k] = k < nc ? __ldg(&A[(size_t)k * nd + r]) : 0.0;
+            aw[k] = (k < nc && two) ? __ldg(&A[(size_t)k * nd + r2]) : 0.0;
+        }
+        const double bx = (double)bv.x, by = (double)bv.y, bz = (double)bv.z;
+        const double cx = (double)bw.x, cy = (double)bw.y, cz = (double)bw.z;
+#pragma unroll
+        for (int k = 0; k < kCmsTile; ++k) {
+            acc[3 * k] += av[k] * bx + aw[k] * cx;
+            acc[3 * k + 1] += av[k] * by + aw[k] * cy;
+            acc[3 * k + 2] += av[k] * bz + aw[k] * cz;
         }
     }
     block_sum<3 * kCmsTile>(acc, smem);
@@ -458,13 +508,46 @@ __global__ void __launch_bounds__(256) k_cms_tz(CmsBlocks c, const double* __res
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nd) return;
     const double* A = c.A + c.a_off[d] + r;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < ncol; ++k) {
+    // two interleaved accumulator sets and 8 loads in flight per thread (HBM latency)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, u0 = 0.0, u1 = 0.0, u2 = 0.0;
+    int k = 0;
+    for (; k + 8 <= ncol; k += 8) {
+        double av[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) av[q] = __ldg(&A[(size_t)(k + q) * nd]);
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+            s0 += av[q] * zs[3 * (k + q)]; s1 += av[q] * zs[3 * (k + q) + 1]; s2 += av[q] * zs[3 * (k + q) + 2];
+            u0 += av[q + 1] * zs[3 * (k + q + 1)]; u1 += av[q + 1] * zs[3 * (k + q + 1) + 1];
+            u2 += av[q + 1] * zs[3 * (k + q + 1) + 2];
+        }
+    }
+    for (; k < ncol; ++k) {
         const double a = __ldg(&A[(size_t)k * nd]);
         s0 += a * zs[3 * k]; s1 += a * zs[3 * k + 1]; s2 += a * zs[3 * k + 2];
     }
-    x[c.rows[r0 + r]] = make4<T>((T)s0, (T)s1, (T)s2, T(0));
+    x[c.rows[r0 + r]] = make4<T>((T)(s0 + u0), (T)(s1 + u1), (T)(s2 + u2), T(0));
+}
+
+// z = K_red^-1 y for the symmetric K_red^-1: one warp per row (row i = column i, contiguous),
+// lanes stride the columns, warp-shuffle reduction
+__global__ void __launch_bounds__(256) k_symv3_warp(int m, const double* __restrict__ A, const double* __restrict__ y,
+                                                    double* __restrict__ z) {
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (i >= m) return;
+    const double* row = A + (size_t)i * m;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int j = lane; j < m; j += 32) {
+        const double a = __ldg(&row[j]);
+        s0 += a * y[3 * j]; s1 += a * y[3 * j + 1]; s2 += a * y[3 * j + 2];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) { z[3 * i] = s0; z[3 * i + 1] = s1; z[3 * i + 2] = s2; }
 }
 
 template <typename T>

@@ -1411,7 +1411,7 @@ struct Ctx : CtxBase {
         if (cms_blocked) {
             if (cmsb.ntiles > 0) vk::k_cms_tb<T><<<cmsb.ntiles, 256, 0, stream>>>(cmsb, rhs.p, cms_yd.p);
             vk::k_cms_y<T><<<cdiv(cms_m, 128), 128, 0, stream>>>(cmsb, cms_m, rhs.p, cms_yd.p, cms_y.p);
-            vk::k_symv3<<<cdiv(cms_m, 128), 128, 0, stream>>>(cms_m, cmsKinv.p, cms_y.p, cms_z.p);
+            vk::k_symv3_warp<<<cdiv((size_t)cms_m * 32, 256), 256, 0, stream>>>(cms_m, cmsKinv.p, cms_y.p, cms_z.p);
             CK(cudaMemsetAsync(dx.p, 0, sizeof(V4) * nF, stream));
             if (cmsb.ndom > 0 && cms_max_rows > 0) {
                 const dim3 grid(cdiv(cms_max_rows, 256), cmsb.ndom);
