@@ -248,6 +248,9 @@ struct PcgArgs {
     unsigned long long* rounds;  // optional: executed-PD-round counter
     vec4_t<T>* warm;             // POLY, optional: warm_rounds banks of nF; PD round k < warm_rounds starts
     int warm_rounds;             // from the previous frame's round-k correction and stores its own
+    vec4_t<T>* warm_prev;        // optional: the correction before it; the guess is then the linear
+                                 // extrapolation d_prev + beta (d_prev - d_prevprev)
+    double warm_beta;
 };
 
 template <typename T>
@@ -488,8 +491,9 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
     const int row1 = min(nF, row0 + chunk);
     int parity = 0;
     double rz[3], rzp[3] = {1.0, 1.0, 1.0}, rr, bb;
-    // warm start: PD round k of a frame begins from the previous frame's round-k
-    // correction (same solution to the tolerance, fewer CG iterations)
+    // warm start: PD round k of a frame begins from a guess of its correction, the linear
+    // extrapolation of the previous two frames' round-k corrections (same solution to the
+    // tolerance, fewer CG iterations)
     const int pdi_w = a.pd_iter_dev != nullptr ? *a.pd_iter_dev : a.pd_iter;
     const bool warm = POLY && a.warm != nullptr && a.init == INIT_PD && pdi_w < a.warm_rounds;
     vec4_t<T>* const wb = warm ? a.warm + (size_t)pdi_w * nF : nullptr;
@@ -669,7 +673,17 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
             vec4_t<T> xi = a.x[i];
             xi.x += d.x; xi.y += d.y; xi.z += d.z;
             a.x[i] = xi;
-            if (warm) wb[i] = d;
+            if (warm) {
+                if (a.warm_prev != nullptr) {
+                    vec4_t<T>* wp = a.warm_prev + (size_t)pdi_w * nF;
+                    const vec4_t<T> dp = ld4(&wp[i]);
+                    wp[i] = d;
+                    const T be = (T)a.warm_beta;
+                    wb[i] = make4<T>(d.x + be * (d.x - dp.x), d.y + be * (d.y - dp.y), d.z + be * (d.z - dp.z), T(0));
+                } else {
+                    wb[i] = d;
+                }
+            }
             bad |= !(isfinite(xi.x) && isfinite(xi.y) && isfinite(xi.z));
         } else {
             bad |= !(isfinite(d.x) && isfinite(d.y) && isfinite(d.z));

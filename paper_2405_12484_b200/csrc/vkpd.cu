@@ -206,6 +206,9 @@ struct Ctx : CtxBase {
     std::vector<double> vol2_h;          // 2 V per tet (host)
     DBuf<T> ell_kd;                      // K_ff D^-1 (polynomial preconditioner)
     DBuf<V4> warm0;                      // per-round corrections of the previous frame (solver warm start)
+    DBuf<V4> warm1;                      // the frame before: the guess is the linear extrapolation
+    bool warm_extrap = true;             // d + beta (d - d_before), beta = 1 (env VKPD_WARM_EXTRAP=<beta>,
+    double warm_beta = 1.0;              // 0: the previous correction alone)
     bool warm_start = true;              // env VKPD_WARM=0: off
     int warm_rounds = 3;                 // env VKPD_WARM=<rounds>
     // state
@@ -556,6 +559,7 @@ struct Ctx : CtxBase {
         if (int rc = assemble(wsum)) return rc;
         if (int rc = refresh_precond()) return rc;
         if (warm0.p) CK(cudaMemsetAsync(warm0.p, 0, warm0.n * sizeof(V4), stream));
+        if (warm1.p) CK(cudaMemsetAsync(warm1.p, 0, warm1.n * sizeof(V4), stream));
         if (graph_exec) { cudaGraphExecDestroy(graph_exec); graph_exec = nullptr; }
         CK(cudaStreamSynchronize(stream));
         return VKPD_OK;
@@ -638,6 +642,11 @@ struct Ctx : CtxBase {
         }
         CK(warm0.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
         CK(cudaMemsetAsync(warm0.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
+        if (const char* pe = getenv("VKPD_WARM_EXTRAP")) { warm_beta = atof(pe); warm_extrap = warm_beta != 0.0; }
+        if (warm_extrap) {
+            CK(warm1.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
+            CK(cudaMemsetAsync(warm1.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
+        }
         {
             const char* pe = getenv("VKPD_PD_EXIT");
             pd_early_exit = !(pe && std::string(pe) == "0");
@@ -792,6 +801,7 @@ struct Ctx : CtxBase {
         if (rc) return rc;
         // a new trajectory: no warm start from the previous one (results depend on the state only)
         if (warm0.p) CK(cudaMemsetAsync(warm0.p, 0, warm0.n * sizeof(V4), stream));
+        if (warm1.p) CK(cudaMemsetAsync(warm1.p, 0, warm1.n * sizeof(V4), stream));
         CK(cudaStreamSynchronize(stream));
         return VKPD_OK;
     }
@@ -883,6 +893,8 @@ struct Ctx : CtxBase {
         pa.rounds = init == vk::INIT_PD ? &pstats.p->pd_rounds : nullptr;
         pa.warm = (init == vk::INIT_PD && pcg_poly && warm_start) ? warm0.p : nullptr;
         pa.warm_rounds = warm_rounds;
+        pa.warm_prev = (pa.warm != nullptr && warm_extrap) ? warm1.p : nullptr;
+        pa.warm_beta = warm_beta;
         pa.h = ss.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
         if (init == vk::INIT_PD && ncoll > 0) {
             pa.inv_diag = inv_diag_c.p; pa.cdiag = cdiag.p; pa.cb = cb.p; pa.coll = coll_d.p; pa.ncoll = ncoll;
