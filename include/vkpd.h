@@ -138,6 +138,10 @@ int vkpd_sync(vkpd_ctx* ctx, int* failed_iter);
 int vkpd_profile_step(vkpd_ctx* ctx, int iterations, double damping, double* local_ms,
                       double* global_ms, double* frame_ms);
 
+/* measurement only: `reps` back-to-back launches of the local step on the current state; average
+ * ms of k_local alone and of the local phase of a round (k_local + the robust pass) */
+int vkpd_time_local(vkpd_ctx* ctx, int reps, double* local_ms, double* pass_ms);
+
 int vkpd_elastic_rhs(vkpd_ctx* ctx, const double* x, double* rhs, double* F, double* R, double* V);
 int vkpd_global_solve(vkpd_ctx* ctx, const double* B, const double* pin_vals, double* X, int k);
 int vkpd_apply_K(vkpd_ctx* ctx, const double* X, double* Y);

@@ -28,7 +28,7 @@ EXPORTS = (
     "vkpd_set_gammas", "vkpd_set_yarn_interp", "vkpd_frame_outputs", "vkpd_v2y", "vkpd_equilibrium",
     "vkpd_projection_jacobians", "vkpd_hess_create", "vkpd_hess_destroy", "vkpd_hess_set_gammas",
     "vkpd_hess_energy_grad", "vkpd_hess_gamma_jt", "vkpd_hess_linearize", "vkpd_hess_csr",
-    "vkpd_hess_apply", "vkpd_hess_solve", "vkpd_cms_set_blocks", "vkpd_cms_timing",
+    "vkpd_hess_apply", "vkpd_hess_solve", "vkpd_cms_set_blocks", "vkpd_cms_timing", "vkpd_time_local",
 )
 
 
@@ -107,6 +107,7 @@ def load():
                                C.POINTER(I)]),
         "vkpd_cms_set_blocks": (I, [P, I, P, P, P, P, P, I, C.c_int64, P, P]),
         "vkpd_cms_timing": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "vkpd_time_local": (I, [P, I, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "vkpd_hess_create": (I, [C.POINTER(MeshDesc), I, C.POINTER(P)]),
         "vkpd_hess_destroy": (None, [P]),
         "vkpd_hess_set_gammas": (I, [P, P, P]),
@@ -301,6 +302,12 @@ class Context:
     def sync(self):
         fi = C.c_int(-1)
         check(self.lib.vkpd_sync(self.h, C.byref(fi)))
+
+    def time_local(self, reps=20):
+        """(k_local ms, local phase ms) per launch, back to back on the current state."""
+        a, b = C.c_double(0.0), C.c_double(0.0)
+        check(self.lib.vkpd_time_local(self.h, int(reps), C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def profile_step(self, iterations, damping=1.0):
         a, b, c = C.c_double(), C.c_double(), C.c_double()

@@ -172,6 +172,7 @@ struct CtxBase {
                                const int64_t* colmap, const double* A, int nmodes, int64_t nb, const int64_t* bnd,
                                const double* Kinv) = 0;
     virtual int cms_timing(double* apply_ms, double* sweeps_ms) = 0;
+    virtual int time_local(int reps, double* local_ms, double* pass_ms) = 0;
     virtual int dev_residual(const void* x, const void* xhat, void* r) = 0;
     virtual int dev_apply_K(const void* X, void* Y) = 0;
     virtual int dev_inv_diag(void* out) = 0;
@@ -1109,6 +1110,42 @@ struct Ctx : CtxBase {
         return VKPD_OK;
     }
 
+    // back-to-back launches of the local step on the current state (measurement only), each
+    // bracketed by its own events (all enqueued ahead, so no host gap falls inside a pair):
+    // k_local alone, and k_local + the robust pass (the frame's local phase)
+    int time_local(int reps, double* local_ms, double* pass_ms) override {
+        if (nE == 0) return fail(VKPD_EINVAL, "matrix-only context has no mesh");
+        if (reps < 1 || reps > 1000) return fail(VKPD_EINVAL, "reps must be in [1, 1000]");
+        const vk::LocalArgs<T> la = local_args(x.p);
+        std::vector<cudaEvent_t> e(4 * reps);
+        for (auto& ev : e) CK(cudaEventCreate(&ev));
+        for (int r = 0; r < reps; ++r) {
+            CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
+            CK(cudaEventRecord(e[4 * r], stream));
+            vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+            CK(cudaEventRecord(e[4 * r + 1], stream));
+            CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
+            CK(cudaEventRecord(e[4 * r + 2], stream));
+            if (int rc = launch_local_resid(la, false)) return rc;
+            CK(cudaEventRecord(e[4 * r + 3], stream));
+        }
+        CK(cudaStreamSynchronize(stream));
+        CK(cudaGetLastError());
+        double a = 0.0, b = 0.0;
+        for (int r = 0; r < reps; ++r) {
+            float t1 = 0.f, t2 = 0.f;
+            CK(cudaEventElapsedTime(&t1, e[4 * r], e[4 * r + 1]));
+            CK(cudaEventElapsedTime(&t2, e[4 * r + 2], e[4 * r + 3]));
+            a += t1;
+            b += t2;
+        }
+        for (auto& ev : e) cudaEventDestroy(ev);
+        CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
+        CK(cudaStreamSynchronize(stream));
+        if (local_ms) *local_ms = a / reps;
+        if (pass_ms) *pass_ms = b / reps;
+        return VKPD_OK;
+    }
     int profile(int iterations, double damping, double* lms, double* gms, double* fms) override {
         std::vector<cudaEvent_t> ev(3 * iterations + 2);
         for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -1780,6 +1817,9 @@ int vkpd_cms_set_blocks(vkpd_ctx* ctx, int n_dom, const int64_t* row_ptr, const 
     CTX_CALL(cms_set_blocks(n_dom, row_ptr, rows, col_ptr, colmap, A, n_modes, nb, boundary, Kred_inv));
 }
 int vkpd_cms_timing(vkpd_ctx* ctx, double* apply_ms, double* sweeps_ms) { CTX_CALL(cms_timing(apply_ms, sweeps_ms)); }
+int vkpd_time_local(vkpd_ctx* ctx, int reps, double* local_ms, double* pass_ms) {
+    CTX_CALL(time_local(reps, local_ms, pass_ms));
+}
 int vkpd_cms_solve(vkpd_ctx* ctx, const double* B, const double* P, int k, int sweeps, int aggregation, double omega,
                    int chebyshev, double rho, double* X) {
     if (!B || !X) return fail(VKPD_EINVAL, "null buffer");
