@@ -407,8 +407,11 @@ __device__ __forceinline__ void robust_select_one(const LocalArgs<T>& a, const d
     finish_tet<T, MODE, false>(a, e, g, ws, wv, F, U, W, s);
 }
 
+#ifndef VK_RTASK_MINB
+#define VK_RTASK_MINB 1
+#endif
 template <typename T, int MODE>
-__global__ void __launch_bounds__(128) k_robust_tasks(LocalArgs<T> a, double* __restrict__ res,
+__global__ void __launch_bounds__(128, VK_RTASK_MINB) k_robust_tasks(LocalArgs<T> a, double* __restrict__ res,
                                                       int* __restrict__ okf, int* __restrict__ arrivals, int cap) {
     const int cnt = *a.robust_count;
     if (cnt == 0) return;
