@@ -240,6 +240,7 @@ struct PcgArgs {
     int* reset_count;            // optional: the local step's suspicious-tet queue, zeroed on entry
     vec4_t<T>* h;                // POLY: h = K D^-1 r, updated with r
     double omega;                // POLY: polynomial preconditioner weight
+    int poly_rounds;             // POLY kernel: PD rounds >= poly_rounds use plain Jacobi (<= 0: none)
     const T* ell_kd;             // POLY: ELL values of K_ff D^-1 (no contact diagonal), or null
     int* pd_iter_dev;            // optional: PD iteration index read on the device (graph loop body);
                                  // then fail_iter gets *pd_iter_dev and the count goes to iters_out[*pd_iter_dev]
@@ -496,20 +497,25 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
     // tolerance, fewer CG iterations)
     const int pdi_w = a.pd_iter_dev != nullptr ? *a.pd_iter_dev : a.pd_iter;
     const bool warm = POLY && a.warm != nullptr && a.init == INIT_PD && pdi_w < a.warm_rounds;
+    const bool poly = POLY && (a.poly_rounds <= 0 || a.init != INIT_PD || pdi_w < a.poly_rounds);
     vec4_t<T>* const wb = warm ? a.warm + (size_t)pdi_w * nF : nullptr;
 
     // ---- init: residual, z = D^-1 r, p0 = 0, dx = 0
-    if (!POLY) {
+    if (!poly) {
         double acc[5] = {0, 0, 0, 0, 0};     // rz x3, rr, bb
         for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
             T rx, ry, rzv;
             init_residual_row(a, i, coherent_corners, rx, ry, rzv, acc[4]);
+            if (warm) {
+                const vec4_t<T> kw = k_row(a, wb, i);
+                rx -= kw.x; ry -= kw.y; rzv -= kw.z;
+            }
             const T d = a.inv_diag[i];
             const vec4_t<T> zi = make4<T>(d * rx, d * ry, d * rzv, T(0));
             a.r[i] = make4<T>(rx, ry, rzv, T(0));
             a.z[i] = zi;
             a.p0[i] = make4<T>(T(0), T(0), T(0), T(0));
-            a.dx[i] = make4<T>(T(0), T(0), T(0), T(0));
+            a.dx[i] = warm ? ld4(&wb[i]) : make4<T>(T(0), T(0), T(0), T(0));
             acc[0] += (double)rx * zi.x;
             acc[1] += (double)ry * zi.y;
             acc[2] += (double)rzv * zi.z;
@@ -638,7 +644,7 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
                 ri.x -= ax * qi.x; ri.y -= ay * qi.y; ri.z -= az * qi.z;
                 const T dg = a.inv_diag[i];
                 vec4_t<T> zi;
-                if (POLY) {
+                if (poly) {
                     // h -= alpha K D^-1 q (q of the neighbour rows is complete after the alpha barrier)
                     const vec4_t<T> kq = kdinv_row(a, a.q, i);
                     vec4_t<T> hi = ld4(&a.h[i]);

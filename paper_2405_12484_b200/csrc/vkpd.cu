@@ -208,6 +208,7 @@ struct Ctx : CtxBase {
     DBuf<T> ell_kd;                      // K_ff D^-1 (polynomial preconditioner)
     DBuf<V4> warm0;                      // per-round corrections of the previous frame (solver warm start)
     DBuf<V4> warm1;                      // the frame before: the guess is the linear extrapolation
+    int poly_rounds = 0;                 // env VKPD_POLY_ROUNDS=k: PD rounds >= k use Jacobi-PCG (0: all polynomial)
     bool warm_extrap = true;             // d + beta (d - d_before), beta = 1 (env VKPD_WARM_EXTRAP=<beta>,
     double warm_beta = 1.0;              // 0: the previous correction alone)
     bool warm_start = true;              // env VKPD_WARM=0: off
@@ -643,6 +644,7 @@ struct Ctx : CtxBase {
         }
         CK(warm0.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
         CK(cudaMemsetAsync(warm0.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
+        if (const char* pr = getenv("VKPD_POLY_ROUNDS")) poly_rounds = std::max(0, atoi(pr));
         if (const char* pe = getenv("VKPD_WARM_EXTRAP")) { warm_beta = atof(pe); warm_extrap = warm_beta != 0.0; }
         if (warm_extrap) {
             CK(warm1.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
@@ -896,6 +898,7 @@ struct Ctx : CtxBase {
         pa.warm_rounds = warm_rounds;
         pa.warm_prev = (pa.warm != nullptr && warm_extrap) ? warm1.p : nullptr;
         pa.warm_beta = warm_beta;
+        pa.poly_rounds = poly_rounds;
         pa.h = ss.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
         if (init == vk::INIT_PD && ncoll > 0) {
             pa.inv_diag = inv_diag_c.p; pa.cdiag = cdiag.p; pa.cb = cb.p; pa.coll = coll_d.p; pa.ncoll = ncoll;
