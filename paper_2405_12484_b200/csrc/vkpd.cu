@@ -212,7 +212,8 @@ struct Ctx : CtxBase {
     bool warm_extrap = true;             // d + beta (d - d_before), beta = 1 (env VKPD_WARM_EXTRAP=<beta>,
     double warm_beta = 1.0;              // 0: the previous correction alone)
     bool warm_start = true;              // env VKPD_WARM=0: off
-    int warm_rounds = 3;                 // env VKPD_WARM=<rounds>
+    int warm_rounds = sizeof(T) == 8 ? 32 : 3;   // env VKPD_WARM=<rounds>; fp64 runs every round (no early exit), where
+                                         // all rounds gain (C3: 19.3 -> 15.9 ms/frame); fp32 only the first 3
     // state
     DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
     DBuf<V4> m1, qq, ss, pp;             // pipelined-CG recurrences
@@ -639,7 +640,7 @@ struct Ctx : CtxBase {
         CK(pd_it.alloc(1));
         {
             const char* pw = getenv("VKPD_WARM");
-            if (pw) warm_rounds = std::max(0, std::min(8, atoi(pw)));
+            if (pw) warm_rounds = std::max(0, std::min(32, atoi(pw)));
             warm_start = warm_rounds > 0;
         }
         CK(warm0.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
