@@ -179,6 +179,12 @@ int vkpd_cms_set_basis(vkpd_ctx* ctx, int m, const double* T, const double* Kred
 int vkpd_cms_set_blocks(vkpd_ctx* ctx, int n_dom, const int64_t* row_ptr, const int64_t* rows, const int64_t* col_ptr,
                         const int64_t* colmap, const double* A, int n_modes, int64_t nb, const int64_t* boundary,
                         const double* Kred_inv);
+/* pd_step with GlobalSolver(mode="cms") (pdsolver.py:257-304, 237-246) as one device frame on a mesh
+ * context whose subspace was set with vkpd_cms_set_blocks / vkpd_cms_set_basis: per PD round the local
+ * step, b = rhs + (M/dt^2) xhat, x_f = a_jacobi_refine(K_ff, b_f - K_fp p, T K_red^-1 T^T (b_f - K_fp p)).
+ * Same error contract as vkpd_step. */
+int vkpd_step_cms(vkpd_ctx* ctx, int iterations, double damping, int sweeps, int aggregation, double omega,
+                  int chebyshev, double rho, int* failed_iter);
 /* device times (CUDA events) of the last vkpd_cms_solve's first column group: the subspace
  * apply x0 = T K_red^-1 T^T b and the a_jacobi_refine sweeps */
 int vkpd_cms_timing(vkpd_ctx* ctx, double* apply_ms, double* sweeps_ms);

@@ -29,6 +29,7 @@ EXPORTS = (
     "vkpd_projection_jacobians", "vkpd_hess_create", "vkpd_hess_destroy", "vkpd_hess_set_gammas",
     "vkpd_hess_energy_grad", "vkpd_hess_gamma_jt", "vkpd_hess_linearize", "vkpd_hess_csr",
     "vkpd_hess_apply", "vkpd_hess_solve", "vkpd_cms_set_blocks", "vkpd_cms_timing", "vkpd_time_local",
+    "vkpd_step_cms",
 )
 
 
@@ -108,6 +109,7 @@ def load():
         "vkpd_cms_set_blocks": (I, [P, I, P, P, P, P, P, I, C.c_int64, P, P]),
         "vkpd_cms_timing": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "vkpd_time_local": (I, [P, I, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "vkpd_step_cms": (I, [P, I, C.c_double, I, I, C.c_double, I, C.c_double, C.POINTER(I)]),
         "vkpd_hess_create": (I, [C.POINTER(MeshDesc), I, C.POINTER(P)]),
         "vkpd_hess_destroy": (None, [P]),
         "vkpd_hess_set_gammas": (I, [P, P, P]),
@@ -302,6 +304,12 @@ class Context:
     def sync(self):
         fi = C.c_int(-1)
         check(self.lib.vkpd_sync(self.h, C.byref(fi)))
+
+    def step_cms(self, iterations, damping, sweeps, aggregation, omega, chebyshev, rho):
+        """One pd_step with the cms global solver, entirely on the device."""
+        fi = C.c_int(-1)
+        check(self.lib.vkpd_step_cms(self.h, int(iterations), float(damping), int(sweeps), int(aggregation),
+                                     float(omega), 1 if chebyshev else 0, float(rho), C.byref(fi)))
 
     def time_local(self, reps=20):
         """(k_local ms, local phase ms) per launch, back to back on the current state."""

@@ -258,7 +258,12 @@ class CmsGlobalSolver:
 
 def simulate_cms(mesh, gammas, steps, dt, forces, state, pin_path, iterations, n_domains, modes_per_domain,
                  refine_sweeps, aggregation, chebyshev, damping, precision, labels=None, polish_tol=None):
-    """`simulate_mesh(..., solver_mode="cms")` (`pdsolver.py:734-740`, 749-762)."""
+    """`simulate_mesh(..., solver_mode="cms")` (`pdsolver.py:734-740`, 749-762).
+
+    The subspace is built once (`build_cms`, GPU eigensolves), stored per domain on the mesh's
+    float64 device context, and every frame runs as one device call (`vkpd_step_cms`): local
+    step, b = rhs + (M/dt^2) xhat, subspace apply and A-Jacobi sweeps per PD round.
+    """
     from . import pdsolver
     pins = state.pins
     free = np.setdiff1d(np.arange(mesh.n_nodes), pins)
@@ -266,18 +271,38 @@ def simulate_cms(mesh, gammas, steps, dt, forces, state, pin_path, iterations, n
     Kff = K[free][:, free].tocsc()
     cms = build_cms(Kff, mesh, n_domains=n_domains, modes_per_domain=modes_per_domain, free=free,
                     element_labels=labels)
-    solver = pdsolver.GlobalSolver(K, free, pins, mode="cms", cms=cms, refine_sweeps=refine_sweeps,
-                                   aggregation=aggregation, chebyshev=chebyshev)
+    sweeps = int(refine_sweeps)
+    if sweeps > 0 and aggregation not in (2, 3):
+        raise ValueError("aggregation must be 2 or 3")
+    ctx = pdsolver.device_context(mesh, gammas, dt, pins, "fp64")
+    ctx.cms_set_blocks(basis_blocks(cms))
+    rho = _power_rho(ctx, len(free), JACOBI_OMEGA) if (chebyshev and sweeps > 0) else 0.0
+    ctx.set_state(state.x, state.v)
+    if len(pins):
+        ctx.set_pin_targets(state.pin_targets)
+    const_forces = forces is not None and forces.strides[0] == 0
+    ctx.set_forces(None if forces is None else forces[0])
+    ctx.set_colliders(())
     frames = np.empty((steps, mesh.n_nodes, 3))
     for i in range(steps):
         if pin_path is not None:
             state.pin_targets = pin_path[i]
-        f = None if forces is None else forces[i]
-        pdsolver.pd_step(state, mesh, gammas, iterations=iterations, forces=f, solver=solver,
-                         damping=damping, precision="fp64")
+            ctx.set_pin_targets(pin_path[i])
+        if forces is not None and not const_forces and i > 0:
+            ctx.set_forces(forces[i])
+        try:
+            ctx.step_cms(iterations, damping, sweeps, aggregation, JACOBI_OMEGA, chebyshev, rho)
+        except _abi.NonFiniteError as exc:
+            raise RuntimeError(str(exc)) from None
         if polish_tol is not None:          # pdsolver.py:757-761
-            xh = pdsolver._predicted(state, f, mesh)
-            state.x, _, _ = pdsolver.newton_polish(mesh, gammas, state.x, dt=dt, pins=pins,
-                                                   pin_vals=state.pin_targets, xhat=xh, tol=polish_tol)
-        frames[i] = state.x
+            f = None if forces is None else forces[i]
+            xs, vs = ctx.get_state()
+            st = pdsolver.SimState(x=xs, v=vs, dt=dt, pins=pins, pin_targets=state.pin_targets)
+            xh = pdsolver._predicted(st, f, mesh)
+            xp, _, _ = pdsolver.newton_polish(mesh, gammas, xs, dt=dt, pins=pins, pin_vals=state.pin_targets,
+                                              xhat=xh, tol=polish_tol)
+            ctx.set_state(xp, vs)
+            frames[i] = xp
+            continue
+        ctx.get_state(want_x=True, want_v=False, out_x=frames[i])
     return frames

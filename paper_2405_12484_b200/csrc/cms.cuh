@@ -558,4 +558,32 @@ __global__ void k_cms_xb(CmsBlocks c, const double* __restrict__ z, vec4_t<T>* _
     x[c.bnd[j]] = make4<T>((T)z[3 * g], (T)z[3 * g + 1], (T)z[3 * g + 2], T(0));
 }
 
+// ---------------------------------------------------------------------------
+// Device frame in cms mode (pd_step with GlobalSolver(mode="cms"), pdsolver.py:283-300):
+//   b_f = (sum of the node's rhs corners, tet order) + (m/dt^2) xhat   (pdsolver.py:292-293)
+//   x_f = a_jacobi_refine(K_ff, b_f - K_fp p, T K_red^-1 T^T (b_f - K_fp p))
+template <typename T>
+__global__ void k_cms_b(int nF, const int* __restrict__ inc_ptr, const vec4_t<T>* __restrict__ corner,
+                        const T* __restrict__ m_dt2, const vec4_t<T>* __restrict__ xhat, vec4_t<T>* __restrict__ B) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    T bx = 0, by = 0, bz = 0;
+    for (int k = inc_ptr[i]; k < inc_ptr[i + 1]; ++k) {
+        const vec4_t<T> c = corner[k];
+        bx += c.x; by += c.y; bz += c.z;
+    }
+    const T mm = m_dt2[i];
+    const vec4_t<T> xh = xhat[i];
+    B[i] = make4<T>(mm * xh.x + bx, mm * xh.y + by, mm * xh.z + bz, T(0));
+}
+
+template <typename T>
+__global__ void k_cms_set_x(int nF, const vec4_t<T>* __restrict__ X, vec4_t<T>* __restrict__ x, int* fail_iter, int it) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    const vec4_t<T> v = X[i];
+    x[i] = v;
+    if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z))) atomicMin(fail_iter, it);
+}
+
 }  // namespace vk

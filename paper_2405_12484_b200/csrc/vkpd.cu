@@ -173,6 +173,8 @@ struct CtxBase {
                                const double* Kinv) = 0;
     virtual int cms_timing(double* apply_ms, double* sweeps_ms) = 0;
     virtual int time_local(int reps, double* local_ms, double* pass_ms) = 0;
+    virtual int step_cms(int iterations, double damping, int sweeps, int agg, double omega, int cheb, double rho,
+                         int* failed) = 0;
     virtual int dev_residual(const void* x, const void* xhat, void* r) = 0;
     virtual int dev_apply_K(const void* X, void* Y) = 0;
     virtual int dev_inv_diag(void* out) = 0;
@@ -1311,7 +1313,7 @@ struct Ctx : CtxBase {
     // a_jacobi_refine on K_ff over free-node vectors (pdsolver.py:632-703)
     int run_aj(int ncols, int sweeps, int agg, double omega, int cheb, double rho) {
         const int steps = cheb ? sweeps * agg : sweeps;
-        CK(hist_d.alloc((size_t)3 * (steps + 1)));
+        if (hist_d.n < (size_t)3 * (steps + 1)) CK(hist_d.alloc((size_t)3 * (steps + 1)));
         CK(cudaMemsetAsync(hist_d.p, 0, sizeof(double) * 3 * (steps + 1), stream));
         vk::AJArgs<T> a = aj_args(sweeps, agg, omega, rho, ncols);
         void* args[] = {&a};
@@ -1479,6 +1481,46 @@ struct Ctx : CtxBase {
         }
         CK(cudaGetLastError());
         return VKPD_OK;
+    }
+    // pd_step with GlobalSolver(mode="cms") as one device frame (pdsolver.py:257-304, 237-246): per
+    // PD round the local step in rhs form (+ robust pass), b = rhs + (M/dt^2) xhat on the free rows,
+    // b_f - K_fp p, the subspace apply and the A-Jacobi / Chebyshev sweeps; no host round trip
+    int step_cms(int iterations, double damping, int sweeps, int agg, double omega, int cheb, double rho,
+                 int* failed) override {
+        if (nE == 0) return fail(VKPD_EINVAL, "cms frame needs a mesh context");
+        if (!cms_blocked && cms_m <= 0) return fail(VKPD_EINVAL, "no CMS subspace set (vkpd_cms_set_blocks)");
+        if (iterations < 0 || iterations > 1024) return fail(VKPD_EINVAL, "iterations must be in [0, 1024]");
+        if (sweeps > 0 && agg != 2 && agg != 3) return fail(VKPD_EINVAL, "aggregation must be 2 or 3");
+        if (cheb && sweeps > 0 && !(rho >= 0.0)) return fail(VKPD_EINVAL, "chebyshev needs rho (vkpd_power_rho)");
+        if (int rc = ensure_aj()) return rc;
+        if (failed) *failed = -1;
+        const int nb = cdiv(n, 256);
+        vk::k_prologue<T><<<nb, 256, 0, stream>>>(n, nF, (T)dt, dt2_inv_m.p, has_forces ? f.p : nullptr, pin_tgt.p,
+                                                  x.p, v.p, x_start.p, v_start.p, xhat.p, fail_iter.p);
+        CK(cudaGetLastError());
+        const vk::LocalArgs<T> la = local_args(x.p);
+        for (int it = 0; it < iterations && nF > 0; ++it) {
+            CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
+            vk::k_local<T, vk::MODE_RHS, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+            if (robust_tasks)
+                vk::k_robust_tasks<T, vk::MODE_RHS><<<robust_task_blocks * n_sms, 128, 0, stream>>>(
+                    la, robust_res.p, robust_ok.p, robust_arrivals.p, std::max(1, nE));
+            else
+                vk::k_robust_ws<T, vk::MODE_RHS><<<robust_blocks * n_sms, 128, 0, stream>>>(la);
+            vk::k_cms_b<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, inc_ptr.p, corner.p, m_dt2.p, xhat.p, tmp4a.p);
+            k_rhs_minus_fp<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, tmp4a.p, fp_ptr.p, fp_col.p, fp_val.p, x.p + nF,
+                                                                rhs.p);
+            CK(cudaGetLastError());
+            if (int rc = cms_apply()) return rc;
+            if (sweeps > 0)
+                if (int rc = run_aj(3, sweeps, agg, omega, cheb, rho)) return rc;
+            vk::k_cms_set_x<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, dx.p, x.p, fail_iter.p, it);
+            CK(cudaGetLastError());
+        }
+        vk::k_epilogue<T><<<nb, 256, 0, stream>>>(n, (T)(damping / dt), x.p, x_start.p, v.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h_fail, fail_iter.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        return sync(failed);
     }
     // GlobalSolver.solve in "cms" mode (pdsolver.py:237-246): per column
     // x0 = T K_red^-1 T^T b_f, then a_jacobi_refine(K_ff, b_f, x0, ...).
@@ -1821,6 +1863,10 @@ int vkpd_cms_set_blocks(vkpd_ctx* ctx, int n_dom, const int64_t* row_ptr, const 
     CTX_CALL(cms_set_blocks(n_dom, row_ptr, rows, col_ptr, colmap, A, n_modes, nb, boundary, Kred_inv));
 }
 int vkpd_cms_timing(vkpd_ctx* ctx, double* apply_ms, double* sweeps_ms) { CTX_CALL(cms_timing(apply_ms, sweeps_ms)); }
+int vkpd_step_cms(vkpd_ctx* ctx, int iterations, double damping, int sweeps, int aggregation, double omega,
+                  int chebyshev, double rho, int* failed_iter) {
+    CTX_CALL(step_cms(iterations, damping, sweeps, aggregation, omega, chebyshev, rho, failed_iter));
+}
 int vkpd_time_local(vkpd_ctx* ctx, int reps, double* local_ms, double* pass_ms) {
     CTX_CALL(time_local(reps, local_ms, pass_ms));
 }

@@ -146,3 +146,21 @@ def test_cms_mode_frame_matches_reference(c1sys):
                                 modes_per_domain=12, refine_sweeps=30)
     assert rel_l2(fr[0], g["cms_frame"]) < 1e-9
     assert rel_l2(fr[0] - sc.mesh.nodes, g["cms_frame"] - sc.mesh.nodes) < 1e-6
+
+
+@pytest.mark.parametrize("chebyshev", [False, True])
+def test_cms_device_frame_equals_host_loop(c1sys, chebyshev):
+    """simulate_mesh(solver_mode="cms") runs each frame as one device call (vkpd_step_cms); the
+    reference's loop of pd_step with a GlobalSolver(mode="cms") object gives the same frames."""
+    sc, K, free, Kff = c1sys
+    kw = dict(n_domains=2, modes_per_domain=12, refine_sweeps=10, chebyshev=chebyshev)
+    fr = pdsolver.simulate_mesh(sc.mesh, sc.gammas, 3, sc.dt, forces=sc.forces, pins=sc.pins,
+                                pin_targets=sc.pin_targets, iterations=8, solver_mode="cms", **kw)
+    sub = gcms.build_cms(Kff, sc.mesh, n_domains=2, modes_per_domain=12, free=free)
+    solver = pdsolver.GlobalSolver(pdsolver.assemble_global(sc.mesh, sc.gammas, sc.dt), free, sc.pins, mode="cms",
+                                   cms=sub, refine_sweeps=10, chebyshev=chebyshev)
+    st = pdsolver.SimState(x=sc.mesh.nodes, v=np.zeros_like(sc.mesh.nodes), dt=sc.dt, pins=sc.pins,
+                           pin_targets=sc.pin_targets)
+    for k in range(3):
+        pdsolver.pd_step(st, sc.mesh, sc.gammas, iterations=8, forces=sc.forces, solver=solver, precision="fp64")
+        assert rel_l2(fr[k] - sc.mesh.nodes, st.x - sc.mesh.nodes) < 1e-10, k
