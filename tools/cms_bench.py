@@ -26,6 +26,7 @@ p.add_argument("--modes", type=int, default=20)
 p.add_argument("--sweeps", type=int, default=30)
 p.add_argument("--aggregation", type=int, default=2)
 p.add_argument("--reps", type=int, default=5)
+p.add_argument("--frames", type=int, default=3, help="also time this many cms-mode device frames (30 PD rounds)")
 p.add_argument("--out", default=None)
 a = p.parse_args()
 
@@ -84,6 +85,18 @@ out = {
     "sweep_alg_bytes": sweep_bytes,
     "frame_ms_estimate_30_pd_iters": 30 * (am + sm),
 }
+if a.frames > 0:
+    fctx = pdsolver.device_context(m, sc.gammas, sc.dt, sc.pins, "fp64")
+    fctx.cms_set_blocks(blk)
+    fctx.set_state(m.nodes)
+    fctx.set_pin_targets(sc.pin_targets)
+    fctx.set_forces(sc.forces)
+    fctx.step_cms(sc.iterations, 1.0, a.sweeps, a.aggregation, pdsolver.JACOBI_OMEGA, False, 0.0)   # warm-up
+    t3 = time.perf_counter()
+    for _ in range(a.frames):
+        fctx.step_cms(sc.iterations, 1.0, a.sweeps, a.aggregation, pdsolver.JACOBI_OMEGA, False, 0.0)
+    out["cms_frame_ms"] = 1e3 * (time.perf_counter() - t3) / a.frames
+    out["cms_frame_note"] = "simulate_mesh(solver_mode='cms') frame on the device (vkpd_step_cms), 30 PD rounds"
 line = json.dumps(out)
 print(line)
 if a.out:
