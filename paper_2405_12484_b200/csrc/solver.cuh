@@ -252,6 +252,7 @@ struct PcgArgs {
     vec4_t<T>* warm_prev;        // optional: the correction before it; the guess is then the linear
                                  // extrapolation d_prev + beta (d_prev - d_prevprev)
     double warm_beta;
+    int warm_extrap_rounds;      // rounds < this extrapolate; later warm rounds reuse the last correction
 };
 
 template <typename T>
@@ -680,7 +681,7 @@ __device__ __forceinline__ void pcg_classic_body(const PcgArgs<T>& a, cg::grid_g
             xi.x += d.x; xi.y += d.y; xi.z += d.z;
             a.x[i] = xi;
             if (warm) {
-                if (a.warm_prev != nullptr) {
+                if (a.warm_prev != nullptr && pdi_w < a.warm_extrap_rounds) {
                     vec4_t<T>* wp = a.warm_prev + (size_t)pdi_w * nF;
                     const vec4_t<T> dp = ld4(&wp[i]);
                     wp[i] = d;

@@ -213,6 +213,9 @@ struct Ctx : CtxBase {
     int poly_rounds = 0;                 // env VKPD_POLY_ROUNDS=k: PD rounds >= k use Jacobi-PCG (0: all polynomial)
     bool warm_extrap = true;             // d + beta (d - d_before), beta = 1 (env VKPD_WARM_EXTRAP=<beta>,
     double warm_beta = 1.0;              // 0: the previous correction alone)
+    int warm_extrap_rounds = sizeof(T) == 8 ? 32 : 1;   // env VKPD_WARM_EXTRAP_ROUNDS: fp32 extrapolates
+                                         // round 0 only (later rounds' corrections are noise-level: C3
+                                         // 0.88 ms, C5 2.76 ms; all three rounds: 0.885 / 3.37 ms)
     bool warm_start = true;              // env VKPD_WARM=0: off
     int warm_rounds = sizeof(T) == 8 ? 32 : 3;   // env VKPD_WARM=<rounds>; fp64 runs every round (no early exit), where
                                          // all rounds gain (C3: 19.3 -> 15.9 ms/frame); fp32 only the first 3
@@ -648,6 +651,7 @@ struct Ctx : CtxBase {
         CK(warm0.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
         CK(cudaMemsetAsync(warm0.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
         if (const char* pr = getenv("VKPD_POLY_ROUNDS")) poly_rounds = std::max(0, atoi(pr));
+        if (const char* px = getenv("VKPD_WARM_EXTRAP_ROUNDS")) warm_extrap_rounds = std::max(0, atoi(px));
         if (const char* pe = getenv("VKPD_WARM_EXTRAP")) { warm_beta = atof(pe); warm_extrap = warm_beta != 0.0; }
         if (warm_extrap) {
             CK(warm1.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
@@ -901,6 +905,7 @@ struct Ctx : CtxBase {
         pa.warm_rounds = warm_rounds;
         pa.warm_prev = (pa.warm != nullptr && warm_extrap) ? warm1.p : nullptr;
         pa.warm_beta = warm_beta;
+        pa.warm_extrap_rounds = warm_extrap_rounds;
         pa.poly_rounds = poly_rounds;
         pa.h = ss.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
         if (init == vk::INIT_PD && ncoll > 0) {

@@ -13,6 +13,6 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_pc
     -o $O/pcg_steady python tools/profile_steady.py --warm 10 --frames 2 --graph 0 > $O/f1.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_local --launch-skip 60 -c 1 \
     -o $O/local_steady python tools/profile_steady.py --warm 10 --frames 2 --graph 0 > $O/f2.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_robust_ws --launch-skip 700 -c 1 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_robust_tasks --launch-skip 700 -c 1 \
     -o $O/robust_fold python tools/profile_steady.py --warm 119 --frames 2 --graph 0 > $O/f3.log 2>&1
 ls -la $O
