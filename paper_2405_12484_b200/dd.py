@@ -254,7 +254,11 @@ class DistributedStepper:
         return self.comm.allreduce_sum(t)
 
     # -- the step
-    def step(self, iterations=30, damping=1.0):
+    def step(self, iterations=30, damping=1.0, early_exit=True):
+        """One PD step.  A round whose solve needs zero CG iterations leaves X unchanged, so
+        every later round would repeat it exactly (same local step, same halo): with
+        `early_exit` the loop stops there, as the single-GPU frame does.  The iteration count
+        is identical on every rank (the residual norms are global)."""
         torch = self.torch
         nF, nPo = self.nF, self.nPo
         Xs, Vs = self.X.clone(), self.V.clone()
@@ -295,6 +299,9 @@ class DistributedStepper:
                 red = self._allsum(torch.cat([(R * Z).double().sum(0)[:3], (R * R).double().sum().reshape(1)]))
                 rz_prev, rz, rr = rz, red[:3].clone(), float(red[3])
                 k += 1
+            self.last_rounds = it + 1
+            if k == 0 and early_exit:
+                break
             X[:nF] = X[:nF] + DX
             X = self._halo(X)
             bad = torch.tensor([0.0 if bool(torch.isfinite(X[:nF]).all()) else 1.0], dtype=torch.float64,

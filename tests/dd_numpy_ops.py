@@ -56,7 +56,7 @@ class NumpyOps:
         return out
 
 
-def gloo_worker(rank, world, port, steps, out_dir, kind="numpy", box=(9, 5, 3)):
+def gloo_worker(rank, world, port, steps, out_dir, kind="numpy", box=(9, 5, 3), tol=None, early_exit=True):
     """mp.spawn target: one rank of the domain-decomposed step over gloo."""
     import os
     import torch.distributed as dist
@@ -66,16 +66,18 @@ def gloo_worker(rank, world, port, steps, out_dir, kind="numpy", box=(9, 5, 3)):
     plan = dd.DomainPlan(sc.mesh, sc.pins, world)
     arrays = plan.local_arrays(sc.mesh, sc.gammas, rank)
     if kind == "numpy":
-        ops, tol = NumpyOps(arrays, sc.dt), 1e-13
+        ops, tol = NumpyOps(arrays, sc.dt), (1e-13 if tol is None else tol)
     else:                                       # real CUDA operators (ranks may share one GPU)
-        ops, tol = dd.CudaOps(arrays, sc.dt, precision="fp64"), 1e-12
+        ops, tol = dd.CudaOps(arrays, sc.dt, precision="fp64"), (1e-12 if tol is None else tol)
     st = dd.DistributedStepper(plan, rank, sc.mesh, sc.gammas, sc.dt, ops, dd.Comm(), pin_targets=sc.pin_targets,
                                tol=tol)
     st.set_state(sc.mesh.nodes)
     st.set_forces(sc.forces)
+    rounds = []
     for _ in range(steps):
-        st.step(iterations=10)
+        st.step(iterations=10, early_exit=early_exit)
+        rounds.append(st.last_rounds)
     ids, pos = st.owned_positions()
-    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=ids, pos=pos)
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=ids, pos=pos, rounds=np.array(rounds))
     dist.barrier()
     dist.destroy_process_group()

@@ -57,3 +57,19 @@ def test_plan_ownership_and_halo_consistency():
         assert np.array_equal(np.sort(recv), p.halo)
         for s, g in p.send.items():
             assert np.array_equal(plan.parts[s].recv[p.rank], g)
+
+
+def test_dd_gloo_early_exit_is_exact(tmp_path):
+    """A round whose distributed solve needs zero CG iterations ends the step; the positions
+    are the same bits as running every round (world_size 2, gloo)."""
+    res = {}
+    for ex in (True, False):
+        d = tmp_path / str(ex)
+        d.mkdir()
+        mp.spawn(gloo_worker, args=(2, _free_port(), 3, str(d), "numpy", (9, 5, 3), 1e-3, ex), nprocs=2, join=True)
+        res[ex] = [np.load(d / f"rank{r}.npz") for r in range(2)]
+    for r in range(2):
+        assert np.array_equal(res[True][r]["ids"], res[False][r]["ids"])
+        assert np.array_equal(res[True][r]["pos"], res[False][r]["pos"])
+    assert res[True][0]["rounds"].max() < 10          # the exit was taken
+    assert np.all(res[False][0]["rounds"] == 10)
