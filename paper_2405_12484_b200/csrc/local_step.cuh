@@ -91,6 +91,8 @@ struct LocalArgs {
     ProjStats* stats;
     int* robust_list;            // optional: suspicious elements are queued here (k_robust finishes them)
     int* robust_count;           // [0] queued elements, [1] chunk cursor of the robust pass
+    unsigned long long robust_if;   // nonzero: graph IF-node handle set to 1 when anything is queued
+                                    // (the robust pass is only launched then)
     T* robust_aux;               // optional, 24 per queue slot: the queued element's (sigma, U, W) from
                                  // the first pass, so the robust pass does not redo the SVD
     double* F_out;               // optional (nE,3,3) (RHS mode only)
@@ -144,7 +146,10 @@ __device__ __forceinline__ void local_tet(const LocalArgs<T>& a, int e) {
             const int lane = threadIdx.x & 31;
             const int lead = __ffs(m3) - 1;
             int base = 0;
-            if (lane == lead) base = atomicAdd(a.robust_count, __popc(m3));
+            if (lane == lead) {
+                base = atomicAdd(a.robust_count, __popc(m3));
+                if (a.robust_if != 0) cudaGraphSetConditional((cudaGraphConditionalHandle)a.robust_if, 1u);
+            }
             base = __shfl_sync(am, base, lead);
             if (path == 3) {
                 const int slot = base + __popc(m3 & ((1u << lane) - 1u));

@@ -245,6 +245,7 @@ struct PcgArgs {
     int* pd_iter_dev;            // optional: PD iteration index read on the device (graph loop body);
                                  // then fail_iter gets *pd_iter_dev and the count goes to iters_out[*pd_iter_dev]
     unsigned long long loop_handle;   // nonzero: conditional handle of the PD-iteration loop node
+    unsigned long long robust_if;     // nonzero: the robust pass's IF node handle, cleared here
     int loop_iterations;
     unsigned long long* rounds;  // optional: executed-PD-round counter
     vec4_t<T>* warm;             // POLY, optional: warm_rounds banks of nF; PD round k < warm_rounds starts
@@ -275,6 +276,7 @@ __device__ __forceinline__ void pcg_exit(const PcgArgs<T>& a, bool bad, int it, 
                 for (int j = pdi + 1; j < a.loop_iterations; ++j) a.iters_out[j] = 0;
             *a.pd_iter_dev = pdi + 1;
             cudaGraphSetConditional((cudaGraphConditionalHandle)a.loop_handle, stop ? 0u : 1u);
+            if (a.robust_if != 0) cudaGraphSetConditional((cudaGraphConditionalHandle)a.robust_if, 0u);
         }
     }
 }

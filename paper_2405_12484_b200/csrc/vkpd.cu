@@ -255,6 +255,9 @@ struct Ctx : CtxBase {
     bool pd_early_exit = true;           // loop node with the zero-CG-iteration exit (env VKPD_PD_EXIT=0: off)
     int last_exec_rounds = 0;            // PD rounds of the last directly launched frame
     cudaStream_t body_stream = nullptr;  // captures the loop body
+    cudaStream_t if_stream = nullptr;    // captures the robust pass's IF-node body
+    bool robust_if_node = false;         // env VKPD_ROBUST_IF=1: robust pass inside an IF node set by the
+                                         // local step (measured slower: the node costs more than the launch)
     DBuf<int> pd_it;                     // device PD-iteration counter of the loop node
     int graph_ncoll = 0;
     // colliders (pdsolver.py:125-173, 271-297)
@@ -268,6 +271,7 @@ struct Ctx : CtxBase {
         if (h_fail) cudaFreeHost(h_fail);
         if (own_stream) cudaStreamDestroy(own_stream);
         if (body_stream) cudaStreamDestroy(body_stream);
+        if (if_stream) cudaStreamDestroy(if_stream);
         for (auto& ev : cms_ev)
             if (ev) cudaEventDestroy(ev);
     }
@@ -651,6 +655,7 @@ struct Ctx : CtxBase {
         CK(warm0.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
         CK(cudaMemsetAsync(warm0.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
         if (const char* pr = getenv("VKPD_POLY_ROUNDS")) poly_rounds = std::max(0, atoi(pr));
+        if (const char* pi = getenv("VKPD_ROBUST_IF")) robust_if_node = atoi(pi) != 0;
         if (const char* px = getenv("VKPD_WARM_EXTRAP_ROUNDS")) warm_extrap_rounds = std::max(0, atoi(px));
         if (const char* pe = getenv("VKPD_WARM_EXTRAP")) { warm_beta = atof(pe); warm_extrap = warm_beta != 0.0; }
         if (warm_extrap) {
@@ -869,6 +874,7 @@ struct Ctx : CtxBase {
         la.stats = pstats.p; la.F_out = la.R_out = la.V_out = nullptr;
         la.robust_list = robust_list.p; la.robust_count = robust_count.p;
         la.robust_aux = robust_handoff ? robust_aux.p : nullptr;
+        la.robust_if = 0;
         return la;
     }
     // local step in residual form, suspicious elements compacted into a dense second pass
@@ -899,7 +905,7 @@ struct Ctx : CtxBase {
         pa.max_iters = max_iters; pa.init = init;
         pa.cdiag = nullptr; pa.cb = nullptr; pa.coll = nullptr; pa.ncoll = 0;
         pa.reset_count = nullptr;
-        pa.pd_iter_dev = nullptr; pa.loop_handle = 0; pa.loop_iterations = 0;
+        pa.pd_iter_dev = nullptr; pa.loop_handle = 0; pa.loop_iterations = 0; pa.robust_if = 0;
         pa.rounds = init == vk::INIT_PD ? &pstats.p->pd_rounds : nullptr;
         pa.warm = (init == vk::INIT_PD && pcg_poly && warm_start) ? warm0.p : nullptr;
         pa.warm_rounds = warm_rounds;
@@ -1033,13 +1039,50 @@ struct Ctx : CtxBase {
         cudaStream_t outer = stream;
         stream = body_stream;
         int rc = VKPD_OK;
+        unsigned long long hif_v = 0;
         {
-            const vk::LocalArgs<T> la = local_args(x.p);
-            rc = launch_local_resid(la, false);
+            vk::LocalArgs<T> la = local_args(x.p);
+            if (robust_if_node && robust_tasks) {
+                // local step, then the robust pass inside an IF node that the local step sets
+                // only when it queued a tet (quiet rounds skip the launch); the solver clears it
+                cudaGraphConditionalHandle hif;
+                CK(cudaGraphConditionalHandleCreate(&hif, body, 0, cudaGraphCondAssignDefault));
+                hif_v = (unsigned long long)hif;
+                la.robust_if = hif_v;
+                vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+                CK(cudaGetLastError());
+                cudaStreamCaptureStatus bst;
+                cudaGraph_t bg = nullptr;
+                const cudaGraphNode_t* bdeps = nullptr;
+                size_t nbdeps = 0;
+                CK(cudaStreamGetCaptureInfo(stream, &bst, nullptr, &bg, &bdeps, &nbdeps));
+                cudaGraphNodeParams ip = {};
+                ip.type = cudaGraphNodeTypeConditional;
+                ip.conditional.handle = hif;
+                ip.conditional.type = cudaGraphCondTypeIf;
+                ip.conditional.size = 1;
+                cudaGraphNode_t inode;
+                CK(cudaGraphAddNode(&inode, bg, bdeps, nbdeps, &ip));
+                if (!if_stream) CK(cudaStreamCreateWithFlags(&if_stream, cudaStreamNonBlocking));
+                CK(cudaStreamBeginCaptureToGraph(if_stream, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeThreadLocal));
+                la.robust_if = 0;
+                vk::k_robust_tasks<T, vk::MODE_RESID><<<robust_task_blocks * n_sms, 128, 0, if_stream>>>(
+                    la, robust_res.p, robust_ok.p, robust_arrivals.p, std::max(1, nE));
+                cudaGraph_t ig = nullptr;
+                const cudaError_t ie = cudaGetLastError();
+                const cudaError_t ee = cudaStreamEndCapture(if_stream, &ig);
+                CK(ie);
+                CK(ee);
+                CK(cudaStreamUpdateCaptureDependencies(stream, &inode, 1, cudaStreamSetCaptureDependencies));
+            } else {
+                rc = launch_local_resid(la, false);
+            }
             if (rc == VKPD_OK) {
                 vk::PcgArgs<T> pa = pcg_args(vk::INIT_PD, 0, iters.p);
                 pa.reset_count = robust_count.p;
                 pa.pd_iter_dev = pd_it.p;
+                pa.robust_if = hif_v;
                 pa.loop_handle = (unsigned long long)h;
                 pa.loop_iterations = iterations;
                 cudaError_t e = launch_pcg(pa);
