@@ -246,6 +246,7 @@ struct PcgArgs {
                                  // then fail_iter gets *pd_iter_dev and the count goes to iters_out[*pd_iter_dev]
     unsigned long long loop_handle;   // nonzero: conditional handle of the PD-iteration loop node
     unsigned long long robust_if;     // nonzero: the robust pass's IF node handle, cleared here
+    int* first_stop;             // optional: min over this frame's rounds that met the exit condition (1-based)
     int loop_iterations;
     unsigned long long* rounds;  // optional: executed-PD-round counter
     vec4_t<T>* warm;             // POLY, optional: warm_rounds banks of nF; PD round k < warm_rounds starts
@@ -272,8 +273,10 @@ __device__ __forceinline__ void pcg_exit(const PcgArgs<T>& a, bool bad, int it, 
             // Skipped rounds are recorded with 0 CG iterations.
             const bool stop = pdi + 1 >= a.loop_iterations || (it == 0 && !moved) ||
                               *(volatile int*)a.fail_iter != 0x7fffffff;
-            if (stop)
+            if (stop) {
                 for (int j = pdi + 1; j < a.loop_iterations; ++j) a.iters_out[j] = 0;
+                if (a.first_stop != nullptr && pdi + 1 < *a.first_stop) *a.first_stop = pdi + 1;
+            }
             *a.pd_iter_dev = pdi + 1;
             cudaGraphSetConditional((cudaGraphConditionalHandle)a.loop_handle, stop ? 0u : 1u);
             if (a.robust_if != 0) cudaGraphSetConditional((cudaGraphConditionalHandle)a.robust_if, 0u);

@@ -256,6 +256,13 @@ struct Ctx : CtxBase {
     int last_exec_rounds = 0;            // PD rounds of the last directly launched frame
     cudaStream_t body_stream = nullptr;  // captures the loop body
     cudaStream_t if_stream = nullptr;    // captures the robust pass's IF-node body
+    int unroll_rounds = 0;               // PD rounds captured ahead of the WHILE node (see step_async)
+    int unroll_env = -1;                 // env VKPD_UNROLL: fixed count (-1: adaptive)
+    int graph_unroll = 0;
+    DBuf<int> first_stop;                // rounds the last frame needed (device), mirrored to h_stop
+    int* h_stop = nullptr;
+    int stop_hist[32];
+    int stop_n = 0, stop_pos = 0, stop_fill = 0;
     bool robust_if_node = false;         // env VKPD_ROBUST_IF=1: robust pass inside an IF node set by the
                                          // local step (measured slower: the node costs more than the launch)
     DBuf<int> pd_it;                     // device PD-iteration counter of the loop node
@@ -269,6 +276,7 @@ struct Ctx : CtxBase {
     ~Ctx() override {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (h_fail) cudaFreeHost(h_fail);
+        if (h_stop) cudaFreeHost(h_stop);
         if (own_stream) cudaStreamDestroy(own_stream);
         if (body_stream) cudaStreamDestroy(body_stream);
         if (if_stream) cudaStreamDestroy(if_stream);
@@ -656,6 +664,8 @@ struct Ctx : CtxBase {
         CK(cudaMemsetAsync(warm0.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
         if (const char* pr = getenv("VKPD_POLY_ROUNDS")) poly_rounds = std::max(0, atoi(pr));
         if (const char* pi = getenv("VKPD_ROBUST_IF")) robust_if_node = atoi(pi) != 0;
+        if (const char* pu = getenv("VKPD_UNROLL")) unroll_env = std::max(0, std::min(64, atoi(pu)));
+        unroll_rounds = unroll_env > 0 ? unroll_env : 0;
         if (const char* px = getenv("VKPD_WARM_EXTRAP_ROUNDS")) warm_extrap_rounds = std::max(0, atoi(px));
         if (const char* pe = getenv("VKPD_WARM_EXTRAP")) { warm_beta = atof(pe); warm_extrap = warm_beta != 0.0; }
         if (warm_extrap) {
@@ -672,6 +682,9 @@ struct Ctx : CtxBase {
         CK(stage.alloc((size_t)3 * n));
         CK(cudaHostAlloc(&h_fail, sizeof(int), cudaHostAllocDefault));
         *h_fail = 0x7fffffff;
+        CK(cudaHostAlloc(&h_stop, sizeof(int), cudaHostAllocDefault));
+        *h_stop = 0;
+        CK(first_stop.alloc(1));
         CK(cudaStreamSynchronize(s));
         return VKPD_OK;
     }
@@ -906,6 +919,7 @@ struct Ctx : CtxBase {
         pa.cdiag = nullptr; pa.cb = nullptr; pa.coll = nullptr; pa.ncoll = 0;
         pa.reset_count = nullptr;
         pa.pd_iter_dev = nullptr; pa.loop_handle = 0; pa.loop_iterations = 0; pa.robust_if = 0;
+        pa.first_stop = nullptr;
         pa.rounds = init == vk::INIT_PD ? &pstats.p->pd_rounds : nullptr;
         pa.warm = (init == vk::INIT_PD && pcg_poly && warm_start) ? warm0.p : nullptr;
         pa.warm_rounds = warm_rounds;
@@ -1018,6 +1032,7 @@ struct Ctx : CtxBase {
                                                                       contact_k, inv_diag_c.p, cdiag.p, cb.p);
             CK(cudaGetLastError());
         }
+        CK(cudaMemsetAsync(first_stop.p, 0x7f, sizeof(int), stream));      // 0x7f7f7f7f: no stop yet
         // conditional node after the captured prologue
         cudaStreamCaptureStatus st;
         cudaGraph_t g = nullptr;
@@ -1026,6 +1041,22 @@ struct Ctx : CtxBase {
         CK(cudaStreamGetCaptureInfo(stream, &st, nullptr, &g, &deps, &ndeps));
         cudaGraphConditionalHandle h;
         CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        // the first `unroll_rounds` rounds as plain graph nodes (no conditional-node overhead);
+        // their solves set the loop handle like the loop body's, and a round run after the exit
+        // point is an exact repeat (x unchanged), so the frame's result is the same
+        const int nun = std::min(unroll_rounds, iterations);
+        for (int it = 0; it < nun; ++it) {
+            const vk::LocalArgs<T> la = local_args(x.p);
+            if (int rc = launch_local_resid(la, false)) return rc;
+            vk::PcgArgs<T> pa = pcg_args(vk::INIT_PD, 0, iters.p);
+            pa.reset_count = robust_count.p;
+            pa.pd_iter_dev = pd_it.p;
+            pa.loop_handle = (unsigned long long)h;
+            pa.loop_iterations = iterations;
+            pa.first_stop = first_stop.p;
+            CK(launch_pcg(pa));
+        }
+        CK(cudaStreamGetCaptureInfo(stream, &st, nullptr, &g, &deps, &ndeps));
         cudaGraphNodeParams cp = {};
         cp.type = cudaGraphNodeTypeConditional;
         cp.conditional.handle = h;
@@ -1083,6 +1114,7 @@ struct Ctx : CtxBase {
                 pa.reset_count = robust_count.p;
                 pa.pd_iter_dev = pd_it.p;
                 pa.robust_if = hif_v;
+                pa.first_stop = first_stop.p;
                 pa.loop_handle = (unsigned long long)h;
                 pa.loop_iterations = iterations;
                 cudaError_t e = launch_pcg(pa);
@@ -1098,7 +1130,28 @@ struct Ctx : CtxBase {
         vk::k_epilogue<T><<<nb, 256, 0, stream>>>(n, (T)(damping / dt), x.p, x_start.p, v.p);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h_fail, fail_iter.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(h_stop, first_stop.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
         return VKPD_OK;
+    }
+
+    // Adaptive unrolling: the rounds a recent frame needed (its first round that met the exit
+    // condition, read from pinned memory the graph writes; no synchronization) are sampled at
+    // every launch; the unrolled count becomes the minimum of the last 32 samples (after 8
+    // samples, then every 64), so unrolled rounds are almost never past the exit point (and when
+    // they are, they are exact repeats).
+    void adapt_unroll(int iterations) {
+        if (unroll_env >= 0 || !pd_early_exit) return;
+        const int need = *(volatile int*)h_stop;
+        if (need <= 0) return;                                   // no frame finished yet
+        stop_hist[stop_pos] = std::min(need, iterations);        // 0x7f7f7f7f: every round ran
+        stop_pos = (stop_pos + 1) % 32;
+        stop_fill = std::min(32, stop_fill + 1);
+        ++stop_n;
+        // first decision after 8 samples, then every 64 (a re-capture costs ~0.3 ms of host time)
+        if (!(stop_n == 8 || (stop_n > 8 && (stop_n - 8) % 64 == 0))) return;
+        int m = iterations;
+        for (int k = 0; k < stop_fill; ++k) m = std::min(m, stop_hist[k]);
+        unroll_rounds = m;
     }
 
     int build_graph(int iterations, double damping) {
@@ -1125,6 +1178,7 @@ struct Ctx : CtxBase {
             return VKPD_OK;
         }
         graph_iters = iterations;
+        graph_unroll = unroll_rounds;
         graph_damp = damping;
         graph_forces = has_forces;
         graph_ncoll = ncoll;
@@ -1135,8 +1189,9 @@ struct Ctx : CtxBase {
         if (iterations < 0 || iterations > 1024) return fail(VKPD_EINVAL, "iterations must be in [0, 1024]");
         last_iterations = iterations;
         if (use_graph && !graph_broken) {
+            if (graph_exec && graph_iters == iterations) adapt_unroll(iterations);
             if (!graph_exec || graph_iters != iterations || graph_damp != damping || graph_forces != has_forces ||
-                graph_ncoll != ncoll) {
+                graph_ncoll != ncoll || graph_unroll != unroll_rounds) {
                 int rc = build_graph(iterations, damping);
                 if (rc) return rc;
             }
