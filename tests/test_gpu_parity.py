@@ -268,6 +268,19 @@ def test_pd_loop_early_exit_is_exact(monkeypatch, config, frames, precision):
         assert any(0 in it for it in ib)     # the exit was actually taken (fp64 at 1e-12 rarely exits)
 
 
+@pytest.mark.parametrize("unroll", ["3", "7"])
+def test_unrolled_rounds_are_exact(monkeypatch, unroll):
+    """Leading PD rounds captured as plain graph nodes ahead of the WHILE node (fixed counts here;
+    adaptive by default): a round past the exit point is an exact repeat, so positions and the
+    per-round CG iterations of the executed rounds are the same bits as the loop alone."""
+    sc = scenes.make_scene("C2")
+    monkeypatch.setenv("VKPD_UNROLL", "0")
+    a, ia = _run_frames(sc, 30, "fp32", collect_every=3)
+    monkeypatch.setenv("VKPD_UNROLL", unroll)
+    b, ib = _run_frames(sc, 30, "fp32", collect_every=3)
+    assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("variant", ["ws", "quad"])
 def test_robust_pass_variants_bit_identical(monkeypatch, variant):
     """The default robust pass ((chunk, start) tasks, per-chunk last-arrival select) and the
