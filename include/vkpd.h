@@ -130,6 +130,14 @@ int vkpd_set_colliders(vkpd_ctx* ctx, int n, const int* kinds, const double* par
 /* one implicit-Euler step by `iterations` local/global rounds; blocks until done.
  * On VKPD_ENONFINITE the state is left as it was before the step. */
 int vkpd_step(vkpd_ctx* ctx, int iterations, double damping, int* failed_iter);
+/* simulate_mesh's frame loop (pdsolver.py:744-762): `steps` steps from the current state; forces NULL
+ * (none), (nV,3) constant (forces_per_step = 0) or (steps,nV,3); pin_path NULL (current targets) or
+ * (steps,n_pins,3); frames (steps,nV,3) receives x after every step.  Per-step inputs and outputs
+ * move on a copy stream, overlapping the next frame.  On VKPD_ENONFINITE, *failed_frame / *failed_iter
+ * name the first failing step and its PD iteration (the contents of frames from there on are
+ * undefined). */
+int vkpd_simulate(vkpd_ctx* ctx, int steps, int iterations, double damping, const double* forces, int forces_per_step,
+                  const double* pin_path, double* frames, int* failed_frame, int* failed_iter);
 /* same step, enqueued without waiting; vkpd_sync() reports the outcome */
 int vkpd_step_async(vkpd_ctx* ctx, int iterations, double damping);
 int vkpd_sync(vkpd_ctx* ctx, int* failed_iter);

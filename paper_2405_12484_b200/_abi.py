@@ -29,7 +29,7 @@ EXPORTS = (
     "vkpd_projection_jacobians", "vkpd_hess_create", "vkpd_hess_destroy", "vkpd_hess_set_gammas",
     "vkpd_hess_energy_grad", "vkpd_hess_gamma_jt", "vkpd_hess_linearize", "vkpd_hess_csr",
     "vkpd_hess_apply", "vkpd_hess_solve", "vkpd_cms_set_blocks", "vkpd_cms_timing", "vkpd_time_local",
-    "vkpd_step_cms",
+    "vkpd_step_cms", "vkpd_simulate",
 )
 
 
@@ -110,6 +110,7 @@ def load():
         "vkpd_cms_timing": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "vkpd_time_local": (I, [P, I, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "vkpd_step_cms": (I, [P, I, C.c_double, I, I, C.c_double, I, C.c_double, C.POINTER(I)]),
+        "vkpd_simulate": (I, [P, I, I, C.c_double, P, I, P, P, C.POINTER(I), C.POINTER(I)]),
         "vkpd_hess_create": (I, [C.POINTER(MeshDesc), I, C.POINTER(P)]),
         "vkpd_hess_destroy": (None, [P]),
         "vkpd_hess_set_gammas": (I, [P, P, P]),
@@ -304,6 +305,18 @@ class Context:
     def sync(self):
         fi = C.c_int(-1)
         check(self.lib.vkpd_sync(self.h, C.byref(fi)))
+
+    def simulate(self, steps, iterations, damping, forces=None, forces_per_step=False, pin_path=None, out=None):
+        """`steps` frames from the current state (vkpd_simulate); returns (steps, nV, 3) float64."""
+        frames = np.empty((steps, self.n, 3)) if out is None else out
+        fo = None
+        if forces is not None:
+            fo = f64(forces).reshape((steps if forces_per_step else 1), self.n, 3)
+        pp = None if pin_path is None or self.n_pins == 0 else f64(pin_path).reshape(steps, self.n_pins, 3)
+        ff, fi = C.c_int(-1), C.c_int(-1)
+        check(self.lib.vkpd_simulate(self.h, int(steps), int(iterations), float(damping), ptr(fo),
+                                     1 if forces_per_step else 0, ptr(pp), ptr(frames), C.byref(ff), C.byref(fi)))
+        return frames
 
     def step_cms(self, iterations, damping, sweeps, aggregation, omega, chebyshev, rho):
         """One pd_step with the cms global solver, entirely on the device."""

@@ -13,6 +13,8 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <atomic>
+#include <thread>
 
 #include "../../include/vkpd.h"
 #include "local_step.cuh"
@@ -66,6 +68,26 @@ __global__ void k_scatter_in(int n, const double* __restrict__ src, const int* _
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     dst[int_of_orig[j]] = vk::make4<T>((T)src[3 * j], (T)src[3 * j + 1], (T)src[3 * j + 2], T(0));
+}
+// between two frames of vkpd_simulate, one launch: frame i's positions out (caller order, f64),
+// its failure slot, and frame i+1's inputs in (forces, pin targets) when given
+template <typename T>
+__global__ void k_sim_between(int n, int nP, const vk::vec4_t<T>* __restrict__ x, const int* __restrict__ int_of_orig,
+                              double* __restrict__ out, const int* __restrict__ fail_iter, int* fail_slot,
+                              const double* __restrict__ fin, vk::vec4_t<T>* f, const double* __restrict__ pin,
+                              vk::vec4_t<T>* pin_tgt) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j == 0 && fail_slot) *fail_slot = *fail_iter;
+    if (j < nP && pin) pin_tgt[j] = vk::make4<T>((T)pin[3 * j], (T)pin[3 * j + 1], (T)pin[3 * j + 2], T(0));
+    if (j >= n) return;
+    const int k = int_of_orig[j];
+    if (out) {
+        const vk::vec4_t<T> v = x[k];
+        out[3 * j] = (double)v.x;
+        out[3 * j + 1] = (double)v.y;
+        out[3 * j + 2] = (double)v.z;
+    }
+    if (fin) f[k] = vk::make4<T>((T)fin[3 * j], (T)fin[3 * j + 1], (T)fin[3 * j + 2], T(0));
 }
 template <typename T>
 __global__ void k_gather_out(int n, const vk::vec4_t<T>* __restrict__ src, const int* __restrict__ int_of_orig,
@@ -155,6 +177,8 @@ struct CtxBase {
                             int* failed) = 0;
     virtual int set_colliders(int n, const int* kinds, const double* params, double kc) = 0;
     virtual int step_async(int iterations, double damping) = 0;
+    virtual int simulate(int steps, int iterations, double damping, const double* forces, int forces_per_step,
+                         const double* pin_path, double* frames, int* failed_frame, int* failed_iter) = 0;
     virtual int sync(int* failed) = 0;
     virtual int profile(int iterations, double damping, double* lms, double* gms, double* fms) = 0;
     virtual int elastic_rhs(const double* x, double* rhs, double* F, double* R, double* V) = 0;
@@ -277,6 +301,13 @@ struct Ctx : CtxBase {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (h_fail) cudaFreeHost(h_fail);
         if (h_stop) cudaFreeHost(h_stop);
+        if (sim_hin) cudaFreeHost(sim_hin);
+        if (sim_hout) cudaFreeHost(sim_hout);
+        for (int k = 0; k < 2; ++k)
+            for (cudaEvent_t e : {ev_h2d[k], ev_scat[k], ev_out[k], ev_d2h[k]})
+                if (e) cudaEventDestroy(e);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (in_stream) cudaStreamDestroy(in_stream);
         if (own_stream) cudaStreamDestroy(own_stream);
         if (body_stream) cudaStreamDestroy(body_stream);
         if (if_stream) cudaStreamDestroy(if_stream);
@@ -1203,6 +1234,133 @@ struct Ctx : CtxBase {
         return enqueue_frame(iterations, damping, nullptr);
     }
 
+    // simulate_mesh's frame loop (pdsolver.py:744-762) pipelined: per-step inputs go up and each
+    // frame's positions come down on a copy stream through double-buffered pinned / device staging,
+    // overlapping the next frame's compute; the host copies into `frames` while the GPU runs.
+    // Failures are recorded per frame and reported for the first failing frame after the loop.
+    cudaStream_t copy_stream = nullptr;     // device -> host (positions)
+    cudaStream_t in_stream = nullptr;       // host -> device (per-step inputs); separate so an upload
+                                            // never queues behind the previous frame's download
+    DBuf<double> sim_din, sim_dout;
+    double* sim_hin = nullptr;
+    double* sim_hout = nullptr;
+    size_t sim_cap = 0;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_scat[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr},
+                ev_d2h[2] = {nullptr, nullptr};
+    DBuf<int> fail_hist;
+    int simulate(int steps, int iterations, double damping, const double* forces, int forces_per_step,
+                 const double* pin_path, double* frames, int* failed_frame, int* failed_iter) override {
+        if (failed_frame) *failed_frame = -1;
+        if (failed_iter) *failed_iter = -1;
+        if (steps < 0 || !frames) return fail(VKPD_EINVAL, "bad simulate arguments");
+        if (nE == 0) return fail(VKPD_EINVAL, "matrix-only context has no mesh");
+        if (steps == 0) return VKPD_OK;
+        const size_t n3 = (size_t)3 * n, p3 = (size_t)3 * nP;
+        const size_t slot_in = n3 + p3;
+        if (!copy_stream) {
+            CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&in_stream, cudaStreamNonBlocking));
+            for (int k = 0; k < 2; ++k) {
+                CK(cudaEventCreateWithFlags(&ev_h2d[k], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ev_scat[k], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ev_d2h[k], cudaEventDisableTiming));
+            }
+        }
+        if (sim_cap < slot_in) {
+            if (sim_hin) cudaFreeHost(sim_hin);
+            if (sim_hout) cudaFreeHost(sim_hout);
+            sim_hin = sim_hout = nullptr;
+            CK(cudaHostAlloc(&sim_hin, sizeof(double) * 2 * slot_in, cudaHostAllocDefault));
+            CK(cudaHostAlloc(&sim_hout, sizeof(double) * 2 * n3, cudaHostAllocDefault));
+            CK(sim_din.alloc(2 * slot_in));
+            CK(sim_dout.alloc(2 * n3));
+            sim_cap = slot_in;
+        }
+        if (fail_hist.n < (size_t)steps) CK(fail_hist.alloc(steps));
+        if (forces && !forces_per_step) { if (int rc = set_forces(forces)) return rc; }
+        else if (!forces) has_forces = false;
+        else has_forces = true;
+        const bool up_f = forces && forces_per_step, up_p = pin_path && nP > 0;
+        // positions are copied from pinned staging into `frames` by a helper thread, so writing
+        // (and first-touching) the caller's array never delays enqueueing the next frame
+        std::atomic<int> posted{-1}, copied{-1};
+        std::atomic<bool> werr{false};
+        std::thread writer([&] {
+            cudaSetDevice(device);
+            for (int j = 0; j < steps; ++j) {
+                while (posted.load(std::memory_order_acquire) < j) std::this_thread::yield();
+                if (cudaEventSynchronize(ev_d2h[j & 1]) != cudaSuccess) werr = true;
+                std::memcpy(frames + (size_t)j * n3, sim_hout + (j & 1) * n3, sizeof(double) * n3);
+                copied.store(j, std::memory_order_release);
+            }
+        });
+        int rc_loop = VKPD_OK;
+        const bool up = up_f || up_p;
+        // inputs of frame j: host staging slot j & 1 -> device slot j & 1 on in_stream
+        auto upload = [&](int j) -> bool {
+            const int sl = j & 1;
+            if (j >= 2 && cudaEventSynchronize(ev_h2d[sl]) != cudaSuccess) return false;   // host slot free
+            double* hin = sim_hin + sl * slot_in;
+            if (up_f) std::memcpy(hin, forces + (size_t)j * n3, sizeof(double) * n3);
+            if (up_p) std::memcpy(hin + n3, pin_path + (size_t)j * p3, sizeof(double) * p3);
+            if (j >= 2) cudaStreamWaitEvent(in_stream, ev_scat[sl], 0);             // device slot consumed
+            cudaMemcpyAsync(sim_din.p + sl * slot_in, hin, sizeof(double) * slot_in, cudaMemcpyHostToDevice,
+                            in_stream);
+            cudaEventRecord(ev_h2d[sl], in_stream);
+            return true;
+        };
+        if (up) {
+            if (!upload(0)) rc_loop = VKPD_ECUDA;
+            cudaStreamWaitEvent(stream, ev_h2d[0], 0);
+            k_sim_between<T><<<cdiv(std::max(n, nP), 256), 256, 0, stream>>>(
+                n, nP, x.p, int_of_orig.p, nullptr, fail_iter.p, nullptr, up_f ? sim_din.p : nullptr, f.p,
+                up_p ? sim_din.p + n3 : nullptr, pin_tgt.p);
+            cudaEventRecord(ev_scat[0], stream);
+        }
+        for (int i = 0; i < steps && rc_loop == VKPD_OK; ++i) {
+            const int sl = i & 1, nx = (i + 1) & 1;
+            const bool next = up && i + 1 < steps;
+            if (next && !upload(i + 1)) { rc_loop = VKPD_ECUDA; break; }          // overlaps frame i
+            if ((rc_loop = step_async(iterations, damping)) != VKPD_OK) break;
+            if (i >= 2) cudaStreamWaitEvent(stream, ev_d2h[sl], 0);              // device out slot free
+            if (next) cudaStreamWaitEvent(stream, ev_h2d[nx], 0);
+            k_sim_between<T><<<cdiv(std::max(n, nP), 256), 256, 0, stream>>>(
+                n, nP, x.p, int_of_orig.p, sim_dout.p + sl * n3, fail_iter.p, fail_hist.p + i,
+                (next && up_f) ? sim_din.p + nx * slot_in : nullptr, f.p,
+                (next && up_p) ? sim_din.p + nx * slot_in + n3 : nullptr, pin_tgt.p);
+            cudaEventRecord(ev_out[sl], stream);
+            if (next) cudaEventRecord(ev_scat[nx], stream);
+            cudaStreamWaitEvent(copy_stream, ev_out[sl], 0);
+            // the pinned slot is reused by frame i: the writer must have copied frame i - 2 out
+            while (copied.load(std::memory_order_acquire) < i - 2) std::this_thread::yield();
+            cudaMemcpyAsync(sim_hout + sl * n3, sim_dout.p + sl * n3, sizeof(double) * n3, cudaMemcpyDeviceToHost,
+                            copy_stream);
+            cudaEventRecord(ev_d2h[sl], copy_stream);
+            posted.store(i, std::memory_order_release);
+            if (cudaPeekAtLastError() != cudaSuccess) { rc_loop = VKPD_ECUDA; break; }
+        }
+        if (rc_loop != VKPD_OK) posted.store(steps, std::memory_order_release);   // let the writer drain
+        // (on an early exit the writer may copy stale staging: frames are undefined after an error)
+        writer.join();
+        if (rc_loop != VKPD_OK) return rc_loop == VKPD_ECUDA ? fail(VKPD_ECUDA, cudaGetErrorString(cudaGetLastError()))
+                                                            : rc_loop;
+        if (werr) return fail(VKPD_ECUDA, "device-to-host copy failed");
+        std::vector<int> fh(steps);
+        CK(cudaMemcpyAsync(fh.data(), fail_hist.p, sizeof(int) * steps, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        *h_fail = 0x7fffffff;
+        for (int i = 0; i < steps; ++i)
+            if (fh[i] != 0x7fffffff) {
+                if (failed_frame) *failed_frame = i;
+                if (failed_iter) *failed_iter = fh[i];
+                char buf[128];
+                snprintf(buf, sizeof buf, "projective step produced non-finite positions at iteration %d", fh[i]);
+                return fail(VKPD_ENONFINITE, buf);
+            }
+        return VKPD_OK;
+    }
+
     int sync(int* failed) override {
         CK(cudaStreamSynchronize(stream));
         const int fi = *h_fail;
@@ -1889,6 +2047,11 @@ int vkpd_set_colliders(vkpd_ctx* ctx, int n, const int* kinds, const double* par
     CTX_CALL(set_colliders(n, kinds, params, contact_stiffness));
 }
 int vkpd_step_async(vkpd_ctx* ctx, int iterations, double damping) { CTX_CALL(step_async(iterations, damping)); }
+int vkpd_simulate(vkpd_ctx* ctx, int steps, int iterations, double damping, const double* forces, int forces_per_step,
+                  const double* pin_path, double* frames, int* failed_frame, int* failed_iter) {
+    CTX_CALL(simulate(steps, iterations, damping, forces, forces_per_step, pin_path, frames, failed_frame,
+                      failed_iter));
+}
 int vkpd_sync(vkpd_ctx* ctx, int* failed_iter) { CTX_CALL(sync(failed_iter)); }
 int vkpd_step(vkpd_ctx* ctx, int iterations, double damping, int* failed_iter) {
     if (!ctx) return fail(VKPD_EINVAL, "null context");

@@ -604,6 +604,16 @@ def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=Non
     const_forces = forces is not None and forces.strides[0] == 0      # broadcast (nV,3) input
     ctx.set_forces(None if forces is None else forces[0])
     ctx.set_colliders(state.colliders)
+    if polish_tol is None or state.colliders:
+        # the whole frame loop in one library call: per-step inputs up and positions down on a
+        # copy stream, overlapped with the next frame's compute (vkpd_simulate)
+        try:
+            return ctx.simulate(steps, iterations, damping,
+                                forces=None if forces is None else (forces[0] if const_forces else forces),
+                                forces_per_step=forces is not None and not const_forces,
+                                pin_path=pin_path, out=frames)
+        except _abi.NonFiniteError as exc:
+            raise RuntimeError(str(exc)) from None
     for i in range(steps):
         if pin_path is not None:
             ctx.set_pin_targets(pin_path[i])

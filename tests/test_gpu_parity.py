@@ -204,6 +204,39 @@ def test_device_step_non_finite_abort_keeps_state(c1):
     assert np.all(np.isfinite(st.x))
 
 
+def test_simulate_pipelined_equals_frame_loop():
+    """simulate_mesh runs its frame loop in one library call (vkpd_simulate: inputs up and
+    positions down on a copy stream, overlapping the next frame); same bits as stepping frame by
+    frame with per-step forces and a pin path."""
+    sc = scenes.make_scene("C2")
+    m = sc.mesh
+    steps = 24
+    rng = np.random.default_rng(4)
+    fseq = np.stack([sc.forces * (1.0 + 0.05 * rng.normal()) for _ in range(steps)])
+    path = np.stack([sc.pin_targets + np.array([0.0, 0.0, 2e-4 * k]) for k in range(steps)])
+    fr = pdsolver.simulate_mesh(m, sc.gammas, steps, sc.dt, forces=fseq, pins=sc.pins, pin_targets=path)
+    from paper_2405_12484_b200 import _abi
+    ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s, sc.gammas.gamma_v,
+                       sc.pins, sc.dt, precision="fp32", tol=pdsolver.DEFAULT_TOL["fp32"])
+    ctx.set_state(m.nodes)
+    for k in range(steps):
+        ctx.set_pin_targets(path[k])
+        ctx.set_forces(fseq[k])
+        ctx.step(sc.iterations)
+        assert np.array_equal(ctx.get_state()[0], fr[k]), k
+
+
+def test_simulate_pipelined_non_finite_reports_iteration(c1):
+    f = np.broadcast_to(c1.forces, (4,) + c1.forces.shape).copy()
+    f[2, int(np.setdiff1d(np.arange(c1.n_nodes), c1.pins)[-1]), 1] = np.nan      # step 2 goes bad
+    with pytest.raises(RuntimeError, match="iteration 0"):
+        pdsolver.simulate_mesh(c1.mesh, c1.gammas, 4, c1.dt, forces=f, pins=c1.pins, pin_targets=c1.pin_targets,
+                               iterations=5)
+    fr = pdsolver.simulate_mesh(c1.mesh, c1.gammas, 2, c1.dt, forces=c1.forces, pins=c1.pins,
+                                pin_targets=c1.pin_targets, iterations=5)     # the cached context recovers
+    assert np.all(np.isfinite(fr))
+
+
 def test_objective_monotone_with_device_solver(c1):
     mesh, gam, dt = c1.mesh, c1.gammas, 1e-3
     pins = c1.pins
