@@ -362,7 +362,7 @@ def run_ours(args):
     sol_ms = sum(pst["global_ms"][:n_exec])
     sol_achieved = sol_bytes / (sol_ms * 1e-3) / 1e9 if sol_ms > 0 else None
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:          # rank 0 at N = 1 only
         cpu = cpu_baseline(sc, args.cpu_sample_iters)
     line = {
         "metric": "tet-iters/s (PD local+global), 390K-tet sweater",

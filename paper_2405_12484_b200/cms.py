@@ -134,7 +134,9 @@ class CmsSubspace:
 
     def _context(self):
         if self._ctx is None:
-            self._ctx = _abi.MatrixContext(self._K, np.empty(0, dtype=np.int64), precision="fp64")
+            from .pdsolver import current_device
+            self._ctx = _abi.MatrixContext(self._K, np.empty(0, dtype=np.int64), precision="fp64",
+                                           device=current_device())
             self._ctx.cms_set_blocks(basis_blocks(self))
         return self._ctx
 
@@ -222,7 +224,8 @@ def a_jacobi_refine(K, b, x0, sweeps=30, aggregation=2, omega=JACOBI_OMEGA, cheb
     K = sp.csr_matrix(K)
     if np.any(K.diagonal() <= 0.0):
         raise ValueError("matrix diagonal must be positive")
-    ctx = _abi.MatrixContext(K, np.empty(0, dtype=np.int64), precision=precision)
+    from .pdsolver import current_device
+    ctx = _abi.MatrixContext(K, np.empty(0, dtype=np.int64), precision=precision, device=current_device())
     if chebyshev and rho is None:
         rho = _power_rho(ctx, K.shape[0], omega)
     X, hist, div = ctx.a_jacobi_refine(b, x0, sweeps, aggregation, omega, chebyshev,

@@ -88,11 +88,22 @@ def _ident(arrs):
     return tuple((id(a), a.__array_interface__["data"][0], a.shape) for a in map(np.asarray, arrs))
 
 
+def current_device():
+    """CUDA ordinal for new device contexts: torch's current device when torch has initialised CUDA
+    (one process per GPU: `torch.cuda.set_device(local_rank)`), else $VKPD_DEVICE, else 0."""
+    import os
+    import sys
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_initialized():
+        return int(torch.cuda.current_device())
+    return int(os.environ.get("VKPD_DEVICE", "0"))
+
+
 def _key(mesh, gammas, dt, pins, precision, tol, max_iters):
     """Cache key of the mesh part of a device scene (the material is refreshed in place)."""
     ident = _ident((mesh.tets, mesh.shape_grad, mesh.volume, mesh.node_mass))
     pins = np.asarray(pins, dtype=np.int64)
-    return (ident, float(dt), pins.tobytes(), precision, tol, max_iters)
+    return (ident, float(dt), pins.tobytes(), precision, tol, max_iters, current_device())
 
 
 def invalidate_cache():
@@ -117,7 +128,7 @@ def device_context(mesh, gammas, dt, pins=(), precision="fp32", tol=None, max_it
         ctx = _abi.Context(mesh.n_nodes if hasattr(mesh, "n_nodes") else len(mesh.nodes), mesh.tets,
                            mesh.shape_grad, mesh.volume, mesh.node_mass, gammas.gamma_s,
                            gammas.gamma_v, pins, dt, precision=precision, tol=tol,
-                           max_iters=max_iters)
+                           max_iters=max_iters, device=k[-1])
         _CACHE[k] = [gid, ctx]
         return ctx
     if hit[0] != gid:
@@ -199,7 +210,7 @@ def hess_context(mesh, gammas, dt=1.0, pins=()):
     """Device float64 second-order context for (mesh, pins, dt); gammas refreshed in place."""
     m = mesh if getattr(mesh, "node_mass", None) is not None else _MassShim(mesh)
     k = (_ident((m.tets, m.shape_grad, m.volume, m.node_mass)), float(dt),
-         np.asarray(pins, dtype=np.int64).tobytes())
+         np.asarray(pins, dtype=np.int64).tobytes(), current_device())
     gid = _ident((gammas.gamma_s, gammas.gamma_v))
     hit = _HCACHE.get(k)
     if hit is None:
@@ -208,7 +219,7 @@ def hess_context(mesh, gammas, dt=1.0, pins=()):
         if dt <= 0.0:
             raise ValueError("dt must be positive")
         h = _abi.HessContext(m.n_nodes if hasattr(m, "n_nodes") else len(m.nodes), m.tets, m.shape_grad,
-                             m.volume, m.node_mass, gammas.gamma_s, gammas.gamma_v, pins, dt)
+                             m.volume, m.node_mass, gammas.gamma_s, gammas.gamma_v, pins, dt, device=k[-1])
         _HCACHE[k] = [gid, h]
         return h
     if hit[0] != gid:
@@ -287,7 +298,8 @@ class GlobalSolver:
         expect_free = np.setdiff1d(np.arange(n), self.pins)
         if len(expect_free) != len(self.free) or np.any(np.sort(self.free) != expect_free):
             raise ValueError("free must be the complement of pins")
-        self._ctx = _abi.MatrixContext(K, self.pins, precision=precision, tol=tol, max_iters=max_iters)
+        self._ctx = _abi.MatrixContext(K, self.pins, precision=precision, tol=tol, max_iters=max_iters,
+                                       device=current_device())
         if mode == "cms":
             from .cms import CmsGlobalSolver
             self._cms = CmsGlobalSolver(self._ctx, K, self.free, self.pins, cms, refine_sweeps,
