@@ -493,25 +493,32 @@ __global__ void k_cms_y(CmsBlocks c, int m, const vec4_t<T>* __restrict__ b, con
     y[3 * (size_t)g] = s0; y[3 * (size_t)g + 1] = s1; y[3 * (size_t)g + 2] = s2;
 }
 
-// grid: (row chunks, domains); dynamic smem = 3 * max columns per domain doubles
+// grid: (row chunks, domains, column groups); dynamic smem = 3 * (max columns per group) doubles.
+// Group g covers columns [g ncol / G, (g + 1) ncol / G) of its domain and writes a partial row sum
+// to part[g * total_rows + row]; k_cms_tz_sum adds the G partials in group order (deterministic).
+// Splitting the columns gives G times the CTAs (a domain has only ~13K rows) for the same bytes.
+constexpr int kCmsTzGroups = 4;
 template <typename T>
-__global__ void __launch_bounds__(256) k_cms_tz(CmsBlocks c, const double* __restrict__ z, vec4_t<T>* __restrict__ x) {
+__global__ void __launch_bounds__(256) k_cms_tz(CmsBlocks c, const double* __restrict__ z, double* __restrict__ part,
+                                                int total_rows) {
     extern __shared__ double zs[];
-    const int d = blockIdx.y;
+    const int d = blockIdx.y, gi = blockIdx.z, G = gridDim.z;
     const int r0 = c.row_ptr[d], nd = c.row_ptr[d + 1] - r0;
     const int q0 = c.col_ptr[d], ncol = c.col_ptr[d + 1] - q0;
-    for (int k = threadIdx.x; k < ncol; k += blockDim.x) {
-        const int g = c.colmap[q0 + k];
+    const int c0 = (int)((long long)gi * ncol / G), c1 = (int)((long long)(gi + 1) * ncol / G);
+    const int nc = c1 - c0;
+    for (int k = threadIdx.x; k < nc; k += blockDim.x) {
+        const int g = c.colmap[q0 + c0 + k];
         zs[3 * k] = z[3 * (size_t)g]; zs[3 * k + 1] = z[3 * (size_t)g + 1]; zs[3 * k + 2] = z[3 * (size_t)g + 2];
     }
     __syncthreads();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nd) return;
-    const double* A = c.A + c.a_off[d] + r;
+    const double* A = c.A + c.a_off[d] + (size_t)c0 * nd + r;
     // two interleaved accumulator sets and 8 loads in flight per thread (HBM latency)
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, u0 = 0.0, u1 = 0.0, u2 = 0.0;
     int k = 0;
-    for (; k + 8 <= ncol; k += 8) {
+    for (; k + 8 <= nc; k += 8) {
         double av[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) av[q] = __ldg(&A[(size_t)(k + q) * nd]);
@@ -522,11 +529,25 @@ __global__ void __launch_bounds__(256) k_cms_tz(CmsBlocks c, const double* __res
             u2 += av[q + 1] * zs[3 * (k + q + 1) + 2];
         }
     }
-    for (; k < ncol; ++k) {
+    for (; k < nc; ++k) {
         const double a = __ldg(&A[(size_t)k * nd]);
         s0 += a * zs[3 * k]; s1 += a * zs[3 * k + 1]; s2 += a * zs[3 * k + 2];
     }
-    x[c.rows[r0 + r]] = make4<T>((T)(s0 + u0), (T)(s1 + u1), (T)(s2 + u2), T(0));
+    double* o = part + 3 * ((size_t)gi * total_rows + r0 + r);
+    o[0] = s0 + u0; o[1] = s1 + u1; o[2] = s2 + u2;
+}
+
+template <typename T>
+__global__ void k_cms_tz_sum(CmsBlocks c, int total_rows, int G, const double* __restrict__ part,
+                             vec4_t<T>* __restrict__ x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total_rows) return;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int g = 0; g < G; ++g) {
+        const double* o = part + 3 * ((size_t)g * total_rows + i);
+        s0 += o[0]; s1 += o[1]; s2 += o[2];
+    }
+    x[c.rows[i]] = make4<T>((T)s0, (T)s1, (T)s2, T(0));
 }
 
 // z = K_red^-1 y for the symmetric K_red^-1: one warp per row (row i = column i, contiguous),

@@ -1516,7 +1516,8 @@ struct Ctx : CtxBase {
     int cms_m = 0;
     // blocked basis (cms.cuh CmsBlocks)
     bool cms_blocked = false;
-    DBuf<double> cmsA, cms_yd;
+    DBuf<double> cmsA, cms_yd, cms_part;
+    int cms_total_rows = 0;
     DBuf<long long> cms_aoff;
     DBuf<int> cms_rowp, cms_rows, cms_colp, cms_colmap, cms_tdom, cms_tc0, cms_bnd, cms_ysp, cms_ys;
     vk::CmsBlocks cmsb{};
@@ -1704,11 +1705,13 @@ struct Ctx : CtxBase {
         cmsb.A = cmsA.p; cmsb.a_off = cms_aoff.p; cmsb.row_ptr = cms_rowp.p; cmsb.rows = cms_rows.p;
         cmsb.col_ptr = cms_colp.p; cmsb.colmap = cms_colmap.p; cmsb.tile_dom = cms_tdom.p; cmsb.tile_c0 = cms_tc0.p;
         cmsb.bnd = cms_bnd.p; cmsb.ysrc_ptr = cms_ysp.p; cmsb.ysrc = cms_ys.p;
-        const size_t smem = sizeof(double) * 3 * std::max(1, cms_max_cols);
+        const size_t smem = sizeof(double) * 3 * std::max(1, cdiv(cms_max_cols, vk::kCmsTzGroups) + 1);
         if (smem > 48 * 1024) {
             if (smem > 200 * 1024) return fail(VKPD_EINVAL, "too many basis columns in one domain");
             CK(cudaFuncSetAttribute(vk::k_cms_tz<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         }
+        CK(cms_part.alloc((size_t)3 * vk::kCmsTzGroups * std::max(1, rp[ndom])));
+        cms_total_rows = rp[ndom];
         cms_m = m;
         cms_blocked = true;
         return VKPD_OK;
@@ -1730,9 +1733,11 @@ struct Ctx : CtxBase {
             vk::k_symv3_warp<<<cdiv((size_t)cms_m * 32, 256), 256, 0, stream>>>(cms_m, cmsKinv.p, cms_y.p, cms_z.p);
             CK(cudaMemsetAsync(dx.p, 0, sizeof(V4) * nF, stream));
             if (cmsb.ndom > 0 && cms_max_rows > 0) {
-                const dim3 grid(cdiv(cms_max_rows, 256), cmsb.ndom);
-                vk::k_cms_tz<T><<<grid, 256, sizeof(double) * 3 * std::max(1, cms_max_cols), stream>>>(cmsb, cms_z.p,
-                                                                                                     dx.p);
+                const dim3 grid(cdiv(cms_max_rows, 256), cmsb.ndom, vk::kCmsTzGroups);
+                const size_t zsm = sizeof(double) * 3 * std::max(1, cdiv(cms_max_cols, vk::kCmsTzGroups) + 1);
+                vk::k_cms_tz<T><<<grid, 256, zsm, stream>>>(cmsb, cms_z.p, cms_part.p, cms_total_rows);
+                vk::k_cms_tz_sum<T><<<cdiv(cms_total_rows, 256), 256, 0, stream>>>(cmsb, cms_total_rows,
+                                                                                   vk::kCmsTzGroups, cms_part.p, dx.p);
             }
             if (cmsb.nb > 0) vk::k_cms_xb<T><<<cdiv(cmsb.nb, 256), 256, 0, stream>>>(cmsb, cms_z.p, dx.p);
         } else {
