@@ -600,6 +600,8 @@ def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=Non
         if forces.ndim == 2:
             forces = np.broadcast_to(forces, (steps,) + forces.shape)
     frames = np.empty((steps, mesh.n_nodes, 3))
+    if steps == 0:                      # the reference's loop body never runs (pdsolver.py:749)
+        return frames
     if state.colliders:
         # the reference drops the prefactored solver when colliders exist (pdsolver.py:753)
         _validate_colliders(state.colliders)
