@@ -304,7 +304,10 @@ struct Ctx : CtxBase {
         if (sim_hin) cudaFreeHost(sim_hin);
         if (sim_hout) cudaFreeHost(sim_hout);
         for (int k = 0; k < 2; ++k)
-            for (cudaEvent_t e : {ev_h2d[k], ev_scat[k], ev_out[k], ev_d2h[k]})
+            for (cudaEvent_t e : {ev_h2d[k], ev_scat[k]})
+                if (e) cudaEventDestroy(e);
+        for (int k = 0; k < kOutSlots; ++k)
+            for (cudaEvent_t e : {ev_out[k], ev_d2h[k]})
                 if (e) cudaEventDestroy(e);
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (in_stream) cudaStreamDestroy(in_stream);
@@ -1245,8 +1248,12 @@ struct Ctx : CtxBase {
     double* sim_hin = nullptr;
     double* sim_hout = nullptr;
     size_t sim_cap = 0;
-    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_scat[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr},
-                ev_d2h[2] = {nullptr, nullptr};
+    // positions out: up to kOutSlots staging slots (<= 64 MB), so the host writer can fall a few
+    // frames behind (fold frames are ~2x a steady frame) without stalling the enqueue loop
+    static constexpr int kOutSlots = 8;
+    int out_slots = 2;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_scat[2] = {nullptr, nullptr}, ev_out[kOutSlots] = {},
+                ev_d2h[kOutSlots] = {};
     DBuf<int> fail_hist;
     int simulate(int steps, int iterations, double damping, const double* forces, int forces_per_step,
                  const double* pin_path, double* frames, int* failed_frame, int* failed_iter) override {
@@ -1263,6 +1270,8 @@ struct Ctx : CtxBase {
             for (int k = 0; k < 2; ++k) {
                 CK(cudaEventCreateWithFlags(&ev_h2d[k], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&ev_scat[k], cudaEventDisableTiming));
+            }
+            for (int k = 0; k < kOutSlots; ++k) {
                 CK(cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&ev_d2h[k], cudaEventDisableTiming));
             }
@@ -1271,10 +1280,11 @@ struct Ctx : CtxBase {
             if (sim_hin) cudaFreeHost(sim_hin);
             if (sim_hout) cudaFreeHost(sim_hout);
             sim_hin = sim_hout = nullptr;
+            out_slots = (int)std::max<size_t>(2, std::min<size_t>(kOutSlots, (size_t(64) << 20) / (sizeof(double) * n3)));
             CK(cudaHostAlloc(&sim_hin, sizeof(double) * 2 * slot_in, cudaHostAllocDefault));
-            CK(cudaHostAlloc(&sim_hout, sizeof(double) * 2 * n3, cudaHostAllocDefault));
+            CK(cudaHostAlloc(&sim_hout, sizeof(double) * out_slots * n3, cudaHostAllocDefault));
             CK(sim_din.alloc(2 * slot_in));
-            CK(sim_dout.alloc(2 * n3));
+            CK(sim_dout.alloc((size_t)out_slots * n3));
             sim_cap = slot_in;
         }
         if (fail_hist.n < (size_t)steps) CK(fail_hist.alloc(steps));
@@ -1290,8 +1300,9 @@ struct Ctx : CtxBase {
             cudaSetDevice(device);
             for (int j = 0; j < steps; ++j) {
                 while (posted.load(std::memory_order_acquire) < j) std::this_thread::yield();
-                if (cudaEventSynchronize(ev_d2h[j & 1]) != cudaSuccess) werr = true;
-                std::memcpy(frames + (size_t)j * n3, sim_hout + (j & 1) * n3, sizeof(double) * n3);
+                const int so = j % out_slots;
+                if (cudaEventSynchronize(ev_d2h[so]) != cudaSuccess) werr = true;
+                std::memcpy(frames + (size_t)j * n3, sim_hout + so * n3, sizeof(double) * n3);
                 copied.store(j, std::memory_order_release);
             }
         });
@@ -1319,11 +1330,11 @@ struct Ctx : CtxBase {
             cudaEventRecord(ev_scat[0], stream);
         }
         for (int i = 0; i < steps && rc_loop == VKPD_OK; ++i) {
-            const int sl = i & 1, nx = (i + 1) & 1;
+            const int sl = i % out_slots, nx = (i + 1) & 1;
             const bool next = up && i + 1 < steps;
             if (next && !upload(i + 1)) { rc_loop = VKPD_ECUDA; break; }          // overlaps frame i
             if ((rc_loop = step_async(iterations, damping)) != VKPD_OK) break;
-            if (i >= 2) cudaStreamWaitEvent(stream, ev_d2h[sl], 0);              // device out slot free
+            if (i >= out_slots) cudaStreamWaitEvent(stream, ev_d2h[sl], 0);      // device out slot free
             if (next) cudaStreamWaitEvent(stream, ev_h2d[nx], 0);
             k_sim_between<T><<<cdiv(std::max(n, nP), 256), 256, 0, stream>>>(
                 n, nP, x.p, int_of_orig.p, sim_dout.p + sl * n3, fail_iter.p, fail_hist.p + i,
@@ -1332,8 +1343,8 @@ struct Ctx : CtxBase {
             cudaEventRecord(ev_out[sl], stream);
             if (next) cudaEventRecord(ev_scat[nx], stream);
             cudaStreamWaitEvent(copy_stream, ev_out[sl], 0);
-            // the pinned slot is reused by frame i: the writer must have copied frame i - 2 out
-            while (copied.load(std::memory_order_acquire) < i - 2) std::this_thread::yield();
+            // the pinned slot is reused by frame i: the writer must have copied frame i - out_slots out
+            while (copied.load(std::memory_order_acquire) < i - out_slots) std::this_thread::yield();
             cudaMemcpyAsync(sim_hout + sl * n3, sim_dout.p + sl * n3, sizeof(double) * n3, cudaMemcpyDeviceToHost,
                             copy_stream);
             cudaEventRecord(ev_d2h[sl], copy_stream);
