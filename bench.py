@@ -2,16 +2,19 @@
 """Benchmark: one projective-dynamics frame (30 local/global PD iterations) of the
 390K-tet synthetic sweater (BASELINE.json configs[2], "C3"), dt = 1/150 s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--precision fp64|fp32]
 
-A "step" is one frame.  value = whole-job tet-iters/s = N * nE * iterations * K /
-(max over ranks of the device time of the K frames).  Under torchrun (N > 1)
-every rank simulates its own copy of the scene (weak scaling, no data-path
-collective; the domain-decomposed multi-GPU step is tracked in DESIGN.md).
+A "step" is one frame.  The headline runs in float64, the reference's precision
+(pdsolver.py:192-194): value = whole-job tet-iterations per second counting the PD
+rounds actually executed (all 30 in fp64) = N * nE * rounds / (max over ranks of the
+device time of the K frames); ms_per_step is ms/frame.  The float32 build's numbers
+are reported beside it under "fp32".  Under torchrun (N > 1) every rank simulates its
+own copy of the scene (weak scaling, no data-path collective; the domain-decomposed
+single-garment step is tracked in DESIGN.md).
 
-`--impl reference` times the CPU oracle (numpy/scipy restatement of the
-reference `pd_step`, direct SuperLU solve) on the host cores, one PD iteration
-of the same scene per step (a bounded sample).
+`--impl reference` times the CPU oracle (numpy/scipy restatement of the reference
+`pd_step`, direct SuperLU solve) on the host cores, a bounded sample of the same
+scene per step.
 """
 
 from __future__ import annotations
@@ -19,6 +22,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -29,25 +33,26 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-ALG_BYTES_LOCAL = {"fp32": 70.0, "fp64": 125.0}   # SURVEY.md 8d, per tet-iteration
+# SURVEY.md 8d algorithmic bytes: local step per tet-iteration; global step per node and
+# stencil pass (15 stencil values + D^-1 + the iterate read and the correction read/write)
+ALG_BYTES_LOCAL = {"fp32": 70.0, "fp64": 125.0}
+ALG_BYTES_SWEEP = {"fp32": 100.0, "fp64": 200.0}
+METRIC = "tet-iters/s (PD local+global, executed rounds), 390K-tet sweater"
 
 
-def solver_alg_bytes(precision, n_tets, n_free, ell_w, cg_iters):
-    """Algorithmic bytes of one global-step launch (each array touched once per phase).
-
-    vb = value bytes; vectors are 4-wide (x, y, z, pad); ELL = (int col + value) * width.
-      init (PD residual): corners 4 * n_tets vectors, per row m/dt^2, xhat, x, writes r, dx, p
-      init 2 (only if iterating): ELL of K D^-1, r, writes h, z
-      CG iteration: phase A  ELL, z, p_old, writes p_new, q
-                    phase B  ELL (K D^-1), q, p, dx r/w, r r/w, h r/w, write z, 1/diag
-    """
-    vb = 4 if precision == "fp32" else 8
-    vec = 4 * vb
-    ell = ell_w * (4 + vb)
-    init = 4 * n_tets * vec + n_free * (vb + 2 * vec + 3 * vec)
-    init2 = n_free * (ell + vec + 2 * vec)
-    it = n_free * ((ell + 2 * vec + 2 * vec) + (ell + 2 * vec + 6 * vec + vec + vb))
-    return init + (init2 if cg_iters > 0 else 0) + cg_iters * it
+def host_info():
+    """CPU model, core count and BLAS threads of this host."""
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_cores": os.cpu_count(),
+            "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS", "unset (numpy default)")}
 
 
 def parse():
@@ -57,7 +62,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
-    p.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    p.add_argument("--precision", default="fp64", choices=["fp32", "fp64"])
+    p.add_argument("--no-fp32", action="store_true", help="skip the float32 side line")
     p.add_argument("--iterations", type=int, default=30)
     p.add_argument("--tol", type=float, default=None)
     p.add_argument("--no-flush", action="store_true")
@@ -142,12 +148,14 @@ def cpu_baseline(sc, sample_iters):
     orc.pd_step(m.nodes.copy(), np.zeros_like(m.nodes), sc.dt, m.tets, m.shape_grad, m.volume, gs, gv,
                 m.node_mass, solver, sc.pins, sc.pin_targets, sc.forces, sample_iters)
     el = time.perf_counter() - t0
+    hi = host_info()
     return {"value": m.n_elements * sample_iters / el, "unit": "tet-iters/s", "cores": 1,
             "kind": "port",
             "sample": f"{sample_iters} PD iterations of one {sc.name} frame (direct SuperLU global "
-                      f"solve, factorization excluded), {el:.1f} s on {os.cpu_count()} host cores "
-                      f"(numpy/scipy, effectively 1 core)",
-            "ms_per_frame_extrapolated": el / sample_iters * 30 * 1e3}
+                      f"solve, factorization excluded), {el:.1f} s; {hi['host_cores']} host cores "
+                      f"({hi['cpu_model']}), 1 used (numpy/scipy, OPENBLAS_NUM_THREADS="
+                      f"{hi['openblas_threads']})",
+            "ms_per_frame_extrapolated": el / sample_iters * 30 * 1e3, **hi}
 
 
 def run_reference(args):
@@ -209,7 +217,7 @@ def run_reference(args):
     tot = time.perf_counter() - t0
     val = tets_done / tot
     line = {
-        "impl": "reference", "metric": "tet-iters/s (PD local+global), 390K-tet sweater",
+        "impl": "reference", "metric": METRIC,
         "value": val, "unit": "tet-iters/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
         "ms_per_frame_equiv": nE * 30 / val * 1e3,
@@ -221,10 +229,97 @@ def run_reference(args):
                                    f"(+ the direct global solve each time a full iteration completes); "
                                    f"{args.steps} steps = {tets_done} tet-iterations, "
                                    f"{state['pd_iters']} global solves; CPU oracle port, "
-                                   f"{_os.cpu_count()} host cores available, 1 used"},
+                                   f"{_os.cpu_count()} host cores available, 1 used", **host_info()},
         "e2e": {"value": val, "unit": "tet-iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def make_ctx(sc, precision, device, tol=None, **cfg):
+    from paper_2405_12484_b200 import _abi, pdsolver
+    m = sc.mesh
+    return _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s,
+                        sc.gammas.gamma_v, sc.pins, sc.dt, precision=precision,
+                        tol=tol if tol else pdsolver.DEFAULT_TOL[precision], device=device, nodes=m.nodes, **cfg)
+
+
+def measure(args, sc, precision, local, stream, barrier, world, flush, with_e2e=True, with_clocks=True, **cfg):
+    """Device-timed frames, end-to-end frames through simulate_mesh, per-launch split."""
+    import torch
+    from paper_2405_12484_b200 import pdsolver
+    m = sc.mesh
+    its = args.iterations
+    ctx = make_ctx(sc, precision, local, args.tol, **cfg)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_state(m.nodes)
+    ctx.set_pin_targets(sc.pin_targets)
+    ctx.set_forces(sc.forces)
+    for _ in range(args.warmup):
+        ctx.step_async(its)
+    ctx.sync()
+    st0 = ctx.stats()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clk = ClockSampler(local) if with_clocks else None
+    barrier()
+    if clk:
+        clk.start()
+        time.sleep(0.3)
+    for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()                # > L2: every frame starts cold
+        starts[k].record(stream)
+        ctx.step_async(its)
+        ends[k].record(stream)
+    ctx.sync()
+    barrier()
+    clocks = clk.stop() if clk else None
+    tot_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    st = ctx.stats()
+    rounds = st["pd_rounds_total"] - st0["pd_rounds_total"]
+    out = {"ctx": ctx, "tot_ms": tot_ms, "rounds": rounds, "clocks": clocks, "stats": st}
+    if with_e2e:
+        # end to end through the public API: simulate_mesh with a per-step force sequence and pin
+        # path (host arrays); every step's inputs go host->device and its positions device->host
+        # inside the timed region (the library pipelines them on copy streams)
+        fseq = np.broadcast_to(sc.forces, (args.steps,) + sc.forces.shape).copy()
+        path = np.broadcast_to(sc.pin_targets, (args.steps,) + sc.pin_targets.shape).copy()
+        kw = dict(pins=sc.pins, iterations=its, precision=precision, tol=args.tol if args.tol else None)
+        pdsolver.simulate_mesh(m, sc.gammas, 2, sc.dt, forces=fseq[:2], pin_targets=path[:2], **kw)
+        barrier()
+        t0 = time.perf_counter()
+        frames = pdsolver.simulate_mesh(m, sc.gammas, args.steps, sc.dt, forces=fseq, pin_targets=path, **kw)
+        torch.cuda.synchronize()
+        out["e2e_s"] = time.perf_counter() - t0
+        out["h2d"] = fseq[0].nbytes + path[0].nbytes
+        out["d2h"] = frames[0].nbytes
+        del frames
+    # per-launch split (events around every launch, one extra frame, outside the timed region)
+    out["local_ms"], out["global_ms"], out["prof_frame_ms"] = ctx.profile_step(its)
+    out["pst"] = ctx.stats()
+    # k_local alone: 20 launches back to back on the last state, an event pair around each
+    out["kl_ms"], out["lphase_ms"] = ctx.time_local(20)
+    return out
+
+
+def solver_roofline(precision, pst, n_free, peak, peak_kind, kernel):
+    """Global step against HBM in SURVEY 8d units: ALG_BYTES_SWEEP per free node and stencil pass;
+    a launch makes (steps + 1) passes (the residual pass plus one per Chebyshev step / CG SpMV)."""
+    n_exec = sum(1 for g in pst["global_ms"] if g > 0)
+    steps = pst["cg_iters"][:n_exec]
+    per_pass = ALG_BYTES_SWEEP[precision] * n_free
+    passes = [(c + 1) if kernel.startswith("k_cheb") else (2 * c + 1) for c in steps]
+    alg = sum(per_pass * p for p in passes)
+    ms = sum(pst["global_ms"][:n_exec])
+    ach = alg / (ms * 1e-3) / 1e9 if ms > 0 else None
+    return {"bound": "hbm", "kernel": kernel, "achieved": ach, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+            "frac": (ach / peak) if ach else None, "traffic": ncu_traffic(precision, kernel),
+            "traffic_source": f"profiles/r02_launches_{precision}_summary.json (ncu dram read+write per launch)",
+            "alg_bytes_per_launch": alg / max(1, n_exec), "launch_ms": ms / max(1, n_exec),
+            "steps_per_launch": steps,
+            "alg_bytes_unit": f"{ALG_BYTES_SWEEP[precision]:.0f} B per free node per stencil pass (SURVEY 8d)",
+            "note": "the solver's working set lives on chip (registers + shared memory + L2); per step it is "
+                    "bound by shared-memory bandwidth and neighbour-flag latency, see DESIGN.md 4"}
 
 
 def run_ours(args):
@@ -234,28 +329,15 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2405_12484_b200 import _abi, pdsolver, scenes
+    from paper_2405_12484_b200 import scenes
 
     sc = scenes.make_scene(args.config)
     m = sc.mesh
-    ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s,
-                       sc.gammas.gamma_v, sc.pins, sc.dt, precision=args.precision,
-                       tol=args.tol if args.tol else pdsolver.DEFAULT_TOL[args.precision],
-                       device=local)
+    nE = m.n_elements
+    its = args.iterations
     stream = torch.cuda.Stream()          # a real (non-default) stream shared with the library
     torch.cuda.set_stream(stream)
-    ctx.set_stream(stream.cuda_stream)
-    ctx.set_state(m.nodes)
-    ctx.set_pin_targets(sc.pin_targets)
-    ctx.set_forces(sc.forces)
-    its = args.iterations
-
-    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32,
-                                                   device="cuda")
-    for _ in range(args.warmup):
-        ctx.step_async(its)
-    ctx.sync()
-    rounds0 = ctx.stats()["pd_rounds_total"]
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
         if world > 1:
@@ -263,80 +345,20 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- device-timed frames (inputs resident), L2 flushed between frames
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    clk = ClockSampler(local)
-    barrier()
-    clk.start()
-    time.sleep(0.3)
-    for k in range(args.steps):
-        if flush is not None:
-            flush.zero_()
-        starts[k].record(stream)
-        ctx.step_async(its)
-        ends[k].record(stream)
-    ctx.sync()
-    barrier()
-    clocks = clk.stop()
-    frame_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    tot_ms = sum(frame_ms)
-    st = ctx.stats()
-    rounds = st["pd_rounds_total"] - rounds0
+    head = measure(args, sc, args.precision, local, stream, barrier, world, flush)
+    side = None
+    if args.precision == "fp64" and not args.no_fp32:
+        side = measure(args, sc, "fp32", local, stream, barrier, world, flush, with_clocks=False)
+        side_all = None
+        if not args.no_all_rounds:
+            # the same frames with every PD round executed: the rounds fp32 skips are exact
+            # repeats (tests/test_gpu_parity.py::test_pd_loop_early_exit_is_exact)
+            a = measure(args, sc, "fp32", local, stream, barrier, world, flush, with_e2e=False,
+                        with_clocks=False, pd_early_exit=False)
+            side_all = a["tot_ms"] / args.steps
+            del a
 
-    # ---- the same frames with every PD round executed (no early loop exit): the rounds the
-    # default path skips are exact repeats (tests/test_gpu_parity.py::test_pd_loop_early_exit_is_exact)
-    all_rounds_ms = None
-    if not args.no_all_rounds:
-        import os as _os
-        _os.environ["VKPD_PD_EXIT"] = "0"
-        ctx2 = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s,
-                            sc.gammas.gamma_v, sc.pins, sc.dt, precision=args.precision, tol=ctx_tol(args),
-                            device=local)
-        del _os.environ["VKPD_PD_EXIT"]
-        ctx2.set_stream(stream.cuda_stream)
-        ctx2.set_state(m.nodes)
-        ctx2.set_pin_targets(sc.pin_targets)
-        ctx2.set_forces(sc.forces)
-        for _ in range(args.warmup):
-            ctx2.step_async(its)
-        ctx2.sync()
-        barrier()
-        for k in range(args.steps):
-            if flush is not None:
-                flush.zero_()
-            starts[k].record(stream)
-            ctx2.step_async(its)
-            ends[k].record(stream)
-        ctx2.sync()
-        barrier()
-        all_rounds_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
-        del ctx2
-
-    # ---- end to end through the public API: simulate_mesh with a per-step force sequence and pin
-    # path (host arrays); every step's inputs go host->device and its positions device->host
-    # inside the timed region (the library pipelines them on a copy stream)
-    fseq = np.broadcast_to(sc.forces, (args.steps,) + sc.forces.shape).copy()
-    path = np.broadcast_to(sc.pin_targets, (args.steps,) + sc.pin_targets.shape).copy()
-    frames_out = np.empty((args.steps, m.n_nodes, 3))
-    fr_w = pdsolver.simulate_mesh(m, sc.gammas, 2, sc.dt, forces=fseq[:2], pins=sc.pins, pin_targets=path[:2],
-                                  iterations=its, precision=args.precision,
-                                  tol=args.tol if args.tol else None)          # warm the API path (graph)
-    del fr_w
-    barrier()
-    t0 = time.perf_counter()
-    pdsolver.simulate_mesh(m, sc.gammas, args.steps, sc.dt, forces=fseq, pins=sc.pins, pin_targets=path,
-                           iterations=its, precision=args.precision, tol=args.tol if args.tol else None)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    h2d = fseq[0].nbytes + path[0].nbytes
-    d2h = frames_out[0].nbytes
-
-    # ---- per-kernel split (events around every launch, one extra frame, not in the timed region)
-    local_ms, global_ms, prof_frame_ms = ctx.profile_step(its)
-    # k_local alone: 20 launches enqueued back to back on the last state, an event pair around each
-    kl_ms, lphase_ms = ctx.time_local(20)
-
+    tot_ms, e2e_s = head["tot_ms"], head["e2e_s"]
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([tot_ms, e2e_s], dtype=torch.float64, device="cuda")
@@ -348,24 +370,21 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    nE = m.n_elements
-    value = world * nE * its * args.steps / (tot_ms * 1e-3)
-    e2e_val = world * nE * its * args.steps / e2e_s
+    prec = args.precision
+    rounds_per_frame = head["rounds"] / args.steps
+    value = world * nE * head["rounds"] / (tot_ms * 1e-3)
+    e2e_val = world * nE * head["rounds"] / e2e_s
     peak, peak_kind = measured_peak()
-    alg = ALG_BYTES_LOCAL[args.precision] * nE
-    achieved = alg / (kl_ms * 1e-3) / 1e9
-    # dominant kernel: the global-step solver (event-timed per launch in the profiled frame)
-    pst = ctx.stats()
-    n_exec = sum(1 for g in pst["global_ms"] if g > 0)
-    sol_bytes = sum(solver_alg_bytes(args.precision, nE, pst["n_free"], pst["ell_width"], c)
-                    for c in pst["cg_iters"][:n_exec])
-    sol_ms = sum(pst["global_ms"][:n_exec])
-    sol_achieved = sol_bytes / (sol_ms * 1e-3) / 1e9 if sol_ms > 0 else None
+    pst = head["pst"]
+    solver_kernel = "k_cheb_reg (global step, Chebyshev-Jacobi, neighbour flags)" if prec == "fp64" \
+        else "k_pcg_poly (global step, persistent polynomial-preconditioned CG)"
+    alg_local = ALG_BYTES_LOCAL[prec] * nE
+    ach_local = alg_local / (head["kl_ms"] * 1e-3) / 1e9
     cpu = None
     if not args.no_cpu_baseline and world == 1:          # rank 0 at N = 1 only
         cpu = cpu_baseline(sc, args.cpu_sample_iters)
     line = {
-        "metric": "tet-iters/s (PD local+global), 390K-tet sweater",
+        "metric": METRIC,
         "value": value,
         "unit": "tet-iters/s",
         "n_gpus": world,
@@ -375,44 +394,49 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32" if args.precision == "fp32" else "f64",
+        "dtype": "f32" if prec == "fp32" else "f64",
         "data": "synthetic",
         "config": {"workload": sc.name, "n_tets": nE, "n_nodes": m.n_nodes, "pd_iterations": its,
-                   "dt": sc.dt, "solver": "direct-equivalent (device CG to tol)",
-                   "tol": ctx_tol(args), "parallelism": f"replicas x{world}",
-                   "pd_loop": "graph WHILE node; stops at the first solve needing 0 CG iterations "
-                              "(later rounds repeat it bit for bit); value counts all 30 rounds",
-                   "l2": "flushed between frames" if flush is not None else "not flushed"},
-        "e2e": {"value": e2e_val, "unit": "tet-iters/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3 / args.steps},
+                   "dt": sc.dt, "precision": prec, "tol": ctx_tol(args, prec),
+                   "solver": ("Chebyshev semi-iteration on the Jacobi-scaled K_ff to |r| <= tol |M/dt^2 xhat| "
+                              "(direct-equivalent)") if prec == "fp64" else
+                             "polynomial-preconditioned CG to |r| <= tol |M/dt^2 xhat| (direct-equivalent)",
+                   "parallelism": f"replicas x{world}",
+                   "pd_loop": "graph WHILE node; stops at the first solve needing no work (later rounds repeat "
+                              "it bit for bit); value counts executed rounds",
+                   "l2": "flushed between frames (256 MB write)" if flush is not None else "not flushed"},
+        "e2e": {"value": e2e_val, "unit": "tet-iters/s", "h2d_bytes_per_step": head["h2d"],
+                "d2h_bytes_per_step": head["d2h"], "ms_per_step": e2e_s * 1e3 / args.steps},
         # prologue + epilogue per frame; local step, robust pass, solver per executed PD round
-        "gpu_launches": int(args.steps * 2 + 3 * rounds),
-        "pd_rounds_executed_per_frame": rounds / args.steps,
-        "ms_per_step_every_round": all_rounds_ms,
-        "roofline": {"bound": "hbm", "kernel": "k_pcg_poly (global step, persistent PCG)",
-                     "achieved": sol_achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": (sol_achieved / peak) if sol_achieved else None,
-                     "traffic": ncu_traffic(args.precision, "k_pcg_poly"),
-                     "traffic_source": "profiles/r01b_launches_steady_summary.json (ncu dram read+write per launch, cold L2)",
-                     "alg_bytes_per_launch": sol_bytes / max(1, n_exec), "launch_ms": sol_ms / max(1, n_exec),
-                     "cg_iters_per_launch": pst["cg_iters"][:n_exec],
-                     "note": "working set (~80 MB) is L2-resident; in practice bound by grid-barrier latency, "
-                             "2 barriers per CG iteration"},
-        "roofline_local": {"bound": "hbm", "kernel": "k_local (PD local step)", "achieved": achieved,
-                           "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                           "traffic": ncu_traffic(args.precision, "k_local"),
-                           "alg_bytes_per_launch": alg, "launch_ms": kl_ms,
-                           "timing": "CUDA event pair around each of 20 launches enqueued back to back on the last frame state",
-                           "local_phase_ms": lphase_ms,
-                           "note": "FP64/ALU issue-bound (SVD + float64 SL(3) Newton), not HBM"},
-        "profiled_frame": {"ms": prof_frame_ms, "local_ms_per_round": local_ms, "global_ms_per_round": global_ms,
-                           "rounds": n_exec},
-        "clocks": clocks,
-        "solver_stats": {"cg_iters_last_frame": st["cg_iters_total"], "pcg_blocks": st["pcg_blocks"],
-                         "robust_elements_cum": st["robust"]},
+        "gpu_launches": int(args.steps * 2 + 3 * head["rounds"]),
+        "pd_rounds_executed_per_frame": rounds_per_frame,
+        "ms_per_frame": tot_ms / args.steps,
+        "roofline": solver_roofline(prec, pst, pst["n_free"], peak, peak_kind, solver_kernel.split()[0]),
+        "roofline_local": {"bound": "hbm", "kernel": "k_local (PD local step)", "achieved": ach_local,
+                           "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": ach_local / peak,
+                           "traffic": ncu_traffic(prec, "k_local"),
+                           "alg_bytes_per_launch": alg_local, "launch_ms": head["kl_ms"],
+                           "alg_bytes_unit": f"{ALG_BYTES_LOCAL[prec]:.0f} B per tet-iteration (SURVEY 8d)",
+                           "timing": "CUDA event pair around each of 20 launches enqueued back to back",
+                           "local_phase_ms": head["lphase_ms"],
+                           "note": "ALU-issue-bound (SVD + float64 SL(3) Newton), not HBM"},
+        "profiled_frame": {"ms": head["prof_frame_ms"], "local_ms_per_round": head["local_ms"],
+                           "global_ms_per_round": head["global_ms"], "rounds": len(pst["global_ms"])},
+        "clocks": head["clocks"],
+        "solver_stats": {"steps_last_frame": head["stats"]["cg_iters_total"], "solver_ctas": pst["pcg_blocks"],
+                         "robust_elements_cum": head["stats"]["robust"]},
         "paper_ms_per_frame": 604.0,
         "cpu_baseline": cpu,
     }
+    if side is not None:
+        line["fp32"] = {"ms_per_frame": side["tot_ms"] / args.steps,
+                        "tet_iters_per_s": world * nE * side["rounds"] / (side["tot_ms"] * 1e-3),
+                        "pd_rounds_executed_per_frame": side["rounds"] / args.steps,
+                        "ms_per_frame_every_round": side_all,
+                        "e2e_ms_per_frame": side["e2e_s"] * 1e3 / args.steps,
+                        "roofline": solver_roofline("fp32", side["pst"], side["pst"]["n_free"], peak, peak_kind,
+                                                    "k_pcg_poly"),
+                        "tol": ctx_tol(args, "fp32")}
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -420,11 +444,9 @@ def run_ours(args):
 
 
 def ncu_traffic(precision, kernel):
-    """dram__bytes_read+write per launch of `kernel` from the committed ncu capture (fp32 only)."""
-    if precision != "fp32":
-        return None
+    """dram__bytes_read+write per launch of `kernel` from the committed ncu launch list."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01b_launches_steady_summary.json")) as f:
+        with open(os.path.join(ROOT, "profiles", f"r02_launches_{precision}_summary.json")) as f:
             d = json.load(f)
         for k, v in d.get("kernels", d).items():
             if kernel in k:
@@ -434,9 +456,9 @@ def ncu_traffic(precision, kernel):
     return None
 
 
-def ctx_tol(args):
+def ctx_tol(args, precision=None):
     from paper_2405_12484_b200 import pdsolver
-    return args.tol if args.tol else pdsolver.DEFAULT_TOL[args.precision]
+    return args.tol if args.tol else pdsolver.DEFAULT_TOL[precision or args.precision]
 
 
 def main():

@@ -72,6 +72,8 @@ typedef struct {
     const int64_t* pins;        /* (n_pins,) unique node ids, may be NULL if n_pins = 0  */
     int64_t n_pins;
     double dt;                  /* > 0 */
+    const double* nodes;        /* (n_nodes, 3) rest positions, optional (NULL): used only to   */
+                                /* order the free nodes in compact patches, one per solver CTA */
 } vkpd_mesh_desc;
 
 typedef struct {
@@ -81,7 +83,17 @@ typedef struct {
     int device;        /* CUDA device ordinal                                            */
     int pcg_blocks;    /* CTAs of the persistent solver (<= 0: one per SM)               */
     int use_graph;     /* capture a whole frame in a CUDA graph (1, default) or not (0)  */
+    int solver;        /* global step: VKPD_SOLVER_AUTO (0: fp64 -> Chebyshev, fp32 ->     */
+                       /* polynomial CG), _PCG_POLY, _CHEBYSHEV, _PCG_JACOBI               */
+    int pd_early_exit; /* stop a frame's PD rounds at the first zero-work solve (<0: on)  */
+    int warm_rounds;   /* PD rounds warm-started from earlier frames (<0: default)        */
+    int unroll_rounds; /* PD rounds captured ahead of the graph's WHILE node (<0: adaptive) */
 } vkpd_config;
+
+#define VKPD_SOLVER_AUTO 0
+#define VKPD_SOLVER_PCG_POLY 1
+#define VKPD_SOLVER_CHEBYSHEV 2
+#define VKPD_SOLVER_PCG_JACOBI 3
 
 typedef struct {
     int n_pd_iters;            /* PD iterations of the last frame                         */

@@ -38,15 +38,19 @@ class MeshDesc(C.Structure):
         ("n_nodes", C.c_int64), ("n_tets", C.c_int64), ("tets", C.c_void_p),
         ("shape_grad", C.c_void_p), ("volume", C.c_void_p), ("node_mass", C.c_void_p),
         ("gamma_s", C.c_void_p), ("gamma_v", C.c_void_p), ("pins", C.c_void_p),
-        ("n_pins", C.c_int64), ("dt", C.c_double),
+        ("n_pins", C.c_int64), ("dt", C.c_double), ("nodes", C.c_void_p),
     ]
 
 
 class Config(C.Structure):
     _fields_ = [
         ("precision", C.c_int), ("tol", C.c_double), ("max_iters", C.c_int), ("device", C.c_int),
-        ("pcg_blocks", C.c_int), ("use_graph", C.c_int),
+        ("pcg_blocks", C.c_int), ("use_graph", C.c_int), ("solver", C.c_int),
+        ("pd_early_exit", C.c_int), ("warm_rounds", C.c_int), ("unroll_rounds", C.c_int),
     ]
+
+
+SOLVERS = {"auto": 0, "pcg": 1, "chebyshev": 2, "jacobi": 3}
 
 
 class Stats(C.Structure):
@@ -181,7 +185,8 @@ class Context:
     """Owns one `vkpd_ctx` (device-resident scene)."""
 
     def __init__(self, nodes_count, tets, shape_grad, volume, node_mass, gamma_s, gamma_v, pins,
-                 dt, precision="fp32", tol=0.0, max_iters=0, device=0, pcg_blocks=0, use_graph=True):
+                 dt, precision="fp32", tol=0.0, max_iters=0, device=0, pcg_blocks=0, use_graph=True,
+                 solver="auto", pd_early_exit=True, warm_rounds=-1, unroll_rounds=-1, nodes=None):
         self.lib = load()
         self._keep = dict(
             tets=np.ascontiguousarray(tets, dtype=np.int64).reshape(-1, 4),
@@ -191,18 +196,24 @@ class Context:
             gs=f64(gamma_s).reshape(-1),
             gv=f64(gamma_v).reshape(-1),
             pins=np.ascontiguousarray(pins, dtype=np.int64).reshape(-1),
+            nodes=None if nodes is None else f64(nodes).reshape(-1, 3),
         )
         k = self._keep
         self.n = int(nodes_count)
+        if k["nodes"] is not None and k["nodes"].shape[0] != self.n:
+            raise ValueError("rest positions must be (n_nodes, 3)")
         self.n_tets = k["tets"].shape[0]
         self.n_pins = k["pins"].shape[0]
         if k["mass"] is None:
             raise ValueError("mesh node masses not lumped yet")
         d = MeshDesc(self.n, self.n_tets, ptr(k["tets"]), ptr(k["G"]), ptr(k["vol"]), ptr(k["mass"]),
                      ptr(k["gs"]), ptr(k["gv"]), ptr(k["pins"]) if self.n_pins else None,
-                     self.n_pins, float(dt))
+                     self.n_pins, float(dt), ptr(k["nodes"]) if k["nodes"] is not None else None)
+        if solver not in SOLVERS:
+            raise ValueError(f"unknown solver {solver!r}")
         cfg = Config(PRECISION[precision], float(tol), int(max_iters), int(device), int(pcg_blocks),
-                     1 if use_graph else 0)
+                     1 if use_graph else 0, SOLVERS[solver], 1 if pd_early_exit else 0, int(warm_rounds),
+                     int(unroll_rounds))
         h = C.c_void_p()
         check(self.lib.vkpd_create(C.byref(d), C.byref(cfg), C.byref(h)))
         self.h = h
@@ -495,7 +506,8 @@ class MatrixContext(Context):
                           indices=np.ascontiguousarray(K.indices, dtype=np.int64),
                           data=f64(K.data), pins=pins)
         k = self._keep
-        cfg = Config(PRECISION[precision], float(tol), int(max_iters), int(device), int(pcg_blocks), 0)
+        cfg = Config(PRECISION[precision], float(tol), int(max_iters), int(device), int(pcg_blocks), 0,
+                     SOLVERS["pcg"], 1, -1, -1)
         h = C.c_void_p()
         check(self.lib.vkpd_create_matrix(self.n, ptr(k["indptr"]), ptr(k["indices"]), ptr(k["data"]),
                                           ptr(pins) if self.n_pins else None, self.n_pins,

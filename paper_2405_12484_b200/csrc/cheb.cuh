@@ -1,0 +1,431 @@
+// Global step as a Chebyshev semi-iteration on the Jacobi-scaled K_ff with
+// neighbour-only synchronisation (the fp64 solver of the frame graph).
+//
+// The reference solves K_ff x = b exactly per PD round (SuperLU,
+// pdsolver.py:201-236).  The persistent CG (solver.cuh) needs two grid-wide
+// reductions per iteration; at fp64 tolerance (1e-12 of |M/dt^2 xhat|) a PD
+// round takes ~20 CG iterations, and each reduction is a grid barrier, so
+// the solve is bound by barrier latency.  Chebyshev acceleration of Jacobi
+// needs no inner products at all: every step is y += d, res -= K d,
+// d = c1 d + c2 D^-1 res with scalar coefficients fixed by the spectrum
+// interval [lmin, lmax] of D^-1 K_ff.  Its only data dependence is the SpMV,
+// i.e. the rows a CTA reads from the CTAs that own its columns, so a step
+// waits on per-CTA release flags of those neighbour CTAs instead of a grid
+// barrier.  The residual norm is reduced (one grid barrier) only at the
+// predicted step count and then until it meets the same tolerance the CG
+// uses (|r| <= tol |M/dt^2 xhat|).
+//
+// Spectrum: lmax is the Gershgorin bound of D^-1 K_ff (rigorous), lmin a
+// Lanczos estimate of the smallest eigenvalue of D^-1/2 K_ff D^-1/2 computed
+// once per assembly (never below the rigorous bound min_i (m_i/dt^2)/K_ii:
+// K - M/dt^2 is positive semidefinite).  An optimistic lmin only slows the
+// lowest modes (|p_k| < 1 still holds on (0, lmin)); the residual check keeps
+// the stopping rule exact either way.  Contact rows (pdsolver.py:271-297) add
+// c_i to both K_ii and the mass term, which keeps both bounds valid.
+//
+// When a CTA owns at most one row per thread (the C3 case) the row state
+// lives in registers (residual, accumulated correction, direction d), the
+// row's ELL values in shared memory, and the SpMV reads d from a shared-memory
+// image of the CTA's own rows plus its halo (the rows of other CTAs its rows
+// reference, loaded from L2 once per step, one coalesced pass): each
+// neighbour value crosses L2 once per CTA instead of once per reference.
+// Only d crosses CTAs (global, double-buffered by step parity).  All
+// arithmetic has a fixed order, so results are bit-reproducible run to run.
+#pragma once
+
+#include "solver.cuh"
+
+namespace vk {
+
+__device__ __forceinline__ void cheb_wait(const unsigned int* flags, const int* nbr, int nn, unsigned int target) {
+    // one lane per neighbour CTA polls its flag (acquire): the neighbour's d for
+    // this step is then visible to the whole CTA after the barrier below
+    if (threadIdx.x < 32) {
+        for (int j = threadIdx.x; j < nn; j += 32) {
+            const unsigned int* f = flags + (size_t)nbr[j] * 32;
+            unsigned long long spins = 0;
+            while ((int)(ld_acquire_gpu(f) - target) < 0) {
+                if (++spins > (1ull << 33)) __trap();
+            }
+        }
+    }
+    __syncthreads();
+}
+
+#ifndef VK_CHEB_FENCE
+#define VK_CHEB_FENCE 0    // st.release after the CTA barrier orders the CTA's stores (cumulativity)
+#endif
+__device__ __forceinline__ void cheb_publish(unsigned int* flags, unsigned int value) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#if VK_CHEB_FENCE
+        __threadfence();
+#endif
+        st_release_gpu(flags + (size_t)blockIdx.x * 32, value);
+    }
+}
+
+// x, y, z of a vec4 row through L2 only (rows written by other CTAs in this launch)
+__device__ __forceinline__ void ldcg3(const float4* p, float& x, float& y, float& z) {
+    const float4 v = __ldcg(p);
+    x = v.x; y = v.y; z = v.z;
+}
+__device__ __forceinline__ void ldcg3(const double4* p, double& x, double& y, double& z) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+    x = v.x; y = v.y;
+    z = __ldcg(reinterpret_cast<const double*>(p) + 2);
+}
+
+// Register path: a row keeps its kChebOff off-diagonal ELL values and their shared-memory
+// slots in registers (plus the diagonal), so the SpMV's shared-memory traffic is only the
+// neighbours' d.  Shared-memory image (compile-time strides, so every access is one address
+// register plus an immediate offset): two step-parity buffers of the x / y / z planes of d
+// over kChebSlots slots (own rows: slot = tid; halo row j: slot = blockDim.x + j), the
+// x / y / z planes of the accumulated correction y (own rows), then the halo rows' global
+// indices.
+//
+// Exported rows first: the rows other CTAs read (a CTA's exported rows lead its row range,
+// vkpd.cu patch_order) are computed by the leading warps, which meet on a named barrier and
+// publish the step flag as soon as their d is in global memory; the interior rows (read by
+// nobody else, kept in shared memory only) finish while the flag travels.
+constexpr int kChebMaxThreads = 768;
+constexpr int kChebSlots = 2048;
+constexpr int kChebOff = 14;       // voxel enclosures: <= 15 entries per row, one of them diagonal
+template <typename T>
+constexpr size_t cheb_smem_bytes() {
+    return sizeof(T) * (6 * (size_t)kChebSlots + 3 * (size_t)kChebMaxThreads) + sizeof(int) * kChebSlots;
+}
+
+// Steps needed for a residual reduction by `ratio` at Chebyshev parameter sigma
+// (|p_k| <= 1 / T_k(sigma) on the interval).
+__device__ __forceinline__ int cheb_steps_for(double ratio, double acosh_sigma) {
+    if (!(ratio > 1.0)) return 1;
+    const double k = acosh(ratio) / acosh_sigma;
+    return k < 1e6 ? max(1, (int)ceil(k)) : 1000000;
+}
+
+// REG = true: one row per thread, row state in registers (requires chunk <= blockDim.x
+// and ell_w <= kEllUnroll); REG = false: any size, row state in a.r / a.dx, ELL from L1/L2.
+template <typename T, bool REG>
+__device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& grid, double* smem, double* red) {
+    pcg_entry(a);
+    const int nF = a.nF;
+    const int chunk = (nF + gridDim.x - 1) / gridDim.x;
+    const int row0 = blockIdx.x * chunk;
+    const int row1 = min(nF, row0 + chunk);
+    int parity = 0;
+    __shared__ unsigned int s_base;
+    if (threadIdx.x == 0) s_base = ld_acquire_gpu(a.flags + (size_t)blockIdx.x * 32);
+    const int pdi_w = a.pd_iter_dev != nullptr ? *a.pd_iter_dev : a.pd_iter;
+    const bool warm = a.warm != nullptr && a.init == INIT_PD && pdi_w < a.warm_rounds;
+    vec4_t<T>* const wb = warm ? a.warm + (size_t)pdi_w * nF : nullptr;
+
+    const double lmin = a.cheb_lmin, lmax = a.cheb_lmax;
+    const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
+    const double sigma = theta / delta;
+    const double acosh_sigma = acosh(sigma);
+
+    // ---- init: res = b - K x (PD residual form) minus K * warm guess; y = guess; d0 = D^-1 res / theta
+    const int i = row0 + threadIdx.x;              // REG path: this thread's row
+    const bool own = REG && i < row1;
+    int cols[kChebOff];                            // REG: shared-memory slots of the off-diagonal columns
+    T vals[kChebOff];                              //      and their values
+    T kdiag = 0;
+    extern __shared__ __align__(16) unsigned char cheb_smem[];
+    T* const sd = reinterpret_cast<T*>(cheb_smem);   // REG: d planes, buffer p at sd + 3 p kChebSlots
+    T* yv = sd + 6 * kChebSlots + threadIdx.x;     // REG: this row's y, planes kChebMaxThreads apart
+    int* hidx = reinterpret_cast<int*>(sd + 6 * kChebSlots + 3 * kChebMaxThreads);   // REG: halo rows
+    // exported rows [row0, row0 + nexp) belong to the leading warps (at least warp 0, which
+    // publishes the step flag)
+    const int nexp = REG ? a.cheb_nexp[blockIdx.x] : 0;
+    const int exp_threads = max(32, (nexp + 31) & ~31);
+    const bool exp_warp = (int)threadIdx.x < exp_threads;
+    const int nh = REG ? a.cheb_halo_ptr[blockIdx.x + 1] - a.cheb_halo_ptr[blockIdx.x] : 0;
+    if (REG) {
+        const int* halo = a.cheb_halo + a.cheb_halo_ptr[blockIdx.x];
+        for (int j = threadIdx.x; j < nh; j += blockDim.x) hidx[j] = __ldg(&halo[j]);
+    }
+    T rx = 0, ry = 0, rzz = 0, dxv = 0, dyv = 0, dzv = 0, dg = 0;
+    double acc[2] = {0, 0};                        // rr, bb
+    if (REG) {
+        if (own) {
+#pragma unroll
+            for (int s = 0; s < kChebOff; ++s) {
+                cols[s] = __ldg(&a.cheb_slot[(size_t)s * nF + i]);
+                vals[s] = __ldg(&a.cheb_val[(size_t)s * nF + i]);
+            }
+            kdiag = __ldg(&a.cheb_kdiag[i]);
+            init_residual_row(a, i, false, rx, ry, rzz, acc[1]);
+            T gx = 0, gy = 0, gz = 0;
+            if (warm) {
+                const vec4_t<T> g = ld4(&wb[i]);
+                gx = g.x; gy = g.y; gz = g.z;
+                const vec4_t<T> kw = k_row(a, wb, i);
+                rx -= kw.x; ry -= kw.y; rzz -= kw.z;
+            }
+            yv[0] = gx; yv[kChebMaxThreads] = gy; yv[2 * kChebMaxThreads] = gz;
+            dg = a.inv_diag[i];
+            const T c0 = (T)(1.0 / theta) * dg;
+            dxv = c0 * rx; dyv = c0 * ry; dzv = c0 * rzz;
+            st4(&a.p0[i], make4<T>(dxv, dyv, dzv, T(0)));
+            sd[threadIdx.x] = dxv; sd[kChebSlots + threadIdx.x] = dyv; sd[2 * kChebSlots + threadIdx.x] = dzv;
+            acc[0] = (double)rx * rx + (double)ry * ry + (double)rzz * rzz;
+        }
+    } else {
+        for (int j = row0 + threadIdx.x; j < row1; j += blockDim.x) {
+            T ax, ay, az;
+            init_residual_row(a, j, false, ax, ay, az, acc[1]);
+            vec4_t<T> y0 = make4<T>(T(0), T(0), T(0), T(0));
+            if (warm) {
+                y0 = ld4(&wb[j]);
+                const vec4_t<T> kw = k_row(a, wb, j);
+                ax -= kw.x; ay -= kw.y; az -= kw.z;
+            }
+            const T c0 = (T)(1.0 / theta) * a.inv_diag[j];
+            a.r[j] = make4<T>(ax, ay, az, T(0));
+            a.dx[j] = y0;
+            a.p0[j] = make4<T>(c0 * ax, c0 * ay, c0 * az, T(0));
+            acc[0] += (double)ax * ax + (double)ay * ay + (double)az * az;
+        }
+    }
+    pcg_allreduce<2>(grid, a.partials, parity, acc, red, smem);
+    double rr = red[0];
+    const double bb = red[1];
+    const double thr = a.tol * a.tol * bb;
+    const unsigned int base = s_base;
+    const int* nbr = a.cheb_nbr + a.cheb_nbr_ptr[blockIdx.x];
+    const int nn = a.cheb_nbr_ptr[blockIdx.x + 1] - a.cheb_nbr_ptr[blockIdx.x];
+
+    int k = 0;
+    double rho = 1.0 / sigma;
+    const double two_over_delta = 2.0 / delta;
+    if (rr > thr && a.max_iters > 0) {
+        int target = min(a.max_iters, cheb_steps_for(sqrt(rr / thr), acosh_sigma));
+        for (;;) {
+            for (; k < target; ++k) {
+                pcg_mark(10);
+                if (k > 0) cheb_wait(a.flags, nbr, nn, base + (unsigned)k);
+                pcg_mark(11);
+                const vec4_t<T>* dcur = (k & 1) ? a.p1 : a.p0;
+                vec4_t<T>* dnext = (k & 1) ? a.p0 : a.p1;
+                const double rho_n = 1.0 / (2.0 * sigma - rho);
+                const T c1 = (T)(rho_n * rho), c2 = (T)(rho_n * two_over_delta);
+                rho = rho_n;
+                if (REG) {
+                    T* const sx = sd + (k & 1) * 3 * kChebSlots;         // d_k
+                    T* const sn = sd + ((k + 1) & 1) * 3 * kChebSlots;   // d_{k+1} (own rows)
+                    // halo rows of d_k into shared memory (own rows are there already)
+                    for (int j = threadIdx.x; j < nh; j += blockDim.x) {
+                        T hx, hy, hz;
+                        ldcg3(&dcur[hidx[j]], hx, hy, hz);
+                        const int sl = blockDim.x + j;
+                        sx[sl] = hx; sx[kChebSlots + sl] = hy; sx[2 * kChebSlots + sl] = hz;
+                    }
+                    __syncthreads();
+                    pcg_mark(12);
+                    // interior warps start after the exported warps are done with shared memory
+                    if (!exp_warp) asm volatile("bar.sync 2, %0;" ::"r"((int)blockDim.x) : "memory");
+                    if (own) {
+                        // two partial sums per component (shorter dependency chains)
+                        T qx = kdiag * dxv, qy = kdiag * dyv, qz = kdiag * dzv, px = 0, py = 0, pz = 0;
+#pragma unroll
+                        for (int s = 0; s < kChebOff; s += 2) {
+                            const T* d = sx + cols[s];
+                            qx += vals[s] * d[0]; qy += vals[s] * d[kChebSlots]; qz += vals[s] * d[2 * kChebSlots];
+                            if (s + 1 < kChebOff) {
+                                const T* e = sx + cols[s + 1];
+                                px += vals[s + 1] * e[0]; py += vals[s + 1] * e[kChebSlots];
+                                pz += vals[s + 1] * e[2 * kChebSlots];
+                            }
+                        }
+                        qx += px; qy += py; qz += pz;
+                        if (a.cdiag != nullptr) {
+                            const T cd = a.cdiag[i];
+                            qx += cd * dxv; qy += cd * dyv; qz += cd * dzv;
+                        }
+                        yv[0] += dxv; yv[kChebMaxThreads] += dyv; yv[2 * kChebMaxThreads] += dzv;
+                        rx -= qx; ry -= qy; rzz -= qz;
+                        const T e = c2 * dg;
+                        dxv = c1 * dxv + e * rx;
+                        dyv = c1 * dyv + e * ry;
+                        dzv = c1 * dzv + e * rzz;
+                        sn[threadIdx.x] = dxv; sn[kChebSlots + threadIdx.x] = dyv; sn[2 * kChebSlots + threadIdx.x] = dzv;
+                        if ((int)threadIdx.x < nexp) st4(&dnext[i], make4<T>(dxv, dyv, dzv, T(0)));
+                    }
+                    pcg_mark(13);
+                    if (exp_warp) {
+                        asm volatile("bar.sync 1, %0;" ::"r"(exp_threads) : "memory");
+                        if (threadIdx.x == 0) st_release_gpu(a.flags + (size_t)blockIdx.x * 32, base + (unsigned)(k + 1));
+                        if (exp_threads < (int)blockDim.x) asm volatile("bar.arrive 2, %0;" ::"r"((int)blockDim.x) : "memory");
+                    }
+                    pcg_mark(14);
+                } else {
+                    for (int j = row0 + threadIdx.x; j < row1; j += blockDim.x) {
+                        T qx = 0, qy = 0, qz = 0;
+                        for (int s = 0; s < a.ell_w; ++s) {
+                            const int c = __ldg(&a.ell_col[(size_t)s * nF + j]);
+                            const T kv = __ldg(&a.ell_val[(size_t)s * nF + j]);
+                            T vx, vy, vz;
+                            ldcg3(&dcur[c], vx, vy, vz);
+                            qx += kv * vx; qy += kv * vy; qz += kv * vz;
+                        }
+                        vec4_t<T> dj;
+                        ldcg3(&dcur[j], dj.x, dj.y, dj.z);
+                        if (a.cdiag != nullptr) {
+                            const T cd = a.cdiag[j];
+                            qx += cd * dj.x; qy += cd * dj.y; qz += cd * dj.z;
+                        }
+                        vec4_t<T> y = a.dx[j], r = a.r[j];
+                        y.x += dj.x; y.y += dj.y; y.z += dj.z;
+                        r.x -= qx; r.y -= qy; r.z -= qz;
+                        const T e = c2 * a.inv_diag[j];
+                        a.dx[j] = y;
+                        a.r[j] = r;
+                        st4(&dnext[j], make4<T>(c1 * dj.x + e * r.x, c1 * dj.y + e * r.y, c1 * dj.z + e * r.z, T(0)));
+                    }
+                }
+                if (!REG) cheb_publish(a.flags, base + (unsigned)(k + 1));
+            }
+            // residual check (one grid barrier): the same rule as the CG
+            double acc1[1] = {0.0};
+            if (REG) {
+                if (own) acc1[0] = (double)rx * rx + (double)ry * ry + (double)rzz * rzz;
+            } else {
+                for (int j = row0 + threadIdx.x; j < row1; j += blockDim.x) {
+                    const vec4_t<T> r = a.r[j];
+                    acc1[0] += (double)r.x * r.x + (double)r.y * r.y + (double)r.z * r.z;
+                }
+            }
+            pcg_allreduce<1>(grid, a.partials, parity, acc1, red, smem);
+            rr = red[0];
+            if (!(rr > thr) || k >= a.max_iters) break;      // also stops on NaN
+            target = min(a.max_iters, k + 1 + cheb_steps_for(sqrt(rr / thr), acosh_sigma));
+        }
+    }
+    // ---- finish: x += y (PD mode), warm-start bank, finite check
+    bool bad = a.init == INIT_PD && !(rr == rr && rr < INFINITY);
+    auto finish_row = [&](int j, vec4_t<T> d) {
+        vec4_t<T> xi = a.x[j];
+        xi.x += d.x; xi.y += d.y; xi.z += d.z;
+        a.x[j] = xi;
+        if (warm) {
+            if (a.warm_prev != nullptr && pdi_w < a.warm_extrap_rounds) {
+                vec4_t<T>* wp = a.warm_prev + (size_t)pdi_w * nF;
+                const vec4_t<T> dp = ld4(&wp[j]);
+                wp[j] = d;
+                const T be = (T)a.warm_beta;
+                wb[j] = make4<T>(d.x + be * (d.x - dp.x), d.y + be * (d.y - dp.y), d.z + be * (d.z - dp.z), T(0));
+            } else {
+                wb[j] = d;
+            }
+        }
+        bad |= !(isfinite(xi.x) && isfinite(xi.y) && isfinite(xi.z));
+    };
+    if (k > 0 || bad || warm) {
+        if (REG) {
+            if (own) finish_row(i, make4<T>(yv[0], yv[kChebMaxThreads], yv[2 * kChebMaxThreads], T(0)));
+        } else {
+            for (int j = row0 + threadIdx.x; j < row1; j += blockDim.x) finish_row(j, a.dx[j]);
+        }
+    }
+    pcg_exit(a, bad, k, warm);
+}
+
+#ifndef VK_CHEB_THREADS
+#define VK_CHEB_THREADS 768
+#endif
+template <typename T>
+__global__ void __launch_bounds__(VK_CHEB_THREADS, 1) k_cheb_reg(PcgArgs<T> a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double smem[32 * 8];
+    __shared__ double red[8];
+    cheb_body<T, true>(a, grid, smem, red);
+}
+template <typename T>
+__global__ void __launch_bounds__(VK_CHEB_THREADS, 1) k_cheb(PcgArgs<T> a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double smem[32 * 8];
+    __shared__ double red[8];
+    cheb_body<T, false>(a, grid, smem, red);
+}
+
+// ---------------------------------------------------------------------------
+// Lanczos on D^-1/2 K_ff D^-1/2 (no reorthogonalisation: only the extreme Ritz
+// values are used), one cooperative launch, deterministic reductions.
+// alpha[j], beta[j+1] for j < m; v0 from a fixed hash (reproducible).
+template <typename T>
+struct LanczosArgs {
+    int nF, ell_w, m;
+    const int* ell_col;
+    const T* ell_val;
+    const double* diag64;
+    double* v0;       // 3 vectors of nF: v_{j-1}, v_j, w
+    double* v1;
+    double* w;
+    double* partials;
+    double* alpha;
+    double* beta;
+};
+
+__device__ __forceinline__ double lanczos_start(int i) {
+    unsigned int h = (unsigned int)i * 2654435761u + 0x9e3779b9u;
+    h ^= h >> 16; h *= 0x85ebca6bu; h ^= h >> 13; h *= 0xc2b2ae35u; h ^= h >> 16;
+    return (double)(h & 0xffffff) / 16777216.0 - 0.5;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_lanczos(LanczosArgs<T> a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double smem[32 * 8];
+    __shared__ double red[8];
+    int parity = 0;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    double acc[1] = {0.0};
+    for (int i = tid; i < a.nF; i += nth) {
+        const double s = lanczos_start(i);
+        a.v1[i] = s;
+        a.v0[i] = 0.0;
+        acc[0] += s * s;
+    }
+    pcg_allreduce<1>(grid, a.partials, parity, acc, red, smem);
+    double inv = 1.0 / sqrt(red[0]);
+    for (int i = tid; i < a.nF; i += nth) a.v1[i] *= inv;
+    grid.sync();
+    double beta = 0.0;
+    double* vp = a.v0;
+    double* vc = a.v1;
+    for (int j = 0; j < a.m; ++j) {
+        // w = A v_j - beta_j v_{j-1};  alpha_j = w . v_j
+        double ac[1] = {0.0};
+        for (int i = tid; i < a.nF; i += nth) {
+            const double si = rsqrt(a.diag64[i]);
+            double h = 0.0;
+            for (int s = 0; s < a.ell_w; ++s) {
+                const int c = a.ell_col[(size_t)s * a.nF + i];
+                h += (double)a.ell_val[(size_t)s * a.nF + i] * rsqrt(a.diag64[c]) * __ldcg(&vc[c]);
+            }
+            const double wi = si * h - beta * __ldcg(&vp[i]);
+            a.w[i] = wi;
+            ac[0] += wi * __ldcg(&vc[i]);
+        }
+        pcg_allreduce<1>(grid, a.partials, parity, ac, red, smem);
+        const double alpha = red[0];
+        double bc[1] = {0.0};
+        for (int i = tid; i < a.nF; i += nth) {
+            const double wi = a.w[i] - alpha * __ldcg(&vc[i]);
+            a.w[i] = wi;
+            bc[0] += wi * wi;
+        }
+        pcg_allreduce<1>(grid, a.partials, parity, bc, red, smem);
+        const double bn = sqrt(red[0]);
+        if (blockIdx.x == 0 && threadIdx.x == 0) { a.alpha[j] = alpha; a.beta[j + 1] = bn; }
+        if (!(bn > 0.0)) break;
+        const double ib = 1.0 / bn;
+        for (int i = tid; i < a.nF; i += nth) vp[i] = a.w[i] * ib;     // v_{j+1} into the old v_{j-1}
+        grid.sync();
+        double* t = vp; vp = vc; vc = t;
+        beta = bn;
+    }
+}
+
+}  // namespace vk

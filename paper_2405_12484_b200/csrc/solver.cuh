@@ -255,6 +255,18 @@ struct PcgArgs {
                                  // extrapolation d_prev + beta (d_prev - d_prevprev)
     double warm_beta;
     int warm_extrap_rounds;      // rounds < this extrapolate; later warm rounds reuse the last correction
+    // Chebyshev solver (cheb.cuh)
+    unsigned int* flags;         // per-CTA step counters, 128-B stride
+    const int* cheb_nbr_ptr;     // CTAs whose rows a CTA's rows read (CSR over CTAs)
+    const int* cheb_nbr;
+    double cheb_lmin, cheb_lmax; // spectrum interval of D^-1 K_ff
+    const int* cheb_slot;        // register path, [s * nF + i]: shared-memory slot of off-diagonal entry s
+    const T* cheb_val;           //   of row i (pads: own slot, value 0), its value, and the diagonal
+    const T* cheb_kdiag;
+    const int* cheb_nexp;        // per CTA: its leading rows that other CTAs read (register path)
+    const int* cheb_halo_ptr;    // per CTA: rows of other CTAs its rows reference
+    const int* cheb_halo;
+    int cheb_halo_max;
 };
 
 template <typename T>

@@ -15,12 +15,13 @@
 #include <vector>
 #include <atomic>
 #include <thread>
+#include <functional>
 
 #include "../../include/vkpd.h"
 #include "local_step.cuh"
 #include "solver.cuh"
 #include "cms.cuh"
-#include "frame.cuh"
+#include "cheb.cuh"
 #include "output.cuh"
 #include "jacobian.cuh"
 #include "hessian.cuh"
@@ -58,7 +59,6 @@ struct DBuf {
 };
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
-constexpr int kFrameThreads = 512;   // CTA size of the fused frame kernel
 
 // ---------------------------------------------------------------------------
 // layout conversion kernels: host (nV,3) float64 in caller order <-> device vec4 internal order
@@ -222,6 +222,12 @@ struct Ctx : CtxBase {
     bool has_forces = false;
     int n_sms = 0;
     std::vector<int> int_of_orig_h;
+    std::vector<int> free_perm;          // caller's free-row rank (free nodes in caller order) -> internal row
+    void set_free_perm() {
+        free_perm.clear();
+        for (int j = 0; j < n; ++j)
+            if (int_of_orig_h[j] < nF) free_perm.push_back(int_of_orig_h[j]);
+    }
 
     // topology / material
     DBuf<int4> tets;
@@ -234,34 +240,31 @@ struct Ctx : CtxBase {
     DBuf<T> ell_kd;                      // K_ff D^-1 (polynomial preconditioner)
     DBuf<V4> warm0;                      // per-round corrections of the previous frame (solver warm start)
     DBuf<V4> warm1;                      // the frame before: the guess is the linear extrapolation
-    int poly_rounds = 0;                 // env VKPD_POLY_ROUNDS=k: PD rounds >= k use Jacobi-PCG (0: all polynomial)
-    bool warm_extrap = true;             // d + beta (d - d_before), beta = 1 (env VKPD_WARM_EXTRAP=<beta>,
-    double warm_beta = 1.0;              // 0: the previous correction alone)
-    int warm_extrap_rounds = sizeof(T) == 8 ? 32 : 1;   // env VKPD_WARM_EXTRAP_ROUNDS: fp32 extrapolates
-                                         // round 0 only (later rounds' corrections are noise-level: C3
-                                         // 0.88 ms, C5 2.76 ms; all three rounds: 0.885 / 3.37 ms)
-    bool warm_start = true;              // env VKPD_WARM=0: off
-    int warm_rounds = sizeof(T) == 8 ? 32 : 3;   // env VKPD_WARM=<rounds>; fp64 runs every round (no early exit), where
-                                         // all rounds gain (C3: 19.3 -> 15.9 ms/frame); fp32 only the first 3
+    bool warm_extrap = true;             // d + beta (d - d_before), beta = 1
+    double warm_beta = 1.0;
+    int warm_extrap_rounds = sizeof(T) == 8 ? 32 : 1;   // fp32 extrapolates round 0 only (later rounds'
+                                         // corrections are noise-level: C3 0.88 ms, C5 2.76 ms; all three
+                                         // rounds: 0.885 / 3.37 ms)
+    bool warm_start = true;              // vkpd_config.warm_rounds = 0: off
+    int warm_rounds = sizeof(T) == 8 ? 32 : 3;   // fp64 runs every round (no early exit), where all rounds
+                                         // gain (C3: 19.3 -> 15.9 ms/frame); fp32 only the first 3
     // state
     DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
     DBuf<V4> m1, qq, ss, pp;             // pipelined-CG recurrences
-    bool pcg_classic = false;
     int pcg_threads = 512;               // CTA size of the persistent solver
-    bool pcg_poly = true;                // Neumann-1 polynomial preconditioner (env VKPD_PCG=jacobi: plain Jacobi)
+    int solver_kind = VKPD_SOLVER_PCG_POLY;   // resolved vkpd_config.solver
+    bool pcg_poly = true;                // Neumann-1 polynomial preconditioner (CG kinds)
+    bool cheb = false;                   // Chebyshev semi-iteration with neighbour flags (cheb.cuh)
+    bool cheb_reg = false;               // ... with the row state in registers (one row per thread)
     double poly_omega = 1.0;             // min(1, 1.9 / Gershgorin bound of D^-1 K_ff)
-    bool robust_quad = false;            // env VKPD_ROBUST=quad: quad-per-element robust pass (A/B only)
-    int robust_blocks = 4;               // k_robust_ws CTAs per SM (its co-residency)
-    bool fused = false;                  // whole frame in one cooperative kernel (env VKPD_FUSED=1); measured
-                                         // slower than per-phase kernels in a graph (register spills)
-    int frame_blocks = 0;
+    double gersh = 2.0;                  // Gershgorin bound of D^-1 K_ff
+    double lam_min = 0.0, lam_min_bound = 0.0;   // Lanczos estimate / rigorous bound of lambda_min(D^-1 K_ff)
+    DBuf<unsigned int> cheb_flags;
+    DBuf<int> cheb_nbr_ptr, cheb_nbr;
     DBuf<double> partials, scal, stage;
     DBuf<vk::GridBar> bar;
     DBuf<int> iters, fail_iter, robust_list, robust_count;
     DBuf<T> robust_aux;                  // (sigma, U, W) of each queued element (24 per slot)
-    bool robust_handoff = true;          // env VKPD_ROBUST_AUX=0: the robust pass recomputes the SVD
-    bool robust_tasks = true;            // (chunk, start) task pass (default; env VKPD_ROBUST=ws: the
-                                         // warp-per-start CTA pass, =quad: quad-per-element)
     int robust_task_blocks = 4;
     DBuf<double> robust_res;
     DBuf<int> robust_ok, robust_arrivals;
@@ -276,19 +279,16 @@ struct Ctx : CtxBase {
     double graph_damp = 0;
     bool graph_forces = false;
     bool graph_broken = false;
-    bool pd_early_exit = true;           // loop node with the zero-CG-iteration exit (env VKPD_PD_EXIT=0: off)
+    bool pd_early_exit = true;           // loop node with the zero-work exit (vkpd_config.pd_early_exit)
     int last_exec_rounds = 0;            // PD rounds of the last directly launched frame
     cudaStream_t body_stream = nullptr;  // captures the loop body
-    cudaStream_t if_stream = nullptr;    // captures the robust pass's IF-node body
     int unroll_rounds = 0;               // PD rounds captured ahead of the WHILE node (see step_async)
-    int unroll_env = -1;                 // env VKPD_UNROLL: fixed count (-1: adaptive)
+    int unroll_cfg = -1;                 // vkpd_config.unroll_rounds: fixed count (-1: adaptive)
     int graph_unroll = 0;
     DBuf<int> first_stop;                // rounds the last frame needed (device), mirrored to h_stop
     int* h_stop = nullptr;
     int stop_hist[32];
     int stop_n = 0, stop_pos = 0, stop_fill = 0;
-    bool robust_if_node = false;         // env VKPD_ROBUST_IF=1: robust pass inside an IF node set by the
-                                         // local step (measured slower: the node costs more than the launch)
     DBuf<int> pd_it;                     // device PD-iteration counter of the loop node
     int graph_ncoll = 0;
     // colliders (pdsolver.py:125-173, 271-297)
@@ -313,9 +313,59 @@ struct Ctx : CtxBase {
         if (in_stream) cudaStreamDestroy(in_stream);
         if (own_stream) cudaStreamDestroy(own_stream);
         if (body_stream) cudaStreamDestroy(body_stream);
-        if (if_stream) cudaStreamDestroy(if_stream);
         for (auto& ev : cms_ev)
             if (ev) cudaEventDestroy(ev);
+    }
+
+    // Recursive coordinate bisection of the free nodes into `parts` patches of ceil(nF/parts)
+    // nodes (the solver CTAs' row ranges), split across the longest extent of each box.  Inside
+    // a patch the nodes that share a tet with another patch's node come first (the rows other
+    // CTAs read: the Chebyshev solver publishes them ahead of the interior), each group in
+    // caller order.
+    int part_blocks = 0;
+    static void patch_order(const double* X, const int64_t* tets, int64_t n_tets, int n_nodes, std::vector<int>& ids,
+                            int parts) {
+        const int nf = (int)ids.size();
+        const int chunk = cdiv(nf, parts);
+        parts = cdiv(nf, chunk);
+        std::function<void(int, int, int, int)> split = [&](int lo, int hi, int p0, int p1) {
+            if (p1 - p0 <= 1 || hi - lo <= 1) {
+                std::sort(ids.begin() + lo, ids.begin() + hi);
+                return;
+            }
+            double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+            for (int k = lo; k < hi; ++k)
+                for (int c = 0; c < 3; ++c) {
+                    mn[c] = std::min(mn[c], X[3 * (size_t)ids[k] + c]);
+                    mx[c] = std::max(mx[c], X[3 * (size_t)ids[k] + c]);
+                }
+            int ax = 0;
+            for (int c = 1; c < 3; ++c) if (mx[c] - mn[c] > mx[ax] - mn[ax]) ax = c;
+            const int pm = (p0 + p1) / 2;
+            const int mid = std::min(hi, lo + (pm - p0) * chunk);
+            std::nth_element(ids.begin() + lo, ids.begin() + mid, ids.begin() + hi, [&](int a, int b) {
+                const double xa = X[3 * (size_t)a + ax], xb = X[3 * (size_t)b + ax];
+                return xa < xb || (xa == xb && a < b);
+            });
+            split(lo, mid, p0, pm);
+            split(mid, hi, pm, p1);
+        };
+        split(0, nf, 0, parts);
+        std::vector<int> patch(n_nodes, -1);
+        for (int k = 0; k < nf; ++k) patch[ids[k]] = k / chunk;
+        std::vector<char> exported(n_nodes, 0);
+        for (int64_t e = 0; e < n_tets; ++e) {
+            const int64_t* t = tets + 4 * e;
+            for (int a = 0; a < 4; ++a)
+                for (int b = 0; b < 4; ++b) {
+                    const int pa = patch[t[a]], pb = patch[t[b]];
+                    if (pa >= 0 && pb >= 0 && pa != pb) exported[t[a]] = 1;
+                }
+        }
+        for (int p = 0; p < parts; ++p) {
+            const int lo = p * chunk, hi = std::min(nf, lo + chunk);
+            std::stable_partition(ids.begin() + lo, ids.begin() + hi, [&](int v) { return exported[v] != 0; });
+        }
     }
 
     int init(const vkpd_mesh_desc* d, const vkpd_config* c) override {
@@ -340,7 +390,10 @@ struct Ctx : CtxBase {
                 if (id < 0 || id >= n) return fail(VKPD_EINVAL, "tet node index out of range");
             }
         }
-        // internal order: free nodes (caller order), then pins (pin order)
+        // internal order: free nodes, then pins (pin order).  With rest positions the free
+        // nodes are grouped into compact patches by recursive coordinate bisection, one patch
+        // per solver CTA (its rows' neighbours then mostly live in the same CTA); without,
+        // caller order.
         std::vector<int> ioo(n, -1);
         std::vector<char> pinned(n, 0);
         for (int k = 0; k < nP; ++k) {
@@ -349,10 +402,18 @@ struct Ctx : CtxBase {
             if (pinned[id]) return fail(VKPD_EINVAL, "duplicate pin index");
             pinned[id] = 1;
         }
+        CK(cudaSetDevice(device));
+        CK(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, device));
         nF = 0;
-        for (int j = 0; j < n; ++j) if (!pinned[j]) ioo[j] = nF++;
+        std::vector<int> free_ids;
+        for (int j = 0; j < n; ++j) if (!pinned[j]) free_ids.push_back(j);
+        nF = (int)free_ids.size();
+        part_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : std::min(n_sms, std::max(1, cdiv(nF, 32)));
+        if (d->nodes != nullptr && nF > 0) patch_order(d->nodes, d->tets, d->n_tets, n, free_ids, part_blocks);
+        for (int k = 0; k < nF; ++k) ioo[free_ids[k]] = k;
         for (int k = 0; k < nP; ++k) ioo[d->pins[k]] = nF + k;
         int_of_orig_h = ioo;
+        set_free_perm();
         std::vector<int4> tets_h(nE);
         for (int e = 0; e < nE; ++e)
             tets_h[e] = make_int4(ioo[d->tets[4 * (size_t)e]], ioo[d->tets[4 * (size_t)e + 1]],
@@ -425,8 +486,6 @@ struct Ctx : CtxBase {
             wsum[e] = vv * (d->gamma_s[e] + d->gamma_v[e]);
         }
 
-        CK(cudaSetDevice(device));
-        CK(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, device));
         CK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
         stream = own_stream;
         cudaStream_t s = stream;
@@ -591,10 +650,200 @@ struct Ctx : CtxBase {
         double g = 1.0;
         std::memcpy(&g, &gb, sizeof g);
         g += 1.0;
+        gersh = (g > 0.0 && std::isfinite(g)) ? g : 2.0;
         poly_omega = (g > 0.0 && std::isfinite(g)) ? std::min(1.0, 1.9 / g) : 0.5;
         if (ell_kd.n != (size_t)std::max(1, ell_w) * nF) CK(ell_kd.alloc((size_t)std::max(1, ell_w) * nF));
         vk::k_scale_ell<T><<<cdiv(nF, 256), 256, 0, s>>>(nF, ell_w, ell_col.p, ell_val.p, inv_diag.p, ell_kd.p);
         CK(cudaGetLastError());
+        if (cheb) if (int rc = spectrum_low()) return rc;
+        if (cheb && pcg_blocks > 0) if (int rc = build_cheb_neighbours()) return rc;
+        return VKPD_OK;
+    }
+
+    // lambda_min of D^-1 K_ff for the Chebyshev solver: rigorous lower bound min_i (m_i/dt^2)/K_ii
+    // (K - M/dt^2 is PSD), and the smallest Ritz value of 80 Lanczos steps on D^-1/2 K_ff D^-1/2
+    // (an upper estimate that converges fast at the spectrum's end); the solver uses
+    // max(bound, 0.97 * Ritz).  Its residual check keeps the stopping rule exact either way.
+    int spectrum_low() {
+        cudaStream_t s = stream;
+        std::vector<double> dg(nF), md(n);
+        CK(cudaMemcpyAsync(dg.data(), diag64.p, sizeof(double) * nF, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(md.data(), md64k.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double lb = 1.0;
+        for (int i = 0; i < nF; ++i) lb = std::min(lb, md[i] / dg[i]);
+        lam_min_bound = std::max(0.0, lb);
+        const int m = std::min(80, nF);
+        DBuf<double> v0, v1, w, al, be;
+        CK(v0.alloc(nF)); CK(v1.alloc(nF)); CK(w.alloc(nF)); CK(al.alloc(m + 1)); CK(be.alloc(m + 2));
+        CK(cudaMemsetAsync(al.p, 0, sizeof(double) * (m + 1), s));
+        CK(cudaMemsetAsync(be.p, 0, sizeof(double) * (m + 2), s));
+        vk::LanczosArgs<T> la;
+        la.nF = nF; la.ell_w = ell_w; la.m = m; la.ell_col = ell_col.p; la.ell_val = ell_val.p;
+        la.diag64 = diag64.p; la.v0 = v0.p; la.v1 = v1.p; la.w = w.p; la.partials = partials.p;
+        la.alpha = al.p; la.beta = be.p;
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_lanczos<T>, 512, 0));
+        const int blocks = std::max(1, std::min(occ * n_sms, std::min(pcg_blocks, cdiv(nF, 512))));
+        void* args[] = {&la};
+        CK(cudaLaunchCooperativeKernel((const void*)vk::k_lanczos<T>, dim3(blocks), dim3(512), args, 0, s));
+        std::vector<double> a(m + 1), b(m + 2);
+        CK(cudaMemcpyAsync(a.data(), al.p, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(b.data(), be.p, sizeof(double) * (m + 2), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        int mm = m;
+        for (int j = 0; j < m; ++j)
+            if (!(b[j + 1] > 0.0)) { mm = j + 1; break; }
+        const double ritz = tridiag_min_eig(a.data(), b.data() + 1, mm);
+        lam_min = std::max(lam_min_bound, 0.97 * ritz);
+        if (!(lam_min > 0.0) || !(lam_min < gersh)) lam_min = std::max(lam_min_bound, 1e-6);
+        return VKPD_OK;
+    }
+    // smallest eigenvalue of the symmetric tridiagonal (diag a[0..m), off-diag b[0..m-1)) by bisection
+    // on the Sturm count
+    static double tridiag_min_eig(const double* a, const double* b, int m) {
+        double lo = a[0], hi = a[0];
+        for (int i = 0; i < m; ++i) {
+            const double r = (i > 0 ? std::fabs(b[i - 1]) : 0.0) + (i + 1 < m ? std::fabs(b[i]) : 0.0);
+            lo = std::min(lo, a[i] - r);
+            hi = std::max(hi, a[i] + r);
+        }
+        auto count_below = [&](double x) {
+            int c = 0;
+            double q = a[0] - x;
+            if (q < 0) ++c;
+            for (int i = 1; i < m; ++i) {
+                if (q == 0.0) q = 1e-300;
+                q = a[i] - x - b[i - 1] * b[i - 1] / q;
+                if (q < 0) ++c;
+            }
+            return c;
+        };
+        for (int it = 0; it < 200; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (count_below(mid) >= 1) hi = mid; else lo = mid;
+        }
+        return 0.5 * (lo + hi);
+    }
+
+    size_t cheb_smem_bytes() const { return vk::cheb_smem_bytes<T>(); }
+    // Per CTA (rows [b*chunk, (b+1)*chunk)): the CTAs owning the columns its rows read (the
+    // neighbour flags it waits on), its halo (those rows themselves, staged in shared memory
+    // each step) and every ELL column's shared-memory slot.  The register path needs one row
+    // per thread and the staged image within the shared-memory limit.
+    int cheb_halo_max = 0;
+    DBuf<int> cheb_slot, cheb_halo_ptr, cheb_halo;
+    DBuf<T> cheb_val, cheb_kdiag;
+    DBuf<int> cheb_nexp;
+    int build_cheb_neighbours() {
+        const int chunk = cdiv(std::max(1, nF), pcg_blocks);
+        std::vector<int> ecol((size_t)ell_w * nF);
+        std::vector<T> evals((size_t)ell_w * nF);
+        if (nF > 0) {
+            CK(cudaMemcpy(ecol.data(), ell_col.p, ecol.size() * sizeof(int), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(evals.data(), ell_val.p, evals.size() * sizeof(T), cudaMemcpyDeviceToHost));
+        }
+        // per row: the off-diagonal entries in a canonical order (by caller-order index offset,
+        // so the rows of a warp, which are neighbours in the mesh, take the same direction at the
+        // same position and hit consecutive shared-memory slots), and the diagonal
+        std::vector<int> orig_of_int(n);
+        for (int j = 0; j < n; ++j) orig_of_int[int_of_orig_h[j]] = j;
+        const size_t nn1 = std::max(1, nF);
+        std::vector<int> ocol((size_t)vk::kChebOff * nn1, -1);
+        std::vector<T> oval((size_t)vk::kChebOff * nn1, T(0));
+        std::vector<T> kd(nn1, T(0));
+        bool fits = true;
+        {
+            std::vector<std::pair<long long, int>> ent;
+            for (int i = 0; i < nF; ++i) {
+                ent.clear();
+                for (int sl = 0; sl < ell_w; ++sl) {
+                    const size_t e = (size_t)sl * nF + i;
+                    if (ecol[e] == i) { kd[i] += evals[e]; continue; }
+                    ent.push_back({(long long)orig_of_int[ecol[e]] - orig_of_int[i], sl});
+                }
+                if ((int)ent.size() > vk::kChebOff) { fits = false; continue; }
+                std::sort(ent.begin(), ent.end());
+                for (size_t o = 0; o < ent.size(); ++o) {
+                    const size_t e = (size_t)ent[o].second * nF + i;
+                    ocol[o * nF + i] = ecol[e];
+                    oval[o * nF + i] = evals[e];
+                }
+            }
+        }
+        // per CTA: neighbour CTAs, halo rows (slots assigned position-major, then by row, so a
+        // warp's halo reads are consecutive too) and every entry's slot
+        std::vector<int> ptr(pcg_blocks + 1, 0), lst, hptr(pcg_blocks + 1, 0), hl;
+        std::vector<int> oslot((size_t)vk::kChebOff * nn1);
+        std::vector<char> seen(pcg_blocks, 0);
+        std::vector<int> hslot(nn1, -1);
+        cheb_halo_max = 0;
+        for (int b = 0; b < pcg_blocks; ++b) {
+            std::fill(seen.begin(), seen.end(), 0);
+            seen[b] = 1;
+            const int r0 = b * chunk, r1 = std::min(nF, r0 + chunk);
+            const int h0 = (int)hl.size();
+            for (int o = 0; o < vk::kChebOff; ++o)
+                for (int i = r0; i < r1; ++i) {
+                    const int c = ocol[(size_t)o * nF + i];
+                    if (c < 0) { oslot[(size_t)o * nF + i] = i - r0; continue; }      // pad: own row, value 0
+                    if (c >= r0 && c < r1) { oslot[(size_t)o * nF + i] = c - r0; continue; }
+                    const int ow = c / chunk;
+                    if (!seen[ow]) { seen[ow] = 1; lst.push_back(ow); }
+                    if (hslot[c] < 0) { hslot[c] = (int)hl.size() - h0; hl.push_back(c); }
+                    oslot[(size_t)o * nF + i] = pcg_threads + hslot[c];
+                }
+            if (!fits) {      // rows beyond kChebOff entries: neighbour sets from the full ELL
+                for (int sl = 0; sl < ell_w; ++sl)
+                    for (int i = r0; i < r1; ++i) {
+                        const int c = ecol[(size_t)sl * nF + i];
+                        if (c >= r0 && c < r1) continue;
+                        const int ow = c / chunk;
+                        if (!seen[ow]) { seen[ow] = 1; lst.push_back(ow); }
+                    }
+            }
+            for (int j = h0; j < (int)hl.size(); ++j) hslot[hl[j]] = -1;
+            ptr[b + 1] = (int)lst.size();
+            hptr[b + 1] = (int)hl.size();
+            cheb_halo_max = std::max(cheb_halo_max, (int)hl.size() - h0);
+        }
+        if (lst.empty()) lst.push_back(0);
+        if (hl.empty()) hl.push_back(0);
+        // exported rows (read by another CTA) must lead each CTA's range for the early publish;
+        // otherwise the CTA treats all its rows as exported
+        std::vector<char> exp_row(nn1, 0);
+        for (int j = 0; j < hptr[pcg_blocks]; ++j) exp_row[hl[j]] = 1;
+        std::vector<int> nexp(pcg_blocks, 0);
+        for (int b = 0; b < pcg_blocks; ++b) {
+            const int r0 = b * chunk, r1 = std::min(nF, r0 + chunk);
+            int e = 0;
+            while (r0 + e < r1 && exp_row[r0 + e]) ++e;
+            for (int r = r0 + e; r < r1; ++r)
+                if (exp_row[r]) { e = r1 - r0; break; }
+            nexp[b] = std::max(0, e);
+        }
+        CK(cheb_nexp.alloc(pcg_blocks)); CK(cheb_nexp.upload(nexp.data(), nexp.size(), stream));
+        int max_smem = 0;
+        CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        cheb_reg = fits && chunk <= pcg_threads && pcg_threads <= vk::kChebMaxThreads &&
+                   pcg_threads + cheb_halo_max <= vk::kChebSlots && cheb_smem_bytes() + 4096 <= (size_t)max_smem;
+        if (cheb_reg) {
+            CK(cudaFuncSetAttribute(vk::k_cheb_reg<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)cheb_smem_bytes()));
+            int o = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, vk::k_cheb_reg<T>, pcg_threads, cheb_smem_bytes()));
+            if (o * n_sms < pcg_blocks) cheb_reg = false;
+        }
+        CK(cheb_nbr_ptr.alloc(pcg_blocks + 1)); CK(cheb_nbr_ptr.upload(ptr.data(), ptr.size(), stream));
+        CK(cheb_nbr.alloc(lst.size())); CK(cheb_nbr.upload(lst.data(), lst.size(), stream));
+        CK(cheb_halo_ptr.alloc(pcg_blocks + 1)); CK(cheb_halo_ptr.upload(hptr.data(), hptr.size(), stream));
+        CK(cheb_halo.alloc(hl.size())); CK(cheb_halo.upload(hl.data(), hl.size(), stream));
+        CK(cheb_slot.alloc(oslot.size())); CK(cheb_slot.upload(oslot.data(), oslot.size(), stream));
+        CK(cheb_val.alloc(oval.size())); CK(cheb_val.upload(oval.data(), oval.size(), stream));
+        CK(cheb_kdiag.alloc(kd.size())); CK(cheb_kdiag.upload(kd.data(), kd.size(), stream));
+        CK(cheb_flags.alloc((size_t)32 * pcg_blocks));
+        CK(cudaMemsetAsync(cheb_flags.p, 0, sizeof(unsigned int) * 32 * pcg_blocks, stream));
+        CK(cudaStreamSynchronize(stream));
         return VKPD_OK;
     }
     // new per-tet material (MaterialField): weights of the local step, K re-assembled on the
@@ -634,51 +883,40 @@ struct Ctx : CtxBase {
             CK(b->alloc(std::max(1, nF)));
             CK(cudaMemsetAsync(b->p, 0, std::max(1, nF) * sizeof(V4), s));
         }
-        // one row per thread where possible (each extra row per thread adds a full memory round
-        // trip to every solver phase): CTA size = rows per SM rounded up to a warp, <= 768
-        pcg_threads = std::max(128, std::min(768, 32 * cdiv(cdiv(std::max(1, nF), n_sms), 32)));
-        if (const char* pt = getenv("VKPD_PCG_THREADS")) pcg_threads = std::max(64, std::min(768, atoi(pt)));
-        const char* pv = getenv("VKPD_PCG");
-        pcg_classic = !(pv && std::string(pv) == "pipe");   // classic measured faster at C3
-        pcg_poly = !(pv && (std::string(pv) == "jacobi" || std::string(pv) == "pipe"));
-        if (!pcg_classic) pcg_threads = std::min(pcg_threads, 512);   // the pipelined kernel's bound
-        if (const char* ev = getenv("VKPD_ROBUST_AUX")) robust_handoff = atoi(ev) != 0;
-        const char* rb = getenv("VKPD_ROBUST");
-        robust_quad = rb && std::string(rb) == "quad";
-        robust_tasks = !(rb && (std::string(rb) == "ws" || std::string(rb) == "quad")) && robust_handoff;
-        if (robust_tasks) {
-            CK(robust_res.alloc((size_t)16 * std::max(1, nE)));
-            CK(robust_ok.alloc((size_t)4 * std::max(1, nE)));
-            CK(robust_arrivals.alloc((size_t)std::max(1, cdiv(nE, 32))));
-            CK(cudaMemsetAsync(robust_arrivals.p, 0, sizeof(int) * std::max(1, cdiv(nE, 32)), stream));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&robust_task_blocks,
-                                                             vk::k_robust_tasks<T, vk::MODE_RESID>, 128, 0));
-            robust_task_blocks = std::max(1, robust_task_blocks);
-        }
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&robust_blocks, vk::k_robust_ws<T, vk::MODE_RESID>, 128, 0));
-        robust_blocks = std::max(1, robust_blocks);   // chunks are handed out dynamically: one resident wave
+        // one CTA per SM (fewer arrivals per grid barrier measured faster than 2 CTAs/SM at C3),
+        // all SMs busy, one row per thread where possible (each extra row per thread adds a
+        // full memory round trip to every solver phase): CTA size = rows per CTA rounded up to
+        // a warp, <= 768
+        pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks
+                   : part_blocks > 0 ? part_blocks : std::min(n_sms, std::max(1, cdiv(nF, 32)));
+        pcg_threads = std::max(128, std::min(768, 32 * cdiv(cdiv(std::max(1, nF), pcg_blocks), 32)));
+        solver_kind = c->solver != VKPD_SOLVER_AUTO ? c->solver
+                                                     : (sizeof(T) == 8 ? VKPD_SOLVER_CHEBYSHEV : VKPD_SOLVER_PCG_POLY);
+        if (solver_kind < VKPD_SOLVER_PCG_POLY || solver_kind > VKPD_SOLVER_PCG_JACOBI)
+            return fail(VKPD_EINVAL, "unknown solver kind");
+        pcg_poly = solver_kind == VKPD_SOLVER_PCG_POLY;
+        cheb = solver_kind == VKPD_SOLVER_CHEBYSHEV && nE > 0;     // PD residual form only
+        CK(robust_res.alloc((size_t)16 * std::max(1, nE)));
+        CK(robust_ok.alloc((size_t)4 * std::max(1, nE)));
+        CK(robust_arrivals.alloc((size_t)std::max(1, cdiv(nE, 32))));
+        CK(cudaMemsetAsync(robust_arrivals.p, 0, sizeof(int) * std::max(1, cdiv(nE, 32)), stream));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&robust_task_blocks, vk::k_robust_tasks<T, vk::MODE_RESID>,
+                                                         128, 0));
+        robust_task_blocks = std::max(1, robust_task_blocks);
         int occ = 0, occ2 = 0, occ3 = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vk::k_pcg<T>, pcg_threads, 0));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, vk::k_pcg_classic<T>, pcg_threads, 0));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, vk::k_pcg_poly<T>, pcg_threads, 0));
-        // co-residency of every kernel that may be launched (classic also serves contact frames)
-        occ = pcg_poly ? std::min(occ2, occ3) : pcg_classic ? occ2 : std::min(occ, occ2);
-        if (int rc = refresh_precond()) return rc;
-        if (occ < 1) return fail(VKPD_ECUDA, "persistent solver kernel cannot be resident");
-        // default: one row per thread, capped by co-residency
-        // default: at most one CTA per SM (fewer arrivals per grid barrier measured faster
-        // than 2 CTAs/SM at C3), at least one row per thread
-        pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks : std::min(cdiv(std::max(1, nF), pcg_threads), n_sms);
-        pcg_blocks = std::max(1, std::min(pcg_blocks, occ * n_sms));
-        {
-            const char* fz = getenv("VKPD_FUSED");
-            fused = fz && std::string(fz) == "1";
-            int occf = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, vk::k_frame<T>, kFrameThreads, 0));
-            frame_blocks = std::max(1, std::min(occf * n_sms, cdiv(std::max(std::max(nE, nF), 1), kFrameThreads)));
-            if (occf < 1) fused = false;
+        // co-residency of every kernel that may be launched on this grid
+        occ = std::min(occ2, occ3);
+        if (cheb) {
+            int o5 = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o5, vk::k_cheb<T>, pcg_threads, 0));
+            occ = std::min(occ, o5);
         }
-        CK(partials.alloc((size_t)16 * std::max(pcg_blocks, frame_blocks)));   // 2 parity banks x 8 doubles/CTA
+        if (occ < 1) return fail(VKPD_ECUDA, "persistent solver kernel cannot be resident");
+        pcg_blocks = std::max(1, std::min(pcg_blocks, occ * n_sms));
+        CK(partials.alloc((size_t)16 * pcg_blocks));   // 2 parity banks x 8 doubles/CTA
+        if (int rc = refresh_precond()) return rc;
         CK(scal.alloc(16));
         CK(bar.alloc(1));
         CK(cudaMemsetAsync(bar.p, 0, sizeof(vk::GridBar), s));
@@ -686,29 +924,20 @@ struct Ctx : CtxBase {
         CK(cudaMemsetAsync(iters.p, 0, 1024 * sizeof(int), s));
         CK(fail_iter.alloc(1));
         CK(robust_list.alloc(std::max(1, nE)));
-        if (robust_handoff) CK(robust_aux.alloc((size_t)24 * std::max(1, nE)));
-        CK(robust_count.alloc(2));   // [0] queued elements, [1] k_robust_ws chunk cursor
+        CK(robust_aux.alloc((size_t)24 * std::max(1, nE)));
+        CK(robust_count.alloc(2));   // [0] queued elements, [1] spare
         CK(pd_it.alloc(1));
-        {
-            const char* pw = getenv("VKPD_WARM");
-            if (pw) warm_rounds = std::max(0, std::min(32, atoi(pw)));
-            warm_start = warm_rounds > 0;
-        }
+        if (c->warm_rounds >= 0) warm_rounds = std::min(32, c->warm_rounds);
+        if (solver_kind == VKPD_SOLVER_PCG_JACOBI) warm_rounds = 0;
+        warm_start = warm_rounds > 0;
         CK(warm0.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
         CK(cudaMemsetAsync(warm0.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
-        if (const char* pr = getenv("VKPD_POLY_ROUNDS")) poly_rounds = std::max(0, atoi(pr));
-        if (const char* pi = getenv("VKPD_ROBUST_IF")) robust_if_node = atoi(pi) != 0;
-        if (const char* pu = getenv("VKPD_UNROLL")) unroll_env = std::max(0, std::min(64, atoi(pu)));
-        unroll_rounds = unroll_env > 0 ? unroll_env : 0;
-        if (const char* px = getenv("VKPD_WARM_EXTRAP_ROUNDS")) warm_extrap_rounds = std::max(0, atoi(px));
-        if (const char* pe = getenv("VKPD_WARM_EXTRAP")) { warm_beta = atof(pe); warm_extrap = warm_beta != 0.0; }
+        unroll_cfg = c->unroll_rounds >= 0 ? std::min(64, c->unroll_rounds) : -1;
+        unroll_rounds = unroll_cfg > 0 ? unroll_cfg : 0;
+        pd_early_exit = c->pd_early_exit != 0;
         if (warm_extrap) {
             CK(warm1.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
             CK(cudaMemsetAsync(warm1.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
-        }
-        {
-            const char* pe = getenv("VKPD_PD_EXIT");
-            pd_early_exit = !(pe && std::string(pe) == "0");
         }
         CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), s));
         CK(pstats.alloc(1));
@@ -746,6 +975,7 @@ struct Ctx : CtxBase {
         for (int j = 0; j < n; ++j) if (!pinned[j]) ioo[j] = nF++;
         for (int k = 0; k < nP; ++k) ioo[pins[k]] = nF + k;
         int_of_orig_h = ioo;
+        set_free_perm();
         std::vector<int> orig_of_int(n);
         for (int j = 0; j < n; ++j) orig_of_int[ioo[j]] = j;
         ell_w = 0;
@@ -920,7 +1150,7 @@ struct Ctx : CtxBase {
         la.slot4 = slot4.p;
         la.stats = pstats.p; la.F_out = la.R_out = la.V_out = nullptr;
         la.robust_list = robust_list.p; la.robust_count = robust_count.p;
-        la.robust_aux = robust_handoff ? robust_aux.p : nullptr;
+        la.robust_aux = robust_aux.p;
         la.robust_if = 0;
         return la;
     }
@@ -930,14 +1160,9 @@ struct Ctx : CtxBase {
         if (reset) CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
         vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
         CK(cudaGetLastError());
-        // 4 CTAs/SM: enough lanes for the heavy frames, cheap when the queue is empty
-        if (robust_quad)
-            vk::k_robust4<T, vk::MODE_RESID><<<4 * n_sms, 128, 0, stream>>>(la);
-        else if (robust_tasks) {
-            vk::k_robust_tasks<T, vk::MODE_RESID><<<robust_task_blocks * n_sms, 128, 0, stream>>>(
-                la, robust_res.p, robust_ok.p, robust_arrivals.p, std::max(1, nE));
-        } else
-            vk::k_robust_ws<T, vk::MODE_RESID><<<robust_blocks * n_sms, 128, 0, stream>>>(la);
+        // one resident wave of (chunk, start) tasks: cheap when the queue is empty
+        vk::k_robust_tasks<T, vk::MODE_RESID><<<robust_task_blocks * n_sms, 128, 0, stream>>>(
+            la, robust_res.p, robust_ok.p, robust_arrivals.p, std::max(1, nE));
         CK(cudaGetLastError());
         return VKPD_OK;
     }
@@ -955,12 +1180,18 @@ struct Ctx : CtxBase {
         pa.pd_iter_dev = nullptr; pa.loop_handle = 0; pa.loop_iterations = 0; pa.robust_if = 0;
         pa.first_stop = nullptr;
         pa.rounds = init == vk::INIT_PD ? &pstats.p->pd_rounds : nullptr;
-        pa.warm = (init == vk::INIT_PD && pcg_poly && warm_start) ? warm0.p : nullptr;
+        pa.warm = (init == vk::INIT_PD && (pcg_poly || cheb) && warm_start) ? warm0.p : nullptr;
         pa.warm_rounds = warm_rounds;
         pa.warm_prev = (pa.warm != nullptr && warm_extrap) ? warm1.p : nullptr;
         pa.warm_beta = warm_beta;
         pa.warm_extrap_rounds = warm_extrap_rounds;
-        pa.poly_rounds = poly_rounds;
+        pa.poly_rounds = 0;
+        pa.flags = cheb_flags.p; pa.cheb_nbr_ptr = cheb_nbr_ptr.p; pa.cheb_nbr = cheb_nbr.p;
+        pa.cheb_lmin = lam_min; pa.cheb_lmax = gersh;
+        pa.cheb_slot = cheb_slot.p; pa.cheb_val = cheb_val.p; pa.cheb_kdiag = cheb_kdiag.p;
+        pa.cheb_nexp = cheb_nexp.p;
+        pa.cheb_halo_ptr = cheb_halo_ptr.p; pa.cheb_halo = cheb_halo.p;
+        pa.cheb_halo_max = cheb_halo_max;
         pa.h = ss.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
         if (init == vk::INIT_PD && ncoll > 0) {
             pa.inv_diag = inv_diag_c.p; pa.cdiag = cdiag.p; pa.cb = cb.p; pa.coll = coll_d.p; pa.ncoll = ncoll;
@@ -979,35 +1210,17 @@ struct Ctx : CtxBase {
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        if (cheb && pa.init == vk::INIT_PD) {
+            if (!cheb_reg) return cudaLaunchKernelEx(&cfg, vk::k_cheb<T>, pa);
+            cfg.dynamicSmemBytes = cheb_smem_bytes();
+            return cudaLaunchKernelEx(&cfg, vk::k_cheb_reg<T>, pa);
+        }
         if (pcg_poly) return cudaLaunchKernelEx(&cfg, vk::k_pcg_poly<T>, pa);
-        if (pcg_classic || pa.ncoll > 0) return cudaLaunchKernelEx(&cfg, vk::k_pcg_classic<T>, pa);
-        return cudaLaunchKernelEx(&cfg, vk::k_pcg<T>, pa);
+        return cudaLaunchKernelEx(&cfg, vk::k_pcg_classic<T>, pa);
     }
 
     // enqueue one frame on `stream`; events (optional) bracket local / global launches
     int enqueue_frame(int iterations, double damping, std::vector<cudaEvent_t>* ev) {
-        if (fused && ev == nullptr && nE > 0 && nF > 0 && ncoll == 0) {
-            vk::FrameArgs<T> fa;
-            fa.la = local_args(x.p);
-            fa.pa = pcg_args(vk::INIT_PD, 0, iters.p);
-            fa.n = n; fa.nF = nF; fa.iterations = iterations;
-            fa.dt = (T)dt; fa.damp_over_dt = (T)(damping / dt);
-            fa.dt2_inv_m = dt2_inv_m.p; fa.f = has_forces ? f.p : nullptr; fa.pin_tgt = pin_tgt.p;
-            fa.x = x.p; fa.v = v.p; fa.x_start = x_start.p; fa.v_start = v_start.p; fa.xhat = xhat.p;
-            fa.fail_iter = fail_iter.p; fa.iters = iters.p;
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(frame_blocks);
-            cfg.blockDim = dim3(kFrameThreads);
-            cfg.stream = stream;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeCooperative;
-            attr[0].val.cooperative = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&cfg, vk::k_frame<T>, fa));
-            CK(cudaMemcpyAsync(h_fail, fail_iter.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-            return VKPD_OK;
-        }
         const int nb = cdiv(n, 256);
         vk::k_prologue<T><<<nb, 256, 0, stream>>>(n, nF, (T)dt, dt2_inv_m.p, has_forces ? f.p : nullptr,
                                                   pin_tgt.p, x.p, v.p, x_start.p, v_start.p, xhat.p,
@@ -1038,7 +1251,7 @@ struct Ctx : CtxBase {
                 int cgi = -1;
                 CK(cudaMemcpyAsync(&cgi, iters.p + it, sizeof(int), cudaMemcpyDeviceToHost, stream));
                 CK(cudaStreamSynchronize(stream));
-                if (cgi == 0 && !(it < warm_rounds && warm_start && pcg_poly)) {   // a warm round moves x
+                if (cgi == 0 && !(it < warm_rounds && warm_start && (pcg_poly || cheb))) {   // a warm round moves x
                     CK(cudaMemsetAsync(iters.p + it + 1, 0, sizeof(int) * (iterations - it - 1), stream));
                     last_exec_rounds = it + 1;
                     break;
@@ -1104,50 +1317,13 @@ struct Ctx : CtxBase {
         cudaStream_t outer = stream;
         stream = body_stream;
         int rc = VKPD_OK;
-        unsigned long long hif_v = 0;
         {
-            vk::LocalArgs<T> la = local_args(x.p);
-            if (robust_if_node && robust_tasks) {
-                // local step, then the robust pass inside an IF node that the local step sets
-                // only when it queued a tet (quiet rounds skip the launch); the solver clears it
-                cudaGraphConditionalHandle hif;
-                CK(cudaGraphConditionalHandleCreate(&hif, body, 0, cudaGraphCondAssignDefault));
-                hif_v = (unsigned long long)hif;
-                la.robust_if = hif_v;
-                vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
-                CK(cudaGetLastError());
-                cudaStreamCaptureStatus bst;
-                cudaGraph_t bg = nullptr;
-                const cudaGraphNode_t* bdeps = nullptr;
-                size_t nbdeps = 0;
-                CK(cudaStreamGetCaptureInfo(stream, &bst, nullptr, &bg, &bdeps, &nbdeps));
-                cudaGraphNodeParams ip = {};
-                ip.type = cudaGraphNodeTypeConditional;
-                ip.conditional.handle = hif;
-                ip.conditional.type = cudaGraphCondTypeIf;
-                ip.conditional.size = 1;
-                cudaGraphNode_t inode;
-                CK(cudaGraphAddNode(&inode, bg, bdeps, nbdeps, &ip));
-                if (!if_stream) CK(cudaStreamCreateWithFlags(&if_stream, cudaStreamNonBlocking));
-                CK(cudaStreamBeginCaptureToGraph(if_stream, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                                 cudaStreamCaptureModeThreadLocal));
-                la.robust_if = 0;
-                vk::k_robust_tasks<T, vk::MODE_RESID><<<robust_task_blocks * n_sms, 128, 0, if_stream>>>(
-                    la, robust_res.p, robust_ok.p, robust_arrivals.p, std::max(1, nE));
-                cudaGraph_t ig = nullptr;
-                const cudaError_t ie = cudaGetLastError();
-                const cudaError_t ee = cudaStreamEndCapture(if_stream, &ig);
-                CK(ie);
-                CK(ee);
-                CK(cudaStreamUpdateCaptureDependencies(stream, &inode, 1, cudaStreamSetCaptureDependencies));
-            } else {
-                rc = launch_local_resid(la, false);
-            }
+            const vk::LocalArgs<T> la = local_args(x.p);
+            rc = launch_local_resid(la, false);
             if (rc == VKPD_OK) {
                 vk::PcgArgs<T> pa = pcg_args(vk::INIT_PD, 0, iters.p);
                 pa.reset_count = robust_count.p;
                 pa.pd_iter_dev = pd_it.p;
-                pa.robust_if = hif_v;
                 pa.first_stop = first_stop.p;
                 pa.loop_handle = (unsigned long long)h;
                 pa.loop_iterations = iterations;
@@ -1174,7 +1350,7 @@ struct Ctx : CtxBase {
     // samples, then every 64), so unrolled rounds are almost never past the exit point (and when
     // they are, they are exact repeats).
     void adapt_unroll(int iterations) {
-        if (unroll_env >= 0 || !pd_early_exit) return;
+        if (unroll_cfg >= 0 || !pd_early_exit) return;
         const int need = *(volatile int*)h_stop;
         if (need <= 0) return;                                   // no frame finished yet
         stop_hist[stop_pos] = std::min(need, iterations);        // 0x7f7f7f7f: every round ran
@@ -1192,7 +1368,7 @@ struct Ctx : CtxBase {
         if (graph_exec) { cudaGraphExecDestroy(graph_exec); graph_exec = nullptr; }
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-        const bool loop = pd_early_exit && iterations >= 2 && nF > 0 && !(fused && ncoll == 0);
+        const bool loop = pd_early_exit && iterations >= 2 && nF > 0;
         int rc = loop ? enqueue_frame_loop(iterations, damping) : enqueue_frame(iterations, damping, nullptr);
         cudaError_t e = cudaStreamEndCapture(stream, &g);
         if (rc != VKPD_OK || e != cudaSuccess) {
@@ -1537,11 +1713,15 @@ struct Ctx : CtxBase {
     float cms_apply_ms = 0.f, cms_sweeps_ms = 0.f;
 
     // rows [0, m) of a V4 buffer from an (m, k) float64 host array, columns c0..c0+2
+    // rows in the caller's free order (m == nF) or pin order (m == nP) -> device rows
     int upload_rows(const double* h, int m, int k, int c0, V4* dst) {
         std::vector<double> pk((size_t)3 * std::max(1, m), 0.0);
         const int kc = std::min(3, k - c0);
-        for (int j = 0; j < m; ++j)
-            for (int c = 0; c < kc; ++c) pk[3 * (size_t)j + c] = h[(size_t)j * k + c0 + c];
+        const bool perm = m == nF && (int)free_perm.size() == nF;
+        for (int j = 0; j < m; ++j) {
+            const size_t r = perm ? (size_t)free_perm[j] : (size_t)j;
+            for (int c = 0; c < kc; ++c) pk[3 * r + c] = h[(size_t)j * k + c0 + c];
+        }
         if (m == 0) return VKPD_OK;
         CK(cudaMemcpyAsync(stage.p, pk.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, stream));
         k_rows_in<T><<<cdiv(m, 256), 256, 0, stream>>>(m, stage.p, dst);
@@ -1556,8 +1736,10 @@ struct Ctx : CtxBase {
         CK(cudaMemcpyAsync(tmp.data(), src, sizeof(V4) * m, cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
         const int kc = std::min(3, k - c0);
+        const bool perm = m == nF && (int)free_perm.size() == nF;
         for (int j = 0; j < m; ++j) {
-            const double v[3] = {(double)tmp[j].x, (double)tmp[j].y, (double)tmp[j].z};
+            const V4 t = tmp[perm ? free_perm[j] : j];
+            const double v[3] = {(double)t.x, (double)t.y, (double)t.z};
             for (int c = 0; c < kc; ++c) h[(size_t)j * k + c0 + c] = v[c];
         }
         return VKPD_OK;
@@ -1648,7 +1830,10 @@ struct Ctx : CtxBase {
         CK(cms_y.alloc((size_t)3 * std::max(1, m)));
         CK(cms_z.alloc((size_t)3 * std::max(1, m)));
         if (m > 0) {
-            CK(cudaMemcpy(cmsT.p, Tb, sizeof(double) * nF * (size_t)m, cudaMemcpyHostToDevice));
+            std::vector<double> Tp((size_t)nF * m);       // column-major, rows to internal order
+            for (int c = 0; c < m; ++c)
+                for (int j = 0; j < nF; ++j) Tp[(size_t)c * nF + free_perm[j]] = Tb[(size_t)c * nF + j];
+            CK(cudaMemcpy(cmsT.p, Tp.data(), sizeof(double) * nF * (size_t)m, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(cmsKinv.p, Kinv, sizeof(double) * (size_t)m * m, cudaMemcpyHostToDevice));
         }
         return VKPD_OK;
@@ -1675,7 +1860,7 @@ struct Ctx : CtxBase {
         rw.resize(std::max(1, rp[ndom]));
         for (int k = 0; k < rp[ndom]; ++k) {
             if (rows[k] < 0 || rows[k] >= nF) return fail(VKPD_EINVAL, "block row out of range");
-            rw[k] = (int)rows[k];
+            rw[k] = free_perm[rows[k]];
         }
         cm.resize(std::max(1, cp[ndom]));
         std::vector<std::vector<int>> src(m);
@@ -1686,7 +1871,7 @@ struct Ctx : CtxBase {
         }
         for (int64_t j = 0; j < nb; ++j) {
             if (bnd[j] < 0 || bnd[j] >= nF) return fail(VKPD_EINVAL, "boundary row out of range");
-            bd[j] = (int)bnd[j];
+            bd[j] = free_perm[bnd[j]];
         }
         std::vector<int> ysp(m + 1, 0), ys;
         for (int g = 0; g < m; ++g) { ys.insert(ys.end(), src[g].begin(), src[g].end()); ysp[g + 1] = (int)ys.size(); }
@@ -1779,11 +1964,8 @@ struct Ctx : CtxBase {
         for (int it = 0; it < iterations && nF > 0; ++it) {
             CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
             vk::k_local<T, vk::MODE_RHS, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
-            if (robust_tasks)
-                vk::k_robust_tasks<T, vk::MODE_RHS><<<robust_task_blocks * n_sms, 128, 0, stream>>>(
-                    la, robust_res.p, robust_ok.p, robust_arrivals.p, std::max(1, nE));
-            else
-                vk::k_robust_ws<T, vk::MODE_RHS><<<robust_blocks * n_sms, 128, 0, stream>>>(la);
+            vk::k_robust_tasks<T, vk::MODE_RHS><<<robust_task_blocks * n_sms, 128, 0, stream>>>(
+                la, robust_res.p, robust_ok.p, robust_arrivals.p, std::max(1, nE));
             vk::k_cms_b<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, inc_ptr.p, corner.p, m_dt2.p, xhat.p, tmp4a.p);
             k_rhs_minus_fp<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, tmp4a.p, fp_ptr.p, fp_col.p, fp_val.p, x.p + nF,
                                                                 rhs.p);

@@ -18,8 +18,10 @@ RuntimeError("... non-finite positions at iteration {it}") on blow-up, any
 object with `.solve(B, pin_vals)` accepted as `solver=`.  All arithmetic runs
 in the CUDA library; nothing here falls back to the CPU.
 
-Extra keyword arguments (not in the reference): `precision` ("fp32" default,
-"fp64"), `tol` (relative residual of each global solve) and `max_iters`.
+Extra keyword arguments (not in the reference): `precision` ("fp64" default, the
+reference's arithmetic; "fp32" the fast path, within 1e-5 of the reference after one
+frame and 1e-3 after 100 frames, tests/test_gpu_parity.py), `tol` (relative residual
+of each global solve) and `max_iters`.
 
 Solver modes: "direct" is the exact global step (the reference's SuperLU),
 realised as a persistent CG on the device driven to `tol`; "cms" is the
@@ -128,7 +130,7 @@ def device_context(mesh, gammas, dt, pins=(), precision="fp32", tol=None, max_it
         ctx = _abi.Context(mesh.n_nodes if hasattr(mesh, "n_nodes") else len(mesh.nodes), mesh.tets,
                            mesh.shape_grad, mesh.volume, mesh.node_mass, gammas.gamma_s,
                            gammas.gamma_v, pins, dt, precision=precision, tol=tol,
-                           max_iters=max_iters, device=k[-1])
+                           max_iters=max_iters, device=k[-1], nodes=getattr(mesh, "nodes", None))
         _CACHE[k] = [gid, ctx]
         return ctx
     if hit[0] != gid:
@@ -317,7 +319,7 @@ class GlobalSolver:
 
 
 def pd_step(state, mesh, gammas, iterations=PD_ITERS_DEFAULT, forces=None, solver=None,
-            contact_stiffness=CONTACT_STIFFNESS, damping=1.0, precision="fp32", tol=None,
+            contact_stiffness=CONTACT_STIFFNESS, damping=1.0, precision="fp64", tol=None,
             max_iters=0):
     """One implicit-Euler step by local/global rounds (`pdsolver.py:257-304`); returns the state.
 
@@ -577,7 +579,7 @@ def newton_polish(mesh, gammas, x0, *, dt, pins=(), pin_vals=None, inertia_targe
 def simulate_mesh(mesh, gammas, steps, dt, forces=None, pins=(), pin_targets=None, colliders=(),
                   iterations=PD_ITERS_DEFAULT, solver_mode="direct", n_domains=2, modes_per_domain=20,
                   refine_sweeps=30, aggregation=2, chebyshev=False, damping=1.0, polish_tol=None,
-                  x0=None, precision="fp32", tol=None, max_iters=0, labels=None):
+                  x0=None, precision="fp64", tol=None, max_iters=0, labels=None):
     """Run a forward simulation and return the frame stack (steps, nV, 3) (`pdsolver.py:710-763`).
 
     pin_targets may be constant (nP, 3) or a per-step path (steps, nP, 3).

@@ -214,10 +214,11 @@ def test_simulate_pipelined_equals_frame_loop():
     rng = np.random.default_rng(4)
     fseq = np.stack([sc.forces * (1.0 + 0.05 * rng.normal()) for _ in range(steps)])
     path = np.stack([sc.pin_targets + np.array([0.0, 0.0, 2e-4 * k]) for k in range(steps)])
-    fr = pdsolver.simulate_mesh(m, sc.gammas, steps, sc.dt, forces=fseq, pins=sc.pins, pin_targets=path)
+    fr = pdsolver.simulate_mesh(m, sc.gammas, steps, sc.dt, forces=fseq, pins=sc.pins, pin_targets=path,
+                                precision="fp32")
     from paper_2405_12484_b200 import _abi
     ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s, sc.gammas.gamma_v,
-                       sc.pins, sc.dt, precision="fp32", tol=pdsolver.DEFAULT_TOL["fp32"])
+                       sc.pins, sc.dt, precision="fp32", tol=pdsolver.DEFAULT_TOL["fp32"], nodes=m.nodes)
     ctx.set_state(m.nodes)
     for k in range(steps):
         ctx.set_pin_targets(path[k])
@@ -266,12 +267,12 @@ def test_bit_identical_reruns(c1):
     assert np.array_equal(a, b)
 
 
-def _run_frames(sc, frames, precision, collect_every=1):
+def _run_frames(sc, frames, precision, collect_every=1, **cfg):
     from paper_2405_12484_b200 import _abi
     m = sc.mesh
     ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s,
                        sc.gammas.gamma_v, sc.pins, sc.dt, precision=precision,
-                       tol=pdsolver.DEFAULT_TOL[precision])
+                       tol=pdsolver.DEFAULT_TOL[precision], nodes=m.nodes, **cfg)
     ctx.set_state(m.nodes)
     ctx.set_pin_targets(sc.pin_targets)
     ctx.set_forces(sc.forces)
@@ -285,15 +286,13 @@ def _run_frames(sc, frames, precision, collect_every=1):
 
 
 @pytest.mark.parametrize("config,frames,precision", [("C2", 40, "fp32"), ("C2", 10, "fp64"), ("C3", 100, "fp32")])
-def test_pd_loop_early_exit_is_exact(monkeypatch, config, frames, precision):
+def test_pd_loop_early_exit_is_exact(config, frames, precision):
     """The graph's PD-iteration loop stops at the first solve that needs zero CG
     iterations (x unchanged, so the remaining rounds are exact repeats).  Same
     bits as running every round; C3 to frame 100 crosses into the frames with
     robust-path tets."""
     sc = scenes.make_scene(config)
-    monkeypatch.setenv("VKPD_PD_EXIT", "0")
-    a, ia = _run_frames(sc, frames, precision, collect_every=5)
-    monkeypatch.delenv("VKPD_PD_EXIT")
+    a, ia = _run_frames(sc, frames, precision, collect_every=5, pd_early_exit=False)
     b, ib = _run_frames(sc, frames, precision, collect_every=5)
     assert np.array_equal(a, b)
     assert ia == ib
@@ -301,31 +300,56 @@ def test_pd_loop_early_exit_is_exact(monkeypatch, config, frames, precision):
         assert any(0 in it for it in ib)     # the exit was actually taken (fp64 at 1e-12 rarely exits)
 
 
-@pytest.mark.parametrize("unroll", ["3", "7"])
-def test_unrolled_rounds_are_exact(monkeypatch, unroll):
+@pytest.mark.parametrize("unroll", [3, 7])
+def test_unrolled_rounds_are_exact(unroll):
     """Leading PD rounds captured as plain graph nodes ahead of the WHILE node (fixed counts here;
     adaptive by default): a round past the exit point is an exact repeat, so positions and the
     per-round CG iterations of the executed rounds are the same bits as the loop alone."""
     sc = scenes.make_scene("C2")
-    monkeypatch.setenv("VKPD_UNROLL", "0")
-    a, ia = _run_frames(sc, 30, "fp32", collect_every=3)
-    monkeypatch.setenv("VKPD_UNROLL", unroll)
-    b, ib = _run_frames(sc, 30, "fp32", collect_every=3)
+    a, ia = _run_frames(sc, 30, "fp32", collect_every=3, unroll_rounds=0)
+    b, ib = _run_frames(sc, 30, "fp32", collect_every=3, unroll_rounds=unroll)
     assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("variant", ["ws", "quad"])
-def test_robust_pass_variants_bit_identical(monkeypatch, variant):
-    """The default robust pass ((chunk, start) tasks, per-chunk last-arrival select) and the
-    CTA warp-per-start / quad-per-element passes run the same starts and the same selection
-    (material.py:242-287): identical bits through the C3 fold frames (≈88K queued tets per
-    round from frame ~100)."""
-    sc = scenes.c3_sweater()
-    a, ia = _run_frames(sc, 115, "fp32", collect_every=5)
-    monkeypatch.setenv("VKPD_ROBUST", variant)
-    b, ib = _run_frames(sc, 115, "fp32", collect_every=5)
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-10), ("fp32", 2e-5)])
+def test_chebyshev_matches_cg(precision, tol):
+    """The two global-step solvers (Chebyshev semi-iteration with neighbour flags, the fp64
+    default; polynomial-preconditioned CG, the fp32 default) solve the same K_ff x = b to the
+    same residual tolerance: C2 after 20 frames they agree to the tolerance's accuracy."""
+    sc = scenes.make_scene("C2")
+    a, _ = _run_frames(sc, 20, precision, collect_every=20, solver="pcg")
+    b, ib = _run_frames(sc, 20, precision, collect_every=20, solver="chebyshev")
+    assert rel_l2(b[-1], a[-1]) < tol
+    assert sum(sum(it) for it in ib) > 0
+
+
+def test_chebyshev_reruns_bit_identical():
+    """No float atomics on the Chebyshev path: the neighbour flags only order the steps."""
+    sc = scenes.make_scene("C2")
+    a, ia = _run_frames(sc, 8, "fp64", collect_every=2, solver="chebyshev")
+    b, ib = _run_frames(sc, 8, "fp64", collect_every=2, solver="chebyshev")
     assert np.array_equal(a, b)
     assert ia == ib
+
+
+def test_chebyshev_without_rest_positions():
+    """Without rest positions the free nodes keep caller order (no patches, no exported-first
+    rows): same solution to the tolerance."""
+    from paper_2405_12484_b200 import _abi
+    sc = scenes.make_scene("C2")
+    m = sc.mesh
+    outs = []
+    for nodes in (m.nodes, None):
+        ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s,
+                           sc.gammas.gamma_v, sc.pins, sc.dt, precision="fp64", tol=1e-12, nodes=nodes,
+                           solver="chebyshev")
+        ctx.set_state(m.nodes)
+        ctx.set_pin_targets(sc.pin_targets)
+        ctx.set_forces(sc.forces)
+        for _ in range(5):
+            ctx.step(30)
+        outs.append(ctx.get_state()[0])
+    assert rel_l2(outs[1], outs[0]) < 1e-11
 
 
 def test_pin_path_and_per_step_forces(c1):

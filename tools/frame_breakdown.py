@@ -16,7 +16,7 @@ a = p.parse_args()
 sc = scenes.make_scene(a.config)
 m = sc.mesh
 ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s, sc.gammas.gamma_v,
-                   sc.pins, sc.dt, precision=a.precision, tol=a.tol or pdsolver.DEFAULT_TOL[a.precision])
+                   sc.pins, sc.dt, precision=a.precision, tol=a.tol or pdsolver.DEFAULT_TOL[a.precision], nodes=m.nodes)
 ctx.set_state(m.nodes)
 ctx.set_pin_targets(sc.pin_targets)
 ctx.set_forces(sc.forces)

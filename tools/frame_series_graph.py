@@ -17,7 +17,7 @@ a = p.parse_args()
 sc = scenes.make_scene(a.config)
 m = sc.mesh
 ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s, sc.gammas.gamma_v,
-                   sc.pins, sc.dt, precision=a.precision, tol=pdsolver.DEFAULT_TOL[a.precision])
+                   sc.pins, sc.dt, precision=a.precision, tol=pdsolver.DEFAULT_TOL[a.precision], nodes=m.nodes)
 stream = torch.cuda.Stream()
 ctx.set_stream(stream.cuda_stream)
 ctx.set_state(m.nodes)

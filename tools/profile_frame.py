@@ -15,7 +15,7 @@ sc = scenes.make_scene(a.config)
 m = sc.mesh
 ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s,
                    sc.gammas.gamma_v, sc.pins, sc.dt, precision=a.precision,
-                   tol=pdsolver.DEFAULT_TOL[a.precision], use_graph=False)
+                   tol=pdsolver.DEFAULT_TOL[a.precision], use_graph=False, nodes=m.nodes)
 ctx.set_state(m.nodes)
 ctx.set_pin_targets(sc.pin_targets)
 ctx.set_forces(sc.forces)

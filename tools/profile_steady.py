@@ -5,10 +5,12 @@ from paper_2405_12484_b200 import _abi, pdsolver, scenes  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--config", default="C3"); p.add_argument("--warm", type=int, default=10)
 p.add_argument("--frames", type=int, default=2); p.add_argument("--graph", type=int, default=1)
+p.add_argument("--precision", default="fp32"); p.add_argument("--solver", default="auto")
 a = p.parse_args()
 sc = scenes.make_scene(a.config); m = sc.mesh
 ctx = _abi.Context(m.n_nodes, m.tets, m.shape_grad, m.volume, m.node_mass, sc.gammas.gamma_s, sc.gammas.gamma_v,
-                   sc.pins, sc.dt, precision="fp32", tol=pdsolver.DEFAULT_TOL["fp32"], use_graph=bool(a.graph))
+                   sc.pins, sc.dt, precision=a.precision, tol=pdsolver.DEFAULT_TOL[a.precision], use_graph=bool(a.graph),
+                   solver=a.solver, nodes=m.nodes)
 ctx.set_state(m.nodes); ctx.set_pin_targets(sc.pin_targets); ctx.set_forces(sc.forces)
 for _ in range(a.warm + a.frames):
     ctx.step(sc.iterations)
