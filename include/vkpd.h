@@ -176,6 +176,15 @@ int vkpd_get_stats(vkpd_ctx* ctx, vkpd_stats* st);
 int vkpd_dev_residual(vkpd_ctx* ctx, const void* x_int, const void* xhat_int, void* r_free);
 int vkpd_dev_apply_K(vkpd_ctx* ctx, const void* X_int, void* Y_free);
 int vkpd_dev_inv_diag(vkpd_ctx* ctx, void* out_free);
+/*   dev_cheb_step: one step of the distributed Chebyshev solve (dd.py) on the free rows, fused:
+ *                 q = K_ff d_free + K_fp d_pinned (the pinned slots carry the halo), y += d,
+ *                 res -= q, dnext_free = c1 d + c2 D^-1 res (pdsolver.py:225-236 as an
+ *                 iteration; the rank's share of GlobalSolver.solve)                       */
+int vkpd_dev_cheb_step(vkpd_ctx* ctx, const void* d_int, void* res_free, void* y_free, void* dnext_int, double c1,
+                       double c2);
+/* Gershgorin bound of D^-1 K_ff (with_pinned_cols: rows of [K_ff K_fp], a rank's share of the
+ * global bound when the pinned slots are its halo) */
+int vkpd_get_gershgorin(vkpd_ctx* ctx, int with_pinned_cols, double* g);
 int vkpd_get_node_order(vkpd_ctx* ctx, int64_t* int_of_orig);
 int vkpd_get_sizes(vkpd_ctx* ctx, int64_t* n, int64_t* n_free, int64_t* n_pinned, int* precision);
 

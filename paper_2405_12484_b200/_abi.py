@@ -29,7 +29,7 @@ EXPORTS = (
     "vkpd_projection_jacobians", "vkpd_hess_create", "vkpd_hess_destroy", "vkpd_hess_set_gammas",
     "vkpd_hess_energy_grad", "vkpd_hess_gamma_jt", "vkpd_hess_linearize", "vkpd_hess_csr",
     "vkpd_hess_apply", "vkpd_hess_solve", "vkpd_cms_set_blocks", "vkpd_cms_timing", "vkpd_time_local",
-    "vkpd_step_cms", "vkpd_simulate",
+    "vkpd_step_cms", "vkpd_simulate", "vkpd_dev_cheb_step", "vkpd_get_gershgorin",
 )
 
 
@@ -107,6 +107,8 @@ def load():
         "vkpd_set_colliders": (I, [P, I, P, P, C.c_double]),
         "vkpd_dev_apply_K": (I, [P, P, P]),
         "vkpd_dev_inv_diag": (I, [P, P]),
+        "vkpd_dev_cheb_step": (I, [P, P, P, P, P, C.c_double, C.c_double]),
+        "vkpd_get_gershgorin": (I, [P, I, P]),
         "vkpd_get_node_order": (I, [P, P]),
         "vkpd_get_sizes": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                C.POINTER(I)]),
@@ -448,6 +450,15 @@ class Context:
 
     def dev_inv_diag(self, out_ptr):
         check(self.lib.vkpd_dev_inv_diag(self.h, C.c_void_p(out_ptr)))
+
+    def dev_cheb_step(self, d_ptr, res_ptr, y_ptr, dnext_ptr, c1, c2):
+        check(self.lib.vkpd_dev_cheb_step(self.h, C.c_void_p(d_ptr), C.c_void_p(res_ptr), C.c_void_p(y_ptr),
+                                          C.c_void_p(dnext_ptr), float(c1), float(c2)))
+
+    def gershgorin(self, with_pinned_cols=False):
+        g = C.c_double(0.0)
+        check(self.lib.vkpd_get_gershgorin(self.h, 1 if with_pinned_cols else 0, C.byref(g)))
+        return g.value
 
     def matrix_csr(self):
         nnz = C.c_int64(0)

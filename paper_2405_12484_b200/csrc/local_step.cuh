@@ -213,163 +213,15 @@ __device__ __forceinline__ void finish_tet(const LocalArgs<T>& a, int e, const T
     st4(&a.corner[sl.w], make4<T>(f[2][0], f[2][1], f[2][2], T(0)));
 }
 
+#ifndef VK_LOCAL_MINB64
+#define VK_LOCAL_MINB64 8      // float64 build
+#endif
 template <typename T, int MODE, bool WITH_FRV, int PASS = 0>
-__global__ void __launch_bounds__(128, VK_LOCAL_MINB) k_local(LocalArgs<T> a) {
+__global__ void __launch_bounds__(128, sizeof(T) == 8 ? VK_LOCAL_MINB64 : VK_LOCAL_MINB) k_local(LocalArgs<T> a) {
     if (PASS == 1) pcg_mark(8);
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= a.nE) return;
     local_tet<T, MODE, WITH_FRV, false, PASS>(a, e);
-}
-
-// Dense second pass over the queued suspicious elements: the robust
-// multi-start scalar projection (material.py:242-287) for each, then the same
-// corner contributions.  Queue order does not matter (each element writes
-// only its own corner slots), so results are deterministic.
-template <typename T, int MODE>
-__global__ void __launch_bounds__(128) k_robust(LocalArgs<T> a) {
-    const int cnt = *a.robust_count;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
-        local_tet<T, MODE, false, false, 2>(a, a.robust_list[i]);
-}
-
-// Same pass, but the (up to four) Newton starts of each element's robust
-// projection run on the four lanes of a quad in parallel -- the scalar path
-// is a long serial chain (starts x clamp rounds x Newton x line search), so
-// this cuts the pass latency ~4x.  The quad leader then selects the winner
-// exactly as the reference's sequential loop does (material.py:264-280: in
-// start order, replace only when strictly better by 1e-15).
-template <typename T, int MODE>
-__global__ void __launch_bounds__(128) k_robust4(LocalArgs<T> a) {
-    const int cnt = *a.robust_count;
-    const int lane = threadIdx.x & 31, q = lane & 3;
-    const unsigned int qmask = 0xFu << (lane & ~3);
-    const int gq = (blockIdx.x * blockDim.x + threadIdx.x) >> 2;
-    const int nq = (gridDim.x * blockDim.x) >> 2;
-    for (int i = gq; i < cnt; i += nq) {
-        const int e = a.robust_list[i];
-        T g[3][3], F[3][3], ws, wv, U[3][3], W[3][3], sig[3];
-        load_tet<T, false>(a, e, g, ws, wv, F);
-        svd3_rv(F, U, sig, W);
-        const double sd[3] = {(double)sig[0], (double)sig[1], (double)sig[2]};
-        double st[3], sk[3] = {0, 0, 0}, obj = 0.0;
-        const bool use = sl3::robust_start(sd, q, st);
-        const bool ok = use && sl3::robust_try(sd, st, sk, obj);
-        bool have = false;
-        double best = 0.0, s[3] = {0, 0, 0};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int src = (lane & ~3) + k;
-            const bool okk = __shfl_sync(qmask, ok, src);
-            const double ob = __shfl_sync(qmask, obj, src);
-            const double s0 = __shfl_sync(qmask, sk[0], src);
-            const double s1 = __shfl_sync(qmask, sk[1], src);
-            const double s2 = __shfl_sync(qmask, sk[2], src);
-            if (okk && (!have || ob < best - 1e-15)) {
-                have = true;
-                best = ob;
-                s[0] = s0; s[1] = s1; s[2] = s2;
-            }
-        }
-        if (q != 0) continue;
-        if (!have) sl3::robust_fallback(sd, s);
-        if (a.stats) {
-            atomicAdd(&a.stats->robust, 1u);
-            if (!have) atomicAdd(&a.stats->fallback, 1u);
-        }
-        finish_tet<T, MODE, false>(a, e, g, ws, wv, F, U, W, s);
-    }
-}
-
-// Same pass with a warp-per-start layout: a CTA takes 32 queued elements, warp
-// w runs start w of all 32 (lane = element).  Lanes of a warp then follow the
-// same start, whose trip counts are alike across elements (e.g. the sigma/cbrt
-// start usually stalls for all 20 Newton iterations), so a warp costs about
-// its slowest lane instead of the serialised union of four different starts
-// of eight elements, and the four starts still run concurrently on four warps.
-// Warp 0 loads the tet, shares sigma through shared memory, then selects the
-// winner in start order (material.py:264-280) and writes the corners.
-#ifndef VK_ROBUST_MINB
-#define VK_ROBUST_MINB 4
-#endif
-template <typename T, int MODE>
-__global__ void __launch_bounds__(128, VK_ROBUST_MINB) k_robust_ws(LocalArgs<T> a) {
-    // double-buffered per-chunk results: warps 1-3 run the next chunk's starts while warp 0
-    // selects and writes the current one, so each chunk costs one CTA barrier
-    __shared__ double s_sig[2][32][3];
-    __shared__ double s_res[2][4][32][4];
-    __shared__ int s_ok[2][4][32];
-    __shared__ int s_chunk[2];
-    pcg_mark(9);
-    const int cnt = *a.robust_count;
-    if (cnt == 0) return;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const bool have_aux = a.robust_aux != nullptr;
-    if (threadIdx.x == 0) s_chunk[0] = atomicAdd(a.robust_count + 1, 1);
-    __syncthreads();
-    int buf = 0;
-    // warp 0 keeps the current chunk's element data for the finish (no-aux path: its SVD)
-    T g[3][3], F[3][3], ws, wv, U[3][3], W[3][3], sig[3];
-    for (;;) {
-        const int base = s_chunk[buf] * 32;
-        if (base >= cnt) break;
-        const int i = base + lane;
-        const bool act = i < cnt;
-        const int e = act ? a.robust_list[i] : 0;
-        double sd[3] = {0.0, 0.0, 0.0};
-        if (have_aux) {
-            if (act) {
-                const T* ax = a.robust_aux + (size_t)24 * i;
-                sd[0] = (double)ax[0]; sd[1] = (double)ax[1]; sd[2] = (double)ax[2];
-            }
-        } else {
-            if (w == 0 && act) {
-                load_tet<T, false>(a, e, g, ws, wv, F);
-                svd3_rv(F, U, sig, W);
-                s_sig[buf][lane][0] = (double)sig[0];
-                s_sig[buf][lane][1] = (double)sig[1];
-                s_sig[buf][lane][2] = (double)sig[2];
-            }
-            __syncthreads();
-            if (act) { sd[0] = s_sig[buf][lane][0]; sd[1] = s_sig[buf][lane][1]; sd[2] = s_sig[buf][lane][2]; }
-        }
-        if (act) {
-            double st[3], sk[3] = {0, 0, 0}, obj = 0.0;
-            const bool ok = sl3::robust_start(sd, w, st) && sl3::robust_try(sd, st, sk, obj);
-            s_ok[buf][w][lane] = ok;
-            s_res[buf][w][lane][0] = sk[0];
-            s_res[buf][w][lane][1] = sk[1];
-            s_res[buf][w][lane][2] = sk[2];
-            s_res[buf][w][lane][3] = obj;
-        }
-        if (threadIdx.x == 0) s_chunk[buf ^ 1] = atomicAdd(a.robust_count + 1, 1);
-        __syncthreads();
-        if (w == 0 && act) {
-            bool have = false;
-            double best = 0.0, s[3] = {0, 0, 0};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const double ob = s_res[buf][k][lane][3];
-                if (s_ok[buf][k][lane] && (!have || ob < best - 1e-15)) {
-                    have = true;
-                    best = ob;
-                    s[0] = s_res[buf][k][lane][0]; s[1] = s_res[buf][k][lane][1]; s[2] = s_res[buf][k][lane][2];
-                }
-            }
-            if (!have) sl3::robust_fallback(sd, s);
-            if (a.stats) {
-                atomicAdd(&a.stats->robust, 1u);
-                if (!have) atomicAdd(&a.stats->fallback, 1u);
-            }
-            if (have_aux) {
-                load_tet<T, false>(a, e, g, ws, wv, F);
-                const T* ax = a.robust_aux + (size_t)24 * i;
-#pragma unroll
-                for (int k = 0; k < 9; ++k) { U[k / 3][k % 3] = ax[3 + k]; W[k / 3][k % 3] = ax[12 + k]; }
-            }
-            finish_tet<T, MODE, false>(a, e, g, ws, wv, F, U, W, s);
-        }
-        buf ^= 1;
-    }
 }
 
 // Robust pass as independent (chunk, start) tasks (needs the first pass's SVD hand-off).

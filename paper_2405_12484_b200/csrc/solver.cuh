@@ -170,6 +170,22 @@ __global__ void k_gershgorin(int nF, int ell_w, const int* __restrict__ ell_col,
     atomicMax(out, (unsigned long long)__double_as_longlong(g >= 0.0 ? g : 0.0));
 }
 
+// Same bound over the rows of [K_ff K_fp] (the pinned columns of a domain-decomposed rank hold
+// its halo, dd.py): the rank's share of the global Gershgorin bound.
+template <typename T>
+__global__ void k_gershgorin_fp(int nF, int ell_w, const int* __restrict__ ell_col, const T* __restrict__ ell_val,
+                                const int* __restrict__ fp_ptr, const T* __restrict__ fp_val,
+                                const double* __restrict__ diag64, unsigned long long* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    double off = 0.0;
+    for (int s = 0; s < ell_w; ++s)
+        if (ell_col[(size_t)s * nF + i] != i) off += fabs((double)ell_val[(size_t)s * nF + i]);
+    for (int k = fp_ptr[i]; k < fp_ptr[i + 1]; ++k) off += fabs((double)fp_val[k]);
+    const double g = off / diag64[i];
+    atomicMax(out, (unsigned long long)__double_as_longlong(g >= 0.0 ? g : 0.0));
+}
+
 // rhs_i = sum over incidences of corner contributions (tet order) -- the
 // `np.add.at` of pdsolver.py:69-70, without atomics.  All n nodes.
 template <typename T>
@@ -219,10 +235,6 @@ struct PcgArgs {
     vec4_t<T>* p1;
     vec4_t<T>* q;
     vec4_t<T>* dx;
-    vec4_t<T>* m1;               // pipelined CG: second bank of m = D^-1 w
-    vec4_t<T>* qq;
-    vec4_t<T>* ss;
-    vec4_t<T>* pp;
     double* partials;            // gridDim.x * 8
     double* scal;                // 16 published scalars
     GridBar* bar;
@@ -737,187 +749,6 @@ __global__ void __maxnreg__(VK_POLY_MAXNREG) k_pcg_poly(PcgArgs<T> a) {
     __shared__ double smem[32 * 8];
     __shared__ double red[8];
     pcg_classic_body<T, true>(a, grid, smem, red, false);
-}
-
-// ---------------------------------------------------------------------------
-// Pipelined preconditioned CG (Ghysels & Vanroose 2014, Alg. 4), Jacobi M.
-// The dot products of an iteration and the SpMV of the next one are
-// independent, so ONE grid barrier per iteration carries both the neighbour
-// data (m = M w) and the fused deterministic all-reduce (7 doubles: r.u and
-// w.u per column, r.r).  Same solution as `k_pcg_classic` (mathematically
-// identical iterates); two more vector streams per row.
-//   r0 = b - A x0, u0 = M r0, w0 = A u0
-//   per i: g = (r,u), d = (w,u); m = M w; n = A m
-//          b = g/g_old, a = g/(d - b g/a_old)     (i > 0; else b = 0, a = g/d)
-//          z = n + b z; q = m + b q; s = w + b s; p = u + b p
-//          x += a p; r -= a s; u -= a q; w -= a z
-template <typename T>
-__device__ __forceinline__ vec4_t<T> ell_spmv(const PcgArgs<T>& a, const vec4_t<T>* v, int i) {
-    const int nF = a.nF;
-    T qx = 0, qy = 0, qz = 0;
-    if (a.ell_w <= kEllUnroll) {
-        int cols[kEllUnroll];
-        T vals[kEllUnroll];
-#pragma unroll
-        for (int s = 0; s < kEllUnroll; ++s) {
-            cols[s] = s < a.ell_w ? __ldg(&a.ell_col[(size_t)s * nF + i]) : i;
-            vals[s] = s < a.ell_w ? __ldg(&a.ell_val[(size_t)s * nF + i]) : T(0);
-        }
-#pragma unroll
-        for (int s = 0; s < kEllUnroll; ++s) {
-            if (s < a.ell_w) {
-                const vec4_t<T> c = ld4(&v[cols[s]]);
-                qx += vals[s] * c.x; qy += vals[s] * c.y; qz += vals[s] * c.z;
-            }
-        }
-    } else {
-        for (int s = 0; s < a.ell_w; ++s) {
-            const int col = __ldg(&a.ell_col[(size_t)s * nF + i]);
-            const T kv = __ldg(&a.ell_val[(size_t)s * nF + i]);
-            const vec4_t<T> c = ld4(&v[col]);
-            qx += kv * c.x; qy += kv * c.y; qz += kv * c.z;
-        }
-    }
-    return make4<T>(qx, qy, qz, T(0));
-}
-
-template <typename T>
-__device__ __forceinline__ void pipe_dots(double (&acc)[8], const vec4_t<T>& r, const vec4_t<T>& u,
-                                          const vec4_t<T>& w) {
-    acc[0] += (double)r.x * u.x; acc[1] += (double)r.y * u.y; acc[2] += (double)r.z * u.z;
-    acc[3] += (double)w.x * u.x; acc[4] += (double)w.y * u.y; acc[5] += (double)w.z * u.z;
-    acc[6] += (double)r.x * r.x + (double)r.y * r.y + (double)r.z * r.z;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(512) k_pcg(PcgArgs<T> a) {
-    pcg_mark(0);
-    pcg_entry(a);
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double smem[32 * 8];
-    __shared__ double red[8];
-    const int nF = a.nF;
-    const int chunk = (nF + gridDim.x - 1) / gridDim.x;
-    const int row0 = blockIdx.x * chunk;
-    const int row1 = min(nF, row0 + chunk);
-    int parity = 0;
-    vec4_t<T>* const R = a.r;
-    vec4_t<T>* const U = a.z;
-    vec4_t<T>* const Wv = a.p0;
-    vec4_t<T>* const Z = a.q;
-    vec4_t<T>* const Q = a.qq;
-    vec4_t<T>* const S = a.ss;
-    vec4_t<T>* const P = a.pp;
-    vec4_t<T>* const DX = a.dx;
-    const vec4_t<T> zero4 = make4<T>(T(0), T(0), T(0), T(0));
-
-    // ---- init 1: r = b - K x (PD) or rhs; u = M r; zero the recurrences
-    double bb_loc = 0.0;
-    for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
-        T rx, ry, rzv;
-        if (a.init == INIT_PD) {
-            rx = 0; ry = 0; rzv = 0;
-            const int k0 = a.inc_ptr[i], k1 = a.inc_ptr[i + 1];
-#pragma unroll 4
-            for (int k = k0; k < k1; ++k) {
-                const vec4_t<T> c = ldg4(&a.corner[k]);
-                rx += c.x; ry += c.y; rzv += c.z;
-            }
-            const T mm = a.m_dt2[i];
-            const vec4_t<T> xh = a.xhat[i], xi = a.x[i];
-            rx += mm * (xh.x - xi.x);
-            ry += mm * (xh.y - xi.y);
-            rzv += mm * (xh.z - xi.z);
-            const double bx = (double)mm * xh.x, by = (double)mm * xh.y, bz = (double)mm * xh.z;
-            bb_loc += bx * bx + by * by + bz * bz;
-        } else {
-            const vec4_t<T> b = a.rhs[i];
-            rx = b.x; ry = b.y; rzv = b.z;
-            bb_loc += (double)rx * rx + (double)ry * ry + (double)rzv * rzv;
-        }
-        const T d = a.inv_diag[i];
-        R[i] = make4<T>(rx, ry, rzv, T(0));
-        U[i] = make4<T>(d * rx, d * ry, d * rzv, T(0));
-        Z[i] = zero4; Q[i] = zero4; S[i] = zero4; P[i] = zero4; DX[i] = zero4;
-    }
-    grid.sync();
-    // ---- init 2: w = K u, m = M w, dots
-    {
-        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        acc[7] = bb_loc;
-        for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
-            const vec4_t<T> w = ell_spmv(a, U, i);
-            const T d = a.inv_diag[i];
-            Wv[i] = w;
-            a.p1[i] = make4<T>(d * w.x, d * w.y, d * w.z, T(0));
-            pipe_dots<T>(acc, ld4(&R[i]), ld4(&U[i]), w);
-        }
-        pcg_allreduce<8>(grid, a.partials, parity, acc, red, smem);
-    }
-    double g[3], dd[3], g_old[3] = {1, 1, 1}, al_old[3] = {1, 1, 1}, rr, bb = red[7];
-    for (int c = 0; c < 3; ++c) { g[c] = red[c]; dd[c] = red[3 + c]; }
-    rr = red[6];
-
-    int it = 0;
-    for (;; ++it) {
-        if (!(rr > a.tol * a.tol * bb) || it >= a.max_iters) break;      // also stops on NaN
-        double al[3], be[3];
-        for (int c = 0; c < 3; ++c) {
-            if (it == 0) {
-                be[c] = 0.0;
-                al[c] = dd[c] != 0.0 ? g[c] / dd[c] : 0.0;
-            } else {
-                be[c] = g_old[c] != 0.0 ? g[c] / g_old[c] : 0.0;
-                const double den = dd[c] - (al_old[c] != 0.0 ? be[c] * g[c] / al_old[c] : 0.0);
-                al[c] = den != 0.0 ? g[c] / den : 0.0;
-            }
-            g_old[c] = g[c];
-            al_old[c] = al[c];
-        }
-        const T bx = (T)be[0], by = (T)be[1], bz = (T)be[2];
-        const T ax = (T)al[0], ay = (T)al[1], az = (T)al[2];
-        const vec4_t<T>* Mcur = (it & 1) ? a.m1 : a.p1;
-        vec4_t<T>* Mnext = (it & 1) ? a.p1 : a.m1;
-        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
-            const vec4_t<T> n = ell_spmv(a, Mcur, i);
-            const vec4_t<T> m = ld4(&Mcur[i]);
-            vec4_t<T> z = ld4(&Z[i]), q = ld4(&Q[i]), s = ld4(&S[i]), p = ld4(&P[i]);
-            vec4_t<T> u = ld4(&U[i]), w = ld4(&Wv[i]), r = ld4(&R[i]), dx = ld4(&DX[i]);
-            z.x = n.x + bx * z.x; z.y = n.y + by * z.y; z.z = n.z + bz * z.z;
-            q.x = m.x + bx * q.x; q.y = m.y + by * q.y; q.z = m.z + bz * q.z;
-            s.x = w.x + bx * s.x; s.y = w.y + by * s.y; s.z = w.z + bz * s.z;
-            p.x = u.x + bx * p.x; p.y = u.y + by * p.y; p.z = u.z + bz * p.z;
-            dx.x += ax * p.x; dx.y += ay * p.y; dx.z += az * p.z;
-            r.x -= ax * s.x; r.y -= ay * s.y; r.z -= az * s.z;
-            u.x -= ax * q.x; u.y -= ay * q.y; u.z -= az * q.z;
-            w.x -= ax * z.x; w.y -= ay * z.y; w.z -= az * z.z;
-            const T d = a.inv_diag[i];
-            Z[i] = z; Q[i] = q; S[i] = s; P[i] = p; DX[i] = dx; R[i] = r; U[i] = u; Wv[i] = w;
-            Mnext[i] = make4<T>(d * w.x, d * w.y, d * w.z, T(0));
-            pipe_dots<T>(acc, r, u, w);
-        }
-        acc[7] = 0.0;
-        pcg_allreduce<8>(grid, a.partials, parity, acc, red, smem);
-        for (int c = 0; c < 3; ++c) { g[c] = red[c]; dd[c] = red[3 + c]; }
-        rr = red[6];
-    }
-    // ---- finish: x += dx (PD mode), finite check.  Nothing to add after zero
-    // iterations; a non-finite iterate then shows up as a non-finite residual.
-    bool bad = a.init == INIT_PD && !(rr == rr && rr < INFINITY);
-    if (it > 0 || bad)
-    for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
-        const vec4_t<T> d = ld4(&DX[i]);
-        if (a.init == INIT_PD) {
-            vec4_t<T> xi = a.x[i];
-            xi.x += d.x; xi.y += d.y; xi.z += d.z;
-            a.x[i] = xi;
-            bad |= !(isfinite(xi.x) && isfinite(xi.y) && isfinite(xi.z));
-        } else {
-            bad |= !(isfinite(d.x) && isfinite(d.y) && isfinite(d.z));
-        }
-    }
-    pcg_exit(a, bad, it);
 }
 
 }  // namespace vk

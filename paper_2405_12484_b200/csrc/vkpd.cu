@@ -60,6 +60,21 @@ struct DBuf {
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Selects the context's device for the call and restores the caller's current device after it
+// (a torch caller working on another GPU keeps its device).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+
 // ---------------------------------------------------------------------------
 // layout conversion kernels: host (nV,3) float64 in caller order <-> device vec4 internal order
 template <typename T>
@@ -145,6 +160,40 @@ __global__ void k_apply_K(int n, int nF, const int* __restrict__ ell_len, const 
     Y[i] = vk::make4<T>(a, b, c, T(0));
 }
 
+// One Chebyshev step of the domain-decomposed solve on a rank's free rows (dd.py): q = K_ff d_f +
+// K_fp d_p (the pinned columns hold the halo: the neighbours' d of this step), y += d,
+// res -= q, d_next = c1 d + c2 D^-1 res.  d / d_next are full internal vectors (free, pinned,
+// halo); only the free rows of d_next are written.
+template <typename T>
+__global__ void k_dd_cheb_step(int nF, const int* __restrict__ ell_len, const int* __restrict__ ell_col,
+                               const T* __restrict__ ell_val, const int* __restrict__ fp_ptr,
+                               const int* __restrict__ fp_col, const T* __restrict__ fp_val,
+                               const T* __restrict__ inv_diag, const vk::vec4_t<T>* __restrict__ d,
+                               vk::vec4_t<T>* __restrict__ res, vk::vec4_t<T>* __restrict__ y,
+                               vk::vec4_t<T>* __restrict__ dnext, T c1, T c2) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nF) return;
+    T a = 0, b = 0, c = 0;
+    for (int s = 0; s < ell_len[i]; ++s) {
+        const vk::vec4_t<T> x = d[ell_col[(size_t)s * nF + i]];
+        const T v = ell_val[(size_t)s * nF + i];
+        a += v * x.x; b += v * x.y; c += v * x.z;
+    }
+    for (int k = fp_ptr[i]; k < fp_ptr[i + 1]; ++k) {
+        const vk::vec4_t<T> x = d[nF + fp_col[k]];
+        const T v = fp_val[k];
+        a += v * x.x; b += v * x.y; c += v * x.z;
+    }
+    const vk::vec4_t<T> di = d[i];
+    vk::vec4_t<T> yi = y[i], ri = res[i];
+    yi.x += di.x; yi.y += di.y; yi.z += di.z;
+    ri.x -= a; ri.y -= b; ri.z -= c;
+    y[i] = yi;
+    res[i] = ri;
+    const T e = c2 * inv_diag[i];
+    dnext[i] = vk::make4<T>(c1 * di.x + e * ri.x, c1 * di.y + e * ri.y, c1 * di.z + e * ri.z, T(0));
+}
+
 // r_i = sum of corner contributions + (m/dt^2)(xhat_i - x_i) on free rows (= b - K x)
 template <typename T>
 __global__ void k_resid_free(int nF, const int* __restrict__ inc_ptr, const vk::vec4_t<T>* __restrict__ corner,
@@ -202,6 +251,8 @@ struct CtxBase {
     virtual int dev_residual(const void* x, const void* xhat, void* r) = 0;
     virtual int dev_apply_K(const void* X, void* Y) = 0;
     virtual int dev_inv_diag(void* out) = 0;
+    virtual int dev_cheb_step(const void* d, void* res, void* y, void* dnext, double c1, double c2) = 0;
+    virtual int gershgorin(int with_pinned, double* g) = 0;
     virtual int node_order(int64_t* ioo) = 0;
     virtual void sizes(int64_t* n, int64_t* nfree, int64_t* npinned, int* prec) = 0;
     virtual int cms_solve(const double* B, const double* P, int k, int sweeps, int agg, double omega, int cheb,
@@ -250,7 +301,7 @@ struct Ctx : CtxBase {
                                          // gain (C3: 19.3 -> 15.9 ms/frame); fp32 only the first 3
     // state
     DBuf<V4> x, v, x_start, v_start, xhat, f, pin_tgt, corner, r, z, p0, p1, q, dx, rhs, tmp4a, tmp4b;
-    DBuf<V4> m1, qq, ss, pp;             // pipelined-CG recurrences
+    DBuf<V4> hh;                         // polynomial preconditioner: h = K D^-1 r
     int pcg_threads = 512;               // CTA size of the persistent solver
     int solver_kind = VKPD_SOLVER_PCG_POLY;   // resolved vkpd_config.solver
     bool pcg_poly = true;                // Neumann-1 polynomial preconditioner (CG kinds)
@@ -879,7 +930,7 @@ struct Ctx : CtxBase {
         CK(pin_tgt.alloc(std::max(1, nP)));
         CK(cudaMemsetAsync(pin_tgt.p, 0, std::max(1, nP) * sizeof(V4), s));
         CK(corner.alloc((size_t)4 * nE));
-        for (DBuf<V4>* b : {&r, &z, &p0, &p1, &q, &dx, &rhs, &m1, &qq, &ss, &pp}) {
+        for (DBuf<V4>* b : {&r, &z, &p0, &p1, &q, &dx, &rhs, &hh}) {
             CK(b->alloc(std::max(1, nF)));
             CK(cudaMemsetAsync(b->p, 0, std::max(1, nF) * sizeof(V4), s));
         }
@@ -1172,7 +1223,6 @@ struct Ctx : CtxBase {
         pa.inc_ptr = inc_ptr.p; pa.inc_code = inc_code.p; pa.corner = corner.p; pa.m_dt2 = m_dt2.p;
         pa.xhat = xhat.p; pa.rhs = rhs.p; pa.x = x.p; pa.r = r.p; pa.z = z.p; pa.p0 = p0.p; pa.p1 = p1.p;
         pa.q = q.p; pa.dx = dx.p; pa.partials = partials.p; pa.scal = scal.p; pa.bar = bar.p;
-        pa.m1 = m1.p; pa.qq = qq.p; pa.ss = ss.p; pa.pp = pp.p;
         pa.iters_out = iters_slot; pa.fail_iter = fail_iter.p; pa.pd_iter = pd_iter; pa.tol = tol;
         pa.max_iters = max_iters; pa.init = init;
         pa.cdiag = nullptr; pa.cb = nullptr; pa.coll = nullptr; pa.ncoll = 0;
@@ -1192,7 +1242,7 @@ struct Ctx : CtxBase {
         pa.cheb_nexp = cheb_nexp.p;
         pa.cheb_halo_ptr = cheb_halo_ptr.p; pa.cheb_halo = cheb_halo.p;
         pa.cheb_halo_max = cheb_halo_max;
-        pa.h = ss.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
+        pa.h = hh.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
         if (init == vk::INIT_PD && ncoll > 0) {
             pa.inv_diag = inv_diag_c.p; pa.cdiag = cdiag.p; pa.cb = cb.p; pa.coll = coll_d.p; pa.ncoll = ncoll;
             pa.ell_kd = nullptr;                  // D changes with the contact set: scale on the fly
@@ -2051,6 +2101,32 @@ struct Ctx : CtxBase {
         }
         return VKPD_OK;
     }
+    int dev_cheb_step(const void* d, void* res, void* y, void* dnext, double c1, double c2) override {
+        if (nF > 0) {
+            k_dd_cheb_step<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, ell_len.p, ell_col.p, ell_val.p, fp_ptr.p,
+                                                                fp_col.p, fp_val.p, inv_diag.p, (const V4*)d,
+                                                                (V4*)res, (V4*)y, (V4*)dnext, (T)c1, (T)c2);
+            CK(cudaGetLastError());
+        }
+        return VKPD_OK;
+    }
+    int gershgorin(int with_pinned, double* g) override {
+        if (!with_pinned) { *g = gersh; return VKPD_OK; }
+        DBuf<unsigned long long> gmax;
+        CK(gmax.alloc(1));
+        CK(cudaMemsetAsync(gmax.p, 0, sizeof(unsigned long long), stream));
+        if (nF > 0)
+            vk::k_gershgorin_fp<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, ell_w, ell_col.p, ell_val.p, fp_ptr.p,
+                                                                      fp_val.p, diag64.p, gmax.p);
+        CK(cudaGetLastError());
+        unsigned long long b = 0;
+        CK(cudaMemcpyAsync(&b, gmax.p, sizeof b, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        double v = 0.0;
+        std::memcpy(&v, &b, sizeof v);
+        *g = v + 1.0;
+        return VKPD_OK;
+    }
     int dev_inv_diag(void* out) override {
         if (nF > 0) CK(cudaMemcpyAsync(out, inv_diag.p, sizeof(T) * nF, cudaMemcpyDeviceToDevice, stream));
         return VKPD_OK;
@@ -2139,7 +2215,7 @@ int vkpd_create(const vkpd_mesh_desc* mesh, const vkpd_config* cfg, vkpd_ctx** o
     else if (cfg->precision == VKPD_FP64) c->impl.reset(new Ctx<double>());
     else return fail(VKPD_EINVAL, "precision must be 32 or 64");
     c->impl->device = cfg->device;
-    if (cudaSetDevice(cfg->device) != cudaSuccess) return fail(VKPD_ECUDA, "cudaSetDevice failed");
+    DeviceGuard guard_(cfg->device);
     int rc = c->impl->init(mesh, cfg);
     if (rc != VKPD_OK) return rc;
     *out = c.release();
@@ -2159,7 +2235,7 @@ int vkpd_create_matrix(int64_t n, const int64_t* indptr, const int64_t* indices,
     else if (cfg->precision == VKPD_FP64) c->impl.reset(new Ctx<double>());
     else return fail(VKPD_EINVAL, "precision must be 32 or 64");
     c->impl->device = cfg->device;
-    if (cudaSetDevice(cfg->device) != cudaSuccess) return fail(VKPD_ECUDA, "cudaSetDevice failed");
+    DeviceGuard guard_(cfg->device);
     int rc = c->impl->init_matrix(n, indptr, indices, data, pins, n_pins, cfg);
     if (rc != VKPD_OK) return rc;
     *out = c.release();
@@ -2168,11 +2244,15 @@ int vkpd_create_matrix(int64_t n, const int64_t* indptr, const int64_t* indices,
 
 int vkpd_get_matrix_csr(vkpd_ctx* ctx, int64_t* indptr, int64_t* indices, double* data, int64_t* nnz) {
     if (!ctx || !nnz) return fail(VKPD_EINVAL, "null argument");
-    cudaSetDevice(ctx->impl->device);
+    DeviceGuard guard_(ctx->impl->device);
     return ctx->impl->get_csr(indptr, indices, data, nnz);
 }
 
-void vkpd_destroy(vkpd_ctx* ctx) { delete ctx; }
+void vkpd_destroy(vkpd_ctx* ctx) {
+    if (!ctx) return;
+    DeviceGuard guard_(ctx->impl->device);
+    delete ctx;
+}
 
 int vkpd_set_stream(vkpd_ctx* ctx, void* stream) {
     if (!ctx) return fail(VKPD_EINVAL, "null context");
@@ -2184,7 +2264,7 @@ void* vkpd_get_stream(vkpd_ctx* ctx) { return ctx ? (void*)ctx->impl->stream : n
 #define CTX_CALL(expr)                                                                             \
     do {                                                                                           \
         if (!ctx) return fail(VKPD_EINVAL, "null context");                                       \
-        cudaSetDevice(ctx->impl->device);                                                          \
+        DeviceGuard guard_(ctx->impl->device);                                                     \
         return ctx->impl->expr;                                                                    \
     } while (0)
 
@@ -2296,6 +2376,14 @@ int vkpd_dev_inv_diag(vkpd_ctx* ctx, void* out_free) {
     if (!out_free) return fail(VKPD_EINVAL, "null device buffer");
     CTX_CALL(dev_inv_diag(out_free));
 }
+int vkpd_dev_cheb_step(vkpd_ctx* ctx, const void* d_int, void* res_free, void* y_free, void* dnext_int, double c1,
+                       double c2) {
+    CTX_CALL(dev_cheb_step(d_int, res_free, y_free, dnext_int, c1, c2));
+}
+int vkpd_get_gershgorin(vkpd_ctx* ctx, int with_pinned_cols, double* g) {
+    if (!g) return fail(VKPD_EINVAL, "null argument");
+    CTX_CALL(gershgorin(with_pinned_cols, g));
+}
 int vkpd_get_node_order(vkpd_ctx* ctx, int64_t* int_of_orig) {
     if (!int_of_orig) return fail(VKPD_EINVAL, "null buffer");
     CTX_CALL(node_order(int_of_orig));
@@ -2399,6 +2487,7 @@ int vkpd_hess_create(const vkpd_mesh_desc* mesh, int device, vkpd_hess** out) {
     if (vkpd_device_count(&count) != VKPD_OK || count == 0)
         return fail(VKPD_ECUDA, "no CUDA device available (the vkpd library has no CPU path)");
     if (device < 0 || device >= count) return fail(VKPD_EINVAL, "bad device ordinal");
+    DeviceGuard guard_(device);
     std::unique_ptr<vkpd_hess> h(new vkpd_hess);
     int rc = h->impl.init(mesh, device);
     if (rc != VKPD_OK) return rc;
@@ -2407,14 +2496,14 @@ int vkpd_hess_create(const vkpd_mesh_desc* mesh, int device, vkpd_hess** out) {
 }
 void vkpd_hess_destroy(vkpd_hess* h) {
     if (h) {
-        cudaSetDevice(h->impl.device);
+        DeviceGuard guard_(h->impl.device);
         delete h;
     }
 }
 #define HESS_CALL(expr)                                  \
     do {                                                 \
         if (!h) return fail(VKPD_EINVAL, "null context"); \
-        cudaSetDevice(h->impl.device);                   \
+        DeviceGuard guard_(h->impl.device);              \
         return h->impl.expr;                             \
     } while (0)
 int vkpd_hess_set_gammas(vkpd_hess* h, const double* gs, const double* gv) { HESS_CALL(set_gammas(gs, gv)); }

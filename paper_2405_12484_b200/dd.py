@@ -11,11 +11,15 @@ Partition and exchange plan (host bookkeeping, deterministic, identical on every
     coupling to the halo (pdsolver.py:210-229 applied per domain).
 
 Per PD iteration (pdsolver.py:291-300) each rank runs the local step on its tets
-(`vkpd_dev_residual`), then a distributed CG on the global K_ff: per iteration one halo
-exchange of the search direction (point-to-point send/recv, NCCL over NVLink on GPUs),
-one SpMV (`vkpd_dev_apply_K`) and two small all-reduces of per-column dot products.
-After the solve the updated halo positions are exchanged once.  Vector algebra between
-the library calls runs on torch tensors (the carrier).
+(`vkpd_dev_residual`), then the global K_ff solve as the same Chebyshev semi-iteration the
+single-GPU fp64 path uses (cheb.cuh): spectrum bounds are global (Gershgorin max over ranks;
+lambda_min from a distributed Lanczos run once per stepper), and a step needs only the
+neighbours' search direction, so per step the collectives are ONE point-to-point halo
+exchange of the exported rows (NCCL send/recv over NVLink on GPUs, issued on the library
+stream, no host wait) and one fused library kernel (`vkpd_dev_cheb_step`: SpMV over owned and
+halo columns, residual, correction and direction updates).  The residual norm is all-reduced
+(3 doubles) once when the solve starts and at each predicted stopping point, the only host
+reads of a round.  After the solve the updated halo positions are exchanged once.
 
 `Comm` wraps torch.distributed: NCCL exchanges device tensors directly; the gloo
 backend (CPU tests, or ranks sharing one GPU) stages through host memory.
@@ -109,10 +113,19 @@ class Comm:
         return t.cpu() if (self.stage and t.is_cuda) else t
 
     def allreduce_sum(self, t):
+        return self._allreduce(t, self.dist.ReduceOp.SUM)
+
+    def allreduce_max(self, t):
+        return self._allreduce(t, self.dist.ReduceOp.MAX)
+
+    def allreduce_min(self, t):
+        return self._allreduce(t, self.dist.ReduceOp.MIN)
+
+    def _allreduce(self, t, op):
         if not self.on or self.world == 1:
             return t
         w = self._to_wire(t.contiguous())
-        self.dist.all_reduce(w, op=self.dist.ReduceOp.SUM, group=self.group)
+        self.dist.all_reduce(w, op=op, group=self.group)
         return w.to(t.device) if w is not t else w
 
     def exchange(self, sends, recv_shapes, like):
@@ -170,6 +183,15 @@ class CudaOps:
             self.ctx.dev_apply_K(X.data_ptr(), Y.data_ptr())
         return Y
 
+    def cheb_step(self, D, Res, Y, Dn, c1, c2):
+        """Fused step on the free rows (vkpd_dev_cheb_step); D, Dn full internal vectors."""
+        if self.nF:
+            self.ctx.dev_cheb_step(D.data_ptr(), Res.data_ptr(), Y.data_ptr(), Dn.data_ptr(), c1, c2)
+
+    def gershgorin(self):
+        """This rank's rows of the global Gershgorin bound (halo columns included)."""
+        return self.ctx.gershgorin(with_pinned_cols=True)
+
 
 class DistributedStepper:
     """One rank of the domain-decomposed PD step (`pd_step` semantics, no colliders)."""
@@ -183,6 +205,9 @@ class DistributedStepper:
         self.part = p
         ioo = ops.int_of_orig                                   # local -> internal
         self.ioo = torch.as_tensor(ioo, dtype=torch.long)
+        orig_of_int = np.empty(len(ioo), dtype=np.int64)
+        orig_of_int[ioo] = np.arange(len(ioo))
+        self._free_local = orig_of_int[:ops.nF]                # internal free row -> local node
         self.nF, self.n = ops.nF, ops.n
         self.nPo = len(p.pins_owned)
         dev, dt_ = ops.device, ops.dtype
@@ -253,12 +278,95 @@ class DistributedStepper:
     def _allsum(self, t):
         return self.comm.allreduce_sum(t)
 
+    # -- the global solve: Chebyshev semi-iteration on the Jacobi-scaled global K_ff
+    def _spectrum(self):
+        """(lmin, lmax) of D^-1 K_ff over all ranks, computed once (the material and dt are fixed)."""
+        if getattr(self, "_lam", None) is not None:
+            return self._lam
+        torch = self.torch
+        nF, n = self.nF, self.n
+        lmax = float(self.comm.allreduce_max(torch.tensor([self.ops.gershgorin()], dtype=torch.float64,
+                                                          device=self.dev))[0])
+        inv_d = self.ops.inv_diag.double()
+        ratio = (self.m_dt2[:nF].double() * inv_d) if nF else torch.ones(1, dtype=torch.float64, device=self.dev)
+        lb = float(self.comm.allreduce_min(ratio.min().reshape(1))[0])
+        # distributed Lanczos on D^-1/2 K D^-1/2 (column 0 of the 4-wide vectors), fixed start
+        sc = torch.zeros((n, 4), dtype=self.dtype, device=self.dev)
+        sc[:nF, 0] = inv_d.sqrt().to(self.dtype)
+        sc = self._halo(sc)
+        s_own = sc[:nF, 0].double()
+        gid = torch.as_tensor(self.part.nodes[self._free_local], dtype=torch.float64, device=self.dev)
+        v = torch.frac(torch.sin(gid * 12.9898 + 78.233) * 43758.5453) - 0.5
+        v = v / torch.sqrt(self._allsum((v * v).sum().reshape(1)))[0]
+        v_prev = torch.zeros_like(v)
+        alpha, beta, b = [], [], 0.0
+        for _ in range(min(60, max(1, int(self._allsum(torch.tensor([float(nF)], dtype=torch.float64,
+                                                                                device=self.dev))[0])))):
+            u = torch.zeros((n, 4), dtype=self.dtype, device=self.dev)
+            u[:nF, 0] = (s_own * v).to(self.dtype)
+            u = self._halo(u)
+            w = s_own * self.ops.apply_K(u)[:, 0].double() - b * v_prev
+            a = float(self._allsum((w * v).sum().reshape(1))[0])
+            w = w - a * v
+            b = float(torch.sqrt(self._allsum((w * w).sum().reshape(1)))[0])
+            alpha.append(a)
+            if not b > 0.0:
+                break
+            beta.append(b)
+            v_prev, v = v, w / b
+        T = np.diag(alpha) + np.diag(beta[:len(alpha) - 1], 1) + np.diag(beta[:len(alpha) - 1], -1)
+        ritz = float(np.linalg.eigvalsh(T)[0])
+        lmin = max(lb, 0.97 * ritz)
+        if not (0.0 < lmin < lmax):
+            lmin = max(lb, 1e-6)
+        self._lam = (lmin, lmax)
+        return self._lam
+
+    def solve(self, R, bb):
+        """K_ff Y = R to |r| <= tol |M/dt^2 xhat| (the single-GPU rule); returns (Y, steps)."""
+        import math
+        torch = self.torch
+        nF, n = self.nF, self.n
+        lmin, lmax = self._spectrum()
+        theta, delta = 0.5 * (lmax + lmin), 0.5 * (lmax - lmin)
+        sigma = theta / delta
+        acs = math.acosh(sigma)
+        thr = self.tol ** 2 * bb
+        res = R.clone()
+        Y = torch.zeros_like(R)
+        rr = float(self._allsum((res[:, :3].double() ** 2).sum().reshape(1))[0])
+        if not (rr > thr) or self.max_iters <= 0:
+            return Y, 0, rr
+        D = torch.zeros((n, 4), dtype=self.dtype, device=self.dev)
+        Dn = torch.zeros_like(D)
+        D[:nF] = (1.0 / theta) * self.ops.inv_diag[:, None] * res
+        D = self._halo(D)
+
+        def steps_for(ratio):
+            return 1 if not ratio > 1.0 else max(1, int(math.ceil(math.acosh(ratio) / acs)))
+
+        k, rho = 0, 1.0 / sigma
+        target = min(self.max_iters, steps_for(math.sqrt(rr / thr)))
+        while True:
+            while k < target:
+                rho_n = 1.0 / (2.0 * sigma - rho)
+                c1, c2 = rho_n * rho, rho_n * 2.0 / delta
+                rho = rho_n
+                self.ops.cheb_step(D, res, Y, Dn, c1, c2)
+                Dn = self._halo(Dn)
+                D, Dn = Dn, D
+                k += 1
+            rr = float(self._allsum((res[:, :3].double() ** 2).sum().reshape(1))[0])
+            if not (rr > thr) or k >= self.max_iters:
+                return Y, k, rr
+            target = min(self.max_iters, k + 1 + steps_for(math.sqrt(rr / thr)))
+
     # -- the step
     def step(self, iterations=30, damping=1.0, early_exit=True):
-        """One PD step.  A round whose solve needs zero CG iterations leaves X unchanged, so
-        every later round would repeat it exactly (same local step, same halo): with
-        `early_exit` the loop stops there, as the single-GPU frame does.  The iteration count
-        is identical on every rank (the residual norms are global)."""
+        """One PD step.  A round whose solve needs zero steps leaves X unchanged, so every later
+        round would repeat it exactly (same local step, same halo): with `early_exit` the loop
+        stops there, as the single-GPU frame does.  The step counts are identical on every rank
+        (the residual norms are global)."""
         torch = self.torch
         nF, nPo = self.nF, self.nPo
         Xs, Vs = self.X.clone(), self.V.clone()
@@ -271,46 +379,29 @@ class DistributedStepper:
         bb_loc = ((self.m_dt2[:nF, None] * Xhat[:nF, :3]).double() ** 2).sum()
         bb = float(self._allsum(bb_loc.reshape(1))[0])
         failed = -1
+        self.last_steps = []
         for it in range(iterations):
             R = self.ops.residual(X, Xhat)
-            Z = self.ops.inv_diag[:, None] * R
-            P = torch.zeros_like(R)
-            DX = torch.zeros_like(R)
-            red = torch.cat([(R * Z).double().sum(0)[:3], (R * R).double().sum().reshape(1)])
-            red = self._allsum(red)
-            rz, rr = red[:3].clone(), float(red[3])
-            rz_prev = torch.ones_like(rz)
-            k = 0
-            while rr > self.tol ** 2 * bb and k < self.max_iters:
-                beta = torch.where((rz_prev != 0) & (k > 0), rz / torch.where(rz_prev != 0, rz_prev, 1.0),
-                                   torch.zeros_like(rz))
-                bvec = torch.cat([beta, beta.new_zeros(1)]).to(self.dtype)
-                P = Z + bvec * P
-                Pf = torch.zeros((self.n, 4), dtype=self.dtype, device=self.dev)
-                Pf[:nF] = P
-                Pf = self._halo(Pf)
-                Q = self.ops.apply_K(Pf)
-                pq = self._allsum((P * Q).double().sum(0)[:3])
-                alpha = torch.where(pq != 0, rz / torch.where(pq != 0, pq, 1.0), torch.zeros_like(pq))
-                avec = torch.cat([alpha, alpha.new_zeros(1)]).to(self.dtype)
-                DX = DX + avec * P
-                R = R - avec * Q
-                Z = self.ops.inv_diag[:, None] * R
-                red = self._allsum(torch.cat([(R * Z).double().sum(0)[:3], (R * R).double().sum().reshape(1)]))
-                rz_prev, rz, rr = rz, red[:3].clone(), float(red[3])
-                k += 1
+            DX, k, rr = self.solve(R, bb)
+            self.last_steps.append(k)
             self.last_rounds = it + 1
             if k == 0 and early_exit:
+                if not math_isfinite(rr) and failed < 0:
+                    failed = it
                 break
             X[:nF] = X[:nF] + DX
             X = self._halo(X)
-            bad = torch.tensor([0.0 if bool(torch.isfinite(X[:nF]).all()) else 1.0], dtype=torch.float64,
-                               device=self.dev)
-            if float(self._allsum(bad)[0]) > 0 and failed < 0:
+            if not math_isfinite(rr) and failed < 0:
                 failed = it
+                break
         if failed >= 0:
             self.X, self.V = Xs, Vs
             raise RuntimeError(f"projective step produced non-finite positions at iteration {failed}")
         self.V = damping * (X - Xs) / self.dt
         self.X = X
         return self
+
+
+def math_isfinite(v):
+    import math
+    return math.isfinite(v)

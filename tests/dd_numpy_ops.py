@@ -55,27 +55,40 @@ class NumpyOps:
         out[:, :3] = torch.as_tensor(y)
         return out
 
+    def cheb_step(self, D, Res, Y, Dn, c1, c2):
+        q = self.apply_K(D)
+        Y += D[:self.nF]
+        Res -= q
+        Dn[:self.nF] = c1 * D[:self.nF] + c2 * self.inv_diag[:, None] * Res
 
-def gloo_worker(rank, world, port, steps, out_dir, kind="numpy", box=(9, 5, 3), tol=None, early_exit=True):
+    def gershgorin(self):
+        K = self.K[:self.nF]
+        A = abs(K).multiply(1.0 / self.Kff.diagonal()[:, None]).tocsr()
+        return float(A.sum(axis=1).max()) if self.nF else 1.0
+
+
+def gloo_worker(rank, world, port, steps, out_dir, kind="numpy", box=(9, 5, 3), tol=None, early_exit=True,
+                scene=None, iterations=10, precision="fp64"):
     """mp.spawn target: one rank of the domain-decomposed step over gloo."""
     import os
     import torch.distributed as dist
-    from paper_2405_12484_b200 import dd, scenes
+    from paper_2405_12484_b200 import dd, pdsolver, scenes
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    sc = scenes.box_scene(*box)
+    sc = scenes.box_scene(*box) if scene is None else scenes.make_scene(scene)
     plan = dd.DomainPlan(sc.mesh, sc.pins, world)
     arrays = plan.local_arrays(sc.mesh, sc.gammas, rank)
     if kind == "numpy":
         ops, tol = NumpyOps(arrays, sc.dt), (1e-13 if tol is None else tol)
     else:                                       # real CUDA operators (ranks may share one GPU)
-        ops, tol = dd.CudaOps(arrays, sc.dt, precision="fp64"), (1e-12 if tol is None else tol)
+        ops = dd.CudaOps(arrays, sc.dt, precision=precision)
+        tol = pdsolver.DEFAULT_TOL[precision] if tol is None else tol
     st = dd.DistributedStepper(plan, rank, sc.mesh, sc.gammas, sc.dt, ops, dd.Comm(), pin_targets=sc.pin_targets,
                                tol=tol)
     st.set_state(sc.mesh.nodes)
     st.set_forces(sc.forces)
     rounds = []
     for _ in range(steps):
-        st.step(iterations=10, early_exit=early_exit)
+        st.step(iterations=iterations, early_exit=early_exit)
         rounds.append(st.last_rounds)
     ids, pos = st.owned_positions()
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=ids, pos=pos, rounds=np.array(rounds))

@@ -17,7 +17,10 @@ the reference saw.  Per-fixture contents:
   solvers.npz      C1 free-free K: `a_jacobi_refine` (agg 2/3, Chebyshev) from a seeded
                    start, `build_cms(...).solve`, and `simulate_mesh(cms)` 1 frame.
   c2.npz           C2 scarf: `simulate_mesh(direct)` frames 1, 10, 100 (f64).
-  c3.npz           C3 sweater: `simulate_mesh(direct)` frame 1, displacement as f32.
+  c3.npz           C3 sweater: `simulate_mesh(direct)` frame 1, positions (float64).
+  c3fold.npz       C3 sweater, one `pd_step(direct)` frame from a state inside the fold window
+                   (frame 120 of the device fp64 trajectory, rounded to float32 and stored: the
+                   reference and the device start from the same bits); displacement (float64).
   second_order.npz C1: elastic_energy / elastic_gradient / exact_elastic_hessian, newton_polish
                    (dynamic GN + exact, quasi-static exact), simulate_mesh(polish_tol), and
                    fitting.adjoint_gradient on a tracking loss (scenes.TrackingProblem).
@@ -186,6 +189,26 @@ def make_big(key, frames_keep, steps, f32_disp):
     print(key, "seconds", el)
 
 
+def make_c3fold():
+    """One reference frame from the stored fold-window state (tools/c3_state.py writes it on the GPU)."""
+    st = np.load(os.path.join(ROOT, "gpurun_out", "c3_state120.npz"))
+    sc = scenes.make_scene("C3")
+    rm = ref_mesh(sc)
+    gam = ref_mat.MaterialField(sc.gammas.gamma_s, sc.gammas.gamma_v)
+    x0 = st["x"].astype(np.float32).astype(np.float64)
+    v0 = st["v"].astype(np.float32).astype(np.float64)
+    state = ref_pd.SimState(x=x0, v=v0, dt=sc.dt, pins=sc.pins, pin_targets=sc.pin_targets)
+    solver = ref_pd.GlobalSolver(ref_pd.assemble_global(rm, gam, sc.dt),
+                                 np.setdiff1d(np.arange(rm.n_nodes), sc.pins), sc.pins)
+    t0 = time.time()
+    ref_pd.pd_step(state, rm, gam, iterations=30, forces=sc.forces, solver=solver)
+    el = time.time() - t0
+    np.savez_compressed(os.path.join(HERE, "c3fold.npz"), digest=scene_digest(sc), seconds=el,
+                        frame=int(st["frame"]), x0=x0.astype(np.float32), v0=v0.astype(np.float32),
+                        disp=state.x - x0, v=state.v)
+    print("c3fold seconds", el)
+
+
 def make_jacobians():
     """Reference projection_jacobians_batch on 600 cases of the projection set."""
     g = np.load(os.path.join(HERE, "projections.npz"))
@@ -289,4 +312,6 @@ if __name__ == "__main__":
     if what in ("c2", "all"):
         make_big("C2", (1, 10, 100), 100, False)
     if what in ("c3", "all"):
-        make_big("C3", (1,), 1, True)
+        make_big("C3", (1,), 1, False)
+    if what in ("c3fold",):
+        make_c3fold()
