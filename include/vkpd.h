@@ -128,6 +128,16 @@ void* vkpd_get_stream(vkpd_ctx* ctx);
 
 int vkpd_set_state(vkpd_ctx* ctx, const double* x, const double* v);      /* (nV,3) each; v may be NULL (= 0) */
 int vkpd_get_state(vkpd_ctx* ctx, double* x, double* v);                  /* either may be NULL */
+/* The same state transfers with DEVICE pointers (torch tensors' data_ptr(): float64 (n, 3),
+ * C-contiguous, caller node order), enqueued on the context stream (vkpd_set_stream: the
+ * caller's stream) with no host synchronisation -- the PyTorch-carrier form of SimState x / v,
+ * forces and pin targets (pdsolver.py:180-198, 744-752).  set_state keeps the solver's warm
+ * start when the incoming state is bit-identical to the one the context holds (a caller that
+ * feeds back the state it got), and clears it otherwise. */
+int vkpd_set_state_dev(vkpd_ctx* ctx, const void* x, const void* v);      /* v may be NULL (zero) */
+int vkpd_get_state_dev(vkpd_ctx* ctx, void* x, void* v);                  /* either may be NULL */
+int vkpd_set_forces_dev(vkpd_ctx* ctx, const void* f);                    /* NULL: no forces */
+int vkpd_set_pin_targets_dev(vkpd_ctx* ctx, const void* t);               /* (n_pins, 3) */
 int vkpd_set_pin_targets(vkpd_ctx* ctx, const double* targets);           /* (n_pins,3) */
 int vkpd_set_forces(vkpd_ctx* ctx, const double* forces);                 /* (nV,3) or NULL = none */
 /* new per-tet material (MaterialField, material.py:563-590) for the same mesh, pins and dt:

@@ -29,7 +29,8 @@ EXPORTS = (
     "vkpd_projection_jacobians", "vkpd_hess_create", "vkpd_hess_destroy", "vkpd_hess_set_gammas",
     "vkpd_hess_energy_grad", "vkpd_hess_gamma_jt", "vkpd_hess_linearize", "vkpd_hess_csr",
     "vkpd_hess_apply", "vkpd_hess_solve", "vkpd_cms_set_blocks", "vkpd_cms_timing", "vkpd_time_local",
-    "vkpd_step_cms", "vkpd_simulate", "vkpd_dev_cheb_step", "vkpd_get_gershgorin",
+    "vkpd_step_cms", "vkpd_simulate", "vkpd_dev_cheb_step", "vkpd_get_gershgorin", "vkpd_set_state_dev",
+    "vkpd_get_state_dev", "vkpd_set_forces_dev", "vkpd_set_pin_targets_dev",
 )
 
 
@@ -109,6 +110,10 @@ def load():
         "vkpd_dev_inv_diag": (I, [P, P]),
         "vkpd_dev_cheb_step": (I, [P, P, P, P, P, C.c_double, C.c_double]),
         "vkpd_get_gershgorin": (I, [P, I, P]),
+        "vkpd_set_state_dev": (I, [P, P, P]),
+        "vkpd_get_state_dev": (I, [P, P, P]),
+        "vkpd_set_forces_dev": (I, [P, P]),
+        "vkpd_set_pin_targets_dev": (I, [P, P]),
         "vkpd_get_node_order": (I, [P, P]),
         "vkpd_get_sizes": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                C.POINTER(I)]),
@@ -237,6 +242,9 @@ class Context:
     def set_stream(self, stream_ptr):
         check(self.lib.vkpd_set_stream(self.h, C.c_void_p(stream_ptr) if stream_ptr else None))
 
+    def stream_ptr(self):
+        return self.lib.vkpd_get_stream(self.h) or 0
+
     def set_state(self, x, v=None):
         x = f64(x, (self.n, 3))
         v = None if v is None else f64(v, (self.n, 3))
@@ -247,6 +255,36 @@ class Context:
         v = np.empty((self.n, 3)) if want_v else None
         check(self.lib.vkpd_get_state(self.h, ptr(x), ptr(v)))
         return x, v
+
+    # -- state as torch CUDA tensors (the carrier): float64 (n, 3), caller order, no host copies
+    def _dev(self, t, shape):
+        if t is None:
+            return None
+        if not (getattr(t, "is_cuda", False)):
+            raise TypeError("expected a CUDA tensor")
+        import torch
+        if t.dtype != torch.float64 or tuple(t.shape) != shape or not t.is_contiguous():
+            raise ValueError(f"expected a contiguous float64 tensor of shape {shape}")
+        return C.c_void_p(t.data_ptr())
+
+    def set_state_tensor(self, x, v=None):
+        check(self.lib.vkpd_set_state_dev(self.h, self._dev(x, (self.n, 3)), self._dev(v, (self.n, 3))))
+
+    def get_state_tensor(self, x=None, v=None):
+        """Positions / velocities into new (or given) float64 CUDA tensors, on the context stream."""
+        import torch
+        dev = torch.device("cuda", torch.cuda.current_device())
+        x = torch.empty((self.n, 3), dtype=torch.float64, device=dev) if x is None else x
+        v = torch.empty((self.n, 3), dtype=torch.float64, device=dev) if v is None else v
+        check(self.lib.vkpd_get_state_dev(self.h, self._dev(x, (self.n, 3)), self._dev(v, (self.n, 3))))
+        return x, v
+
+    def set_forces_tensor(self, f):
+        check(self.lib.vkpd_set_forces_dev(self.h, self._dev(f, (self.n, 3))))
+
+    def set_pin_targets_tensor(self, t):
+        if self.n_pins:
+            check(self.lib.vkpd_set_pin_targets_dev(self.h, self._dev(t, (self.n_pins, 3))))
 
     def set_pin_targets(self, t):
         if self.n_pins:

@@ -276,7 +276,8 @@ struct PcgArgs {
     const T* cheb_val;           //   of row i (pads: own slot, value 0), its value, and the diagonal
     const T* cheb_kdiag;
     const int* cheb_nexp;        // per CTA: its leading rows that other CTAs read (register path)
-    const int* cheb_halo_ptr;    // per CTA: rows of other CTAs its rows reference
+    const int* cheb_halo_ptr;    // per CTA: rows of other CTAs its rows reference, grouped by owner CTA
+    const int* cheb_nbr_hend;    // per (CTA, neighbour): end of that neighbour's rows in the CTA's halo
     const int* cheb_halo;
     int cheb_halo_max;
 };

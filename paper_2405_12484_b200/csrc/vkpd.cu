@@ -104,6 +104,27 @@ __global__ void k_sim_between(int n, int nP, const vk::vec4_t<T>* __restrict__ x
     }
     if (fin) f[k] = vk::make4<T>((T)fin[3 * j], (T)fin[3 * j + 1], (T)fin[3 * j + 2], T(0));
 }
+// New state (caller order, float64) into the device state: flags a change (bit pattern) against
+// the current contents, so a caller that feeds back the state it received keeps the solver's warm
+// start (pd_step called frame by frame behaves like simulate_mesh); zero v when src is null.
+template <typename T>
+__global__ void k_state_in(int n, const double* __restrict__ src, const int* __restrict__ int_of_orig,
+                           vk::vec4_t<T>* dst, int* changed) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const vk::vec4_t<T> nv = src ? vk::make4<T>((T)src[3 * j], (T)src[3 * j + 1], (T)src[3 * j + 2], T(0))
+                                 : vk::make4<T>(T(0), T(0), T(0), T(0));
+    const int i = int_of_orig[j];
+    const vk::vec4_t<T> ov = dst[i];
+    if (nv.x != ov.x || nv.y != ov.y || nv.z != ov.z) *changed = 1;
+    dst[i] = nv;
+}
+template <typename T>
+__global__ void k_zero_if(size_t n, vk::vec4_t<T>* a, const int* __restrict__ flag) {
+    if (*flag == 0) return;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        a[i] = vk::make4<T>(T(0), T(0), T(0), T(0));
+}
 template <typename T>
 __global__ void k_gather_out(int n, const vk::vec4_t<T>* __restrict__ src, const int* __restrict__ int_of_orig,
                              double* dst) {
@@ -217,6 +238,10 @@ struct CtxBase {
     virtual int init(const vkpd_mesh_desc* d, const vkpd_config* c) = 0;
     virtual int set_state(const double* x, const double* v) = 0;
     virtual int get_state(double* x, double* v) = 0;
+    virtual int set_state_dev(const void* x, const void* v) = 0;
+    virtual int get_state_dev(void* x, void* v) = 0;
+    virtual int set_forces_dev(const void* f) = 0;
+    virtual int set_pin_targets_dev(const void* t) = 0;
     virtual int set_pin_targets(const double* t) = 0;
     virtual int set_forces(const double* f) = 0;
     virtual int set_gammas(const double* gs, const double* gv) = 0;
@@ -785,7 +810,7 @@ struct Ctx : CtxBase {
     int cheb_halo_max = 0;
     DBuf<int> cheb_slot, cheb_halo_ptr, cheb_halo;
     DBuf<T> cheb_val, cheb_kdiag;
-    DBuf<int> cheb_nexp;
+    DBuf<int> cheb_nexp, cheb_nbr_hend;
     int build_cheb_neighbours() {
         const int chunk = cdiv(std::max(1, nF), pcg_blocks);
         std::vector<int> ecol((size_t)ell_w * nF);
@@ -822,42 +847,61 @@ struct Ctx : CtxBase {
                 }
             }
         }
-        // per CTA: neighbour CTAs, halo rows (slots assigned position-major, then by row, so a
-        // warp's halo reads are consecutive too) and every entry's slot
-        std::vector<int> ptr(pcg_blocks + 1, 0), lst, hptr(pcg_blocks + 1, 0), hl;
+        // per CTA: neighbour CTAs and halo rows, grouped by owner CTA (in neighbour order: the
+        // kernel loads each neighbour's rows as soon as its flag arrives); within a group in
+        // first-use order over (position, row), so a warp's halo reads are consecutive too
+        std::vector<int> ptr(pcg_blocks + 1, 0), lst, hptr(pcg_blocks + 1, 0), hl, hend;
         std::vector<int> oslot((size_t)vk::kChebOff * nn1);
-        std::vector<char> seen(pcg_blocks, 0);
+        std::vector<int> nbr_pos(pcg_blocks, -1);
         std::vector<int> hslot(nn1, -1);
         cheb_halo_max = 0;
         for (int b = 0; b < pcg_blocks; ++b) {
-            std::fill(seen.begin(), seen.end(), 0);
-            seen[b] = 1;
             const int r0 = b * chunk, r1 = std::min(nF, r0 + chunk);
-            const int h0 = (int)hl.size();
+            std::vector<int> first;                     // halo rows in first-use order
+            const int n0 = (int)lst.size();
+            auto note = [&](int c) {
+                const int ow = c / chunk;
+                if (nbr_pos[ow] < 0) { nbr_pos[ow] = (int)lst.size() - n0; lst.push_back(ow); }
+            };
             for (int o = 0; o < vk::kChebOff; ++o)
                 for (int i = r0; i < r1; ++i) {
                     const int c = ocol[(size_t)o * nF + i];
-                    if (c < 0) { oslot[(size_t)o * nF + i] = i - r0; continue; }      // pad: own row, value 0
-                    if (c >= r0 && c < r1) { oslot[(size_t)o * nF + i] = c - r0; continue; }
-                    const int ow = c / chunk;
-                    if (!seen[ow]) { seen[ow] = 1; lst.push_back(ow); }
-                    if (hslot[c] < 0) { hslot[c] = (int)hl.size() - h0; hl.push_back(c); }
-                    oslot[(size_t)o * nF + i] = pcg_threads + hslot[c];
+                    if (c < 0 || (c >= r0 && c < r1)) continue;
+                    note(c);
+                    if (hslot[c] < 0) { hslot[c] = 0; first.push_back(c); }
                 }
-            if (!fits) {      // rows beyond kChebOff entries: neighbour sets from the full ELL
+            if (!fits)
                 for (int sl = 0; sl < ell_w; ++sl)
                     for (int i = r0; i < r1; ++i) {
                         const int c = ecol[(size_t)sl * nF + i];
-                        if (c >= r0 && c < r1) continue;
-                        const int ow = c / chunk;
-                        if (!seen[ow]) { seen[ow] = 1; lst.push_back(ow); }
+                        if (c < r0 || c >= r1) note(c);
                     }
+            std::stable_sort(first.begin(), first.end(),
+                             [&](int x, int y) { return nbr_pos[x / chunk] < nbr_pos[y / chunk]; });
+            const int h0 = (int)hl.size();
+            for (size_t j = 0; j < first.size(); ++j) { hslot[first[j]] = (int)j; hl.push_back(first[j]); }
+            const int nnb = (int)lst.size() - n0;
+            for (int q = 0; q < nnb; ++q) {
+                int e = 0;
+                for (size_t j = 0; j < first.size(); ++j)
+                    if (nbr_pos[first[j] / chunk] <= q) e = (int)j + 1;
+                hend.push_back(e);
             }
+            for (int o = 0; o < vk::kChebOff; ++o)
+                for (int i = r0; i < r1; ++i) {
+                    const int c = ocol[(size_t)o * nF + i];
+                    if (c < 0) oslot[(size_t)o * nF + i] = i - r0;                 // pad: own row, value 0
+                    else if (c >= r0 && c < r1) oslot[(size_t)o * nF + i] = c - r0;
+                    else oslot[(size_t)o * nF + i] = pcg_threads + hslot[c];
+                }
             for (int j = h0; j < (int)hl.size(); ++j) hslot[hl[j]] = -1;
+            for (int q = n0; q < (int)lst.size(); ++q) nbr_pos[lst[q]] = -1;
             ptr[b + 1] = (int)lst.size();
             hptr[b + 1] = (int)hl.size();
             cheb_halo_max = std::max(cheb_halo_max, (int)hl.size() - h0);
         }
+        if (hend.empty()) hend.push_back(0);
+        CK(cheb_nbr_hend.alloc(hend.size())); CK(cheb_nbr_hend.upload(hend.data(), hend.size(), stream));
         if (lst.empty()) lst.push_back(0);
         if (hl.empty()) hl.push_back(0);
         // exported rows (read by another CTA) must lead each CTA's range for the early publish;
@@ -1136,16 +1180,55 @@ struct Ctx : CtxBase {
         return VKPD_OK;
     }
 
-    int set_state(const double* hx, const double* hv) override {
-        int rc = upload_nodes(hx, x.p);
-        if (rc) return rc;
-        if (hv) rc = upload_nodes(hv, v.p);
-        else CK(cudaMemsetAsync(v.p, 0, n * sizeof(V4), stream));
-        if (rc) return rc;
-        // a new trajectory: no warm start from the previous one (results depend on the state only)
-        if (warm0.p) CK(cudaMemsetAsync(warm0.p, 0, warm0.n * sizeof(V4), stream));
-        if (warm1.p) CK(cudaMemsetAsync(warm1.p, 0, warm1.n * sizeof(V4), stream));
-        CK(cudaStreamSynchronize(stream));
+    DBuf<int> state_changed;
+    // x, v (caller order, float64) from host (dev = false) or device memory (dev = true, on the
+    // context stream, no host synchronisation).  A state other than the one the context holds
+    // starts a new trajectory: the warm-start banks are cleared (results depend on the state
+    // only); the state it handed out last keeps them.
+    int set_state_any(const double* sx, const double* sv, bool dev) {
+        if (!state_changed.p) CK(state_changed.alloc(1));
+        CK(cudaMemsetAsync(state_changed.p, 0, sizeof(int), stream));
+        const double* px = sx;
+        const double* pv = sv;
+        if (!dev) {
+            CK(cudaMemcpyAsync(stage.p, sx, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, stream));
+            px = stage.p;
+        }
+        k_state_in<T><<<cdiv(n, 256), 256, 0, stream>>>(n, px, int_of_orig.p, x.p, state_changed.p);
+        CK(cudaGetLastError());
+        if (!dev && sv) {
+            CK(cudaMemcpyAsync(stage.p, sv, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, stream));
+            pv = stage.p;
+        }
+        k_state_in<T><<<cdiv(n, 256), 256, 0, stream>>>(n, pv, int_of_orig.p, v.p, state_changed.p);
+        CK(cudaGetLastError());
+        for (DBuf<V4>* b : {&warm0, &warm1})
+            if (b->p) k_zero_if<T><<<2 * n_sms, 256, 0, stream>>>(b->n, b->p, state_changed.p);
+        CK(cudaGetLastError());
+        if (!dev) CK(cudaStreamSynchronize(stream));
+        return VKPD_OK;
+    }
+    int set_state(const double* hx, const double* hv) override { return set_state_any(hx, hv, false); }
+    int set_state_dev(const void* dx, const void* dv) override {
+        return set_state_any((const double*)dx, (const double*)dv, true);
+    }
+    int get_state_dev(void* dx, void* dv) override {
+        if (dx) k_gather_out<T><<<cdiv(n, 256), 256, 0, stream>>>(n, x.p, int_of_orig.p, (double*)dx);
+        if (dv) k_gather_out<T><<<cdiv(n, 256), 256, 0, stream>>>(n, v.p, int_of_orig.p, (double*)dv);
+        CK(cudaGetLastError());
+        return VKPD_OK;
+    }
+    int set_forces_dev(const void* df) override {
+        if (df == nullptr) { has_forces = false; return VKPD_OK; }
+        has_forces = true;
+        k_scatter_in<T><<<cdiv(n, 256), 256, 0, stream>>>(n, (const double*)df, int_of_orig.p, f.p);
+        CK(cudaGetLastError());
+        return VKPD_OK;
+    }
+    int set_pin_targets_dev(const void* dt_) override {
+        if (nP == 0) return VKPD_OK;
+        k_rows_in<T><<<cdiv(nP, 256), 256, 0, stream>>>(nP, (const double*)dt_, pin_tgt.p);
+        CK(cudaGetLastError());
         return VKPD_OK;
     }
     int get_state(double* hx, double* hv) override {
@@ -1239,7 +1322,7 @@ struct Ctx : CtxBase {
         pa.flags = cheb_flags.p; pa.cheb_nbr_ptr = cheb_nbr_ptr.p; pa.cheb_nbr = cheb_nbr.p;
         pa.cheb_lmin = lam_min; pa.cheb_lmax = gersh;
         pa.cheb_slot = cheb_slot.p; pa.cheb_val = cheb_val.p; pa.cheb_kdiag = cheb_kdiag.p;
-        pa.cheb_nexp = cheb_nexp.p;
+        pa.cheb_nexp = cheb_nexp.p; pa.cheb_nbr_hend = cheb_nbr_hend.p;
         pa.cheb_halo_ptr = cheb_halo_ptr.p; pa.cheb_halo = cheb_halo.p;
         pa.cheb_halo_max = cheb_halo_max;
         pa.h = hh.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
@@ -2273,6 +2356,16 @@ int vkpd_set_state(vkpd_ctx* ctx, const double* x, const double* v) {
     CTX_CALL(set_state(x, v));
 }
 int vkpd_get_state(vkpd_ctx* ctx, double* x, double* v) { CTX_CALL(get_state(x, v)); }
+int vkpd_set_state_dev(vkpd_ctx* ctx, const void* x, const void* v) {
+    if (!x) return fail(VKPD_EINVAL, "null positions");
+    CTX_CALL(set_state_dev(x, v));
+}
+int vkpd_get_state_dev(vkpd_ctx* ctx, void* x, void* v) { CTX_CALL(get_state_dev(x, v)); }
+int vkpd_set_forces_dev(vkpd_ctx* ctx, const void* f) { CTX_CALL(set_forces_dev(f)); }
+int vkpd_set_pin_targets_dev(vkpd_ctx* ctx, const void* t) {
+    if (!t) return fail(VKPD_EINVAL, "null pin targets");
+    CTX_CALL(set_pin_targets_dev(t));
+}
 int vkpd_set_pin_targets(vkpd_ctx* ctx, const double* t) {
     if (!t) return fail(VKPD_EINVAL, "null pin targets");
     CTX_CALL(set_pin_targets(t));

@@ -61,6 +61,18 @@ class SimState:
     colliders: tuple = ()
 
     def __post_init__(self):
+        if _is_cuda_tensor(self.x):
+            # PyTorch carrier: x / v stay float64 CUDA tensors and pd_step keeps them on the device
+            import torch
+            self.x = self.x.detach().to(torch.float64).reshape(-1, 3).contiguous().clone()
+            v = self.v if _is_cuda_tensor(self.v) else torch.as_tensor(np.asarray(self.v, dtype=float))
+            self.v = v.detach().to(device=self.x.device, dtype=torch.float64).reshape(-1, 3).contiguous().clone()
+            self.pins = np.asarray(self.pins, dtype=int)
+            if self.pin_targets is None and len(self.pins):
+                self.pin_targets = self.x[torch.as_tensor(self.pins, device=self.x.device)].clone()
+            if self.dt <= 0.0:
+                raise ValueError("dt must be positive")
+            return
         self.x = np.asarray(self.x, dtype=float).reshape(-1, 3).copy()
         self.v = np.asarray(self.v, dtype=float).reshape(-1, 3).copy()
         self.pins = np.asarray(self.pins, dtype=int)
@@ -68,6 +80,10 @@ class SimState:
             self.pin_targets = self.x[self.pins].copy()
         if self.dt <= 0.0:
             raise ValueError("dt must be positive")
+
+
+def _is_cuda_tensor(a):
+    return getattr(a, "is_cuda", False) and hasattr(a, "data_ptr")
 
 
 def _check_inputs(mesh, gammas, dt):
@@ -336,17 +352,42 @@ def pd_step(state, mesh, gammas, iterations=PD_ITERS_DEFAULT, forces=None, solve
     # with colliders the reference re-assembles K with the contact diagonal and ignores
     # `solver` (pdsolver.py:273-281); the device step adds the contact terms per step
     ctx = device_context(mesh, gammas, state.dt, state.pins, precision, tol, max_iters)
-    ctx.set_state(state.x, state.v)
-    if len(state.pins):
-        ctx.set_pin_targets(state.pin_targets)
-    ctx.set_forces(forces)
+    on_device = _is_cuda_tensor(state.x)
+    if on_device:
+        # torch tensors in, torch tensors out, ordered after / before the caller's stream: no
+        # host copies of the state
+        import torch
+        caller = torch.cuda.current_stream(state.x.device)
+        lib_stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=state.x.device)
+        lib_stream.wait_stream(caller)
+        ctx.set_state_tensor(state.x, state.v)
+        if len(state.pins):
+            if _is_cuda_tensor(state.pin_targets):
+                ctx.set_pin_targets_tensor(state.pin_targets.to(torch.float64).contiguous())
+            else:
+                ctx.set_pin_targets(state.pin_targets)
+        if _is_cuda_tensor(forces):
+            ctx.set_forces_tensor(forces.to(torch.float64).reshape(-1, 3).contiguous())
+        else:
+            ctx.set_forces(forces)
+    else:
+        ctx.set_state(state.x, state.v)
+        if len(state.pins):
+            ctx.set_pin_targets(state.pin_targets)
+        ctx.set_forces(forces)
     ctx.set_colliders(state.colliders, contact_stiffness)
     try:
         ctx.step(iterations, damping)
     except _abi.NonFiniteError as exc:
         raise RuntimeError(str(exc)) from None
-    x, v = ctx.get_state()
-    state.x, state.v = x, v
+    if on_device:
+        with torch.cuda.stream(lib_stream):
+            state.x, state.v = ctx.get_state_tensor()
+        caller.wait_stream(lib_stream)
+        state.x.record_stream(caller)
+        state.v.record_stream(caller)
+    else:
+        state.x, state.v = ctx.get_state()
     return state
 
 

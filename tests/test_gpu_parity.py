@@ -637,3 +637,29 @@ def test_projection_jacobians_finite_difference(rng):
         Rm, Vm = material.batch_projections(F - dF)
         assert np.abs((Rp - Rm).reshape(-1, 9) / (2 * h) - JR[:, :, k]).max() < 1e-5
         assert np.abs((Vp - Vm).reshape(-1, 9) / (2 * h) - JV[:, :, k]).max() < 1e-5
+
+
+def test_pd_step_with_torch_cuda_state(c1):
+    """PyTorch carrier: SimState x / v as float64 CUDA tensors stay on the device through
+    pd_step (vkpd_set_state_dev / get_state_dev on the library stream) and give the same bits
+    as the numpy path; feeding the returned state back keeps the warm start, as stepping the
+    context does."""
+    import torch
+    pdsolver.invalidate_cache()
+    sa = pdsolver.SimState(x=c1.mesh.nodes, v=np.zeros_like(c1.mesh.nodes), dt=c1.dt, pins=c1.pins,
+                           pin_targets=c1.pin_targets)
+    xa = []
+    for _ in range(3):
+        pdsolver.pd_step(sa, c1.mesh, c1.gammas, iterations=30, forces=c1.forces)
+        xa.append((sa.x.copy(), sa.v.copy()))
+    pdsolver.invalidate_cache()
+    xt = torch.as_tensor(c1.mesh.nodes, device="cuda")
+    sb = pdsolver.SimState(x=xt, v=torch.zeros_like(xt), dt=c1.dt, pins=c1.pins,
+                           pin_targets=torch.as_tensor(c1.pin_targets, device="cuda"))
+    ft = torch.as_tensor(c1.forces, device="cuda")
+    for k in range(3):
+        pdsolver.pd_step(sb, c1.mesh, c1.gammas, iterations=30, forces=ft)
+        assert sb.x.is_cuda and sb.v.is_cuda
+        assert np.array_equal(sb.x.cpu().numpy(), xa[k][0])
+        assert np.array_equal(sb.v.cpu().numpy(), xa[k][1])
+    assert rel_l2(sb.x.cpu().numpy(), golden("c1.npz")["frames"][2]) < 1e-10
