@@ -460,8 +460,7 @@ def run_ours(args):
     e2e_val = world * nE * head["rounds"] / e2e_s
     peak, peak_kind = measured_peak()
     pst = head["pst"]
-    solver_kernel = "k_cheb_reg (global step, Chebyshev-Jacobi, neighbour flags)" if prec == "fp64" \
-        else "k_pcg_poly (global step, persistent polynomial-preconditioned CG)"
+    solver_kernel = "k_cheb_reg (global step, Chebyshev-Jacobi, neighbour flags)"
     alg_local = ALG_BYTES_LOCAL[prec] * nE
     ach_local = alg_local / (head["kl_ms"] * 1e-3) / 1e9
     cpu = None
@@ -482,9 +481,8 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": sc.name, "n_tets": nE, "n_nodes": m.n_nodes, "pd_iterations": its,
                    "dt": sc.dt, "precision": prec, "tol": ctx_tol(args, prec),
-                   "solver": ("Chebyshev semi-iteration on the Jacobi-scaled K_ff to |r| <= tol |M/dt^2 xhat| "
-                              "(direct-equivalent)") if prec == "fp64" else
-                             "polynomial-preconditioned CG to |r| <= tol |M/dt^2 xhat| (direct-equivalent)",
+                   "solver": "Chebyshev semi-iteration on the Jacobi-scaled K_ff to |r| <= tol |M/dt^2 xhat| "
+                             "(direct-equivalent)",
                    "parallelism": "single GPU (C4 runs under torchrun: one garment over N GPUs)",
                    "pd_loop": "graph WHILE node; stops at the first solve needing no work (later rounds repeat "
                               "it bit for bit); value counts executed rounds",
@@ -519,7 +517,7 @@ def run_ours(args):
                         "ms_per_frame_every_round": side_all,
                         "e2e_ms_per_frame": side["e2e_s"] * 1e3 / args.steps,
                         "roofline": solver_roofline("fp32", side["pst"], side["pst"]["n_free"], peak, peak_kind,
-                                                    "k_pcg_poly"),
+                                                    "k_cheb_reg"),
                         "tol": ctx_tol(args, "fp32")}
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -986,7 +986,7 @@ struct Ctx : CtxBase {
                    : part_blocks > 0 ? part_blocks : std::min(n_sms, std::max(1, cdiv(nF, 32)));
         pcg_threads = std::max(128, std::min(768, 32 * cdiv(cdiv(std::max(1, nF), pcg_blocks), 32)));
         solver_kind = c->solver != VKPD_SOLVER_AUTO ? c->solver
-                                                     : (sizeof(T) == 8 ? VKPD_SOLVER_CHEBYSHEV : VKPD_SOLVER_PCG_POLY);
+                                                     : VKPD_SOLVER_CHEBYSHEV;
         if (solver_kind < VKPD_SOLVER_PCG_POLY || solver_kind > VKPD_SOLVER_PCG_JACOBI)
             return fail(VKPD_EINVAL, "unknown solver kind");
         pcg_poly = solver_kind == VKPD_SOLVER_PCG_POLY;
