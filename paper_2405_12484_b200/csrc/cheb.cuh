@@ -204,8 +204,7 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
         for (;;) {
             for (; k < target; ++k) {
                 pcg_mark(10);
-                if (k > 0) cheb_wait(a.flags, nbr, nn, base + (unsigned)k);
-                pcg_mark(11);
+                if (!REG && k > 0) cheb_wait(a.flags, nbr, nn, base + (unsigned)k);
                 const vec4_t<T>* dcur = (k & 1) ? a.p1 : a.p0;
                 vec4_t<T>* dnext = (k & 1) ? a.p0 : a.p1;
                 const double rho_n = 1.0 / (2.0 * sigma - rho);
@@ -214,23 +213,41 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                 if (REG) {
                     T* const sx = sd + (k & 1) * 3 * kChebSlots;         // d_k
                     T* const sn = sd + ((k + 1) & 1) * 3 * kChebSlots;   // d_{k+1} (own rows)
-                    // halo rows of d_k into shared memory (own rows are there already); one
-                    // poll of all neighbour flags (warp 0), then every thread loads: measured
-                    // faster than a warp per neighbour polling and loading on its own (4.8 vs
-                    // 4.1 us per step at C3: a warp's serial load round trips dominate)
-                    for (int j = threadIdx.x; j < nh; j += blockDim.x) {
-                        T hx, hy, hz;
-                        ldcg3(&dcur[hidx[j]], hx, hy, hz);
-                        const int sl = blockDim.x + j;
-                        sx[sl] = hx; sx[kChebSlots + sl] = hy; sx[2 * kChebSlots + sl] = hz;
+                    // every own row's d_k is in shared memory (written by step k-1)
+                    if (k > 0) __syncthreads();
+                    if (exp_warp) {
+                        // exported warps: neighbours' step flags (warp 0), their rows of d_k into the
+                        // halo slots, the exported rows, then publish this CTA's step flag.  (Doing
+                        // the own-column part of the exported rows before the wait and only the
+                        // halo columns after it measured slower: 12.9 vs 9.0 ms/frame at C3 fp64,
+                        // the per-entry predicates diverge within warps.)
+                        if (k > 0) {
+                            if (threadIdx.x < 32) {
+                                for (int j = threadIdx.x; j < nn; j += 32) {
+                                    const unsigned int* f = a.flags + (size_t)nbr[j] * 32;
+                                    const unsigned int target = base + (unsigned)k;
+                                    unsigned long long spins = 0;
+                                    while ((int)(ld_acquire_gpu(f) - target) < 0) {
+                                        if (++spins > (1ull << 33)) __trap();
+                                    }
+                                }
+                            }
+                            asm volatile("bar.sync 1, %0;" ::"r"(exp_threads) : "memory");
+                        }
+                        pcg_mark(11);
+                        for (int j = threadIdx.x; j < nh; j += exp_threads) {
+                            T hx, hy, hz;
+                            ldcg3(&dcur[hidx[j]], hx, hy, hz);
+                            const int sl = blockDim.x + j;
+                            sx[sl] = hx; sx[kChebSlots + sl] = hy; sx[2 * kChebSlots + sl] = hz;
+                        }
+                        asm volatile("bar.sync 1, %0;" ::"r"(exp_threads) : "memory");
+                        pcg_mark(12);
                     }
-                    __syncthreads();
-                    pcg_mark(12);
-                    // interior warps start after the exported warps are done with shared memory
-                    if (!exp_warp) asm volatile("bar.sync 2, %0;" ::"r"((int)blockDim.x) : "memory");
+                    // interior warps run their rows meanwhile: they read own rows only
+                    T qx = kdiag * dxv, qy = kdiag * dyv, qz = kdiag * dzv, px = 0, py = 0, pz = 0;
                     if (own) {
                         // two partial sums per component (shorter dependency chains)
-                        T qx = kdiag * dxv, qy = kdiag * dyv, qz = kdiag * dzv, px = 0, py = 0, pz = 0;
 #pragma unroll
                         for (int s = 0; s < kChebOff; s += 2) {
                             const T* d = sx + cols[s];
@@ -241,6 +258,8 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                                 pz += vals[s + 1] * e[2 * kChebSlots];
                             }
                         }
+                    }
+                    if (own) {
                         qx += px; qy += py; qz += pz;
                         if (a.cdiag != nullptr) {
                             const T cd = a.cdiag[i];
@@ -259,7 +278,6 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                     if (exp_warp) {
                         asm volatile("bar.sync 1, %0;" ::"r"(exp_threads) : "memory");
                         if (threadIdx.x == 0) st_release_gpu(a.flags + (size_t)blockIdx.x * 32, base + (unsigned)(k + 1));
-                        if (exp_threads < (int)blockDim.x) asm volatile("bar.arrive 2, %0;" ::"r"((int)blockDim.x) : "memory");
                     }
                     pcg_mark(14);
                 } else {
