@@ -460,7 +460,8 @@ def run_ours(args):
     e2e_val = world * nE * head["rounds"] / e2e_s
     peak, peak_kind = measured_peak()
     pst = head["pst"]
-    solver_kernel = "k_cheb_reg (global step, Chebyshev-Jacobi, neighbour flags)"
+    solver_kernel = ("k_cheb_reg (global step, Chebyshev-Jacobi, neighbour flags)" if pst["solver"] == "chebyshev"
+                     else "k_pcg_poly (global step, persistent polynomial-preconditioned CG)")
     alg_local = ALG_BYTES_LOCAL[prec] * nE
     ach_local = alg_local / (head["kl_ms"] * 1e-3) / 1e9
     cpu = None
@@ -505,7 +506,8 @@ def run_ours(args):
         "profiled_frame": {"ms": head["prof_frame_ms"], "local_ms_per_round": head["local_ms"],
                            "global_ms_per_round": head["global_ms"], "rounds": len(pst["global_ms"])},
         "clocks": head["clocks"],
-        "solver_stats": {"steps_last_frame": head["stats"]["cg_iters_total"], "solver_ctas": pst["pcg_blocks"],
+        "solver_stats": {"solver": pst["solver"], "steps_last_frame": head["stats"]["cg_iters_total"],
+                         "solver_ctas": pst["pcg_blocks"],
                          "robust_elements_cum": head["stats"]["robust"]},
         "paper_ms_per_frame": 604.0,
         "cpu_baseline": cpu,
@@ -517,7 +519,8 @@ def run_ours(args):
                         "ms_per_frame_every_round": side_all,
                         "e2e_ms_per_frame": side["e2e_s"] * 1e3 / args.steps,
                         "roofline": solver_roofline("fp32", side["pst"], side["pst"]["n_free"], peak, peak_kind,
-                                                    "k_cheb_reg"),
+                                                    "k_cheb_reg" if side["pst"]["solver"] == "chebyshev"
+                                                    else "k_pcg_poly"),
                         "tol": ctx_tol(args, "fp32")}
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -108,6 +108,7 @@ typedef struct {
     double global_ms[256];
     unsigned long long pd_rounds_total; /* PD rounds executed since creation: a frame stops early once a
                                            solve needs zero CG iterations (the rest would repeat it exactly) */
+    int solver;                /* the global-step solver in use (VKPD_SOLVER_*; AUTO resolved)     */
 } vkpd_stats;
 
 const char* vkpd_last_error(void);

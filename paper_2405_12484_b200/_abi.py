@@ -59,7 +59,7 @@ class Stats(C.Structure):
         ("n_pd_iters", C.c_int), ("cg_iters", C.c_int * 256), ("cg_iters_total", C.c_int),
         ("robust", C.c_uint), ("fallback", C.c_uint), ("pcg_blocks", C.c_int),
         ("ell_width", C.c_int), ("n_free", C.c_int64), ("local_ms", C.c_double * 256),
-        ("global_ms", C.c_double * 256), ("pd_rounds_total", C.c_ulonglong),
+        ("global_ms", C.c_double * 256), ("pd_rounds_total", C.c_ulonglong), ("solver", C.c_int),
     ]
 
 
@@ -514,7 +514,8 @@ class Context:
         return dict(cg_iters=list(st.cg_iters[:n]), cg_iters_total=st.cg_iters_total,
                     robust=st.robust, fallback=st.fallback, pcg_blocks=st.pcg_blocks,
                     ell_width=st.ell_width, n_free=st.n_free, local_ms=list(st.local_ms[:n]),
-                    global_ms=list(st.global_ms[:n]), pd_rounds_total=st.pd_rounds_total)
+                    global_ms=list(st.global_ms[:n]), pd_rounds_total=st.pd_rounds_total,
+                    solver={v: k for k, v in SOLVERS.items()}.get(st.solver, str(st.solver)))
 
 
 def projection_jacobians(F):

@@ -329,6 +329,7 @@ struct Ctx : CtxBase {
     DBuf<V4> hh;                         // polynomial preconditioner: h = K D^-1 r
     int pcg_threads = 512;               // CTA size of the persistent solver
     int solver_kind = VKPD_SOLVER_PCG_POLY;   // resolved vkpd_config.solver
+    bool solver_auto = true;
     bool pcg_poly = true;                // Neumann-1 polynomial preconditioner (CG kinds)
     bool cheb = false;                   // Chebyshev semi-iteration with neighbour flags (cheb.cuh)
     bool cheb_reg = false;               // ... with the row state in registers (one row per thread)
@@ -732,7 +733,14 @@ struct Ctx : CtxBase {
         vk::k_scale_ell<T><<<cdiv(nF, 256), 256, 0, s>>>(nF, ell_w, ell_col.p, ell_val.p, inv_diag.p, ell_kd.p);
         CK(cudaGetLastError());
         if (cheb) if (int rc = spectrum_low()) return rc;
-        if (cheb && pcg_blocks > 0) if (int rc = build_cheb_neighbours()) return rc;
+        if (cheb && pcg_blocks > 0) {
+            if (int rc = build_cheb_neighbours()) return rc;
+            if (solver_auto && !cheb_reg) {
+                cheb = false;
+                pcg_poly = true;
+                solver_kind = VKPD_SOLVER_PCG_POLY;
+            }
+        }
         return VKPD_OK;
     }
 
@@ -985,8 +993,12 @@ struct Ctx : CtxBase {
         pcg_blocks = c->pcg_blocks > 0 ? c->pcg_blocks
                    : part_blocks > 0 ? part_blocks : std::min(n_sms, std::max(1, cdiv(nF, 32)));
         pcg_threads = std::max(128, std::min(768, 32 * cdiv(cdiv(std::max(1, nF), pcg_blocks), 32)));
-        solver_kind = c->solver != VKPD_SOLVER_AUTO ? c->solver
-                                                     : VKPD_SOLVER_CHEBYSHEV;
+        // AUTO: the Chebyshev solver where its register path applies (one row per thread, the
+        // CTA's rows + halo staged in shared memory: C3 0.89 / 8.9 ms per frame fp32 / fp64 vs
+        // 0.62 / 16.1 for CG), else the polynomial CG (C5, 7K rows per CTA: the generic
+        // Chebyshev path streams the ELL from HBM every step, 148 vs 122 ms per fp64 frame)
+        solver_auto = c->solver == VKPD_SOLVER_AUTO;
+        solver_kind = solver_auto ? VKPD_SOLVER_CHEBYSHEV : c->solver;
         if (solver_kind < VKPD_SOLVER_PCG_POLY || solver_kind > VKPD_SOLVER_PCG_JACOBI)
             return fail(VKPD_EINVAL, "unknown solver kind");
         pcg_poly = solver_kind == VKPD_SOLVER_PCG_POLY;
@@ -2246,6 +2258,7 @@ struct Ctx : CtxBase {
         st->robust = ps.robust;
         st->fallback = ps.fallback;
         st->pd_rounds_total = ps.pd_rounds;
+        st->solver = solver_kind;
         st->pcg_blocks = pcg_blocks;
         st->ell_width = ell_w;
         st->n_free = nF;
