@@ -260,6 +260,15 @@ int vkpd_frame_outputs(vkpd_ctx* ctx, double* yarn, double* det_deviation);
 int vkpd_v2y(int64_t n_yarn, const int64_t* indptr, const int64_t* indices, const double* data, int64_t n_nodes,
              const double* x, double* y);
 
+/* Per-frame OBJ text of `volknit simulate` (cli.py:538-547, _write_obj): an optional "# comment"
+ * line, "v x y z" per vertex with %.17g (Python's format(v, ".17g")), then "f a b c" per
+ * triangle (1-based) and "l i j ..." per polyline (1-based; line_ptr has n_lines + 1 offsets
+ * into line_idx).  Host code, no device needed.  Writes at most `cap` bytes into `out` and
+ * returns the total length (call with out = NULL to size the buffer). */
+int64_t vkpd_format_obj(const double* vertices, int64_t n_vertices, const int64_t* faces, int64_t n_faces,
+                        const int64_t* line_ptr, const int64_t* line_idx, int64_t n_lines, const char* comment,
+                        char* out, int64_t cap);
+
 /* ---- fitting-side second order, float64, caller node order ----------------
  * One handle per (mesh, pins, dt); gammas refreshable.  Vectors are (nV,3) row-major doubles.
  *   vkpd_hess_energy_grad  elastic_energy (pdsolver.py:72-82) and elastic_gradient

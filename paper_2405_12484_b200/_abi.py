@@ -30,7 +30,7 @@ EXPORTS = (
     "vkpd_hess_energy_grad", "vkpd_hess_gamma_jt", "vkpd_hess_linearize", "vkpd_hess_csr",
     "vkpd_hess_apply", "vkpd_hess_solve", "vkpd_cms_set_blocks", "vkpd_cms_timing", "vkpd_time_local",
     "vkpd_step_cms", "vkpd_simulate", "vkpd_dev_cheb_step", "vkpd_get_gershgorin", "vkpd_set_state_dev",
-    "vkpd_get_state_dev", "vkpd_set_forces_dev", "vkpd_set_pin_targets_dev",
+    "vkpd_get_state_dev", "vkpd_set_forces_dev", "vkpd_set_pin_targets_dev", "vkpd_format_obj",
 )
 
 
@@ -114,6 +114,7 @@ def load():
         "vkpd_get_state_dev": (I, [P, P, P]),
         "vkpd_set_forces_dev": (I, [P, P]),
         "vkpd_set_pin_targets_dev": (I, [P, P]),
+        "vkpd_format_obj": (C.c_int64, [P, C.c_int64, P, C.c_int64, P, P, C.c_int64, C.c_char_p, P, C.c_int64]),
         "vkpd_get_node_order": (I, [P, P]),
         "vkpd_get_sizes": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                C.POINTER(I)]),

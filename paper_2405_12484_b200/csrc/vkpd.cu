@@ -2391,6 +2391,32 @@ int vkpd_set_yarn_interp(vkpd_ctx* ctx, int64_t n_yarn, const int64_t* indptr, c
 int vkpd_frame_outputs(vkpd_ctx* ctx, double* yarn, double* det_deviation) {
     CTX_CALL(frame_outputs(yarn, det_deviation));
 }
+int64_t vkpd_format_obj(const double* v, int64_t nv, const int64_t* faces, int64_t nf, const int64_t* line_ptr,
+                        const int64_t* line_idx, int64_t nl, const char* comment, char* out, int64_t cap) {
+    std::string s;
+    s.reserve((size_t)nv * 72 + (size_t)nf * 24 + 64);
+    char buf[128];
+    if (comment && comment[0]) { s += "# "; s += comment; s += '\n'; }
+    for (int64_t i = 0; i < nv; ++i) {
+        const int m = std::snprintf(buf, sizeof buf, "v %.17g %.17g %.17g\n", v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+        s.append(buf, (size_t)m);
+    }
+    for (int64_t i = 0; i < nf; ++i) {
+        const int m = std::snprintf(buf, sizeof buf, "f %lld %lld %lld\n", (long long)faces[3 * i] + 1,
+                                    (long long)faces[3 * i + 1] + 1, (long long)faces[3 * i + 2] + 1);
+        s.append(buf, (size_t)m);
+    }
+    for (int64_t l = 0; l < nl; ++l) {
+        s += 'l';
+        for (int64_t k = line_ptr[l]; k < line_ptr[l + 1]; ++k) {
+            const int m = std::snprintf(buf, sizeof buf, " %lld", (long long)line_idx[k] + 1);
+            s.append(buf, (size_t)m);
+        }
+        s += '\n';
+    }
+    if (out && cap > 0) std::memcpy(out, s.data(), (size_t)std::min<int64_t>(cap, (int64_t)s.size()));
+    return (int64_t)s.size();
+}
 int vkpd_v2y(int64_t n_yarn, const int64_t* indptr, const int64_t* indices, const double* data, int64_t n_nodes,
              const double* x, double* y) {
     if (n_yarn < 0 || n_nodes < 0 || (n_yarn > 0 && (!indptr || !indices || !data || !y)) || (n_nodes > 0 && !x))
