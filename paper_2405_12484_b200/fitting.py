@@ -71,6 +71,7 @@ class AdjointState:
     J: sp.csr_matrix          # residual derivative in gamma, free rows
     lam: np.ndarray           # adjoint vector
     grad: np.ndarray          # loss gradient in gamma, length 2nE
+    hctx: object = None       # device float64 Hessian context (pdsolver.hess_context), not in the reference
 
 
 class EquilibriumGateError(RuntimeError):
@@ -126,7 +127,28 @@ def adjoint_gradient(problem, sample, gammas, x, residual=None, logger=None, wit
     if with_matrices:
         H = h.csr()[fdofs][:, fdofs].tocsc()
         J = gamma_jacobian(mesh, x)[fdofs]
-    return AdjointState(x=x, residual=residual, fdofs=fdofs, H=H, J=J, lam=lam.reshape(-1)[fdofs], grad=grad)
+    return AdjointState(x=x, residual=residual, fdofs=fdofs, H=H, J=J, lam=lam.reshape(-1)[fdofs], grad=grad,
+                        hctx=h)
+
+
+def _sensitivities(problem, state, Jk):
+    """S = H_ff^-1 J column by column with the device MINRES of the equilibrium Jacobian
+    (linearised at state.x); None when a column does not reach ADJOINT_ACCEPT."""
+    h = state.hctx
+    n = problem.mesh.n_nodes
+    h.linearize(state.x)
+    fd = state.fdofs
+    Jc = sp.csc_matrix(Jk)
+    S = np.empty(Jc.shape)
+    b = np.zeros(3 * n)
+    for j in range(Jc.shape[1]):
+        b[:] = 0.0
+        b[fd] = Jc[:, j].toarray().ravel()
+        x, _, rr = h.solve(b.reshape(-1, 3), mass_scale=0.0, tol=SOLVE_TOL)
+        if not (rr <= ADJOINT_ACCEPT) or not np.all(np.isfinite(x)):
+            return None
+        S[:, j] = x.reshape(-1)[fd]
+    return S
 
 
 def reduce_columns(J, basis):
@@ -135,10 +157,12 @@ def reduce_columns(J, basis):
     return np.hstack([J[:, :nE] @ basis, J[:, nE:] @ basis])
 
 
-DENSE_GN_MAX = 24000        # largest nf or m of the device dense Gauss-Newton solve
+DENSE_GN_MAX = 24000        # largest m (coefficient columns) of the dense reduced system
+DENSE_H_MAX = 6000          # above this many free DOFs, S = H^-1 J comes from the device solver
+SOLVE_TOL = 1e-13           # MINRES relative tolerance of the sensitivity columns
 
 
-def adjoint_gauss_newton(problem, sample, state, kappa=None, basis=None, frozen=None):
+def adjoint_gauss_newton(problem, sample, state, kappa=None, basis=None, frozen=None, dense_h_max=DENSE_H_MAX):
     """Gauss-Newton direction d with (J^T H^-1 G H^-1 J + kappa I) d = -grad (`fitting.py:251-313`).
 
     The reference eliminates v, u from its sparse symmetric block system
@@ -146,11 +170,16 @@ def adjoint_gauss_newton(problem, sample, state, kappa=None, basis=None, frozen=
         [ H  -G   0 ] [u] = [ 0    ]
         [ J^T 0  -kI] [d]   [ grad ]
     by one sparse LU.  On the B200 the same direction comes from the equivalent reduced
-    system, dense on the device in float64: S = H^-1 J (LU of the exact equilibrium
-    Jacobian, cuSOLVER through torch), P = S^T G S (DGEMM), then a Cholesky solve of
-    P + kappa I.  Same `basis` / `frozen` reductions, the same default kappa and the same
-    (d, kappa, ok) contract: ok False when the factorization fails, the result is not
-    finite, or d is not a descent direction.  Sizes up to DENSE_GN_MAX rows/columns.
+    system in float64: S = H^-1 J, P = S^T G S (DGEMM), then a Cholesky solve of P + kappa I
+    (the ridge kappa = 1e-6 mean diag G makes P too ill-conditioned for an iterative outer
+    solve; the reference factorizes for the same reason).  S comes from the device solver:
+    one preconditioned-MINRES solve of the exact equilibrium Jacobian per column of J
+    (`vkpd_hess_solve`, the adjoint solve of adjoint_gradient), so the mesh size is not
+    bounded -- a large garment takes the `basis` reduction (m = 2r columns); for at most
+    `dense_h_max` free DOFs an LU of H on the device is faster and is used instead.  Same
+    `basis` / `frozen` reductions, the same default kappa and the same (d, kappa, ok)
+    contract: ok False when a solve or the factorization fails, the result is not finite,
+    or d is not a descent direction.  m up to DENSE_GN_MAX columns.
     """
     import scipy.sparse as sps
     import torch
@@ -172,22 +201,32 @@ def adjoint_gauss_newton(problem, sample, state, kappa=None, basis=None, frozen=
     Jk = J[:, keep] if keep is not None else J
     gk = grad[keep] if keep is not None else grad
     nf, m = Jk.shape
-    if nf > DENSE_GN_MAX or m > DENSE_GN_MAX:
-        raise NotImplementedError(f"dense device Gauss-Newton solve limited to {DENSE_GN_MAX} rows/columns")
+    if m > DENSE_GN_MAX:
+        raise NotImplementedError(f"reduced Gauss-Newton system limited to {DENSE_GN_MAX} columns; "
+                                  f"pass a basis")
     dev = torch.device("cuda")
     f64 = torch.float64
-    H = torch.as_tensor(state.H.toarray(), dtype=f64, device=dev)
-    Jd = torch.as_tensor(Jk.toarray(), dtype=f64, device=dev)
-    Gd = torch.as_tensor(G.toarray(), dtype=f64, device=dev)
     g = torch.as_tensor(np.asarray(gk, dtype=float), dtype=f64, device=dev)
     d = np.zeros(J.shape[1])
-    LU, piv, info = torch.linalg.lu_factor_ex(H)
-    if int(info.item()) != 0:
-        return None, kappa, False
-    S = torch.linalg.lu_solve(LU, piv, Jd)
+    if nf <= dense_h_max or state.hctx is None:
+        if nf > DENSE_GN_MAX:
+            raise NotImplementedError("state without a device Hessian context: dense path only")
+        H = torch.as_tensor(state.H.toarray(), dtype=f64, device=dev)
+        Jd = torch.as_tensor(Jk.toarray(), dtype=f64, device=dev)
+        LU, piv, info = torch.linalg.lu_factor_ex(H)
+        if int(info.item()) != 0:
+            return None, kappa, False
+        S = torch.linalg.lu_solve(LU, piv, Jd)
+    else:
+        S = _sensitivities(problem, state, Jk)
+        if S is None:
+            return None, kappa, False
+        S = torch.as_tensor(S, dtype=f64, device=dev)
     if not bool(torch.isfinite(S).all()):
         return None, kappa, False
-    P = S.T @ (Gd @ S)
+    Gs = torch.sparse_csr_tensor(torch.as_tensor(G.indptr, dtype=torch.int64), torch.as_tensor(G.indices, dtype=torch.int64),
+                                 torch.as_tensor(G.data, dtype=f64), size=G.shape).to(dev)
+    P = S.T @ (Gs @ S)
     P = 0.5 * (P + P.T)
     P.diagonal().add_(kappa)
     L, info = torch.linalg.cholesky_ex(P)

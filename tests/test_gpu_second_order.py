@@ -224,3 +224,17 @@ def test_adjoint_gauss_newton_matches_reference(so, tag):
     assert rel_l2(d, g[f"gn_{tag}_d"]) < 1e-6
     if tag == "frozen":
         assert np.all(d[g["gn_frozen"]] == 0.0)
+
+
+def test_adjoint_gauss_newton_device_solver_path(so):
+    """The sensitivity columns S = H^-1 J from the device MINRES of the equilibrium Jacobian
+    (the path meshes beyond DENSE_H_MAX free DOFs take; forced here on C1 with the rank-10
+    basis, m = 20 columns): the same direction as the reference (fitting.py:251-313)."""
+    g, sc = so
+    _, a, _, weight, shift, sample = scenes.adjoint_case()
+    x = g["qs_x"]
+    prob = scenes.TrackingProblem(sc.mesh, sc.dt, x + shift, weight)
+    st = fitting.adjoint_gradient(prob, sample, sc.gammas, x)
+    d, kap, ok = fitting.adjoint_gauss_newton(prob, sample, st, basis=g["gn_basis"], dense_h_max=0)
+    assert ok == bool(g["gn_basis_ok"])
+    assert rel_l2(d, g["gn_basis_d"]) < 1e-6
