@@ -78,59 +78,123 @@ class CmsSubspace:
     """Craig-Bampton basis T = [Phi blocks | I_b + Psi blocks] and K_red = T^T K T.
 
     `solve(b)` = T K_red^-1 T^T b on the device.  Attributes mirror the
-    reference: `blocks` [(sel, Phi, Psi) | None], `T` (CSR), `K_red` (CSC).
+    reference: `blocks` [(sel, Phi, Psi) | None], `T` (CSR, built on first use), `K_red` (CSC).
+
+    The build scales with the domain size (`pdsolver.py:521-590` forms dense eigensystems and a
+    dense n x m_tot T; at C3 with 8 domains that is 36 s and 4.9 GB):
+      * Phi_d: the m lowest eigenpairs of K_ii -- dense `eigh` up to DENSE_EIG_MAX interior
+        nodes (the reference's exact route for small domains), else Chebyshev-filtered subspace
+        iteration on the sparse K_ii on the GPU (K_ii is mass-dominated, condition number ~100)
+        to a Ritz residual of EIG_TOL;
+      * Psi_d = -K_ii^-1 K_ib only on the boundary columns adjacent to d (K_ib is zero on the
+        others, so Psi is too): block conjugate gradients on the sparse K_ii with all adjacent
+        columns at once, to PSI_TOL, on the GPU (Cholesky of the dense K_ii for small domains);
+      * K_red from the blocks: Phi^T K_ii Phi per domain, Phi^T (K_ib + K_ii Psi), and
+        S = K_bb + sum_d (K_bi Psi + Psi^T K_ib + Psi^T K_ii Psi) -- no dense T.
     """
+
+    DENSE_EIG_MAX = 3000
+    EIG_TOL = 1e-12          # Ritz residual of the filtered subspace iteration, relative to |A|
+    PSI_TOL = 1e-13
 
     def __init__(self, K, interior_sets, boundary, modes_per_domain=20):
         torch = _torch()
         dev = torch.device("cuda")
+        f64 = torch.float64
         K = sp.csr_matrix(K)
         self.n = K.shape[0]
         self.boundary = np.asarray(boundary, dtype=int)
         nb = len(self.boundary)
-        blocks = []
+        bpos = -np.ones(self.n, dtype=np.int64)
+        bpos[self.boundary] = np.arange(nb)
+        blocks, red_parts = [], []
+        Kbb = K[self.boundary][:, self.boundary].toarray() if nb else np.zeros((0, 0))
+        S = torch.as_tensor(Kbb, dtype=f64, device=dev)
+        n_modes_tot = sum(min(modes_per_domain, len(s)) for s in interior_sets if len(s))
+        cross = torch.zeros((n_modes_tot, nb), dtype=f64, device=dev)
+        lam_blocks = []
+        c0 = 0
         for sel in interior_sets:
             sel = np.asarray(sel, dtype=int)
             if len(sel) == 0:
                 blocks.append(None)
                 continue
-            Kii = torch.from_numpy(K[sel][:, sel].toarray()).to(dev)
+            Kii_sp = K[sel][:, sel].tocsr()
             m = min(modes_per_domain, len(sel))
-            w, v = torch.linalg.eigh(Kii)
-            Phi = v[:, :m].cpu().numpy()
-            Psi = None
+            Kii = _to_torch_csr(torch, Kii_sp, dev)
+            if len(sel) <= self.DENSE_EIG_MAX:
+                Kd = torch.as_tensor(Kii_sp.toarray(), dtype=f64, device=dev)
+                w, v = torch.linalg.eigh(Kd)
+                Phi = v[:, :m]
+            else:
+                Kd = None
+                gersh = float(abs(Kii_sp).sum(axis=1).max())
+                Phi = _lowest_modes(torch, Kii, Kii_sp.diagonal(), m, self.EIG_TOL, dev, lam_hi=gersh)
+            Psi_adj, adj = None, np.zeros(0, dtype=np.int64)
             if nb:
-                Kib = torch.from_numpy(K[sel][:, self.boundary].toarray()).to(dev)
-                L = torch.linalg.cholesky(Kii)
-                Psi = (-torch.cholesky_solve(Kib, L)).cpu().numpy()
-            blocks.append((sel, Phi, Psi))
+                Kib_sp = K[sel][:, self.boundary].tocsc()
+                adj = np.flatnonzero(np.diff(Kib_sp.indptr) > 0)       # boundary columns touching d
+                if len(adj):
+                    Kib = torch.as_tensor(Kib_sp[:, adj].toarray(), dtype=f64, device=dev)
+                    if Kd is not None:
+                        L = torch.linalg.cholesky(Kd)
+                        Psi_adj = -torch.cholesky_solve(Kib, L)
+                    else:
+                        Psi_adj = _block_cg(torch, Kii, torch.as_tensor(1.0 / Kii_sp.diagonal(), dtype=f64,
+                                                                          device=dev), -Kib, self.PSI_TOL)
+                    # Schur complement contributions and the mode/boundary coupling
+                    KiiPsi = Kii @ Psi_adj
+                    adj_t = torch.as_tensor(adj, device=dev)
+                    Sd = Kib.T @ Psi_adj
+                    Sd = Sd + Sd.T + Psi_adj.T @ KiiPsi
+                    S[adj_t[:, None], adj_t[None, :]] += Sd
+                    cross[c0:c0 + m, adj_t] = Phi.T @ (Kib + KiiPsi)
+            lam_blocks.append(Phi.T @ (Kii @ Phi))
+            Psi_full = None
+            if Psi_adj is not None:
+                Psi_full = _embed_columns(Psi_adj.cpu().numpy(), adj, len(sel), nb)
+            blocks.append((sel, Phi.cpu().numpy(), Psi_full))
+            c0 += m
         self.blocks = blocks
-        n_modes = sum(b[1].shape[1] for b in blocks if b is not None)
-        m_tot = n_modes + nb
-        Td = np.zeros((self.n, m_tot), order="F")
-        c0 = 0
-        for blk in blocks:
-            if blk is None:
-                continue
-            sel, Phi, Psi = blk
-            Td[sel, c0:c0 + Phi.shape[1]] = Phi
-            c0 += Phi.shape[1]
-        Td[self.boundary, c0 + np.arange(nb)] = 1.0
-        for blk in blocks:
-            if blk is not None and blk[2] is not None:
-                Td[blk[0], c0:c0 + nb] = blk[2]
-        self.T_dense = Td
-        self.T = sp.csr_matrix(Td)
-        Tt = torch.from_numpy(np.ascontiguousarray(Td)).to(dev)
-        Ks = torch.sparse_csr_tensor(torch.from_numpy(K.indptr.astype(np.int64)),
-                                     torch.from_numpy(K.indices.astype(np.int64)),
-                                     torch.from_numpy(K.data.astype(np.float64)), size=K.shape).to(dev)
-        Kr = Tt.T @ (Ks @ Tt)
+        m_tot = n_modes_tot + nb
+        Kr = torch.zeros((m_tot, m_tot), dtype=f64, device=dev)
+        r0 = 0
+        for Lb in lam_blocks:
+            k = Lb.shape[0]
+            Kr[r0:r0 + k, r0:r0 + k] = Lb
+            r0 += k
+        Kr[:n_modes_tot, n_modes_tot:] = cross
+        Kr[n_modes_tot:, :n_modes_tot] = cross.T
+        Kr[n_modes_tot:, n_modes_tot:] = S
         Kr = 0.5 * (Kr + Kr.T)
         self.K_red = sp.csc_matrix(Kr.cpu().numpy())
         self.K_red_inv = torch.linalg.inv(Kr).cpu().numpy() if m_tot else np.zeros((0, 0))
+        self._T = None
         self._ctx = None
         self._K = K
+
+    @property
+    def T(self):
+        """The basis as a sparse (n, m_tot) matrix (`pdsolver.py:560-575`), built on first use."""
+        if self._T is None:
+            nb = len(self.boundary)
+            rows, cols, vals = [], [], []
+            c0 = 0
+            for blk in self.blocks:
+                if blk is None:
+                    continue
+                sel, Phi, _ = blk
+                r, c = np.meshgrid(sel, np.arange(Phi.shape[1]), indexing="ij")
+                rows.append(r.reshape(-1)); cols.append(c0 + c.reshape(-1)); vals.append(Phi.reshape(-1))
+                c0 += Phi.shape[1]
+            rows.append(self.boundary); cols.append(c0 + np.arange(nb)); vals.append(np.ones(nb))
+            for blk in self.blocks:
+                if blk is not None and blk[2] is not None:
+                    P = sp.coo_matrix(blk[2])
+                    rows.append(blk[0][P.row]); cols.append(c0 + P.col); vals.append(P.data)
+            self._T = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                                    shape=(self.n, c0 + nb))
+        return self._T
 
     def _context(self):
         if self._ctx is None:
@@ -146,6 +210,83 @@ class CmsSubspace:
         X = self._context().cms_solve(b[:, None] if one else b, np.zeros((0, 1 if one else b.shape[1])),
                                       0, 2, JACOBI_OMEGA, False, 0.0)
         return X[:, 0] if one else X
+
+
+def _to_torch_csr(torch, A, dev):
+    A = sp.csr_matrix(A)
+    return torch.sparse_csr_tensor(torch.from_numpy(A.indptr.astype(np.int64)), torch.from_numpy(A.indices.astype(np.int64)),
+                                   torch.from_numpy(A.data.astype(np.float64)), size=A.shape).to(dev)
+
+
+def _embed_columns(P, adj, n_rows, nb):
+    """Dense (n_rows, len(adj)) block as a sparse (n_rows, nb) CSC matrix on columns `adj`
+    (stored densely per column: no scan for zeros)."""
+    counts = np.zeros(nb, dtype=np.int64)
+    counts[adj] = n_rows
+    indptr = np.concatenate([[0], np.cumsum(counts)])
+    indices = np.tile(np.arange(n_rows, dtype=np.int64), len(adj))
+    return sp.csc_matrix((np.asfortranarray(P).reshape(-1, order="F"), indices, indptr), shape=(n_rows, nb))
+
+
+def _block_cg(torch, A, inv_diag, B, tol, max_iter=2000):
+    """Jacobi-preconditioned CG on SPD sparse A with all columns of B at once (per-column
+    recurrences), to |r_j| <= tol |b_j|."""
+    X = torch.zeros_like(B)
+    R = B.clone()
+    Z = inv_diag[:, None] * R
+    P = Z.clone()
+    rz = (R * Z).sum(0)
+    bn = torch.linalg.norm(B, dim=0)
+    for _ in range(max_iter):
+        Q = A @ P
+        alpha = rz / (P * Q).sum(0).clamp_min(1e-300)
+        X += alpha * P
+        R -= alpha * Q
+        if bool((torch.linalg.norm(R, dim=0) <= tol * bn).all()):
+            break
+        Z = inv_diag[:, None] * R
+        rz_new = (R * Z).sum(0)
+        P = Z + (rz_new / rz.clamp_min(1e-300)) * P
+        rz = rz_new
+    return X
+
+
+def _lowest_modes(torch, A, diag, m, tol, dev, lam_hi=None):
+    """m lowest eigenvectors of the sparse SPD A, orthonormal: Chebyshev-filtered subspace
+    iteration on a block of m + 8 vectors (a degree-24 filter that damps [cut, lam_hi], where cut
+    is the block's largest Ritz value), QR and Rayleigh-Ritz each round, until every wanted
+    Ritz pair has |A x - theta x| <= tol |A|.  The block's spectrum edge is mass-dominated
+    (condition number ~100), so a few rounds suffice."""
+    n = A.shape[0]
+    k = min(n, m)
+    p = min(n, k + 8)
+    if lam_hi is None:
+        lam_hi = float(diag.max()) * 2.0
+    gen = torch.Generator(device="cpu").manual_seed(0)
+    X = torch.randn((n, p), generator=gen, dtype=torch.float64).to(dev)
+    X, _ = torch.linalg.qr(X)
+    H = X.T @ (A @ X)
+    w, U = torch.linalg.eigh(0.5 * (H + H.T))
+    X = X @ U
+    deg = 24
+    for _ in range(60):
+        cut = float(w[-1])
+        e, c = 0.5 * (lam_hi - cut), 0.5 * (lam_hi + cut)
+        # three-term Chebyshev recurrence of the filter on [cut, lam_hi]
+        Y = (A @ X - c * X) / e
+        Xp = X
+        for _ in range(2, deg + 1):
+            Yn = 2.0 * (A @ Y - c * Y) / e - Xp
+            Xp, Y = Y, Yn
+        Q, _ = torch.linalg.qr(Y)
+        AQ = A @ Q
+        H = Q.T @ AQ
+        w, U = torch.linalg.eigh(0.5 * (H + H.T))
+        X = Q @ U
+        R = AQ @ U - X * w[None, :]
+        if bool((torch.linalg.norm(R[:, :k], dim=0) <= tol * lam_hi).all()):
+            break
+    return X[:, :k]
 
 
 def basis_blocks(cms):
@@ -168,10 +309,16 @@ def basis_blocks(cms):
         cols = list(range(c0, c0 + m))
         mats = [np.asarray(Phi, dtype=float)]
         if Psi is not None and nb:
-            Psi = np.asarray(Psi.toarray() if hasattr(Psi, "toarray") else Psi, dtype=float)
-            adj = np.flatnonzero(np.any(Psi != 0.0, axis=0))
+            if sp.issparse(Psi):
+                Pc = sp.csc_matrix(Psi)
+                adj = np.flatnonzero(np.diff(Pc.indptr) > 0)
+                Pa = Pc[:, adj].toarray()
+            else:
+                Psi = np.asarray(Psi, dtype=float)
+                adj = np.flatnonzero(np.any(Psi != 0.0, axis=0))
+                Pa = Psi[:, adj]
             cols += list(n_modes + adj)
-            mats.append(Psi[:, adj])
+            mats.append(Pa)
         c0 += m
         A = np.hstack(mats) if len(mats) > 1 else mats[0]
         parts.append(np.asfortranarray(A).reshape(-1, order="F"))
