@@ -363,8 +363,22 @@ class Context:
         frames = np.empty((steps, self.n, 3)) if out is None else out
         fo = None
         if forces is not None:
-            fo = f64(forces).reshape((steps if forces_per_step else 1), self.n, 3)
-        pp = None if pin_path is None or self.n_pins == 0 else f64(pin_path).reshape(steps, self.n_pins, 3)
+            # the reference indexes forces[i] / pin_path[i] (pdsolver.py:744-752): longer sequences
+            # are fine, shorter ones raise as indexing would
+            fo = f64(forces)
+            if forces_per_step:
+                fo = fo.reshape(-1, self.n, 3)
+                if fo.shape[0] < steps:
+                    raise IndexError(f"forces has {fo.shape[0]} steps, {steps} requested")
+                fo = np.ascontiguousarray(fo[:steps])
+            else:
+                fo = fo.reshape(1, self.n, 3)
+        pp = None
+        if pin_path is not None and self.n_pins:
+            pp = f64(pin_path).reshape(-1, self.n_pins, 3)
+            if pp.shape[0] < steps:
+                raise IndexError(f"pin path has {pp.shape[0]} steps, {steps} requested")
+            pp = np.ascontiguousarray(pp[:steps])
         ff, fi = C.c_int(-1), C.c_int(-1)
         check(self.lib.vkpd_simulate(self.h, int(steps), int(iterations), float(damping), ptr(fo),
                                      1 if forces_per_step else 0, ptr(pp), ptr(frames), C.byref(ff), C.byref(fi)))

@@ -147,11 +147,14 @@ def device_context(mesh, gammas, dt, pins=(), precision="fp32", tol=None, max_it
                            mesh.shape_grad, mesh.volume, mesh.node_mass, gammas.gamma_s,
                            gammas.gamma_v, pins, dt, precision=precision, tol=tol,
                            max_iters=max_iters, device=k[-1], nodes=getattr(mesh, "nodes", None))
-        _CACHE[k] = [gid, ctx]
+        # the entry keeps the gamma arrays it was built from alive, so their ids cannot be reused
+        # by a later MaterialField (which would skip a needed refresh)
+        _CACHE[k] = [gid, ctx, (gammas.gamma_s, gammas.gamma_v)]
         return ctx
     if hit[0] != gid:
         hit[1].set_gammas(gammas.gamma_s, gammas.gamma_v)
         hit[0] = gid
+        hit[2] = (gammas.gamma_s, gammas.gamma_v)
     return hit[1]
 
 
@@ -238,11 +241,12 @@ def hess_context(mesh, gammas, dt=1.0, pins=()):
             raise ValueError("dt must be positive")
         h = _abi.HessContext(m.n_nodes if hasattr(m, "n_nodes") else len(m.nodes), m.tets, m.shape_grad,
                              m.volume, m.node_mass, gammas.gamma_s, gammas.gamma_v, pins, dt, device=k[-1])
-        _HCACHE[k] = [gid, h]
+        _HCACHE[k] = [gid, h, (gammas.gamma_s, gammas.gamma_v)]
         return h
     if hit[0] != gid:
         hit[1].set_gammas(gammas.gamma_s, gammas.gamma_v)
         hit[0] = gid
+        hit[2] = (gammas.gamma_s, gammas.gamma_v)
     return hit[1]
 
 
