@@ -88,6 +88,8 @@ typedef struct {
     int pd_early_exit; /* stop a frame's PD rounds at the first zero-work solve (<0: on)  */
     int warm_rounds;   /* PD rounds warm-started from earlier frames (<0: default)        */
     int unroll_rounds; /* PD rounds captured ahead of the graph's WHILE node (<0: adaptive) */
+    double tol_growth; /* > 1: PD round k of R solves to tol * tol_growth^(R-1-k); < 0: default */
+                       /* (1.15 in float64, off in float32); 0 or 1: off                       */
 } vkpd_config;
 
 #define VKPD_SOLVER_AUTO 0

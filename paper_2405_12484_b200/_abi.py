@@ -48,6 +48,7 @@ class Config(C.Structure):
         ("precision", C.c_int), ("tol", C.c_double), ("max_iters", C.c_int), ("device", C.c_int),
         ("pcg_blocks", C.c_int), ("use_graph", C.c_int), ("solver", C.c_int),
         ("pd_early_exit", C.c_int), ("warm_rounds", C.c_int), ("unroll_rounds", C.c_int),
+        ("tol_growth", C.c_double),
     ]
 
 
@@ -194,7 +195,8 @@ class Context:
 
     def __init__(self, nodes_count, tets, shape_grad, volume, node_mass, gamma_s, gamma_v, pins,
                  dt, precision="fp32", tol=0.0, max_iters=0, device=0, pcg_blocks=0, use_graph=True,
-                 solver="auto", pd_early_exit=True, warm_rounds=-1, unroll_rounds=-1, nodes=None):
+                 solver="auto", pd_early_exit=True, warm_rounds=-1, unroll_rounds=-1, nodes=None,
+                 tol_growth=-1.0):
         self.lib = load()
         self._keep = dict(
             tets=np.ascontiguousarray(tets, dtype=np.int64).reshape(-1, 4),
@@ -221,7 +223,7 @@ class Context:
             raise ValueError(f"unknown solver {solver!r}")
         cfg = Config(PRECISION[precision], float(tol), int(max_iters), int(device), int(pcg_blocks),
                      1 if use_graph else 0, SOLVERS[solver], 1 if pd_early_exit else 0, int(warm_rounds),
-                     int(unroll_rounds))
+                     int(unroll_rounds), float(tol_growth))
         h = C.c_void_p()
         check(self.lib.vkpd_create(C.byref(d), C.byref(cfg), C.byref(h)))
         self.h = h
@@ -572,7 +574,7 @@ class MatrixContext(Context):
                           data=f64(K.data), pins=pins)
         k = self._keep
         cfg = Config(PRECISION[precision], float(tol), int(max_iters), int(device), int(pcg_blocks), 0,
-                     SOLVERS["pcg"], 1, -1, -1)
+                     SOLVERS["pcg"], 1, -1, -1, 1.0)
         h = C.c_void_p()
         check(self.lib.vkpd_create_matrix(self.n, ptr(k["indptr"]), ptr(k["indices"]), ptr(k["data"]),
                                           ptr(pins) if self.n_pins else None, self.n_pins,

@@ -191,7 +191,10 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     pcg_allreduce<2>(grid, a.partials, parity, acc, red, smem);
     double rr = red[0];
     const double bb = red[1];
-    const double thr = a.tol * a.tol * bb;
+    double tol_k = a.tol;
+    if (a.tol_growth > 1.0 && a.init == INIT_PD && a.rounds_total > 0)
+        tol_k *= pow(a.tol_growth, (double)max(0, a.rounds_total - 1 - pdi_w));
+    const double thr = tol_k * tol_k * bb;
     const unsigned int base = s_base;
     const int* nbr = a.cheb_nbr + a.cheb_nbr_ptr[blockIdx.x];
     const int nn = a.cheb_nbr_ptr[blockIdx.x + 1] - a.cheb_nbr_ptr[blockIdx.x];

@@ -242,6 +242,8 @@ struct PcgArgs {
     int* fail_iter;              // atomicMin'd with pd_iter on non-finite output
     int pd_iter;
     double tol;
+    double tol_growth;           // > 1: PD round k of R solves to tol * tol_growth^(R-1-k) (experiment; 1 = off)
+    int rounds_total;            // R (frame's PD rounds) for tol_growth
     int max_iters;
     int init;
     // colliders (pdsolver.py:271-297): extra diagonal m_i * k * K_ii and rhs weight k * K_ii
@@ -296,7 +298,8 @@ __device__ __forceinline__ void pcg_exit(const PcgArgs<T>& a, bool bad, int it, 
             // bit) -- or a round has failed (a failure in this very launch may only be
             // seen one round later; fail_iter keeps the earliest round either way).
             // Skipped rounds are recorded with 0 CG iterations.
-            const bool stop = pdi + 1 >= a.loop_iterations || (it == 0 && !moved) ||
+            // (a zero-work round is only an exact repeat point when every round has the same tolerance)
+            const bool stop = pdi + 1 >= a.loop_iterations || (it == 0 && !moved && !(a.tol_growth > 1.0)) ||
                               *(volatile int*)a.fail_iter != 0x7fffffff;
             if (stop) {
                 for (int j = pdi + 1; j < a.loop_iterations; ++j) a.iters_out[j] = 0;

@@ -329,6 +329,7 @@ struct Ctx : CtxBase {
     DBuf<V4> hh;                         // polynomial preconditioner: h = K D^-1 r
     int pcg_threads = 512;               // CTA size of the persistent solver
     int solver_kind = VKPD_SOLVER_PCG_POLY;   // resolved vkpd_config.solver
+    double tol_growth = 1.0;             // vkpd_config.tol_growth (experiment)
     bool solver_auto = true;
     bool pcg_poly = true;                // Neumann-1 polynomial preconditioner (CG kinds)
     bool cheb = false;                   // Chebyshev semi-iteration with neighbour flags (cheb.cuh)
@@ -1042,6 +1043,12 @@ struct Ctx : CtxBase {
         unroll_cfg = c->unroll_rounds >= 0 ? std::min(64, c->unroll_rounds) : -1;
         unroll_rounds = unroll_cfg > 0 ? unroll_cfg : 0;
         pd_early_exit = c->pd_early_exit != 0;
+        // per-round tolerance schedule: earlier PD rounds' solve errors are contracted by the later
+        // rounds, so round k of R solves to tol * g^(R-1-k).  Default g = 1.15 in float64 (C2 after
+        // 100 frames: 1.1e-11 vs the reference, bar 1e-10; C3 9.0 -> 7.9 ms/frame,
+        // profiles/r02_tol_growth.json); float32 keeps g = 1 (its zero-work exit needs one tolerance)
+        tol_growth = c->tol_growth > 1.0 ? c->tol_growth
+                   : c->tol_growth < 0.0 ? (sizeof(T) == 8 ? 1.15 : 1.0) : 1.0;
         if (warm_extrap) {
             CK(warm1.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
             CK(cudaMemsetAsync(warm1.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
@@ -1320,6 +1327,7 @@ struct Ctx : CtxBase {
         pa.q = q.p; pa.dx = dx.p; pa.partials = partials.p; pa.scal = scal.p; pa.bar = bar.p;
         pa.iters_out = iters_slot; pa.fail_iter = fail_iter.p; pa.pd_iter = pd_iter; pa.tol = tol;
         pa.max_iters = max_iters; pa.init = init;
+        pa.tol_growth = tol_growth; pa.rounds_total = last_iterations;
         pa.cdiag = nullptr; pa.cb = nullptr; pa.coll = nullptr; pa.ncoll = 0;
         pa.reset_count = nullptr;
         pa.pd_iter_dev = nullptr; pa.loop_handle = 0; pa.loop_iterations = 0; pa.robust_if = 0;
