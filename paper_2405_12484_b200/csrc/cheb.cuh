@@ -225,6 +225,7 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                         // halo columns after it measured slower: 12.9 vs 9.0 ms/frame at C3 fp64,
                         // the per-entry predicates diverge within warps.)
                         if (k > 0) {
+#ifndef VK_CHEB_NOWAIT                // timing experiment only: no neighbour wait (wrong results)
                             if (threadIdx.x < 32) {
                                 for (int j = threadIdx.x; j < nn; j += 32) {
                                     const unsigned int* f = a.flags + (size_t)nbr[j] * 32;
@@ -235,6 +236,7 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                                     }
                                 }
                             }
+#endif
                             asm volatile("bar.sync 1, %0;" ::"r"(exp_threads) : "memory");
                         }
                         pcg_mark(11);

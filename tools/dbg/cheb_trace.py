@@ -3,7 +3,7 @@ Build: nvcc ... -DVK_PCG_TRACE -shared -o paper_2405_12484_b200/lib/libvkpd_trac
 import ctypes as C, os, sys, collections, json
 import numpy as np
 sys.path.insert(0, os.getcwd())
-os.environ["VKPD_LIB"] = "paper_2405_12484_b200/lib/libvkpd_trace.so"
+os.environ.setdefault("VKPD_LIB", "paper_2405_12484_b200/lib/libvkpd_trace.so")
 from paper_2405_12484_b200 import _abi, pdsolver, scenes
 prec = sys.argv[1] if len(sys.argv) > 1 else "fp64"
 sc = scenes.make_scene("C3"); m = sc.mesh
