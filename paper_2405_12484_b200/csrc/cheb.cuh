@@ -339,8 +339,16 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                 vec4_t<T>* wp = a.warm_prev + (size_t)pdi_w * nF;
                 const vec4_t<T> dp = ld4(&wp[j]);
                 wp[j] = d;
-                const T be = (T)a.warm_beta;
-                wb[j] = make4<T>(d.x + be * (d.x - dp.x), d.y + be * (d.y - dp.y), d.z + be * (d.z - dp.z), T(0));
+                if (a.warm_prev2 != nullptr) {          // quadratic: 3 d - 3 d' + d''
+                    vec4_t<T>* wq = a.warm_prev2 + (size_t)pdi_w * nF;
+                    const vec4_t<T> dq = ld4(&wq[j]);
+                    wq[j] = dp;
+                    wb[j] = make4<T>(T(3) * (d.x - dp.x) + dq.x, T(3) * (d.y - dp.y) + dq.y,
+                                     T(3) * (d.z - dp.z) + dq.z, T(0));
+                } else {
+                    const T be = (T)a.warm_beta;
+                    wb[j] = make4<T>(d.x + be * (d.x - dp.x), d.y + be * (d.y - dp.y), d.z + be * (d.z - dp.z), T(0));
+                }
             } else {
                 wb[j] = d;
             }

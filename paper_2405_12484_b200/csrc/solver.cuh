@@ -268,6 +268,7 @@ struct PcgArgs {
     vec4_t<T>* warm_prev;        // optional: the correction before it; the guess is then the linear
                                  // extrapolation d_prev + beta (d_prev - d_prevprev)
     double warm_beta;
+    vec4_t<T>* warm_prev2;       // optional (cheb.cuh): the frame before that; quadratic extrapolation
     int warm_extrap_rounds;      // rounds < this extrapolate; later warm rounds reuse the last correction
     // Chebyshev solver (cheb.cuh)
     unsigned int* flags;         // per-CTA step counters, 128-B stride

@@ -316,6 +316,8 @@ struct Ctx : CtxBase {
     DBuf<T> ell_kd;                      // K_ff D^-1 (polynomial preconditioner)
     DBuf<V4> warm0;                      // per-round corrections of the previous frame (solver warm start)
     DBuf<V4> warm1;                      // the frame before: the guess is the linear extrapolation
+    DBuf<V4> warm2;                      // the frame before that (warm_order 2): quadratic extrapolation
+    int warm_order = sizeof(T) == 8 ? 2 : 1;   // fp64 C3: 8.03 -> 7.69 ms/frame steady; fp32 unchanged
     bool warm_extrap = true;             // d + beta (d - d_before), beta = 1
     double warm_beta = 1.0;
     int warm_extrap_rounds = sizeof(T) == 8 ? 32 : 1;   // fp32 extrapolates round 0 only (later rounds'
@@ -820,6 +822,89 @@ struct Ctx : CtxBase {
     DBuf<int> cheb_slot, cheb_halo_ptr, cheb_halo;
     DBuf<T> cheb_val, cheb_kdiag;
     DBuf<int> cheb_nexp, cheb_nbr_hend;
+    // Entry positions of one half-warp's rows (<= 16 lanes) without shared-memory bank
+    // conflicts.  k_cheb_reg's SpMV loads d[slot[o]] for o = 0..13 at once across a warp; a
+    // 64-bit load is served per half-warp and costs as many wavefronts as the most distinct
+    // slots that share a bank pair (slot mod 16).  The rows' entries form a bipartite multigraph
+    // lanes x bank pairs; an edge colouring with D = max(14, max degree) colours (Konig:
+    // alternating-path recolouring) puts distinct bank pairs at each position.  Colours >= 14
+    // (an overloaded bank pair) fold into a lane's free position where they add the least; pad
+    // positions (value 0) read a slot another lane already reads there (broadcast).  C3 fp64:
+    // 3.6 -> 2.1 wavefronts per gather (tools/dbg/bank_model.py).
+    static void conflict_free_positions(int lanes, const int* ent_n, const int (*ent_slot)[vk::kChebOff],
+                                        const int* own_slot, int (*pos_of)[vk::kChebOff],
+                                        int (*pad_slot)[vk::kChebOff]) {
+        constexpr int K = vk::kChebOff;
+        int deg[16] = {0};
+        int ne = 0;
+        for (int u = 0; u < lanes; ++u)
+            for (int t = 0; t < ent_n[u]; ++t) { ++deg[ent_slot[u][t] & 15]; ++ne; }
+        int D = K;
+        for (int b = 0; b < 16; ++b) D = std::max(D, deg[b]);
+        std::vector<int> eu(ne), ev(ne), et(ne), ec(ne, -1);
+        std::vector<int> U((size_t)16 * D, -1), V((size_t)16 * D, -1);
+        int id = 0;
+        for (int u = 0; u < lanes; ++u)
+            for (int t = 0; t < ent_n[u]; ++t) { eu[id] = u; ev[id] = ent_slot[u][t] & 15; et[id] = t; ++id; }
+        std::vector<int> path;
+        for (int e = 0; e < ne; ++e) {
+            const int u = eu[e], v = ev[e];
+            int a = 0, b = 0;
+            while (U[(size_t)u * D + a] >= 0) ++a;
+            while (V[(size_t)v * D + b] >= 0) ++b;
+            if (V[(size_t)v * D + a] >= 0) {
+                // flip the a/b alternating path that starts at v with colour a
+                path.clear();
+                bool at_v = true;
+                int node = v, col = a;
+                for (;;) {
+                    const int f = at_v ? V[(size_t)node * D + col] : U[(size_t)node * D + col];
+                    if (f < 0) break;
+                    path.push_back(f);
+                    node = at_v ? eu[f] : ev[f];
+                    at_v = !at_v;
+                    col = col == a ? b : a;
+                }
+                for (int f : path) { U[(size_t)eu[f] * D + ec[f]] = -1; V[(size_t)ev[f] * D + ec[f]] = -1; }
+                for (int f : path) {
+                    ec[f] = ec[f] == a ? b : a;
+                    U[(size_t)eu[f] * D + ec[f]] = f; V[(size_t)ev[f] * D + ec[f]] = f;
+                }
+            }
+            ec[e] = a; U[(size_t)u * D + a] = e; V[(size_t)v * D + a] = e;
+        }
+        // positions: colour c < K is position c; later colours fold into free positions
+        std::vector<std::vector<int>> at((size_t)K * 16);      // (position, bank pair) -> slots
+        for (int u = 0; u < lanes; ++u) for (int o = 0; o < K; ++o) pos_of[u][o] = -1;
+        auto add = [&](int o, int sl) {
+            auto& L = at[(size_t)o * 16 + (sl & 15)];
+            if (std::find(L.begin(), L.end(), sl) == L.end()) L.push_back(sl);
+        };
+        for (int e = 0; e < ne; ++e)
+            if (ec[e] < K) { pos_of[eu[e]][ec[e]] = et[e]; add(ec[e], ent_slot[eu[e]][et[e]]); }
+        for (int e = 0; e < ne; ++e) {
+            if (ec[e] < K) continue;
+            const int u = eu[e], sl = ent_slot[u][et[e]];
+            int best = -1;
+            size_t bc = 0;
+            for (int o = 0; o < K; ++o) {
+                if (pos_of[u][o] >= 0) continue;
+                const auto& L = at[(size_t)o * 16 + (sl & 15)];
+                const size_t c = std::find(L.begin(), L.end(), sl) != L.end() ? 0 : L.size();
+                if (best < 0 || c < bc) { best = o; bc = c; }
+            }
+            pos_of[u][best] = et[e];
+            add(best, sl);
+        }
+        for (int u = 0; u < lanes; ++u)
+            for (int o = 0; o < K; ++o) {
+                pad_slot[u][o] = own_slot[u];
+                if (pos_of[u][o] >= 0) continue;
+                for (int b = 0; b < 16; ++b)
+                    if (!at[(size_t)o * 16 + b].empty()) { pad_slot[u][o] = at[(size_t)o * 16 + b][0]; break; }
+                if (at[(size_t)o * 16 + (pad_slot[u][o] & 15)].empty()) add(o, pad_slot[u][o]);
+            }
+    }
     int build_cheb_neighbours() {
         const int chunk = cdiv(std::max(1, nF), pcg_blocks);
         std::vector<int> ecol((size_t)ell_w * nF);
@@ -903,6 +988,31 @@ struct Ctx : CtxBase {
                     else if (c >= r0 && c < r1) oslot[(size_t)o * nF + i] = c - r0;
                     else oslot[(size_t)o * nF + i] = pcg_threads + hslot[c];
                 }
+            if (fits)
+                for (int h0 = r0; h0 < r1; h0 += 16) {
+                    const int lanes = std::min(16, r1 - h0);
+                    int en[16], es[16][vk::kChebOff], own_s[16], pos[16][vk::kChebOff], pad[16][vk::kChebOff];
+                    T ev[16][vk::kChebOff];
+                    for (int u = 0; u < lanes; ++u) {
+                        const int i = h0 + u;
+                        own_s[u] = i - r0;
+                        en[u] = 0;
+                        for (int o = 0; o < vk::kChebOff; ++o)
+                            if (ocol[(size_t)o * nF + i] >= 0) {
+                                es[u][en[u]] = oslot[(size_t)o * nF + i];
+                                ev[u][en[u]] = oval[(size_t)o * nF + i];
+                                ++en[u];
+                            }
+                    }
+                    conflict_free_positions(lanes, en, es, own_s, pos, pad);
+                    for (int u = 0; u < lanes; ++u)
+                        for (int o = 0; o < vk::kChebOff; ++o) {
+                            const size_t x = (size_t)o * nF + h0 + u;
+                            const int t = pos[u][o];
+                            oslot[x] = t >= 0 ? es[u][t] : pad[u][o];
+                            oval[x] = t >= 0 ? ev[u][t] : T(0);
+                        }
+                }
             for (int j = h0; j < (int)hl.size(); ++j) hslot[hl[j]] = -1;
             for (int q = n0; q < (int)lst.size(); ++q) nbr_pos[lst[q]] = -1;
             ptr[b + 1] = (int)lst.size();
@@ -967,6 +1077,7 @@ struct Ctx : CtxBase {
         if (int rc = refresh_precond()) return rc;
         if (warm0.p) CK(cudaMemsetAsync(warm0.p, 0, warm0.n * sizeof(V4), stream));
         if (warm1.p) CK(cudaMemsetAsync(warm1.p, 0, warm1.n * sizeof(V4), stream));
+        if (warm2.p) CK(cudaMemsetAsync(warm2.p, 0, warm2.n * sizeof(V4), stream));
         if (graph_exec) { cudaGraphExecDestroy(graph_exec); graph_exec = nullptr; }
         CK(cudaStreamSynchronize(stream));
         return VKPD_OK;
@@ -1052,6 +1163,10 @@ struct Ctx : CtxBase {
         if (warm_extrap) {
             CK(warm1.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
             CK(cudaMemsetAsync(warm1.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
+            if (warm_order == 2) {
+                CK(warm2.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
+                CK(cudaMemsetAsync(warm2.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
+            }
         }
         CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), s));
         CK(pstats.alloc(1));
@@ -1221,7 +1336,7 @@ struct Ctx : CtxBase {
         }
         k_state_in<T><<<cdiv(n, 256), 256, 0, stream>>>(n, pv, int_of_orig.p, v.p, state_changed.p);
         CK(cudaGetLastError());
-        for (DBuf<V4>* b : {&warm0, &warm1})
+        for (DBuf<V4>* b : {&warm0, &warm1, &warm2})
             if (b->p) k_zero_if<T><<<2 * n_sms, 256, 0, stream>>>(b->n, b->p, state_changed.p);
         CK(cudaGetLastError());
         if (!dev) CK(cudaStreamSynchronize(stream));
@@ -1337,6 +1452,7 @@ struct Ctx : CtxBase {
         pa.warm_rounds = warm_rounds;
         pa.warm_prev = (pa.warm != nullptr && warm_extrap) ? warm1.p : nullptr;
         pa.warm_beta = warm_beta;
+        pa.warm_prev2 = (pa.warm_prev != nullptr && cheb) ? warm2.p : nullptr;
         pa.warm_extrap_rounds = warm_extrap_rounds;
         pa.poly_rounds = 0;
         pa.flags = cheb_flags.p; pa.cheb_nbr_ptr = cheb_nbr_ptr.p; pa.cheb_nbr = cheb_nbr.p;
