@@ -76,6 +76,59 @@ __device__ __forceinline__ void ldcg3(const double4* p, double& x, double& y, do
     z = __ldcg(reinterpret_cast<const double*>(p) + 2);
 }
 
+// Exported rows cross CTAs in a flag-in-data format (the LL idea of NCCL's low-latency protocol):
+// every 8-byte word carries 4 bytes of d and the 4-byte step tag, written and read as 16-byte
+// vectors with relaxed gpu-scope accesses.  An aligned 8-byte word is single-copy atomic, so a
+// consumer that sees the tag in every word of a row has that row's d of that step: no separate
+// flag, no release barrier after the stores, no acquire round trip before the loads.  Row
+// layout: fp64 3 x {lo, tag, hi, tag}; fp32 {x, tag, y, tag}, {z, tag, 0, tag}.
+template <typename T> struct LLRow;
+template <> struct LLRow<double> { static constexpr int W = 3; };
+template <> struct LLRow<float> { static constexpr int W = 2; };
+
+__device__ __forceinline__ void ll_st(uint4* p, unsigned a, unsigned b, unsigned c, unsigned d) {
+    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ll_ld(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void ll_store(uint4* p, double x, double y, double z, unsigned tag) {
+    const unsigned long long a = __double_as_longlong(x), b = __double_as_longlong(y), c = __double_as_longlong(z);
+    ll_st(p, (unsigned)a, tag, (unsigned)(a >> 32), tag);
+    ll_st(p + 1, (unsigned)b, tag, (unsigned)(b >> 32), tag);
+    ll_st(p + 2, (unsigned)c, tag, (unsigned)(c >> 32), tag);
+}
+__device__ __forceinline__ void ll_store(uint4* p, float x, float y, float z, unsigned tag) {
+    ll_st(p, __float_as_uint(x), tag, __float_as_uint(y), tag);
+    ll_st(p + 1, __float_as_uint(z), tag, 0u, tag);
+}
+__device__ __forceinline__ bool ll_ok(const uint4& v, unsigned tag) { return v.y == tag && v.w == tag; }
+// spin until the row carries `tag` (traps after ~2^33 polls: a lost producer)
+__device__ __forceinline__ void ll_load(const uint4* p, unsigned tag, double& x, double& y, double& z) {
+    uint4 a = ll_ld(p), b = ll_ld(p + 1), c = ll_ld(p + 2);
+    unsigned long long spins = 0;
+    while (!(ll_ok(a, tag) && ll_ok(b, tag) && ll_ok(c, tag))) {
+        if (++spins > (1ull << 33)) __trap();
+        a = ll_ld(p); b = ll_ld(p + 1); c = ll_ld(p + 2);
+    }
+    x = __longlong_as_double(((unsigned long long)a.z << 32) | a.x);
+    y = __longlong_as_double(((unsigned long long)b.z << 32) | b.x);
+    z = __longlong_as_double(((unsigned long long)c.z << 32) | c.x);
+}
+__device__ __forceinline__ void ll_load(const uint4* p, unsigned tag, float& x, float& y, float& z) {
+    uint4 a = ll_ld(p), b = ll_ld(p + 1);
+    unsigned long long spins = 0;
+    while (!(ll_ok(a, tag) && ll_ok(b, tag))) {
+        if (++spins > (1ull << 33)) __trap();
+        a = ll_ld(p); b = ll_ld(p + 1);
+    }
+    x = __uint_as_float(a.x); y = __uint_as_float(a.z); z = __uint_as_float(b.x);
+}
+
 // Register path: a row keeps its kChebOff off-diagonal ELL values and their shared-memory
 // slots in registers (plus the diagonal), so the SpMV's shared-memory traffic is only the
 // neighbours' d.  Shared-memory image (compile-time strides, so every access is one address
@@ -109,6 +162,7 @@ __device__ __forceinline__ int cheb_steps_for(double ratio, double acosh_sigma) 
 template <typename T, bool REG>
 __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& grid, double* smem, double* red) {
     pcg_entry(a);
+    pcg_mark(15);
     const int nF = a.nF;
     const int chunk = (nF + gridDim.x - 1) / gridDim.x;
     const int row0 = blockIdx.x * chunk;
@@ -124,6 +178,9 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
     const double sigma = theta / delta;
     const double acosh_sigma = acosh(sigma);
+    double tol_k = a.tol;
+    if (a.tol_growth > 1.0 && a.init == INIT_PD && a.rounds_total > 0)
+        tol_k *= pow(a.tol_growth, (double)max(0, a.rounds_total - 1 - pdi_w));
 
     // ---- init: res = b - K x (PD residual form) minus K * warm guess; y = guess; d0 = D^-1 res / theta
     const int i = row0 + threadIdx.x;              // REG path: this thread's row
@@ -138,9 +195,10 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     // exported rows [row0, row0 + nexp) belong to the leading warps (at least warp 0, which
     // publishes the step flag)
     const int nexp = REG ? a.cheb_nexp[blockIdx.x] : 0;
-    const int exp_threads = max(32, (nexp + 31) & ~31);
-    const bool exp_warp = (int)threadIdx.x < exp_threads;
+    // the exported-warp group also covers the halo rows: one halo row per thread, one L2 round trip
     const int nh = REG ? a.cheb_halo_ptr[blockIdx.x + 1] - a.cheb_halo_ptr[blockIdx.x] : 0;
+    const int exp_threads = min((int)blockDim.x, max(32, (max(nexp, nh) + 31) & ~31));
+    const bool exp_warp = (int)threadIdx.x < exp_threads;
     if (REG) {
         const int* halo = a.cheb_halo + a.cheb_halo_ptr[blockIdx.x];
         for (int j = threadIdx.x; j < nh; j += blockDim.x) hidx[j] = __ldg(&halo[j]);
@@ -148,6 +206,9 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     T rx = 0, ry = 0, rzz = 0, dxv = 0, dyv = 0, dzv = 0, dg = 0;
     double acc[2] = {0, 0};                        // rr, bb
     if (REG) {
+        // residual first (the corner gather's loads), then the row's ELL into registers
+        if (own) init_residual_row(a, i, false, rx, ry, rzz, acc[1]);
+        pcg_mark(16);
         if (own) {
 #pragma unroll
             for (int s = 0; s < kChebOff; ++s) {
@@ -155,19 +216,46 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                 vals[s] = __ldg(&a.cheb_val[(size_t)s * nF + i]);
             }
             kdiag = __ldg(&a.cheb_kdiag[i]);
-            init_residual_row(a, i, false, rx, ry, rzz, acc[1]);
+            dg = a.inv_diag[i];
+        }
+        if (warm) {
+            // K * guess from shared memory like a step: own rows' guesses and the halo rows'
+            // (written by the previous frame's launch: plain loads) into buffer 1's planes
+            T* const sg = sd + 3 * kChebSlots;
             T gx = 0, gy = 0, gz = 0;
-            if (warm) {
+            __syncthreads();                       // hidx
+            if (own) {
                 const vec4_t<T> g = ld4(&wb[i]);
                 gx = g.x; gy = g.y; gz = g.z;
-                const vec4_t<T> kw = k_row(a, wb, i);
-                rx -= kw.x; ry -= kw.y; rzz -= kw.z;
+                sg[threadIdx.x] = gx; sg[kChebSlots + threadIdx.x] = gy; sg[2 * kChebSlots + threadIdx.x] = gz;
+            }
+            for (int j = threadIdx.x; j < nh; j += blockDim.x) {
+                const vec4_t<T> g = ld4(&wb[hidx[j]]);
+                const int sl = blockDim.x + j;
+                sg[sl] = g.x; sg[kChebSlots + sl] = g.y; sg[2 * kChebSlots + sl] = g.z;
+            }
+            __syncthreads();
+            if (own) {
+                T qx = kdiag * gx, qy = kdiag * gy, qz = kdiag * gz;
+#pragma unroll
+                for (int s = 0; s < kChebOff; ++s) {
+                    const T* d = sg + cols[s];
+                    qx += vals[s] * d[0]; qy += vals[s] * d[kChebSlots]; qz += vals[s] * d[2 * kChebSlots];
+                }
+                if (a.cdiag != nullptr) {
+                    const T cd = a.cdiag[i];
+                    qx += cd * gx; qy += cd * gy; qz += cd * gz;
+                }
+                rx -= qx; ry -= qy; rzz -= qz;
             }
             yv[0] = gx; yv[kChebMaxThreads] = gy; yv[2 * kChebMaxThreads] = gz;
-            dg = a.inv_diag[i];
+        } else {
+            yv[0] = T(0); yv[kChebMaxThreads] = T(0); yv[2 * kChebMaxThreads] = T(0);
+        }
+        pcg_mark(17);
+        if (own) {
             const T c0 = (T)(1.0 / theta) * dg;
             dxv = c0 * rx; dyv = c0 * ry; dzv = c0 * rzz;
-            st4(&a.p0[i], make4<T>(dxv, dyv, dzv, T(0)));
             sd[threadIdx.x] = dxv; sd[kChebSlots + threadIdx.x] = dyv; sd[2 * kChebSlots + threadIdx.x] = dzv;
             acc[0] = (double)rx * rx + (double)ry * ry + (double)rzz * rzz;
         }
@@ -191,9 +279,6 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     pcg_allreduce<2>(grid, a.partials, parity, acc, red, smem);
     double rr = red[0];
     const double bb = red[1];
-    double tol_k = a.tol;
-    if (a.tol_growth > 1.0 && a.init == INIT_PD && a.rounds_total > 0)
-        tol_k *= pow(a.tol_growth, (double)max(0, a.rounds_total - 1 - pdi_w));
     const double thr = tol_k * tol_k * bb;
     const unsigned int base = s_base;
     const int* nbr = a.cheb_nbr + a.cheb_nbr_ptr[blockIdx.x];
@@ -202,8 +287,10 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     int k = 0;
     double rho = 1.0 / sigma;
     const double two_over_delta = 2.0 / delta;
+    constexpr int LLW = LLRow<T>::W;
     if (rr > thr && a.max_iters > 0) {
         int target = min(a.max_iters, cheb_steps_for(sqrt(rr / thr), acosh_sigma));
+        if (REG && own && (int)threadIdx.x < nexp) ll_store(a.cheb_ll + (size_t)i * LLW, dxv, dyv, dzv, base);
         for (;;) {
             for (; k < target; ++k) {
                 pcg_mark(10);
@@ -219,30 +306,15 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                     // every own row's d_k is in shared memory (written by step k-1)
                     if (k > 0) __syncthreads();
                     if (exp_warp) {
-                        // exported warps: neighbours' step flags (warp 0), their rows of d_k into the
-                        // halo slots, the exported rows, then publish this CTA's step flag.  (Doing
-                        // the own-column part of the exported rows before the wait and only the
-                        // halo columns after it measured slower: 12.9 vs 9.0 ms/frame at C3 fp64,
-                        // the per-entry predicates diverge within warps.)
-                        if (k > 0) {
-#ifndef VK_CHEB_NOWAIT                // timing experiment only: no neighbour wait (wrong results)
-                            if (threadIdx.x < 32) {
-                                for (int j = threadIdx.x; j < nn; j += 32) {
-                                    const unsigned int* f = a.flags + (size_t)nbr[j] * 32;
-                                    const unsigned int target = base + (unsigned)k;
-                                    unsigned long long spins = 0;
-                                    while ((int)(ld_acquire_gpu(f) - target) < 0) {
-                                        if (++spins > (1ull << 33)) __trap();
-                                    }
-                                }
-                            }
-#endif
-                            asm volatile("bar.sync 1, %0;" ::"r"(exp_threads) : "memory");
-                        }
+                        // exported warps: the halo rows of d_k (flag-in-data, each row spins on its
+                        // own tag), then the exported rows.  (Doing the own-column part of the
+                        // exported rows before the halo and only the halo columns after it measured
+                        // slower: 12.9 vs 9.0 ms/frame at C3 fp64, per-entry predicates diverge.)
                         pcg_mark(11);
+                        const uint4* src = a.cheb_ll + (size_t)(k & 1) * nF * LLW;
                         for (int j = threadIdx.x; j < nh; j += exp_threads) {
                             T hx, hy, hz;
-                            ldcg3(&dcur[hidx[j]], hx, hy, hz);
+                            ll_load(src + (size_t)hidx[j] * LLW, base + (unsigned)k, hx, hy, hz);
                             const int sl = blockDim.x + j;
                             sx[sl] = hx; sx[kChebSlots + sl] = hy; sx[2 * kChebSlots + sl] = hz;
                         }
@@ -277,14 +349,11 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                         dyv = c1 * dyv + e * ry;
                         dzv = c1 * dzv + e * rzz;
                         sn[threadIdx.x] = dxv; sn[kChebSlots + threadIdx.x] = dyv; sn[2 * kChebSlots + threadIdx.x] = dzv;
-                        if ((int)threadIdx.x < nexp) st4(&dnext[i], make4<T>(dxv, dyv, dzv, T(0)));
+                        if ((int)threadIdx.x < nexp)
+                            ll_store(a.cheb_ll + (size_t)((k + 1) & 1) * nF * LLW + (size_t)i * LLW, dxv, dyv, dzv,
+                                     base + (unsigned)(k + 1));
                     }
                     pcg_mark(13);
-                    if (exp_warp) {
-                        asm volatile("bar.sync 1, %0;" ::"r"(exp_threads) : "memory");
-                        if (threadIdx.x == 0) st_release_gpu(a.flags + (size_t)blockIdx.x * 32, base + (unsigned)(k + 1));
-                    }
-                    pcg_mark(14);
                 } else {
                     for (int j = row0 + threadIdx.x; j < row1; j += blockDim.x) {
                         T qx = 0, qy = 0, qz = 0;
@@ -328,6 +397,8 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
             target = min(a.max_iters, k + 1 + cheb_steps_for(sqrt(rr / thr), acosh_sigma));
         }
     }
+    // REG: the next launch's tags start above every tag this one wrote
+    if (REG && threadIdx.x == 0) a.flags[(size_t)blockIdx.x * 32] = base + (unsigned)k + 1u;
     // ---- finish: x += y (PD mode), warm-start bank, finite check
     bool bad = a.init == INIT_PD && !(rr == rr && rr < INFINITY);
     auto finish_row = [&](int j, vec4_t<T> d) {
@@ -362,7 +433,9 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
             for (int j = row0 + threadIdx.x; j < row1; j += blockDim.x) finish_row(j, a.dx[j]);
         }
     }
+    pcg_mark(19);
     pcg_exit(a, bad, k, warm);
+    pcg_mark(20);
 }
 
 #ifndef VK_CHEB_THREADS

@@ -283,6 +283,7 @@ struct PcgArgs {
     const int* cheb_nbr_hend;    // per (CTA, neighbour): end of that neighbour's rows in the CTA's halo
     const int* cheb_halo;
     int cheb_halo_max;
+    uint4* cheb_ll;              // REG: exported rows of d, flag-in-data, two step-parity buffers of nF rows
 };
 
 template <typename T>

@@ -340,6 +340,7 @@ struct Ctx : CtxBase {
     double gersh = 2.0;                  // Gershgorin bound of D^-1 K_ff
     double lam_min = 0.0, lam_min_bound = 0.0;   // Lanczos estimate / rigorous bound of lambda_min(D^-1 K_ff)
     DBuf<unsigned int> cheb_flags;
+    DBuf<uint4> cheb_ll;
     DBuf<int> cheb_nbr_ptr, cheb_nbr;
     DBuf<double> partials, scal, stage;
     DBuf<vk::GridBar> bar;
@@ -1057,6 +1058,9 @@ struct Ctx : CtxBase {
         CK(cheb_kdiag.alloc(kd.size())); CK(cheb_kdiag.upload(kd.data(), kd.size(), stream));
         CK(cheb_flags.alloc((size_t)32 * pcg_blocks));
         CK(cudaMemsetAsync(cheb_flags.p, 0, sizeof(unsigned int) * 32 * pcg_blocks, stream));
+        // tags restart with the flags: no stale row may carry a tag the next launches wait for
+        CK(cheb_ll.alloc((size_t)2 * vk::LLRow<T>::W * std::max(1, nF)));
+        CK(cudaMemsetAsync(cheb_ll.p, 0xff, cheb_ll.n * sizeof(uint4), stream));
         CK(cudaStreamSynchronize(stream));
         return VKPD_OK;
     }
@@ -1456,6 +1460,7 @@ struct Ctx : CtxBase {
         pa.warm_extrap_rounds = warm_extrap_rounds;
         pa.poly_rounds = 0;
         pa.flags = cheb_flags.p; pa.cheb_nbr_ptr = cheb_nbr_ptr.p; pa.cheb_nbr = cheb_nbr.p;
+        pa.cheb_ll = cheb_ll.p;
         pa.cheb_lmin = lam_min; pa.cheb_lmax = gersh;
         pa.cheb_slot = cheb_slot.p; pa.cheb_val = cheb_val.p; pa.cheb_kdiag = cheb_kdiag.p;
         pa.cheb_nexp = cheb_nexp.p; pa.cheb_nbr_hend = cheb_nbr_hend.p;
