@@ -144,9 +144,22 @@ __device__ __forceinline__ void ll_load(const uint4* p, unsigned tag, float& x, 
 constexpr int kChebMaxThreads = 768;
 constexpr int kChebSlots = 2048;
 constexpr int kChebOff = 14;       // voxel enclosures: <= 15 entries per row, one of them diagonal
+// Type of the shared-memory / cross-CTA image of the direction d.  float64 solves apply the
+// float32-rounded direction: y += fl(d) and r -= K fl(d) (K, r, y in float64), so y and r stay
+// consistent (r is the residual of y to float64 rounding) and the stopping test is unchanged;
+// only the Chebyshev direction carries a 6e-8 relative perturbation, which the recurrence damps
+// like any other.  Halves the SpMV's shared-memory wavefronts and the halo bytes.
+#ifndef VK_CHEB_D32
+#define VK_CHEB_D32 1
+#endif
+template <typename T> struct ChebImage { using type = T; };
+#if VK_CHEB_D32
+template <> struct ChebImage<double> { using type = float; };
+#endif
 template <typename T>
 constexpr size_t cheb_smem_bytes() {
-    return sizeof(T) * (6 * (size_t)kChebSlots + 3 * (size_t)kChebMaxThreads) + sizeof(int) * kChebSlots;
+    return sizeof(typename ChebImage<T>::type) * 6 * (size_t)kChebSlots + sizeof(T) * 3 * (size_t)kChebMaxThreads +
+           sizeof(int) * kChebSlots;
 }
 
 // Steps needed for a residual reduction by `ratio` at Chebyshev parameter sigma
@@ -189,9 +202,11 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     T vals[kChebOff];                              //      and their values
     T kdiag = 0;
     extern __shared__ __align__(16) unsigned char cheb_smem[];
-    T* const sd = reinterpret_cast<T*>(cheb_smem);   // REG: d planes, buffer p at sd + 3 p kChebSlots
-    T* yv = sd + 6 * kChebSlots + threadIdx.x;     // REG: this row's y, planes kChebMaxThreads apart
-    int* hidx = reinterpret_cast<int*>(sd + 6 * kChebSlots + 3 * kChebMaxThreads);   // REG: halo rows
+    using DS = typename ChebImage<T>::type;
+    DS* const sd = reinterpret_cast<DS*>(cheb_smem);   // REG: d planes, buffer p at sd + 3 p kChebSlots
+    T* const yv0 = reinterpret_cast<T*>(sd + 6 * kChebSlots);
+    T* yv = yv0 + threadIdx.x;                     // REG: this row's y, planes kChebMaxThreads apart
+    int* hidx = reinterpret_cast<int*>(yv0 + 3 * kChebMaxThreads);   // REG: halo rows
     // exported rows [row0, row0 + nexp) belong to the leading warps (at least warp 0, which
     // publishes the step flag)
     const int nexp = REG ? a.cheb_nexp[blockIdx.x] : 0;
@@ -221,26 +236,26 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
         if (warm) {
             // K * guess from shared memory like a step: own rows' guesses and the halo rows'
             // (written by the previous frame's launch: plain loads) into buffer 1's planes
-            T* const sg = sd + 3 * kChebSlots;
+            DS* const sg = sd + 3 * kChebSlots;
             T gx = 0, gy = 0, gz = 0;
             __syncthreads();                       // hidx
             if (own) {
                 const vec4_t<T> g = ld4(&wb[i]);
-                gx = g.x; gy = g.y; gz = g.z;
+                gx = (T)(DS)g.x; gy = (T)(DS)g.y; gz = (T)(DS)g.z;     // the guess as applied
                 sg[threadIdx.x] = gx; sg[kChebSlots + threadIdx.x] = gy; sg[2 * kChebSlots + threadIdx.x] = gz;
             }
             for (int j = threadIdx.x; j < nh; j += blockDim.x) {
                 const vec4_t<T> g = ld4(&wb[hidx[j]]);
                 const int sl = blockDim.x + j;
-                sg[sl] = g.x; sg[kChebSlots + sl] = g.y; sg[2 * kChebSlots + sl] = g.z;
+                sg[sl] = (DS)g.x; sg[kChebSlots + sl] = (DS)g.y; sg[2 * kChebSlots + sl] = (DS)g.z;
             }
             __syncthreads();
             if (own) {
                 T qx = kdiag * gx, qy = kdiag * gy, qz = kdiag * gz;
 #pragma unroll
                 for (int s = 0; s < kChebOff; ++s) {
-                    const T* d = sg + cols[s];
-                    qx += vals[s] * d[0]; qy += vals[s] * d[kChebSlots]; qz += vals[s] * d[2 * kChebSlots];
+                    const DS* d = sg + cols[s];
+                    qx += vals[s] * (T)d[0]; qy += vals[s] * (T)d[kChebSlots]; qz += vals[s] * (T)d[2 * kChebSlots];
                 }
                 if (a.cdiag != nullptr) {
                     const T cd = a.cdiag[i];
@@ -256,7 +271,7 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
         if (own) {
             const T c0 = (T)(1.0 / theta) * dg;
             dxv = c0 * rx; dyv = c0 * ry; dzv = c0 * rzz;
-            sd[threadIdx.x] = dxv; sd[kChebSlots + threadIdx.x] = dyv; sd[2 * kChebSlots + threadIdx.x] = dzv;
+            sd[threadIdx.x] = (DS)dxv; sd[kChebSlots + threadIdx.x] = (DS)dyv; sd[2 * kChebSlots + threadIdx.x] = (DS)dzv;
             acc[0] = (double)rx * rx + (double)ry * ry + (double)rzz * rzz;
         }
     } else {
@@ -287,10 +302,11 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     int k = 0;
     double rho = 1.0 / sigma;
     const double two_over_delta = 2.0 / delta;
-    constexpr int LLW = LLRow<T>::W;
+    constexpr int LLW = LLRow<DS>::W;
     if (rr > thr && a.max_iters > 0) {
         int target = min(a.max_iters, cheb_steps_for(sqrt(rr / thr), acosh_sigma));
-        if (REG && own && (int)threadIdx.x < nexp) ll_store(a.cheb_ll + (size_t)i * LLW, dxv, dyv, dzv, base);
+        if (REG && own && (int)threadIdx.x < nexp)
+            ll_store(a.cheb_ll + (size_t)i * LLW, (DS)dxv, (DS)dyv, (DS)dzv, base);
         for (;;) {
             for (; k < target; ++k) {
                 pcg_mark(10);
@@ -301,8 +317,8 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                 const T c1 = (T)(rho_n * rho), c2 = (T)(rho_n * two_over_delta);
                 rho = rho_n;
                 if (REG) {
-                    T* const sx = sd + (k & 1) * 3 * kChebSlots;         // d_k
-                    T* const sn = sd + ((k + 1) & 1) * 3 * kChebSlots;   // d_{k+1} (own rows)
+                    DS* const sx = sd + (k & 1) * 3 * kChebSlots;         // d_k
+                    DS* const sn = sd + ((k + 1) & 1) * 3 * kChebSlots;   // d_{k+1} (own rows)
                     // every own row's d_k is in shared memory (written by step k-1)
                     if (k > 0) __syncthreads();
                     if (exp_warp) {
@@ -313,7 +329,7 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                         pcg_mark(11);
                         const uint4* src = a.cheb_ll + (size_t)(k & 1) * nF * LLW;
                         for (int j = threadIdx.x; j < nh; j += exp_threads) {
-                            T hx, hy, hz;
+                            DS hx, hy, hz;
                             ll_load(src + (size_t)hidx[j] * LLW, base + (unsigned)k, hx, hy, hz);
                             const int sl = blockDim.x + j;
                             sx[sl] = hx; sx[kChebSlots + sl] = hy; sx[2 * kChebSlots + sl] = hz;
@@ -322,17 +338,19 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                         pcg_mark(12);
                     }
                     // interior warps run their rows meanwhile: they read own rows only
-                    T qx = kdiag * dxv, qy = kdiag * dyv, qz = kdiag * dzv, px = 0, py = 0, pz = 0;
+                    // the applied direction (own row): the image's rounding of d_k
+                    const T ax = (T)(DS)dxv, ay = (T)(DS)dyv, az = (T)(DS)dzv;
+                    T qx = kdiag * ax, qy = kdiag * ay, qz = kdiag * az, px = 0, py = 0, pz = 0;
                     if (own) {
                         // two partial sums per component (shorter dependency chains)
 #pragma unroll
                         for (int s = 0; s < kChebOff; s += 2) {
-                            const T* d = sx + cols[s];
-                            qx += vals[s] * d[0]; qy += vals[s] * d[kChebSlots]; qz += vals[s] * d[2 * kChebSlots];
+                            const DS* d = sx + cols[s];
+                            qx += vals[s] * (T)d[0]; qy += vals[s] * (T)d[kChebSlots]; qz += vals[s] * (T)d[2 * kChebSlots];
                             if (s + 1 < kChebOff) {
-                                const T* e = sx + cols[s + 1];
-                                px += vals[s + 1] * e[0]; py += vals[s + 1] * e[kChebSlots];
-                                pz += vals[s + 1] * e[2 * kChebSlots];
+                                const DS* e = sx + cols[s + 1];
+                                px += vals[s + 1] * (T)e[0]; py += vals[s + 1] * (T)e[kChebSlots];
+                                pz += vals[s + 1] * (T)e[2 * kChebSlots];
                             }
                         }
                     }
@@ -340,18 +358,18 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                         qx += px; qy += py; qz += pz;
                         if (a.cdiag != nullptr) {
                             const T cd = a.cdiag[i];
-                            qx += cd * dxv; qy += cd * dyv; qz += cd * dzv;
+                            qx += cd * ax; qy += cd * ay; qz += cd * az;
                         }
-                        yv[0] += dxv; yv[kChebMaxThreads] += dyv; yv[2 * kChebMaxThreads] += dzv;
+                        yv[0] += ax; yv[kChebMaxThreads] += ay; yv[2 * kChebMaxThreads] += az;
                         rx -= qx; ry -= qy; rzz -= qz;
                         const T e = c2 * dg;
                         dxv = c1 * dxv + e * rx;
                         dyv = c1 * dyv + e * ry;
                         dzv = c1 * dzv + e * rzz;
-                        sn[threadIdx.x] = dxv; sn[kChebSlots + threadIdx.x] = dyv; sn[2 * kChebSlots + threadIdx.x] = dzv;
+                        sn[threadIdx.x] = (DS)dxv; sn[kChebSlots + threadIdx.x] = (DS)dyv; sn[2 * kChebSlots + threadIdx.x] = (DS)dzv;
                         if ((int)threadIdx.x < nexp)
-                            ll_store(a.cheb_ll + (size_t)((k + 1) & 1) * nF * LLW + (size_t)i * LLW, dxv, dyv, dzv,
-                                     base + (unsigned)(k + 1));
+                            ll_store(a.cheb_ll + (size_t)((k + 1) & 1) * nF * LLW + (size_t)i * LLW, (DS)dxv, (DS)dyv,
+                                     (DS)dzv, base + (unsigned)(k + 1));
                     }
                     pcg_mark(13);
                 } else {
@@ -442,6 +460,7 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
 #define VK_CHEB_THREADS 768
 #endif
 template <typename T>
+// (80 registers: up to 6 warps per SM sub-partition of 16K registers; 88 would need <= 20 warps)
 __global__ void __launch_bounds__(VK_CHEB_THREADS, 1) k_cheb_reg(PcgArgs<T> a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double smem[32 * 8];

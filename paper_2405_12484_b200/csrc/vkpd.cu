@@ -823,30 +823,31 @@ struct Ctx : CtxBase {
     DBuf<int> cheb_slot, cheb_halo_ptr, cheb_halo;
     DBuf<T> cheb_val, cheb_kdiag;
     DBuf<int> cheb_nexp, cheb_nbr_hend;
-    // Entry positions of one half-warp's rows (<= 16 lanes) without shared-memory bank
-    // conflicts.  k_cheb_reg's SpMV loads d[slot[o]] for o = 0..13 at once across a warp; a
-    // 64-bit load is served per half-warp and costs as many wavefronts as the most distinct
-    // slots that share a bank pair (slot mod 16).  The rows' entries form a bipartite multigraph
+    // Entry positions of one wavefront group's rows without shared-memory bank conflicts.
+    // k_cheb_reg's SpMV loads d[slot[o]] for o = 0..13 at once across a warp; a 32-bit load is
+    // served per warp (32 lanes, bank = slot mod 32), a 64-bit one per half-warp (16 lanes, bank
+    // pair = slot mod 16), and costs as many wavefronts as the most distinct slots that share a
+    // bank (C = number of banks).  The rows' entries form a bipartite multigraph
     // lanes x bank pairs; an edge colouring with D = max(14, max degree) colours (Konig:
     // alternating-path recolouring) puts distinct bank pairs at each position.  Colours >= 14
     // (an overloaded bank pair) fold into a lane's free position where they add the least; pad
     // positions (value 0) read a slot another lane already reads there (broadcast).  C3 fp64:
     // 3.6 -> 2.1 wavefronts per gather (tools/dbg/bank_model.py).
-    static void conflict_free_positions(int lanes, const int* ent_n, const int (*ent_slot)[vk::kChebOff],
+    static void conflict_free_positions(int lanes, int C, const int* ent_n, const int (*ent_slot)[vk::kChebOff],
                                         const int* own_slot, int (*pos_of)[vk::kChebOff],
                                         int (*pad_slot)[vk::kChebOff]) {
         constexpr int K = vk::kChebOff;
-        int deg[16] = {0};
+        int deg[32] = {0};
         int ne = 0;
         for (int u = 0; u < lanes; ++u)
-            for (int t = 0; t < ent_n[u]; ++t) { ++deg[ent_slot[u][t] & 15]; ++ne; }
+            for (int t = 0; t < ent_n[u]; ++t) { ++deg[ent_slot[u][t] % C]; ++ne; }
         int D = K;
-        for (int b = 0; b < 16; ++b) D = std::max(D, deg[b]);
+        for (int b = 0; b < C; ++b) D = std::max(D, deg[b]);
         std::vector<int> eu(ne), ev(ne), et(ne), ec(ne, -1);
-        std::vector<int> U((size_t)16 * D, -1), V((size_t)16 * D, -1);
+        std::vector<int> U((size_t)32 * D, -1), V((size_t)C * D, -1);
         int id = 0;
         for (int u = 0; u < lanes; ++u)
-            for (int t = 0; t < ent_n[u]; ++t) { eu[id] = u; ev[id] = ent_slot[u][t] & 15; et[id] = t; ++id; }
+            for (int t = 0; t < ent_n[u]; ++t) { eu[id] = u; ev[id] = ent_slot[u][t] % C; et[id] = t; ++id; }
         std::vector<int> path;
         for (int e = 0; e < ne; ++e) {
             const int u = eu[e], v = ev[e];
@@ -875,10 +876,10 @@ struct Ctx : CtxBase {
             ec[e] = a; U[(size_t)u * D + a] = e; V[(size_t)v * D + a] = e;
         }
         // positions: colour c < K is position c; later colours fold into free positions
-        std::vector<std::vector<int>> at((size_t)K * 16);      // (position, bank pair) -> slots
+        std::vector<std::vector<int>> at((size_t)K * C);       // (position, bank) -> slots
         for (int u = 0; u < lanes; ++u) for (int o = 0; o < K; ++o) pos_of[u][o] = -1;
         auto add = [&](int o, int sl) {
-            auto& L = at[(size_t)o * 16 + (sl & 15)];
+            auto& L = at[(size_t)o * C + sl % C];
             if (std::find(L.begin(), L.end(), sl) == L.end()) L.push_back(sl);
         };
         for (int e = 0; e < ne; ++e)
@@ -890,7 +891,7 @@ struct Ctx : CtxBase {
             size_t bc = 0;
             for (int o = 0; o < K; ++o) {
                 if (pos_of[u][o] >= 0) continue;
-                const auto& L = at[(size_t)o * 16 + (sl & 15)];
+                const auto& L = at[(size_t)o * C + sl % C];
                 const size_t c = std::find(L.begin(), L.end(), sl) != L.end() ? 0 : L.size();
                 if (best < 0 || c < bc) { best = o; bc = c; }
             }
@@ -901,9 +902,9 @@ struct Ctx : CtxBase {
             for (int o = 0; o < K; ++o) {
                 pad_slot[u][o] = own_slot[u];
                 if (pos_of[u][o] >= 0) continue;
-                for (int b = 0; b < 16; ++b)
-                    if (!at[(size_t)o * 16 + b].empty()) { pad_slot[u][o] = at[(size_t)o * 16 + b][0]; break; }
-                if (at[(size_t)o * 16 + (pad_slot[u][o] & 15)].empty()) add(o, pad_slot[u][o]);
+                for (int b = 0; b < C; ++b)
+                    if (!at[(size_t)o * C + b].empty()) { pad_slot[u][o] = at[(size_t)o * C + b][0]; break; }
+                if (at[(size_t)o * C + pad_slot[u][o] % C].empty()) add(o, pad_slot[u][o]);
             }
     }
     int build_cheb_neighbours() {
@@ -989,11 +990,13 @@ struct Ctx : CtxBase {
                     else if (c >= r0 && c < r1) oslot[(size_t)o * nF + i] = c - r0;
                     else oslot[(size_t)o * nF + i] = pcg_threads + hslot[c];
                 }
+            // wavefront group: 32 lanes for a 4-byte direction image, 16 for an 8-byte one
+            constexpr int G = sizeof(typename vk::ChebImage<T>::type) == 4 ? 32 : 16;
             if (fits)
-                for (int h0 = r0; h0 < r1; h0 += 16) {
-                    const int lanes = std::min(16, r1 - h0);
-                    int en[16], es[16][vk::kChebOff], own_s[16], pos[16][vk::kChebOff], pad[16][vk::kChebOff];
-                    T ev[16][vk::kChebOff];
+                for (int h0 = r0; h0 < r1; h0 += G) {
+                    const int lanes = std::min(G, r1 - h0);
+                    int en[32], es[32][vk::kChebOff], own_s[32], pos[32][vk::kChebOff], pad[32][vk::kChebOff];
+                    T ev[32][vk::kChebOff];
                     for (int u = 0; u < lanes; ++u) {
                         const int i = h0 + u;
                         own_s[u] = i - r0;
@@ -1005,7 +1008,7 @@ struct Ctx : CtxBase {
                                 ++en[u];
                             }
                     }
-                    conflict_free_positions(lanes, en, es, own_s, pos, pad);
+                    conflict_free_positions(lanes, G, en, es, own_s, pos, pad);
                     for (int u = 0; u < lanes; ++u)
                         for (int o = 0; o < vk::kChebOff; ++o) {
                             const size_t x = (size_t)o * nF + h0 + u;
@@ -1059,7 +1062,7 @@ struct Ctx : CtxBase {
         CK(cheb_flags.alloc((size_t)32 * pcg_blocks));
         CK(cudaMemsetAsync(cheb_flags.p, 0, sizeof(unsigned int) * 32 * pcg_blocks, stream));
         // tags restart with the flags: no stale row may carry a tag the next launches wait for
-        CK(cheb_ll.alloc((size_t)2 * vk::LLRow<T>::W * std::max(1, nF)));
+        CK(cheb_ll.alloc((size_t)2 * vk::LLRow<typename vk::ChebImage<T>::type>::W * std::max(1, nF)));
         CK(cudaMemsetAsync(cheb_ll.p, 0xff, cheb_ll.n * sizeof(uint4), stream));
         CK(cudaStreamSynchronize(stream));
         return VKPD_OK;
