@@ -162,6 +162,43 @@ constexpr size_t cheb_smem_bytes() {
            sizeof(int) * kChebSlots;
 }
 
+// Shared-memory loads at an absolute shared-window address plus a compile-time offset (the
+// plane and step-parity offsets of the direction image): one LDS per value, no address math.
+template <int OFF> __device__ __forceinline__ float lds_img(unsigned addr, float*) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
+    return v;
+}
+template <int OFF> __device__ __forceinline__ double lds_img(unsigned addr, double*) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(addr), "n"(OFF));
+    return v;
+}
+// q += sum_s vals[s] d[slot_s] over the image buffer P (x / y / z planes), two partial sums per
+// component.  colp: two 16-bit absolute shared addresses (buffer 0, x plane) per register.
+static_assert(kChebSlots * 8 + 16384 < 65536, "16-bit shared addresses of the direction image");
+template <int P, typename DS, typename T>
+__device__ __forceinline__ void spmv_img(const unsigned (&colp)[(kChebOff + 1) / 2], const T (&vals)[kChebOff],
+                                         T& qx, T& qy, T& qz) {
+    constexpr int PL = kChebSlots * (int)sizeof(DS);
+    constexpr int B = P * 3 * PL;
+    T px = 0, py = 0, pz = 0;
+#pragma unroll
+    for (int h = 0; h < (kChebOff + 1) / 2; ++h) {
+        const unsigned c0 = colp[h] & 0xffffu, c1 = colp[h] >> 16;
+        const int s = 2 * h;
+        qx += vals[s] * (T)lds_img<B>(c0, (DS*)nullptr);
+        qy += vals[s] * (T)lds_img<B + PL>(c0, (DS*)nullptr);
+        qz += vals[s] * (T)lds_img<B + 2 * PL>(c0, (DS*)nullptr);
+        if (s + 1 < kChebOff) {
+            px += vals[s + 1] * (T)lds_img<B>(c1, (DS*)nullptr);
+            py += vals[s + 1] * (T)lds_img<B + PL>(c1, (DS*)nullptr);
+            pz += vals[s + 1] * (T)lds_img<B + 2 * PL>(c1, (DS*)nullptr);
+        }
+    }
+    qx += px; qy += py; qz += pz;
+}
+
 // Steps needed for a residual reduction by `ratio` at Chebyshev parameter sigma
 // (|p_k| <= 1 / T_k(sigma) on the interval).
 __device__ __forceinline__ int cheb_steps_for(double ratio, double acosh_sigma) {
@@ -198,8 +235,8 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     // ---- init: res = b - K x (PD residual form) minus K * warm guess; y = guess; d0 = D^-1 res / theta
     const int i = row0 + threadIdx.x;              // REG path: this thread's row
     const bool own = REG && i < row1;
-    int cols[kChebOff];                            // REG: shared-memory slots of the off-diagonal columns
-    T vals[kChebOff];                              //      and their values
+    unsigned colp[(kChebOff + 1) / 2];             // REG: shared addresses of the off-diagonal columns
+    T vals[kChebOff];                              //      (two 16-bit per register) and their values
     T kdiag = 0;
     extern __shared__ __align__(16) unsigned char cheb_smem[];
     using DS = typename ChebImage<T>::type;
@@ -225,11 +262,16 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
         if (own) init_residual_row(a, i, false, rx, ry, rzz, acc[1]);
         pcg_mark(16);
         if (own) {
+            const unsigned sbase = (unsigned)__cvta_generic_to_shared(sd);
 #pragma unroll
-            for (int s = 0; s < kChebOff; ++s) {
-                cols[s] = __ldg(&a.cheb_slot[(size_t)s * nF + i]);
-                vals[s] = __ldg(&a.cheb_val[(size_t)s * nF + i]);
+            for (int h = 0; h < (kChebOff + 1) / 2; ++h) {
+                const unsigned c0 = sbase + (unsigned)sizeof(DS) * __ldg(&a.cheb_slot[(size_t)(2 * h) * nF + i]);
+                const unsigned c1 = 2 * h + 1 < kChebOff
+                    ? sbase + (unsigned)sizeof(DS) * __ldg(&a.cheb_slot[(size_t)(2 * h + 1) * nF + i]) : 0u;
+                colp[h] = c0 | (c1 << 16);
             }
+#pragma unroll
+            for (int s = 0; s < kChebOff; ++s) vals[s] = __ldg(&a.cheb_val[(size_t)s * nF + i]);
             kdiag = __ldg(&a.cheb_kdiag[i]);
             dg = a.inv_diag[i];
         }
@@ -252,11 +294,7 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
             __syncthreads();
             if (own) {
                 T qx = kdiag * gx, qy = kdiag * gy, qz = kdiag * gz;
-#pragma unroll
-                for (int s = 0; s < kChebOff; ++s) {
-                    const DS* d = sg + cols[s];
-                    qx += vals[s] * (T)d[0]; qy += vals[s] * (T)d[kChebSlots]; qz += vals[s] * (T)d[2 * kChebSlots];
-                }
+                spmv_img<1, DS>(colp, vals, qx, qy, qz);
                 if (a.cdiag != nullptr) {
                     const T cd = a.cdiag[i];
                     qx += cd * gx; qy += cd * gy; qz += cd * gz;
@@ -340,22 +378,10 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                     // interior warps run their rows meanwhile: they read own rows only
                     // the applied direction (own row): the image's rounding of d_k
                     const T ax = (T)(DS)dxv, ay = (T)(DS)dyv, az = (T)(DS)dzv;
-                    T qx = kdiag * ax, qy = kdiag * ay, qz = kdiag * az, px = 0, py = 0, pz = 0;
+                    T qx = kdiag * ax, qy = kdiag * ay, qz = kdiag * az;
                     if (own) {
-                        // two partial sums per component (shorter dependency chains)
-#pragma unroll
-                        for (int s = 0; s < kChebOff; s += 2) {
-                            const DS* d = sx + cols[s];
-                            qx += vals[s] * (T)d[0]; qy += vals[s] * (T)d[kChebSlots]; qz += vals[s] * (T)d[2 * kChebSlots];
-                            if (s + 1 < kChebOff) {
-                                const DS* e = sx + cols[s + 1];
-                                px += vals[s + 1] * (T)e[0]; py += vals[s + 1] * (T)e[kChebSlots];
-                                pz += vals[s + 1] * (T)e[2 * kChebSlots];
-                            }
-                        }
-                    }
-                    if (own) {
-                        qx += px; qy += py; qz += pz;
+                        if (k & 1) spmv_img<1, DS>(colp, vals, qx, qy, qz);
+                        else spmv_img<0, DS>(colp, vals, qx, qy, qz);
                         if (a.cdiag != nullptr) {
                             const T cd = a.cdiag[i];
                             qx += cd * ax; qy += cd * ay; qz += cd * az;
