@@ -85,6 +85,7 @@ __device__ __forceinline__ void ldcg3(const double4* p, double& x, double& y, do
 template <typename T> struct LLRow;
 template <> struct LLRow<double> { static constexpr int W = 3; };
 template <> struct LLRow<float> { static constexpr int W = 2; };
+template <> struct LLRow<unsigned> { static constexpr int W = 2; };
 
 __device__ __forceinline__ void ll_st(uint4* p, unsigned a, unsigned b, unsigned c, unsigned d) {
     asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
@@ -105,6 +106,10 @@ __device__ __forceinline__ void ll_store(uint4* p, double x, double y, double z,
 __device__ __forceinline__ void ll_store(uint4* p, float x, float y, float z, unsigned tag) {
     ll_st(p, __float_as_uint(x), tag, __float_as_uint(y), tag);
     ll_st(p + 1, __float_as_uint(z), tag, 0u, tag);
+}
+__device__ __forceinline__ void ll_store(uint4* p, unsigned x, unsigned y, unsigned z, unsigned tag) {
+    ll_st(p, x, tag, y, tag);
+    ll_st(p + 1, z, tag, 0u, tag);
 }
 __device__ __forceinline__ bool ll_ok(const uint4& v, unsigned tag) { return v.y == tag && v.w == tag; }
 // spin until the row carries `tag` (traps after ~2^33 polls: a lost producer)
@@ -128,6 +133,11 @@ __device__ __forceinline__ void ll_load(const uint4* p, unsigned tag, float& x, 
     }
     x = __uint_as_float(a.x); y = __uint_as_float(a.z); z = __uint_as_float(b.x);
 }
+__device__ __forceinline__ void ll_load(const uint4* p, unsigned tag, unsigned& x, unsigned& y, unsigned& z) {
+    float fx, fy, fz;
+    ll_load(p, tag, fx, fy, fz);
+    x = __float_as_uint(fx); y = __float_as_uint(fy); z = __float_as_uint(fz);
+}
 
 // Register path: a row keeps its kChebOff off-diagonal ELL values and their shared-memory
 // slots in registers (plus the diagonal), so the SpMV's shared-memory traffic is only the
@@ -144,22 +154,37 @@ __device__ __forceinline__ void ll_load(const uint4* p, unsigned tag, float& x, 
 constexpr int kChebMaxThreads = 768;
 constexpr int kChebSlots = 2048;
 constexpr int kChebOff = 14;       // voxel enclosures: <= 15 entries per row, one of them diagonal
-// Type of the shared-memory / cross-CTA image of the direction d.  float64 solves apply the
-// float32-rounded direction: y += fl(d) and r -= K fl(d) (K, r, y in float64), so y and r stay
+// Type of the shared-memory / cross-CTA image of the direction d.  float64 solves apply a
+// 32-bit rounding of the direction, the upper word of the double (sign, 11-bit exponent, 20-bit
+// mantissa, rounded to nearest): y += h(d) and r -= K h(d) (K, r, y in float64), so y and r stay
 // consistent (r is the residual of y to float64 rounding) and the stopping test is unchanged;
-// only the Chebyshev direction carries a 6e-8 relative perturbation, which the recurrence damps
-// like any other.  Halves the SpMV's shared-memory wavefronts and the halo bytes.
+// only the Chebyshev direction carries a 5e-7 relative perturbation, which the recurrence damps
+// like any other.  Halves the SpMV's shared-memory wavefronts and the halo bytes, and decoding
+// is a register pair {0, h}: no F2F conversion (a quarter-rate pipe) per gathered value.
 #ifndef VK_CHEB_D32
 #define VK_CHEB_D32 1
 #endif
 template <typename T> struct ChebImage { using type = T; };
 #if VK_CHEB_D32
-template <> struct ChebImage<double> { using type = float; };
+template <> struct ChebImage<double> { using type = unsigned; };
 #endif
+__device__ __forceinline__ float img_enc(float x) { return x; }
+__device__ __forceinline__ float img_dec(float x) { return x; }
+__device__ __forceinline__ double img_dec(double x) { return x; }
+__device__ __forceinline__ double img_dec(unsigned h) { return __hiloint2double((int)h, 0); }
+template <typename DS> __device__ __forceinline__ DS img_enc64(double x);
+template <> __device__ __forceinline__ double img_enc64<double>(double x) { return x; }
+template <> __device__ __forceinline__ unsigned img_enc64<unsigned>(double x) {
+    return (unsigned)(((unsigned long long)__double_as_longlong(x) + 0x80000000ull) >> 32);
+}
+template <typename DS, typename T> __device__ __forceinline__ DS img_enc(T x) {
+    if constexpr (sizeof(T) == 4) return x;
+    else return img_enc64<DS>(x);
+}
 template <typename T>
 constexpr size_t cheb_smem_bytes() {
-    return sizeof(typename ChebImage<T>::type) * 6 * (size_t)kChebSlots + sizeof(T) * 3 * (size_t)kChebMaxThreads +
-           sizeof(int) * kChebSlots;
+    return sizeof(typename ChebImage<T>::type) * 6 * (size_t)kChebSlots +
+           sizeof(T) * (3 + kChebOff) * (size_t)kChebMaxThreads + sizeof(int) * kChebSlots;
 }
 
 // Shared-memory loads at an absolute shared-window address plus a compile-time offset (the
@@ -169,34 +194,38 @@ template <int OFF> __device__ __forceinline__ float lds_img(unsigned addr, float
     asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
     return v;
 }
+template <int OFF> __device__ __forceinline__ unsigned lds_img(unsigned addr, unsigned*) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF));
+    return v;
+}
 template <int OFF> __device__ __forceinline__ double lds_img(unsigned addr, double*) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(addr), "n"(OFF));
     return v;
 }
-// q += sum_s vals[s] d[slot_s] over the image buffer P (x / y / z planes), two partial sums per
-// component.  colp: two 16-bit absolute shared addresses (buffer 0, x plane) per register.
-static_assert(kChebSlots * 8 + 16384 < 65536, "16-bit shared addresses of the direction image");
+// q += sum_s vals[s] d[slot_s] over the image buffer P (x / y / z planes), one sum per component.
+// colp: two 16-bit byte offsets (into the buffer-0 x plane) per register.  Plain shared loads,
+// so the compiler can keep several in flight.
 template <int P, typename DS, typename T>
-__device__ __forceinline__ void spmv_img(const unsigned (&colp)[(kChebOff + 1) / 2], const T (&vals)[kChebOff],
-                                         T& qx, T& qy, T& qz) {
-    constexpr int PL = kChebSlots * (int)sizeof(DS);
-    constexpr int B = P * 3 * PL;
-    T px = 0, py = 0, pz = 0;
+__device__ __forceinline__ void spmv_img(const DS* sd, const unsigned (&colp)[(kChebOff + 1) / 2],
+                                         const T* sv, T& qx, T& qy, T& qz) {
+    const char* const b = reinterpret_cast<const char*>(sd + P * 3 * kChebSlots);
 #pragma unroll
     for (int h = 0; h < (kChebOff + 1) / 2; ++h) {
-        const unsigned c0 = colp[h] & 0xffffu, c1 = colp[h] >> 16;
-        const int s = 2 * h;
-        qx += vals[s] * (T)lds_img<B>(c0, (DS*)nullptr);
-        qy += vals[s] * (T)lds_img<B + PL>(c0, (DS*)nullptr);
-        qz += vals[s] * (T)lds_img<B + 2 * PL>(c0, (DS*)nullptr);
-        if (s + 1 < kChebOff) {
-            px += vals[s + 1] * (T)lds_img<B>(c1, (DS*)nullptr);
-            py += vals[s + 1] * (T)lds_img<B + PL>(c1, (DS*)nullptr);
-            pz += vals[s + 1] * (T)lds_img<B + 2 * PL>(c1, (DS*)nullptr);
+        const DS* d0 = reinterpret_cast<const DS*>(b + (colp[h] & 0xffffu));
+        const T v0 = sv[(2 * h) * kChebMaxThreads];
+        qx += v0 * (T)img_dec(d0[0]);
+        qy += v0 * (T)img_dec(d0[kChebSlots]);
+        qz += v0 * (T)img_dec(d0[2 * kChebSlots]);
+        if (2 * h + 1 < kChebOff) {
+            const DS* d1 = reinterpret_cast<const DS*>(b + (colp[h] >> 16));
+            const T v1 = sv[(2 * h + 1) * kChebMaxThreads];
+            qx += v1 * (T)img_dec(d1[0]);
+            qy += v1 * (T)img_dec(d1[kChebSlots]);
+            qz += v1 * (T)img_dec(d1[2 * kChebSlots]);
         }
     }
-    qx += px; qy += py; qz += pz;
 }
 
 // Steps needed for a residual reduction by `ratio` at Chebyshev parameter sigma
@@ -235,15 +264,16 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     // ---- init: res = b - K x (PD residual form) minus K * warm guess; y = guess; d0 = D^-1 res / theta
     const int i = row0 + threadIdx.x;              // REG path: this thread's row
     const bool own = REG && i < row1;
-    unsigned colp[(kChebOff + 1) / 2];             // REG: shared addresses of the off-diagonal columns
-    T vals[kChebOff];                              //      (two 16-bit per register) and their values
+    unsigned colp[(kChebOff + 1) / 2];             // REG: image byte offsets of the off-diagonal columns
+                                                   //      (two 16-bit per register)
     T kdiag = 0;
     extern __shared__ __align__(16) unsigned char cheb_smem[];
     using DS = typename ChebImage<T>::type;
     DS* const sd = reinterpret_cast<DS*>(cheb_smem);   // REG: d planes, buffer p at sd + 3 p kChebSlots
     T* const yv0 = reinterpret_cast<T*>(sd + 6 * kChebSlots);
     T* yv = yv0 + threadIdx.x;                     // REG: this row's y, planes kChebMaxThreads apart
-    int* hidx = reinterpret_cast<int*>(yv0 + 3 * kChebMaxThreads);   // REG: halo rows
+    T* const sv = yv0 + 3 * kChebMaxThreads + threadIdx.x;   // REG: this row's ELL values, planes apart
+    int* hidx = reinterpret_cast<int*>(yv0 + (3 + kChebOff) * kChebMaxThreads);   // REG: halo rows
     // exported rows [row0, row0 + nexp) belong to the leading warps (at least warp 0, which
     // publishes the step flag)
     const int nexp = REG ? a.cheb_nexp[blockIdx.x] : 0;
@@ -262,16 +292,15 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
         if (own) init_residual_row(a, i, false, rx, ry, rzz, acc[1]);
         pcg_mark(16);
         if (own) {
-            const unsigned sbase = (unsigned)__cvta_generic_to_shared(sd);
 #pragma unroll
             for (int h = 0; h < (kChebOff + 1) / 2; ++h) {
-                const unsigned c0 = sbase + (unsigned)sizeof(DS) * __ldg(&a.cheb_slot[(size_t)(2 * h) * nF + i]);
+                const unsigned c0 = (unsigned)sizeof(DS) * __ldg(&a.cheb_slot[(size_t)(2 * h) * nF + i]);
                 const unsigned c1 = 2 * h + 1 < kChebOff
-                    ? sbase + (unsigned)sizeof(DS) * __ldg(&a.cheb_slot[(size_t)(2 * h + 1) * nF + i]) : 0u;
+                    ? (unsigned)sizeof(DS) * __ldg(&a.cheb_slot[(size_t)(2 * h + 1) * nF + i]) : 0u;
                 colp[h] = c0 | (c1 << 16);
             }
 #pragma unroll
-            for (int s = 0; s < kChebOff; ++s) vals[s] = __ldg(&a.cheb_val[(size_t)s * nF + i]);
+            for (int s = 0; s < kChebOff; ++s) sv[s * kChebMaxThreads] = __ldg(&a.cheb_val[(size_t)s * nF + i]);
             kdiag = __ldg(&a.cheb_kdiag[i]);
             dg = a.inv_diag[i];
         }
@@ -283,18 +312,20 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
             __syncthreads();                       // hidx
             if (own) {
                 const vec4_t<T> g = ld4(&wb[i]);
-                gx = (T)(DS)g.x; gy = (T)(DS)g.y; gz = (T)(DS)g.z;     // the guess as applied
-                sg[threadIdx.x] = gx; sg[kChebSlots + threadIdx.x] = gy; sg[2 * kChebSlots + threadIdx.x] = gz;
+                gx = (T)img_dec(img_enc<DS>(g.x)); gy = (T)img_dec(img_enc<DS>(g.y));   // the guess as applied
+                gz = (T)img_dec(img_enc<DS>(g.z));
+                sg[threadIdx.x] = img_enc<DS>(gx); sg[kChebSlots + threadIdx.x] = img_enc<DS>(gy);
+                sg[2 * kChebSlots + threadIdx.x] = img_enc<DS>(gz);
             }
             for (int j = threadIdx.x; j < nh; j += blockDim.x) {
                 const vec4_t<T> g = ld4(&wb[hidx[j]]);
                 const int sl = blockDim.x + j;
-                sg[sl] = (DS)g.x; sg[kChebSlots + sl] = (DS)g.y; sg[2 * kChebSlots + sl] = (DS)g.z;
+                sg[sl] = img_enc<DS>(g.x); sg[kChebSlots + sl] = img_enc<DS>(g.y); sg[2 * kChebSlots + sl] = img_enc<DS>(g.z);
             }
             __syncthreads();
             if (own) {
                 T qx = kdiag * gx, qy = kdiag * gy, qz = kdiag * gz;
-                spmv_img<1, DS>(colp, vals, qx, qy, qz);
+                spmv_img<1, DS>(sd, colp, sv, qx, qy, qz);
                 if (a.cdiag != nullptr) {
                     const T cd = a.cdiag[i];
                     qx += cd * gx; qy += cd * gy; qz += cd * gz;
@@ -309,7 +340,8 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
         if (own) {
             const T c0 = (T)(1.0 / theta) * dg;
             dxv = c0 * rx; dyv = c0 * ry; dzv = c0 * rzz;
-            sd[threadIdx.x] = (DS)dxv; sd[kChebSlots + threadIdx.x] = (DS)dyv; sd[2 * kChebSlots + threadIdx.x] = (DS)dzv;
+            sd[threadIdx.x] = img_enc<DS>(dxv); sd[kChebSlots + threadIdx.x] = img_enc<DS>(dyv);
+            sd[2 * kChebSlots + threadIdx.x] = img_enc<DS>(dzv);
             acc[0] = (double)rx * rx + (double)ry * ry + (double)rzz * rzz;
         }
     } else {
@@ -344,7 +376,7 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     if (rr > thr && a.max_iters > 0) {
         int target = min(a.max_iters, cheb_steps_for(sqrt(rr / thr), acosh_sigma));
         if (REG && own && (int)threadIdx.x < nexp)
-            ll_store(a.cheb_ll + (size_t)i * LLW, (DS)dxv, (DS)dyv, (DS)dzv, base);
+            ll_store(a.cheb_ll + (size_t)i * LLW, img_enc<DS>(dxv), img_enc<DS>(dyv), img_enc<DS>(dzv), base);
         for (;;) {
             for (; k < target; ++k) {
                 pcg_mark(10);
@@ -377,11 +409,12 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                     }
                     // interior warps run their rows meanwhile: they read own rows only
                     // the applied direction (own row): the image's rounding of d_k
-                    const T ax = (T)(DS)dxv, ay = (T)(DS)dyv, az = (T)(DS)dzv;
+                    const DS ex = img_enc<DS>(dxv), ey = img_enc<DS>(dyv), ez = img_enc<DS>(dzv);
+                    const T ax = (T)img_dec(ex), ay = (T)img_dec(ey), az = (T)img_dec(ez);
                     T qx = kdiag * ax, qy = kdiag * ay, qz = kdiag * az;
                     if (own) {
-                        if (k & 1) spmv_img<1, DS>(colp, vals, qx, qy, qz);
-                        else spmv_img<0, DS>(colp, vals, qx, qy, qz);
+                        if (k & 1) spmv_img<1, DS>(sd, colp, sv, qx, qy, qz);
+                        else spmv_img<0, DS>(sd, colp, sv, qx, qy, qz);
                         if (a.cdiag != nullptr) {
                             const T cd = a.cdiag[i];
                             qx += cd * ax; qy += cd * ay; qz += cd * az;
@@ -392,10 +425,11 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                         dxv = c1 * dxv + e * rx;
                         dyv = c1 * dyv + e * ry;
                         dzv = c1 * dzv + e * rzz;
-                        sn[threadIdx.x] = (DS)dxv; sn[kChebSlots + threadIdx.x] = (DS)dyv; sn[2 * kChebSlots + threadIdx.x] = (DS)dzv;
+                        const DS nx = img_enc<DS>(dxv), ny = img_enc<DS>(dyv), nz = img_enc<DS>(dzv);
+                        sn[threadIdx.x] = nx; sn[kChebSlots + threadIdx.x] = ny; sn[2 * kChebSlots + threadIdx.x] = nz;
                         if ((int)threadIdx.x < nexp)
-                            ll_store(a.cheb_ll + (size_t)((k + 1) & 1) * nF * LLW + (size_t)i * LLW, (DS)dxv, (DS)dyv,
-                                     (DS)dzv, base + (unsigned)(k + 1));
+                            ll_store(a.cheb_ll + (size_t)((k + 1) & 1) * nF * LLW + (size_t)i * LLW, nx, ny, nz,
+                                     base + (unsigned)(k + 1));
                     }
                     pcg_mark(13);
                 } else {
