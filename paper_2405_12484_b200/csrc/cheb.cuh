@@ -288,22 +288,18 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     T rx = 0, ry = 0, rzz = 0, dxv = 0, dyv = 0, dzv = 0, dg = 0;
     double acc[2] = {0, 0};                        // rr, bb
     if (REG) {
-        // residual first (the corner gather's loads), then the row's ELL into registers
-        if (own) init_residual_row(a, i, false, rx, ry, rzz, acc[1]);
-        pcg_mark(16);
+        // the residual's corner gather, then the row's ELL (loading it first, live across the
+        // gather, measured slower: 25 vs 21 us per launch)
         if (own) {
+            init_residual_row(a, i, false, rx, ry, rzz, acc[1]);
 #pragma unroll
-            for (int h = 0; h < (kChebOff + 1) / 2; ++h) {
-                const unsigned c0 = (unsigned)sizeof(DS) * __ldg(&a.cheb_slot[(size_t)(2 * h) * nF + i]);
-                const unsigned c1 = 2 * h + 1 < kChebOff
-                    ? (unsigned)sizeof(DS) * __ldg(&a.cheb_slot[(size_t)(2 * h + 1) * nF + i]) : 0u;
-                colp[h] = c0 | (c1 << 16);
-            }
+            for (int h = 0; h < (kChebOff + 1) / 2; ++h) colp[h] = __ldg(&a.cheb_slot[(size_t)h * nF + i]);
 #pragma unroll
             for (int s = 0; s < kChebOff; ++s) sv[s * kChebMaxThreads] = __ldg(&a.cheb_val[(size_t)s * nF + i]);
             kdiag = __ldg(&a.cheb_kdiag[i]);
             dg = a.inv_diag[i];
         }
+        pcg_mark(16);
         if (warm) {
             // K * guess from shared memory like a step: own rows' guesses and the halo rows'
             // (written by the previous frame's launch: plain loads) into buffer 1's planes

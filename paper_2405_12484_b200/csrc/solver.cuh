@@ -275,8 +275,9 @@ struct PcgArgs {
     const int* cheb_nbr_ptr;     // CTAs whose rows a CTA's rows read (CSR over CTAs)
     const int* cheb_nbr;
     double cheb_lmin, cheb_lmax; // spectrum interval of D^-1 K_ff
-    const int* cheb_slot;        // register path, [s * nF + i]: shared-memory slot of off-diagonal entry s
-    const T* cheb_val;           //   of row i (pads: own slot, value 0), its value, and the diagonal
+    const unsigned* cheb_slot;   // register path, [h * nF + i]: direction-image byte offsets of off-diagonal
+                                 //   entries 2h, 2h+1 of row i (16 bits each; pads: a read slot, value 0),
+    const T* cheb_val;           //   [s * nF + i] the entry values, and the diagonal
     const T* cheb_kdiag;
     const int* cheb_nexp;        // per CTA: its leading rows that other CTAs read (register path)
     const int* cheb_halo_ptr;    // per CTA: rows of other CTAs its rows reference, grouped by owner CTA

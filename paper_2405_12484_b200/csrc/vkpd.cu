@@ -820,7 +820,8 @@ struct Ctx : CtxBase {
     // each step) and every ELL column's shared-memory slot.  The register path needs one row
     // per thread and the staged image within the shared-memory limit.
     int cheb_halo_max = 0;
-    DBuf<int> cheb_slot, cheb_halo_ptr, cheb_halo;
+    DBuf<unsigned> cheb_slot;
+    DBuf<int> cheb_halo_ptr, cheb_halo;
     DBuf<T> cheb_val, cheb_kdiag;
     DBuf<int> cheb_nexp, cheb_nbr_hend;
     // Entry positions of one wavefront group's rows without shared-memory bank conflicts.
@@ -1056,7 +1057,17 @@ struct Ctx : CtxBase {
         CK(cheb_nbr.alloc(lst.size())); CK(cheb_nbr.upload(lst.data(), lst.size(), stream));
         CK(cheb_halo_ptr.alloc(pcg_blocks + 1)); CK(cheb_halo_ptr.upload(hptr.data(), hptr.size(), stream));
         CK(cheb_halo.alloc(hl.size())); CK(cheb_halo.upload(hl.data(), hl.size(), stream));
-        CK(cheb_slot.alloc(oslot.size())); CK(cheb_slot.upload(oslot.data(), oslot.size(), stream));
+        // slots as packed byte offsets into the direction image (two 16-bit per word)
+        constexpr unsigned kImg = (unsigned)sizeof(typename vk::ChebImage<T>::type);
+        constexpr int kHalf = (vk::kChebOff + 1) / 2;
+        std::vector<unsigned> opack((size_t)kHalf * nn1, 0u);
+        for (int h = 0; h < kHalf; ++h)
+            for (int i = 0; i < nF; ++i) {
+                const unsigned c0 = kImg * (unsigned)oslot[(size_t)(2 * h) * nF + i];
+                const unsigned c1 = 2 * h + 1 < vk::kChebOff ? kImg * (unsigned)oslot[(size_t)(2 * h + 1) * nF + i] : 0u;
+                opack[(size_t)h * nF + i] = c0 | (c1 << 16);
+            }
+        CK(cheb_slot.alloc(opack.size())); CK(cheb_slot.upload(opack.data(), opack.size(), stream));
         CK(cheb_val.alloc(oval.size())); CK(cheb_val.upload(oval.data(), oval.size(), stream));
         CK(cheb_kdiag.alloc(kd.size())); CK(cheb_kdiag.upload(kd.data(), kd.size(), stream));
         CK(cheb_flags.alloc((size_t)32 * pcg_blocks));
