@@ -252,6 +252,24 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     const int pdi_w = a.pd_iter_dev != nullptr ? *a.pd_iter_dev : a.pd_iter;
     const bool warm = a.warm != nullptr && a.init == INIT_PD && pdi_w < a.warm_rounds;
     vec4_t<T>* const wb = warm ? a.warm + (size_t)pdi_w * nF : nullptr;
+    // ring of the last three frames' round corrections (frame f writes bank f % 3): the guess
+    // 3 d_{f-1} - 3 d_{f-2} + d_{f-3} is formed where it is read, and the finish stores one bank
+    const bool ring = REG && warm && a.warm_ring != nullptr;
+    const vec4_t<T>* g1 = nullptr;
+    const vec4_t<T>* g2 = nullptr;
+    vec4_t<T>* gw = nullptr;
+    if (ring) {
+        const unsigned f = *a.warm_ring;
+        vec4_t<T>* const R[3] = {a.warm, a.warm_prev, a.warm_prev2};
+        gw = R[f % 3u] + (size_t)pdi_w * nF;
+        g1 = R[(f + 2u) % 3u] + (size_t)pdi_w * nF;
+        g2 = R[(f + 1u) % 3u] + (size_t)pdi_w * nF;
+    }
+    auto guess_at = [&](int j) -> vec4_t<T> {
+        if (!ring) return ld4(&wb[j]);
+        const vec4_t<T> p = ld4(&g1[j]), q = ld4(&g2[j]), o = ld4(&gw[j]);
+        return make4<T>(T(3) * (p.x - q.x) + o.x, T(3) * (p.y - q.y) + o.y, T(3) * (p.z - q.z) + o.z, T(0));
+    };
 
     const double lmin = a.cheb_lmin, lmax = a.cheb_lmax;
     const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
@@ -307,14 +325,14 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
             T gx = 0, gy = 0, gz = 0;
             __syncthreads();                       // hidx
             if (own) {
-                const vec4_t<T> g = ld4(&wb[i]);
+                const vec4_t<T> g = guess_at(i);
                 gx = (T)img_dec(img_enc<DS>(g.x)); gy = (T)img_dec(img_enc<DS>(g.y));   // the guess as applied
                 gz = (T)img_dec(img_enc<DS>(g.z));
                 sg[threadIdx.x] = img_enc<DS>(gx); sg[kChebSlots + threadIdx.x] = img_enc<DS>(gy);
                 sg[2 * kChebSlots + threadIdx.x] = img_enc<DS>(gz);
             }
             for (int j = threadIdx.x; j < nh; j += blockDim.x) {
-                const vec4_t<T> g = ld4(&wb[hidx[j]]);
+                const vec4_t<T> g = guess_at(hidx[j]);
                 const int sl = blockDim.x + j;
                 sg[sl] = img_enc<DS>(g.x); sg[kChebSlots + sl] = img_enc<DS>(g.y); sg[2 * kChebSlots + sl] = img_enc<DS>(g.z);
             }
@@ -479,7 +497,9 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
         vec4_t<T> xi = a.x[j];
         xi.x += d.x; xi.y += d.y; xi.z += d.z;
         a.x[j] = xi;
-        if (warm) {
+        if (ring) {
+            gw[j] = d;
+        } else if (warm) {
             if (a.warm_prev != nullptr && pdi_w < a.warm_extrap_rounds) {
                 vec4_t<T>* wp = a.warm_prev + (size_t)pdi_w * nF;
                 const vec4_t<T> dp = ld4(&wp[j]);

@@ -96,13 +96,14 @@ template <typename T>
 __global__ void k_prologue(int n, int nF, T dt, const T* __restrict__ dt2_inv_m, const vec4_t<T>* __restrict__ f,
                            const vec4_t<T>* __restrict__ pin_tgt, vec4_t<T>* x, vec4_t<T>* v,
                            vec4_t<T>* x_start, vec4_t<T>* v_start, vec4_t<T>* xhat, int* fail_iter,
-                           int* zero2 = nullptr, int* zero1 = nullptr) {
+                           int* zero2 = nullptr, int* zero1 = nullptr, unsigned* frame_ctr = nullptr) {
     pcg_mark(10);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0) {
         *fail_iter = 0x7fffffff;
         if (zero2) { zero2[0] = 0; zero2[1] = 0; }     // suspicious-tet queue of the first local step
         if (zero1) *zero1 = 0;                          // PD-iteration counter of the loop node
+        if (frame_ctr) *frame_ctr += 1u;                // warm-start ring index (cheb.cuh)
     }
     if (i >= n) return;
     const vec4_t<T> xi = x[i], vi = v[i];
@@ -269,6 +270,8 @@ struct PcgArgs {
                                  // extrapolation d_prev + beta (d_prev - d_prevprev)
     double warm_beta;
     vec4_t<T>* warm_prev2;       // optional (cheb.cuh): the frame before that; quadratic extrapolation
+    const unsigned* warm_ring;   // optional (cheb.cuh register path): frame counter; warm, warm_prev and
+                                 // warm_prev2 are then a ring of the last three frames' corrections
     int warm_extrap_rounds;      // rounds < this extrapolate; later warm rounds reuse the last correction
     // Chebyshev solver (cheb.cuh)
     unsigned int* flags;         // per-CTA step counters, 128-B stride

@@ -317,6 +317,7 @@ struct Ctx : CtxBase {
     DBuf<V4> warm0;                      // per-round corrections of the previous frame (solver warm start)
     DBuf<V4> warm1;                      // the frame before: the guess is the linear extrapolation
     DBuf<V4> warm2;                      // the frame before that (warm_order 2): quadratic extrapolation
+    DBuf<unsigned> warm_ctr;             // frames started (k_prologue): index of the register path's ring
     int warm_order = sizeof(T) == 8 ? 2 : 1;   // fp64 C3: 8.03 -> 7.69 ms/frame steady; fp32 unchanged
     bool warm_extrap = true;             // d + beta (d - d_before), beta = 1
     double warm_beta = 1.0;
@@ -1181,6 +1182,8 @@ struct Ctx : CtxBase {
         if (warm_extrap) {
             CK(warm1.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
             CK(cudaMemsetAsync(warm1.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
+            CK(warm_ctr.alloc(1));
+            CK(cudaMemsetAsync(warm_ctr.p, 0, sizeof(unsigned), s));
             if (warm_order == 2) {
                 CK(warm2.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
                 CK(cudaMemsetAsync(warm2.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
@@ -1471,6 +1474,8 @@ struct Ctx : CtxBase {
         pa.warm_prev = (pa.warm != nullptr && warm_extrap) ? warm1.p : nullptr;
         pa.warm_beta = warm_beta;
         pa.warm_prev2 = (pa.warm_prev != nullptr && cheb) ? warm2.p : nullptr;
+        pa.warm_ring = (pa.warm_prev2 != nullptr && cheb_reg && warm_extrap_rounds >= warm_rounds) ? warm_ctr.p
+                                                                                                  : nullptr;
         pa.warm_extrap_rounds = warm_extrap_rounds;
         pa.poly_rounds = 0;
         pa.flags = cheb_flags.p; pa.cheb_nbr_ptr = cheb_nbr_ptr.p; pa.cheb_nbr = cheb_nbr.p;
@@ -1512,7 +1517,7 @@ struct Ctx : CtxBase {
         const int nb = cdiv(n, 256);
         vk::k_prologue<T><<<nb, 256, 0, stream>>>(n, nF, (T)dt, dt2_inv_m.p, has_forces ? f.p : nullptr,
                                                   pin_tgt.p, x.p, v.p, x_start.p, v_start.p, xhat.p,
-                                                  fail_iter.p);
+                                                  fail_iter.p, nullptr, nullptr, warm_ctr.p);
         CK(cudaGetLastError());
         if (ncoll > 0 && nF > 0) {
             vk::k_contact_setup<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, xhat.p, diag64.p, coll_d.p, ncoll,
@@ -1560,7 +1565,7 @@ struct Ctx : CtxBase {
         const int nb = cdiv(n, 256);
         vk::k_prologue<T><<<nb, 256, 0, stream>>>(n, nF, (T)dt, dt2_inv_m.p, has_forces ? f.p : nullptr,
                                                   pin_tgt.p, x.p, v.p, x_start.p, v_start.p, xhat.p,
-                                                  fail_iter.p, robust_count.p, pd_it.p);
+                                                  fail_iter.p, robust_count.p, pd_it.p, warm_ctr.p);
         CK(cudaGetLastError());
         if (ncoll > 0) {
             vk::k_contact_setup<T><<<cdiv(nF, 256), 256, 0, stream>>>(nF, xhat.p, diag64.p, coll_d.p, ncoll,
