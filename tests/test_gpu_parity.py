@@ -384,7 +384,8 @@ def test_c3_frame_matches_reference(prec, tol_pos, tol_disp):
     assert rel_l2(fr[0] - sc.mesh.nodes, ref - sc.mesh.nodes) < tol_disp
 
 
-@pytest.mark.parametrize("prec,tol_pos,tol_disp", [("fp32", 1e-5, 5e-2), ("fp64", 1e-10, 1e-7)])
+# measured on B200: fp64 position 9.3e-14, displacement and velocity 5.7e-11; fp32 5.8e-7 / 3.6e-4
+@pytest.mark.parametrize("prec,tol_pos,tol_disp", [("fp32", 1e-5, 5e-3), ("fp64", 1e-12, 1e-9)])
 def test_c3_fold_frame_matches_reference(prec, tol_pos, tol_disp):
     """One C3 frame inside the fold window (from the stored frame-120 state), where about 88K tets
     per PD round take the robust SL(3) path (material.py:242-287, `k_robust_tasks`), against the

@@ -9,7 +9,7 @@ for P in fp64 fp32; do
   timeout 900 ncu --metrics $M --clock-control none --csv --log-file $O/launches_$P.csv \
       python tools/profile_steady.py --warm 10 --frames 1 --graph 0 --precision $P > $O/l_$P.log 2>&1
   python tools/ncu_summarize.py $O/launches_$P.csv $O/launches_${P}_summary.json --last-frame > /dev/null
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_cheb_reg --launch-skip 300 -c 1 \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_cheb_reg --launch-skip $([ $P = fp64 ] && echo 300 || echo 40) -c 1 \
       -o $O/cheb_$P python tools/profile_steady.py --warm 10 --frames 1 --graph 0 --precision $P > $O/f_cheb_$P.log 2>&1
 done
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_local --launch-skip 300 -c 1 \
