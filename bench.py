@@ -320,7 +320,7 @@ def solver_roofline(precision, pst, n_free, peak, peak_kind, kernel):
             "steps_per_launch": steps,
             "alg_bytes_unit": f"{ALG_BYTES_SWEEP[precision]:.0f} B per free node per stencil pass (SURVEY 8d)",
             "note": "the solver's working set lives on chip (registers + shared memory + L2); per step it is "
-                    "bound by shared-memory bandwidth and neighbour-flag latency, see DESIGN.md 4"}
+                    "bound by the L2 round trip of the flag-in-data halo exchange and the exported rows' shared-memory SpMV, see DESIGN.md 4.2"}
 
 
 def run_dd(args):
@@ -460,7 +460,7 @@ def run_ours(args):
     e2e_val = world * nE * head["rounds"] / e2e_s
     peak, peak_kind = measured_peak()
     pst = head["pst"]
-    solver_kernel = ("k_cheb_reg (global step, Chebyshev-Jacobi, neighbour flags)" if pst["solver"] == "chebyshev"
+    solver_kernel = ("k_cheb_reg (global step, Chebyshev-Jacobi, neighbour-only halo exchange)" if pst["solver"] == "chebyshev"
                      else "k_pcg_poly (global step, persistent polynomial-preconditioned CG)")
     alg_local = ALG_BYTES_LOCAL[prec] * nE
     ach_local = alg_local / (head["kl_ms"] * 1e-3) / 1e9
