@@ -265,7 +265,7 @@ __device__ __forceinline__ void robust_select_one(const LocalArgs<T>& a, const d
 }
 
 #ifndef VK_RTASK_MINB
-#define VK_RTASK_MINB 1
+#define VK_RTASK_MINB 5        // 96 registers, 5 CTAs per SM: fold frame 10.0 -> 9.65 ms (1: 116 registers; 6: 80 + spills, 9.85)
 #endif
 template <typename T, int MODE>
 __global__ void __launch_bounds__(128, VK_RTASK_MINB) k_robust_tasks(LocalArgs<T> a, double* __restrict__ res,

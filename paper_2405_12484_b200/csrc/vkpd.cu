@@ -318,7 +318,10 @@ struct Ctx : CtxBase {
     DBuf<V4> warm1;                      // the frame before: the guess is the linear extrapolation
     DBuf<V4> warm2;                      // the frame before that (warm_order 2): quadratic extrapolation
     DBuf<unsigned> warm_ctr;             // frames started (k_prologue): index of the register path's ring
-    int warm_order = sizeof(T) == 8 ? 2 : 1;   // fp64 C3: 8.03 -> 7.69 ms/frame steady; fp32 unchanged
+#ifndef VK_WARM_ORDER64
+#define VK_WARM_ORDER64 2
+#endif
+    int warm_order = sizeof(T) == 8 ? VK_WARM_ORDER64 : 1;   // fp64 C3: 8.03 -> 7.69 ms/frame steady; fp32 unchanged
     bool warm_extrap = true;             // d + beta (d - d_before), beta = 1
     double warm_beta = 1.0;
     int warm_extrap_rounds = sizeof(T) == 8 ? 32 : 1;   // fp32 extrapolates round 0 only (later rounds'
