@@ -27,9 +27,6 @@ namespace sl3 {
 constexpr double kFloor = 0.01;     // material.py:25
 constexpr double kTol = 1e-12;      // material.py:30
 constexpr int kIters = 20;          // material.py:29
-#ifndef VK_SL3_LS_SEQ
-#define VK_SL3_LS_SEQ 0
-#endif
 
 // instrumentation hook for tests/native probes (iteration / line-search / round counters)
 #ifndef VK_SL3_PROBE
@@ -285,16 +282,6 @@ VK_HD bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, cons
             // steps 1/2 .. 1/32 (material.py:203-211), evaluated independently
             double step = 0.5;
             int take = 5;
-#if VK_SL3_LS_SEQ
-            for (int t = 1; t < 6; ++t) {
-                double st[3];
-#pragma unroll
-                for (int i = 0; i < 3; ++i) st[i] = fr[i] ? s[i] + step * d[i] : s[i];
-                const double rt = free_resnorm(sig, st, lam + step * d[3], fr);
-                if (rt < rn || rt < kTol) { take = t; break; }
-                step *= 0.5;
-            }
-#else
 #pragma unroll
             for (int t = 1; t < 6; ++t) {
                 double st[3];
@@ -304,7 +291,6 @@ VK_HD bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, cons
                 if (take == 5 && (rt < rn || rt < kTol)) take = t;
                 step *= 0.5;
             }
-#endif
             step = ldexp(1.0, -take);
 #pragma unroll
             for (int i = 0; i < 3; ++i) sn[i] = fr[i] ? s[i] + step * d[i] : s[i];
