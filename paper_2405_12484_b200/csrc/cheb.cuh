@@ -418,7 +418,8 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
                             const int sl = blockDim.x + j;
                             sx[sl] = hx; sx[kChebSlots + sl] = hy; sx[2 * kChebSlots + sl] = hz;
                         }
-                        asm volatile("bar.sync 1, %0;" ::"r"(exp_threads) : "memory");
+                        // non-.aligned barrier: the halo loop before it leaves the warp's lanes diverged
+                        asm volatile("barrier.sync 1, %0;" ::"r"(exp_threads) : "memory");
                         pcg_mark(12);
                     }
                     // interior warps run their rows meanwhile: they read own rows only
