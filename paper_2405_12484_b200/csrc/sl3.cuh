@@ -176,15 +176,18 @@ VK_HD int argmin3(const double (&a)[3]) {
     return j;
 }
 
-// residual of the frozen-entry system (material.py:163-168), max-norm over free + constraint
-VK_HD double free_resnorm(const double (&sig)[3], const double (&s)[3], double lam,
-                                               const bool (&fr)[3]) {
+// Residual of the frozen-entry system (material.py:163-168), max-norm over free + constraint,
+// compared with the line search's bar: rnorm < rn || rnorm < kTol, decided without forming the norm: the
+// NaN-propagating max is below thr = fmax(rn, kTol) iff every entry is (a NaN entry fails its
+// comparison; fmax(NaN, kTol) = kTol keeps the `< kTol` branch when rn is NaN).  The line search's
+// candidate steps only need this decision; it halves their FP64 compare/select work.
+VK_HD bool free_accept(const double (&sig)[3], const double (&s)[3], double lam, const bool (&fr)[3], double thr) {
     double p[3];
     pairprod(s, p);
-    double rn = fabs(s[0] * s[1] * s[2] - 1.0);
+    bool ok = fabs(s[0] * s[1] * s[2] - 1.0) < thr;     // (bitwise: no branches)
     for (int i = 0; i < 3; ++i)
-        if (fr[i]) rn = nanmax(rn, fabs(s[i] - sig[i] + lam * p[i]));
-    return rn;
+        ok &= !fr[i] || fabs(s[i] - sig[i] + lam * p[i]) < thr;
+    return ok;
 }
 
 // same residual, also returning the masked residual vector and the pair products
@@ -282,13 +285,13 @@ VK_HD bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, cons
             // steps 1/2 .. 1/32 (material.py:203-211), evaluated independently
             double step = 0.5;
             int take = 5;
+            const double thr = fmax(rn, kTol);
 #pragma unroll
             for (int t = 1; t < 6; ++t) {
                 double st[3];
 #pragma unroll
                 for (int i = 0; i < 3; ++i) st[i] = fr[i] ? s[i] + step * d[i] : s[i];
-                const double rt = free_resnorm(sig, st, lam + step * d[3], fr);
-                if (take == 5 && (rt < rn || rt < kTol)) take = t;
+                if (take == 5 && free_accept(sig, st, lam + step * d[3], fr, thr)) take = t;
                 step *= 0.5;
             }
             step = ldexp(1.0, -take);
