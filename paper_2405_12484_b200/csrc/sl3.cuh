@@ -294,7 +294,11 @@ VK_HD bool newton_free(const double (&sig)[3], double (&s)[3], double& lam, cons
                 if (take == 5 && free_accept(sig, st, lam + step * d[3], fr, thr)) take = t;
                 step *= 0.5;
             }
+#ifdef __CUDA_ARCH__
+            step = __longlong_as_double((long long)(1023 - take) << 52);   // 2^-take, exact
+#else
             step = ldexp(1.0, -take);
+#endif
 #pragma unroll
             for (int i = 0; i < 3; ++i) sn[i] = fr[i] ? s[i] + step * d[i] : s[i];
             ln = lam + step * d[3];
