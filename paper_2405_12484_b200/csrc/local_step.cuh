@@ -98,6 +98,17 @@ struct LocalArgs {
     double* F_out;               // optional (nE,3,3) (RHS mode only)
     double* R_out;
     double* V_out;
+    // optional (frame path, residual mode): warp-segmented node reduction.  The 32 tets of warp w
+    // touch wr_ptr[w+1] - wr_ptr[w] distinct nodes; entry E sums the warp's staged corner values
+    // wr_code[w*128 + wr_beg[E] ..] (lane*4 + corner) and writes node partial wpart[wr_slot[E]]
+    // (node-sorted, warps in order).  Queued (robust) tets contribute zero there and write their
+    // corners to `corner` later and mark their incidences in robust_flag (the gather clears them).
+    const int* wr_ptr;
+    const int* wr_slot;
+    const unsigned char* wr_beg;
+    const unsigned char* wr_code;
+    vec4_t<T>* wpart;
+    unsigned char* robust_flag;
 };
 
 // One tet of the local step.  COH selects coherent loads of x: required when
@@ -168,6 +179,14 @@ __device__ __forceinline__ void local_tet(const LocalArgs<T>& a, int e) {
     finish_tet<T, MODE, WITH_FRV>(a, e, g, ws, wv, F, U, W, s);
 }
 
+template <typename T>
+__device__ __forceinline__ void corner_forces(const T (&P)[3][3], const T (&g)[3][3], T (&f)[3][3]) {
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) f[n][i] = P[i][0] * g[n][0] + P[i][1] * g[n][1] + P[i][2] * g[n][2];
+}
+
 // P = U diag(ws + wv s) W^T (minus (ws+wv) F in residual mode), optional
 // (F, R, V) outputs, and the four corner contributions 2V P g_n.
 template <typename T, int MODE, bool WITH_FRV>
@@ -199,10 +218,7 @@ __device__ __forceinline__ void finish_tet(const LocalArgs<T>& a, int e, const T
     }
     // f_n = P g_n for n = 1..3, f_0 = -(f_1 + f_2 + f_3)
     T f[3][3];
-#pragma unroll
-    for (int n = 0; n < 3; ++n)
-#pragma unroll
-        for (int i = 0; i < 3; ++i) f[n][i] = P[i][0] * g[n][0] + P[i][1] * g[n][1] + P[i][2] * g[n][2];
+    corner_forces(P, g, f);
     // scatter into each node's incidence run (slot precomputed): writes are
     // fire-and-forget, and the later per-node gather reads a contiguous run
     const int4 sl = __ldg(&a.slot4[e]);
@@ -216,6 +232,92 @@ __device__ __forceinline__ void finish_tet(const LocalArgs<T>& a, int e, const T
 #ifndef VK_LOCAL_MINB64
 #define VK_LOCAL_MINB64 8      // float64 build
 #endif
+// Residual-mode first pass with the warp-segmented node reduction (north_star (a)): every lane
+// stages its tet's four corner vectors in shared memory, then lane j of the warp sums the
+// contributions of the warp's j-th distinct node in a fixed (lane, corner) order and writes one
+// partial per (warp, node).  At C3 a warp's 32 tets touch ~26 nodes and a node gets ~3 partials
+// instead of ~15 corner vectors.  Deterministic: fixed orders everywhere, no atomics.
+template <typename T>
+__device__ __forceinline__ void local_wred(const LocalArgs<T>& a, T (*stage)[128]) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    if ((e & ~31) >= a.nE) return;                 // a warp past the last tet (warp-uniform)
+    const bool valid = e < a.nE;
+    T f4[4][3] = {};
+    bool queued = false;
+    int path = 0;
+    T g[3][3], F[3][3], ws = 0, wv = 0, U[3][3], W[3][3], sig[3];
+    double s[3];
+    if (valid) {
+        load_tet<T, false>(a, e, g, ws, wv, F);
+        path = project_element(F, U, W, sig, s, 1);
+    }
+    const unsigned int m3 = __ballot_sync(0xffffffffu, valid && path == 3);
+    if (m3) {
+        const int lead = __ffs(m3) - 1;
+        int base = 0;
+        if (lane == lead) {
+            base = atomicAdd(a.robust_count, __popc(m3));
+            if (a.robust_if != 0) cudaGraphSetConditional((cudaGraphConditionalHandle)a.robust_if, 1u);
+        }
+        base = __shfl_sync(0xffffffffu, base, lead);
+        if (valid && path == 3) {
+            queued = true;
+            const int slot = base + __popc(m3 & ((1u << lane) - 1u));
+            a.robust_list[slot] = e;
+            if (a.robust_aux != nullptr) {
+                T* ax = a.robust_aux + (size_t)24 * slot;
+                ax[0] = sig[0]; ax[1] = sig[1]; ax[2] = sig[2];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) { ax[3 + k] = U[k / 3][k % 3]; ax[12 + k] = W[k / 3][k % 3]; }
+            }
+        }
+    }
+    if (valid && !queued) {
+        const T d[3] = {ws + wv * (T)s[0], ws + wv * (T)s[1], ws + wv * (T)s[2]};
+        T P[3][3];
+        udw(U, d, W, P);
+        const T c = ws + wv;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) P[i][j] -= c * F[i][j];
+        T f[3][3];
+        corner_forces(P, g, f);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            f4[0][i] = -(f[0][i] + f[1][i] + f[2][i]);
+            f4[1][i] = f[0][i]; f4[2][i] = f[1][i]; f4[3][i] = f[2][i];
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) stage[i][lane * 4 + n] = f4[n][i];
+    __syncwarp();
+    const int w = e >> 5;
+    const int e0 = w << 5;
+    const int cnt = 4 * min(32, a.nE - e0);
+    const int E0 = __ldg(&a.wr_ptr[w]), m = __ldg(&a.wr_ptr[w + 1]) - E0;
+    const unsigned char* code = a.wr_code + (size_t)w * 128;
+    for (int j = lane; j < m; j += 32) {
+        const int b = a.wr_beg[E0 + j], en = j + 1 < m ? a.wr_beg[E0 + j + 1] : cnt;
+        T sx = 0, sy = 0, sz = 0;
+        for (int k = b; k < en; ++k) {
+            const int c = code[k];
+            sx += stage[0][c]; sy += stage[1][c]; sz += stage[2][c];
+        }
+        st4(&a.wpart[__ldg(&a.wr_slot[E0 + j])], make4<T>(sx, sy, sz, T(0)));
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128, sizeof(T) == 8 ? VK_LOCAL_MINB64 : VK_LOCAL_MINB) k_local_wred(LocalArgs<T> a) {
+    pcg_mark(8);
+    __shared__ T stage[4][3][128];
+    local_wred<T>(a, stage[threadIdx.x >> 5]);
+}
+
 template <typename T, int MODE, bool WITH_FRV, int PASS = 0>
 __global__ void __launch_bounds__(128, sizeof(T) == 8 ? VK_LOCAL_MINB64 : VK_LOCAL_MINB) k_local(LocalArgs<T> a) {
     if (PASS == 1) pcg_mark(8);
@@ -262,6 +364,10 @@ __device__ __forceinline__ void robust_select_one(const LocalArgs<T>& a, const d
 #pragma unroll
     for (int k = 0; k < 9; ++k) { U[k / 3][k % 3] = ax[3 + k]; W[k / 3][k % 3] = ax[12 + k]; }
     finish_tet<T, MODE, false>(a, e, g, ws, wv, F, U, W, s);
+    if (a.wpart != nullptr) {                      // warp-reduced first pass: flag the 4 incidences
+        const int4 sl = __ldg(&a.slot4[e]);
+        a.robust_flag[sl.x] = 1; a.robust_flag[sl.y] = 1; a.robust_flag[sl.z] = 1; a.robust_flag[sl.w] = 1;
+    }
 }
 
 #ifndef VK_RTASK_MINB
@@ -271,6 +377,7 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(128, VK_RTASK_MINB) k_robust_tasks(LocalArgs<T> a, double* __restrict__ res,
                                                       int* __restrict__ okf, int* __restrict__ arrivals, int cap) {
     const int cnt = *a.robust_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.robust_count[2] = cnt;   // for the solver's gather (kept)
     if (cnt == 0) return;
     const int nch = (cnt + 31) >> 5;
     const int lane = threadIdx.x & 31;

@@ -226,6 +226,13 @@ struct PcgArgs {
     const int* inc_ptr;
     const int* inc_code;
     const vec4_t<T>* corner;
+    // optional (frame path): node partials of the local step's warp-segmented reduction
+    // (part_ptr runs over wpart) plus, when robust_present[0] > 0, the corners of the tets the
+    // robust pass finished (incidence flags robust_flag[k], cleared by the gather that reads them)
+    const int* part_ptr;
+    const vec4_t<T>* wpart;
+    unsigned char* robust_flag;
+    const int* robust_present;
     const T* m_dt2;
     const vec4_t<T>* xhat;
     const vec4_t<T>* rhs;
@@ -411,11 +418,28 @@ __device__ __forceinline__ void init_residual_row(const PcgArgs<T>& a, int i, bo
                                                   T& rzv, double& bb) {
     if (a.init == INIT_PD) {
         rx = 0; ry = 0; rzv = 0;
-        const int k0 = a.inc_ptr[i], k1 = a.inc_ptr[i + 1];
+        if (a.part_ptr != nullptr) {
+            const int p0 = __ldg(&a.part_ptr[i]), p1 = __ldg(&a.part_ptr[i + 1]);
+            for (int k = p0; k < p1; ++k) {
+                const vec4_t<T> c = ldg4(&a.wpart[k]);
+                rx += c.x; ry += c.y; rzv += c.z;
+            }
+            if (*a.robust_present > 0) {
+                const int k0 = a.inc_ptr[i], k1 = a.inc_ptr[i + 1];
+                for (int k = k0; k < k1; ++k) {
+                    if (!a.robust_flag[k]) continue;
+                    a.robust_flag[k] = 0;
+                    const vec4_t<T> c = ldg4(&a.corner[k]);
+                    rx += c.x; ry += c.y; rzv += c.z;
+                }
+            }
+        } else {
+            const int k0 = a.inc_ptr[i], k1 = a.inc_ptr[i + 1];
 #pragma unroll 4
-        for (int k = k0; k < k1; ++k) {
-            const vec4_t<T> c = coherent_corners ? ld4(&a.corner[k]) : ldg4(&a.corner[k]);
-            rx += c.x; ry += c.y; rzv += c.z;
+            for (int k = k0; k < k1; ++k) {
+                const vec4_t<T> c = coherent_corners ? ld4(&a.corner[k]) : ldg4(&a.corner[k]);
+                rx += c.x; ry += c.y; rzv += c.z;
+            }
         }
         const T m = a.m_dt2[i];
         const vec4_t<T> xh = a.xhat[i], xi = a.x[i];

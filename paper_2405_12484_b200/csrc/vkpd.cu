@@ -310,6 +310,10 @@ struct Ctx : CtxBase {
     DBuf<T> G, w, inv_diag, ell_val, fp_val, m_dt2, dt2_inv_m;
     DBuf<int> ell_col, ell_len, fp_ptr, fp_col, inc_ptr, inc_code, int_of_orig;
     DBuf<int4> slot4;
+    // warp-segmented reduction of the local step's corner vectors (frame path, local_step.cuh)
+    DBuf<int> wr_ptr, wr_slot, part_ptr;
+    DBuf<unsigned char> wr_beg, wr_code, robust_flag;
+    DBuf<V4> wpart;
     DBuf<double> diag64;
     DBuf<double> G64k, md64k;            // float64 shape gradients and m/dt^2 (re-assembly)
     std::vector<double> vol2_h;          // 2 V per tet (host)
@@ -520,6 +524,44 @@ struct Ctx : CtxBase {
                 icode[fillp[t[a]]++] = a * nE + e;
             }
         }
+        // warp-segmented reduction tables: the 32 tets of warp w (internal order) and their 128
+        // corners grouped by node (ascending node, then lane*4 + corner); node partial slots in
+        // warp order (part_ptr over nodes)
+        const int nW = cdiv(std::max(1, nE), 32);
+        std::vector<int> wrp(nW + 1, 0), pcount(n + 1, 0);
+        std::vector<std::pair<int, int>> pr;
+        auto warp_pairs = [&](int wq) {
+            pr.clear();
+            for (int l = 0; l < 32; ++l) {
+                const int e = wq * 32 + l;
+                if (e >= nE) break;
+                const int* t = &tets_h[e].x;
+                for (int c = 0; c < 4; ++c) pr.push_back({t[c], l * 4 + c});
+            }
+            std::sort(pr.begin(), pr.end());
+        };
+        for (int wq = 0; wq < nW; ++wq) {
+            warp_pairs(wq);
+            int m = 0;
+            for (size_t k = 0; k < pr.size(); ++k)
+                if (k == 0 || pr[k].first != pr[k - 1].first) { ++m; pcount[pr[k].first + 1]++; }
+            wrp[wq + 1] = wrp[wq] + m;
+        }
+        for (int i = 0; i < n; ++i) pcount[i + 1] += pcount[i];
+        std::vector<int> wslot(std::max(1, wrp[nW])), pfill(pcount.begin(), pcount.end() - 1);
+        std::vector<unsigned char> wbeg(std::max(1, wrp[nW])), wcode((size_t)nW * 128, 0);
+        for (int wq = 0; wq < nW; ++wq) {
+            warp_pairs(wq);
+            int E = wrp[wq];
+            for (size_t k = 0; k < pr.size(); ++k) {
+                wcode[(size_t)wq * 128 + k] = (unsigned char)pr[k].second;
+                if (k == 0 || pr[k].first != pr[k - 1].first) {
+                    wbeg[E] = (unsigned char)k;
+                    wslot[E] = pfill[pr[k].first]++;
+                    ++E;
+                }
+            }
+        }
         // neighbour sets of free rows -> ELL (free cols) + K_fp CSR (pin slots)
         std::vector<std::vector<int>> nb(nF);
         ell_w = 0;
@@ -581,6 +623,14 @@ struct Ctx : CtxBase {
         CK(w.alloc((size_t)2 * nE)); CK(w.upload(wp.data(), wp.size(), s));
         CK(inc_ptr.alloc(n + 1)); CK(inc_ptr.upload(iptr.data(), n + 1, s));
         CK(inc_code.alloc(icode.size())); CK(inc_code.upload(icode.data(), icode.size(), s));
+        CK(wr_ptr.alloc(wrp.size())); CK(wr_ptr.upload(wrp.data(), wrp.size(), s));
+        CK(wr_slot.alloc(wslot.size())); CK(wr_slot.upload(wslot.data(), wslot.size(), s));
+        CK(wr_beg.alloc(wbeg.size())); CK(wr_beg.upload(wbeg.data(), wbeg.size(), s));
+        CK(wr_code.alloc(wcode.size())); CK(wr_code.upload(wcode.data(), wcode.size(), s));
+        CK(part_ptr.alloc(pcount.size())); CK(part_ptr.upload(pcount.data(), pcount.size(), s));
+        CK(wpart.alloc(std::max(1, pcount[n])));
+        CK(robust_flag.alloc(std::max<size_t>(1, icode.size())));
+        CK(cudaMemsetAsync(robust_flag.p, 0, std::max<size_t>(1, icode.size()), s));
         CK(int_of_orig.alloc(n)); CK(int_of_orig.upload(ioo.data(), n, s));
         CK(ell_col.alloc(ecol.size())); CK(ell_col.upload(ecol.data(), ecol.size(), s));
         CK(ell_val.alloc(ecol.size()));
@@ -1166,7 +1216,7 @@ struct Ctx : CtxBase {
         CK(fail_iter.alloc(1));
         CK(robust_list.alloc(std::max(1, nE)));
         CK(robust_aux.alloc((size_t)24 * std::max(1, nE)));
-        CK(robust_count.alloc(2));   // [0] queued elements, [1] spare
+        CK(robust_count.alloc(3));   // [0] queued elements, [1] task cursor, [2] last pass's count
         CK(pd_it.alloc(1));
         if (c->warm_rounds >= 0) warm_rounds = std::min(32, c->warm_rounds);
         if (solver_kind == VKPD_SOLVER_PCG_JACOBI) warm_rounds = 0;
@@ -1192,7 +1242,7 @@ struct Ctx : CtxBase {
                 CK(cudaMemsetAsync(warm2.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
             }
         }
-        CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), s));
+        CK(cudaMemsetAsync(robust_count.p, 0, 3 * sizeof(int), s));
         CK(pstats.alloc(1));
         CK(cudaMemsetAsync(pstats.p, 0, sizeof(vk::ProjStats), s));
         CK(stage.alloc((size_t)3 * n));
@@ -1436,8 +1486,10 @@ struct Ctx : CtxBase {
         return upload_nodes(hf, f.p);
     }
 
-    vk::LocalArgs<T> local_args(const V4* xin) {
+    vk::LocalArgs<T> local_args(const V4* xin, bool wred = false) {
         vk::LocalArgs<T> la;
+        la.wr_ptr = wred ? wr_ptr.p : nullptr; la.wr_slot = wr_slot.p; la.wr_beg = wr_beg.p;
+        la.wr_code = wr_code.p; la.wpart = wred ? wpart.p : nullptr; la.robust_flag = robust_flag.p;
         la.nE = nE; la.tets = tets.p; la.G = G.p; la.w = w.p; la.x = xin; la.corner = corner.p;
         la.slot4 = slot4.p;
         la.stats = pstats.p; la.F_out = la.R_out = la.V_out = nullptr;
@@ -1450,7 +1502,8 @@ struct Ctx : CtxBase {
     // reset = false inside a frame: the previous PD iteration's solver kernel zeroed the queue
     int launch_local_resid(const vk::LocalArgs<T>& la, bool reset = true) {
         if (reset) CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
-        vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+        if (la.wpart != nullptr) vk::k_local_wred<T><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+        else vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
         CK(cudaGetLastError());
         // one resident wave of (chunk, start) tasks: cheap when the queue is empty
         vk::k_robust_tasks<T, vk::MODE_RESID><<<robust_task_blocks * n_sms, 128, 0, stream>>>(
@@ -1462,6 +1515,8 @@ struct Ctx : CtxBase {
         vk::PcgArgs<T> pa;
         pa.nF = nF; pa.ell_w = ell_w; pa.ell_col = ell_col.p; pa.ell_val = ell_val.p; pa.inv_diag = inv_diag.p;
         pa.inc_ptr = inc_ptr.p; pa.inc_code = inc_code.p; pa.corner = corner.p; pa.m_dt2 = m_dt2.p;
+        pa.part_ptr = nullptr; pa.wpart = wpart.p; pa.robust_flag = robust_flag.p;
+        pa.robust_present = robust_count.p + 2;
         pa.xhat = xhat.p; pa.rhs = rhs.p; pa.x = x.p; pa.r = r.p; pa.z = z.p; pa.p0 = p0.p; pa.p1 = p1.p;
         pa.q = q.p; pa.dx = dx.p; pa.partials = partials.p; pa.scal = scal.p; pa.bar = bar.p;
         pa.iters_out = iters_slot; pa.fail_iter = fail_iter.p; pa.pd_iter = pd_iter; pa.tol = tol;
@@ -1527,7 +1582,7 @@ struct Ctx : CtxBase {
                                                                       contact_k, inv_diag_c.p, cdiag.p, cb.p);
             CK(cudaGetLastError());
         }
-        const vk::LocalArgs<T> la = local_args(x.p);
+        const vk::LocalArgs<T> la = local_args(x.p, true);
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         CK(cudaStreamIsCapturing(stream, &cap));
         const bool host_exit = pd_early_exit && nF > 0 && cap == cudaStreamCaptureStatusNone;
@@ -1539,6 +1594,7 @@ struct Ctx : CtxBase {
             if (nF > 0) {
                 vk::PcgArgs<T> pa = pcg_args(vk::INIT_PD, it, iters.p + it);
                 pa.reset_count = robust_count.p;      // zero the suspicious-tet queue for the next local step
+                pa.part_ptr = part_ptr.p;             // the local step's node partials
                 CK(launch_pcg(pa));
             }
             if (ev) CK(cudaEventRecord((*ev)[3 * it + 2], stream));
@@ -1589,10 +1645,11 @@ struct Ctx : CtxBase {
         // point is an exact repeat (x unchanged), so the frame's result is the same
         const int nun = std::min(unroll_rounds, iterations);
         for (int it = 0; it < nun; ++it) {
-            const vk::LocalArgs<T> la = local_args(x.p);
+            const vk::LocalArgs<T> la = local_args(x.p, true);
             if (int rc = launch_local_resid(la, false)) return rc;
             vk::PcgArgs<T> pa = pcg_args(vk::INIT_PD, 0, iters.p);
             pa.reset_count = robust_count.p;
+                pa.part_ptr = part_ptr.p;             // the local step's node partials
             pa.pd_iter_dev = pd_it.p;
             pa.loop_handle = (unsigned long long)h;
             pa.loop_iterations = iterations;
@@ -1614,11 +1671,12 @@ struct Ctx : CtxBase {
         stream = body_stream;
         int rc = VKPD_OK;
         {
-            const vk::LocalArgs<T> la = local_args(x.p);
+            const vk::LocalArgs<T> la = local_args(x.p, true);
             rc = launch_local_resid(la, false);
             if (rc == VKPD_OK) {
                 vk::PcgArgs<T> pa = pcg_args(vk::INIT_PD, 0, iters.p);
                 pa.reset_count = robust_count.p;
+                pa.part_ptr = part_ptr.p;             // the local step's node partials
                 pa.pd_iter_dev = pd_it.p;
                 pa.first_stop = first_stop.p;
                 pa.loop_handle = (unsigned long long)h;
