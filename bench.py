@@ -495,7 +495,8 @@ def run_ours(args):
         "pd_rounds_executed_per_frame": rounds_per_frame,
         "ms_per_frame": tot_ms / args.steps,
         "roofline": solver_roofline(prec, pst, pst["n_free"], peak, peak_kind, solver_kernel.split()[0]),
-        "roofline_local": {"bound": "hbm", "kernel": "k_local (PD local step)", "achieved": ach_local,
+        "roofline_local": {"bound": "hbm", "kernel": "k_local_wred (PD local step + warp-segmented node reduction)",
+                           "achieved": ach_local,
                            "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": ach_local / peak,
                            "traffic": ncu_traffic(prec, "k_local"),
                            "alg_bytes_per_launch": alg_local, "launch_ms": head["kl_ms"],

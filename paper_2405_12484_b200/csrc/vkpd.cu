@@ -1924,13 +1924,13 @@ struct Ctx : CtxBase {
     int time_local(int reps, double* local_ms, double* pass_ms) override {
         if (nE == 0) return fail(VKPD_EINVAL, "matrix-only context has no mesh");
         if (reps < 1 || reps > 1000) return fail(VKPD_EINVAL, "reps must be in [1, 1000]");
-        const vk::LocalArgs<T> la = local_args(x.p);
+        const vk::LocalArgs<T> la = local_args(x.p, true);      // the frame's (warp-reduced) pass
         std::vector<cudaEvent_t> e(4 * reps);
         for (auto& ev : e) CK(cudaEventCreate(&ev));
         for (int r = 0; r < reps; ++r) {
             CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
             CK(cudaEventRecord(e[4 * r], stream));
-            vk::k_local<T, vk::MODE_RESID, false, 1><<<cdiv(nE, 128), 128, 0, stream>>>(la);
+            vk::k_local_wred<T><<<cdiv(nE, 128), 128, 0, stream>>>(la);
             CK(cudaEventRecord(e[4 * r + 1], stream));
             CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
             CK(cudaEventRecord(e[4 * r + 2], stream));
@@ -1948,7 +1948,8 @@ struct Ctx : CtxBase {
             b += t2;
         }
         for (auto& ev : e) cudaEventDestroy(ev);
-        CK(cudaMemsetAsync(robust_count.p, 0, 2 * sizeof(int), stream));
+        CK(cudaMemsetAsync(robust_count.p, 0, 3 * sizeof(int), stream));
+        CK(cudaMemsetAsync(robust_flag.p, 0, robust_flag.n, stream));   // no gather consumed these passes
         CK(cudaStreamSynchronize(stream));
         if (local_ms) *local_ms = a / reps;
         if (pass_ms) *pass_ms = b / reps;
