@@ -78,24 +78,26 @@ __device__ __forceinline__ void ldcg3(const double4* p, double& x, double& y, do
 
 // Exported rows cross CTAs in a flag-in-data format (the LL idea of NCCL's low-latency protocol):
 // every 8-byte word carries 4 bytes of d and the 4-byte step tag, written and read as 16-byte
-// vectors with relaxed gpu-scope accesses.  An aligned 8-byte word is single-copy atomic, so a
-// consumer that sees the tag in every word of a row has that row's d of that step: no separate
-// flag, no release barrier after the stores, no acquire round trip before the loads.  Row
+// vectors of two 64-bit elements with relaxed gpu-scope accesses.  Each naturally aligned 64-bit
+// element access is single-copy atomic, so a consumer that sees the tag in every word of a row
+// has that row's d of that step: no separate flag, no release barrier after the stores, no
+// acquire round trip before the loads.  Row
 // layout: fp64 3 x {lo, tag, hi, tag}; fp32 {x, tag, y, tag}, {z, tag, 0, tag}.
 template <typename T> struct LLRow;
 template <> struct LLRow<double> { static constexpr int W = 3; };
 template <> struct LLRow<float> { static constexpr int W = 2; };
 template <> struct LLRow<unsigned> { static constexpr int W = 2; };
 
+// words (a | b << 32), (c | d << 32): the same bytes as {a, b, c, d}
 __device__ __forceinline__ void ll_st(uint4* p, unsigned a, unsigned b, unsigned c, unsigned d) {
-    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
-                 : "memory");
+    const unsigned long long w0 = (unsigned long long)a | ((unsigned long long)b << 32);
+    const unsigned long long w1 = (unsigned long long)c | ((unsigned long long)d << 32);
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1,%2};" :: "l"(p), "l"(w0), "l"(w1) : "memory");
 }
 __device__ __forceinline__ uint4 ll_ld(const uint4* p) {
-    uint4 v;
-    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-    return v;
+    unsigned long long w0, w1;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    return make_uint4((unsigned)w0, (unsigned)(w0 >> 32), (unsigned)w1, (unsigned)(w1 >> 32));
 }
 __device__ __forceinline__ void ll_store(uint4* p, double x, double y, double z, unsigned tag) {
     const unsigned long long a = __double_as_longlong(x), b = __double_as_longlong(y), c = __double_as_longlong(z);
