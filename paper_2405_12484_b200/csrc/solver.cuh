@@ -418,8 +418,12 @@ __device__ __forceinline__ void init_residual_row(const PcgArgs<T>& a, int i, bo
                                                   T& rzv, double& bb) {
     if (a.init == INIT_PD) {
         rx = 0; ry = 0; rzv = 0;
+        // the node's own loads first (independent of the gather; the sums keep their order)
+        const T m = a.m_dt2[i];
+        const vec4_t<T> xh = a.xhat[i], xi = a.x[i];
         if (a.part_ptr != nullptr) {
             const int p0 = __ldg(&a.part_ptr[i]), p1 = __ldg(&a.part_ptr[i + 1]);
+#pragma unroll 4
             for (int k = p0; k < p1; ++k) {
                 const vec4_t<T> c = ldg4(&a.wpart[k]);
                 rx += c.x; ry += c.y; rzv += c.z;
@@ -441,8 +445,6 @@ __device__ __forceinline__ void init_residual_row(const PcgArgs<T>& a, int i, bo
                 rx += c.x; ry += c.y; rzv += c.z;
             }
         }
-        const T m = a.m_dt2[i];
-        const vec4_t<T> xh = a.xhat[i], xi = a.x[i];
         rx += m * (xh.x - xi.x);
         ry += m * (xh.y - xi.y);
         rzv += m * (xh.z - xi.z);
