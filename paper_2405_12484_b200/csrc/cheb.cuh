@@ -10,10 +10,11 @@
 // d = c1 d + c2 D^-1 res with scalar coefficients fixed by the spectrum
 // interval [lmin, lmax] of D^-1 K_ff.  Its only data dependence is the SpMV,
 // i.e. the rows a CTA reads from the CTAs that own its columns, so a step
-// waits on per-CTA release flags of those neighbour CTAs instead of a grid
-// barrier.  The residual norm is reduced (one grid barrier) only at the
-// predicted step count and then until it meets the same tolerance the CG
-// uses (|r| <= tol |M/dt^2 xhat|).
+// waits for those rows only (register path: each row carries its step tag,
+// below; generic path: per-CTA release flags) instead of a grid barrier.  The
+// residual norm is reduced (one grid barrier) only at the predicted step count
+// and then until it meets the same tolerance the CG uses
+// (|r| <= tol |M/dt^2 xhat|).
 //
 // Spectrum: lmax is the Gershgorin bound of D^-1 K_ff (rigorous), lmin a
 // Lanczos estimate of the smallest eigenvalue of D^-1/2 K_ff D^-1/2 computed
@@ -24,13 +25,14 @@
 // c_i to both K_ii and the mass term, which keeps both bounds valid.
 //
 // When a CTA owns at most one row per thread (the C3 case) the row state
-// lives in registers (residual, accumulated correction, direction d), the
-// row's ELL values in shared memory, and the SpMV reads d from a shared-memory
-// image of the CTA's own rows plus its halo (the rows of other CTAs its rows
-// reference, loaded from L2 once per step, one coalesced pass): each
-// neighbour value crosses L2 once per CTA instead of once per reference.
-// Only d crosses CTAs (global, double-buffered by step parity).  All
-// arithmetic has a fixed order, so results are bit-reproducible run to run.
+// lives in registers (residual, direction d, packed column offsets), the
+// row's ELL values and accumulated correction in shared memory, and the SpMV
+// reads a 32-bit image of d from shared memory over the CTA's own rows plus
+// its halo (the rows of other CTAs its rows reference, loaded from L2 once per
+// step): each neighbour value crosses L2 once per CTA instead of once per
+// reference.  Only the exported rows' d crosses CTAs (flag-in-data rows,
+// double-buffered by step parity).  All arithmetic has a fixed order, so
+// results are bit-reproducible run to run.
 #pragma once
 
 #include "solver.cuh"
@@ -141,18 +143,19 @@ __device__ __forceinline__ void ll_load(const uint4* p, unsigned tag, unsigned& 
     x = __float_as_uint(fx); y = __float_as_uint(fy); z = __float_as_uint(fz);
 }
 
-// Register path: a row keeps its kChebOff off-diagonal ELL values and their shared-memory
-// slots in registers (plus the diagonal), so the SpMV's shared-memory traffic is only the
-// neighbours' d.  Shared-memory image (compile-time strides, so every access is one address
-// register plus an immediate offset): two step-parity buffers of the x / y / z planes of d
-// over kChebSlots slots (own rows: slot = tid; halo row j: slot = blockDim.x + j), the
-// x / y / z planes of the accumulated correction y (own rows), then the halo rows' global
-// indices.
+// Register path: a row keeps the shared-memory byte offsets of its kChebOff off-diagonal
+// entries in registers (two 16-bit offsets per register, positions bank-conflict-free per warp,
+// vkpd.cu conflict_free_positions) and the diagonal.  Shared memory (compile-time strides, so
+// every access is one address register plus an immediate offset): two step-parity buffers of
+// the x / y / z planes of the image of d over kChebSlots slots (own rows: slot = tid; halo row
+// j: slot = blockDim.x + j), the x / y / z planes of the accumulated correction y, the 14 planes
+// of the rows' ELL values (thread-indexed: conflict-free), then the halo rows' global indices.
 //
 // Exported rows first: the rows other CTAs read (a CTA's exported rows lead its row range,
-// vkpd.cu patch_order) are computed by the leading warps, which meet on a named barrier and
-// publish the step flag as soon as their d is in global memory; the interior rows (read by
-// nobody else, kept in shared memory only) finish while the flag travels.
+// vkpd.cu patch_order) are computed by the leading warps, which also load the halo rows (one
+// per thread) and store their new d in the flag-in-data format as soon as it is computed; the
+// interior rows (read by nobody else, kept in shared memory only) are computed by the other
+// warps while the exported warps wait for the halo.
 constexpr int kChebMaxThreads = 768;
 constexpr int kChebSlots = 2048;
 constexpr int kChebOff = 14;       // voxel enclosures: <= 15 entries per row, one of them diagonal
@@ -294,8 +297,7 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     T* yv = yv0 + threadIdx.x;                     // REG: this row's y, planes kChebMaxThreads apart
     T* const sv = yv0 + 3 * kChebMaxThreads + threadIdx.x;   // REG: this row's ELL values, planes apart
     int* hidx = reinterpret_cast<int*>(yv0 + (3 + kChebOff) * kChebMaxThreads);   // REG: halo rows
-    // exported rows [row0, row0 + nexp) belong to the leading warps (at least warp 0, which
-    // publishes the step flag)
+    // exported rows [row0, row0 + nexp) belong to the leading warps
     const int nexp = REG ? a.cheb_nexp[blockIdx.x] : 0;
     // the exported-warp group also covers the halo rows: one halo row per thread, one L2 round trip
     const int nh = REG ? a.cheb_halo_ptr[blockIdx.x + 1] - a.cheb_halo_ptr[blockIdx.x] : 0;
