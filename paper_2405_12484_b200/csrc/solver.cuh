@@ -281,7 +281,8 @@ struct PcgArgs {
                                  // warm_prev2 are then a ring of the last three frames' corrections
     int warm_extrap_rounds;      // rounds < this extrapolate; later warm rounds reuse the last correction
     // Chebyshev solver (cheb.cuh)
-    unsigned int* flags;         // per-CTA step counters, 128-B stride
+    unsigned int* flags;         // per-CTA step counters (generic path) / tag base of the next launch
+                                 // (register path), 128-B stride
     const int* cheb_nbr_ptr;     // CTAs whose rows a CTA's rows read (CSR over CTAs)
     const int* cheb_nbr;
     double cheb_lmin, cheb_lmax; // spectrum interval of D^-1 K_ff
