@@ -4,7 +4,10 @@ Rebuilds the library's row layout on the host (patch_order: RCB patches, exporte
 build_cheb_neighbours: canonical entry order, halo slots) and counts, per warp and entry
 position, the wavefronts of the 64-bit shared loads: a warp's LDS.64 is served per half-warp,
 and a half-warp needs as many wavefronts as the most distinct slots that share a bank pair
-(slot mod 16).  Compares orderings of the rows inside a patch.
+(slot mod 16).  Compares orderings of the rows inside a patch, and bounds what re-assigning
+entries to positions can reach (the bipartite edge colouring the library now does per warp in
+vkpd.cu conflict_free_positions; the shipped image of d is 32-bit, served per 32-lane warp with
+bank = slot mod 32, and the same colouring is applied with 32 lanes x 32 banks).
 
     python tools/dbg/bank_model.py [C3|C2]
 """
