@@ -352,6 +352,47 @@ def test_chebyshev_without_rest_positions():
     assert rel_l2(outs[1], outs[0]) < 1e-11
 
 
+def _c2_frames_ctx(tets, shape_grad, volume, gs, gv, frames=5, **cfg):
+    from paper_2405_12484_b200 import _abi
+    sc = scenes.make_scene("C2")
+    m = sc.mesh
+    ctx = _abi.Context(m.n_nodes, tets, shape_grad, volume, m.node_mass, gs, gv, sc.pins, sc.dt,
+                       precision="fp64", tol=1e-12, nodes=m.nodes, **cfg)
+    ctx.set_state(m.nodes)
+    ctx.set_pin_targets(sc.pin_targets)
+    ctx.set_forces(sc.forces)
+    for _ in range(frames):
+        ctx.step(30)
+    return ctx.get_state()[0]
+
+
+def test_shuffled_tet_order_same_frames():
+    """The local step's warp-segmented node reduction groups each warp's 32 tets by node; with the
+    tets in random order a warp touches ~100 distinct nodes (more than its 32 lanes, the
+    multi-pass branch) and a node gets partials from many warps.  Same physics, different
+    summation order: C2 after 5 frames to 1e-11."""
+    sc = scenes.make_scene("C2")
+    m = sc.mesh
+    perm = np.random.default_rng(7).permutation(m.n_elements)
+    a = _c2_frames_ctx(m.tets, m.shape_grad, m.volume, sc.gammas.gamma_s, sc.gammas.gamma_v)
+    b = _c2_frames_ctx(np.ascontiguousarray(m.tets[perm]), np.ascontiguousarray(m.shape_grad[perm]),
+                       np.ascontiguousarray(m.volume[perm]), np.ascontiguousarray(sc.gammas.gamma_s[perm]),
+                       np.ascontiguousarray(sc.gammas.gamma_v[perm]))
+    assert rel_l2(b, a) < 1e-11
+
+
+@pytest.mark.parametrize("blocks", [37, 100])
+def test_chebyshev_cta_count_same_frames(blocks):
+    """Other CTA counts give other patches, halos, exported sets and bank colourings of the
+    Chebyshev register path (flag-in-data exchange): same solution to the tolerance."""
+    sc = scenes.make_scene("C2")
+    m = sc.mesh
+    a = _c2_frames_ctx(m.tets, m.shape_grad, m.volume, sc.gammas.gamma_s, sc.gammas.gamma_v)
+    b = _c2_frames_ctx(m.tets, m.shape_grad, m.volume, sc.gammas.gamma_s, sc.gammas.gamma_v,
+                       pcg_blocks=blocks, solver="chebyshev")
+    assert rel_l2(b, a) < 1e-11
+
+
 def test_pin_path_and_per_step_forces(c1):
     steps = 3
     path = np.stack([c1.pin_targets + np.array([0.0, 0.0, 1e-3 * k]) for k in range(steps)])
