@@ -83,8 +83,9 @@ typedef struct {
     int device;        /* CUDA device ordinal                                            */
     int pcg_blocks;    /* CTAs of the persistent solver (<= 0: one per SM)               */
     int use_graph;     /* capture a whole frame in a CUDA graph (1, default) or not (0)  */
-    int solver;        /* global step: VKPD_SOLVER_AUTO (0: fp64 -> Chebyshev, fp32 ->     */
-                       /* polynomial CG), _PCG_POLY, _CHEBYSHEV, _PCG_JACOBI               */
+    int solver;        /* global step: VKPD_SOLVER_AUTO (0: Chebyshev where its register   */
+                       /* path applies -- one row per thread -- else polynomial CG),       */
+                       /* _PCG_POLY, _CHEBYSHEV, _PCG_JACOBI                                */
     int pd_early_exit; /* stop a frame's PD rounds at the first zero-work solve (<0: on)  */
     int warm_rounds;   /* PD rounds warm-started from earlier frames (<0: default)        */
     int unroll_rounds; /* PD rounds captured ahead of the graph's WHILE node (<0: adaptive) */

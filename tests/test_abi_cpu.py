@@ -73,3 +73,26 @@ def test_kernel_math_on_host_matches_reference(host_proj_binary, tmp_path, prec,
     RV = np.fromfile(fout).reshape(2, -1, 3, 3)
     assert np.abs(RV[0] - g["R"]).max() < tol_r
     assert np.abs(RV[1] - g["V"]).max() < tol_v
+
+
+def _header_struct_fields(name):
+    """Field names of `typedef struct { ... } name;` in include/vkpd.h, in order."""
+    import re
+    txt = open(os.path.join(ROOT, "include", "vkpd.h")).read()
+    end = re.search(r"\}\s*" + name + ";", txt).start()
+    body = txt[txt.rindex("typedef struct {", 0, end) + len("typedef struct {"):end]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    return [re.findall(r"(\w+)\s*;", d)[0] for d in body.split(";")[:-1] for d in [d + ";"]]
+
+
+def test_ctypes_structs_mirror_the_header():
+    """The ctypes mirrors (the package's and the one INTEGRATION.md shows a maintainer) have the
+    header's fields in the header's order: a drifted struct would pass garbage to the library."""
+    import re
+    from paper_2405_12484_b200 import _abi
+    for struct, cls in (("vkpd_config", _abi.Config), ("vkpd_mesh_desc", _abi.MeshDesc)):
+        assert [f[0] for f in cls._fields_] == _header_struct_fields(struct), struct
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    snippet = re.search(r"class Config\(C\.Structure\):(.*?)\]\s", doc, re.S).group(1)
+    assert re.findall(r'\("(\w+)"', snippet) == _header_struct_fields("vkpd_config")
+
