@@ -381,10 +381,12 @@ def test_shuffled_tet_order_same_frames():
     assert rel_l2(b, a) < 1e-11
 
 
-@pytest.mark.parametrize("blocks", [37, 100])
+@pytest.mark.parametrize("blocks", [4, 37, 100])
 def test_chebyshev_cta_count_same_frames(blocks):
     """Other CTA counts give other patches, halos, exported sets and bank colourings of the
-    Chebyshev register path (flag-in-data exchange): same solution to the tolerance."""
+    Chebyshev register path (flag-in-data exchange); 4 CTAs own ~1,900 rows each, more than a
+    CTA's threads, so that run takes the generic Chebyshev path (per-CTA step flags): same
+    solution to the tolerance."""
     sc = scenes.make_scene("C2")
     m = sc.mesh
     a = _c2_frames_ctx(m.tets, m.shape_grad, m.volume, sc.gammas.gamma_s, sc.gammas.gamma_v)
