@@ -262,18 +262,27 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
     const bool ring = REG && warm && a.warm_ring != nullptr;
     const vec4_t<T>* g1 = nullptr;
     const vec4_t<T>* g2 = nullptr;
+    const vec4_t<T>* g3 = nullptr;
     vec4_t<T>* gw = nullptr;
     if (ring) {
         const unsigned f = *a.warm_ring;
-        vec4_t<T>* const R[3] = {a.warm, a.warm_prev, a.warm_prev2};
-        gw = R[f % 3u] + (size_t)pdi_w * nF;
-        g1 = R[(f + 2u) % 3u] + (size_t)pdi_w * nF;
-        g2 = R[(f + 1u) % 3u] + (size_t)pdi_w * nF;
+        vec4_t<T>* const R[4] = {a.warm, a.warm_prev, a.warm_prev2, a.warm_prev3};
+        gw = R[f % 4u] + (size_t)pdi_w * nF;          // d_{f-4}, overwritten by this frame's finish
+        g1 = R[(f + 3u) % 4u] + (size_t)pdi_w * nF;
+        g2 = R[(f + 2u) % 4u] + (size_t)pdi_w * nF;
+        g3 = R[(f + 1u) % 4u] + (size_t)pdi_w * nF;
     }
+    // cubic extrapolation 4 d1 - 6 d2 + 4 d3 - d4 while the motion is smooth (no tet took the
+    // robust SL(3) path this round), quadratic 3 d1 - 3 d2 + d3 otherwise: the cubic saves 9% of
+    // the steps in steady frames and costs 4% in the fold frames (C3 210-frame series)
+    const bool smooth = ring && *a.robust_present == 0;
+    const T w1 = smooth ? T(4) : T(3), w2 = smooth ? T(-6) : T(-3), w3 = smooth ? T(4) : T(1),
+            w4 = smooth ? T(-1) : T(0);
     auto guess_at = [&](int j) -> vec4_t<T> {
         if (!ring) return ld4(&wb[j]);
-        const vec4_t<T> p = ld4(&g1[j]), q = ld4(&g2[j]), o = ld4(&gw[j]);
-        return make4<T>(T(3) * (p.x - q.x) + o.x, T(3) * (p.y - q.y) + o.y, T(3) * (p.z - q.z) + o.z, T(0));
+        const vec4_t<T> p = ld4(&g1[j]), q = ld4(&g2[j]), o = ld4(&g3[j]), u = ld4(&gw[j]);
+        return make4<T>(w1 * p.x + w2 * q.x + w3 * o.x + w4 * u.x, w1 * p.y + w2 * q.y + w3 * o.y + w4 * u.y,
+                        w1 * p.z + w2 * q.z + w3 * o.z + w4 * u.z, T(0));
     };
 
     const double lmin = a.cheb_lmin, lmax = a.cheb_lmax;

@@ -277,6 +277,7 @@ struct PcgArgs {
                                  // extrapolation d_prev + beta (d_prev - d_prevprev)
     double warm_beta;
     vec4_t<T>* warm_prev2;       // optional (cheb.cuh): the frame before that; quadratic extrapolation
+    vec4_t<T>* warm_prev3;       // ring mode: the fourth bank
     const unsigned* warm_ring;   // optional (cheb.cuh register path): frame counter; warm, warm_prev and
                                  // warm_prev2 are then a ring of the last three frames' corrections
     int warm_extrap_rounds;      // rounds < this extrapolate; later warm rounds reuse the last correction

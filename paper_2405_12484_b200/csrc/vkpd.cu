@@ -321,6 +321,7 @@ struct Ctx : CtxBase {
     DBuf<V4> warm0;                      // per-round corrections of the previous frame (solver warm start)
     DBuf<V4> warm1;                      // the frame before: the guess is the linear extrapolation
     DBuf<V4> warm2;                      // the frame before that (warm_order 2): quadratic extrapolation
+    DBuf<V4> warm3;                      // register-path ring: the fourth bank
     DBuf<unsigned> warm_ctr;             // frames started (k_prologue): index of the register path's ring
 #ifndef VK_WARM_ORDER64
 #define VK_WARM_ORDER64 2
@@ -1150,6 +1151,7 @@ struct Ctx : CtxBase {
         if (warm0.p) CK(cudaMemsetAsync(warm0.p, 0, warm0.n * sizeof(V4), stream));
         if (warm1.p) CK(cudaMemsetAsync(warm1.p, 0, warm1.n * sizeof(V4), stream));
         if (warm2.p) CK(cudaMemsetAsync(warm2.p, 0, warm2.n * sizeof(V4), stream));
+        if (warm3.p) CK(cudaMemsetAsync(warm3.p, 0, warm3.n * sizeof(V4), stream));
         if (graph_exec) { cudaGraphExecDestroy(graph_exec); graph_exec = nullptr; }
         CK(cudaStreamSynchronize(stream));
         return VKPD_OK;
@@ -1240,6 +1242,8 @@ struct Ctx : CtxBase {
             if (warm_order == 2) {
                 CK(warm2.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
                 CK(cudaMemsetAsync(warm2.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
+                CK(warm3.alloc((size_t)std::max(1, warm_rounds) * std::max(1, nF)));
+                CK(cudaMemsetAsync(warm3.p, 0, (size_t)std::max(1, warm_rounds) * std::max(1, nF) * sizeof(V4), s));
             }
         }
         CK(cudaMemsetAsync(robust_count.p, 0, 3 * sizeof(int), s));
@@ -1410,7 +1414,7 @@ struct Ctx : CtxBase {
         }
         k_state_in<T><<<cdiv(n, 256), 256, 0, stream>>>(n, pv, int_of_orig.p, v.p, state_changed.p);
         CK(cudaGetLastError());
-        for (DBuf<V4>* b : {&warm0, &warm1, &warm2})
+        for (DBuf<V4>* b : {&warm0, &warm1, &warm2, &warm3})
             if (b->p) k_zero_if<T><<<2 * n_sms, 256, 0, stream>>>(b->n, b->p, state_changed.p);
         CK(cudaGetLastError());
         if (!dev) CK(cudaStreamSynchronize(stream));
@@ -1532,7 +1536,8 @@ struct Ctx : CtxBase {
         pa.warm_prev = (pa.warm != nullptr && warm_extrap) ? warm1.p : nullptr;
         pa.warm_beta = warm_beta;
         pa.warm_prev2 = (pa.warm_prev != nullptr && cheb) ? warm2.p : nullptr;
-        pa.warm_ring = (pa.warm_prev2 != nullptr && cheb_reg && warm_extrap_rounds >= warm_rounds) ? warm_ctr.p
+        pa.warm_prev3 = pa.warm_prev2 != nullptr ? warm3.p : nullptr;
+        pa.warm_ring = (pa.warm_prev3 != nullptr && cheb_reg && warm_extrap_rounds >= warm_rounds) ? warm_ctr.p
                                                                                                   : nullptr;
         pa.warm_extrap_rounds = warm_extrap_rounds;
         pa.poly_rounds = 0;
