@@ -273,10 +273,11 @@ __device__ __forceinline__ void cheb_body(const PcgArgs<T>& a, cg::grid_group& g
         g3 = R[(f + 1u) % 4u] + (size_t)pdi_w * nF;
     }
     // cubic extrapolation 4 d1 - 6 d2 + 4 d3 - d4 while the motion is smooth (no tet took the
-    // robust SL(3) path this round), quadratic 3 d1 - 3 d2 + d3 otherwise: the cubic saves 9% of
-    // the steps in steady frames and costs 4% in the fold frames (C3 210-frame series)
+    // robust SL(3) path this round), the last frame's correction d1 otherwise (C3 210-frame
+    // series, steps per steady / fold frame: quadratic 1,070 / 1,920, cubic 971 / 2,006, linear in
+    // the fold 1,844, constant 1,793)
     const bool smooth = ring && *a.robust_present == 0;
-    const T w1 = smooth ? T(4) : T(3), w2 = smooth ? T(-6) : T(-3), w3 = smooth ? T(4) : T(1),
+    const T w1 = smooth ? T(4) : T(1), w2 = smooth ? T(-6) : T(0), w3 = smooth ? T(4) : T(0),
             w4 = smooth ? T(-1) : T(0);
     auto guess_at = [&](int j) -> vec4_t<T> {
         if (!ring) return ld4(&wb[j]);
