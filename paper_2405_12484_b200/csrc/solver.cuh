@@ -293,7 +293,6 @@ struct PcgArgs {
     const T* cheb_kdiag;
     const int* cheb_nexp;        // per CTA: its leading rows that other CTAs read (register path)
     const int* cheb_halo_ptr;    // per CTA: rows of other CTAs its rows reference, grouped by owner CTA
-    const int* cheb_nbr_hend;    // per (CTA, neighbour): end of that neighbour's rows in the CTA's halo
     const int* cheb_halo;
     int cheb_halo_max;
     uint4* cheb_ll;              // REG: exported rows of d, flag-in-data, two step-parity buffers of nF rows

@@ -878,7 +878,7 @@ struct Ctx : CtxBase {
     DBuf<unsigned> cheb_slot;
     DBuf<int> cheb_halo_ptr, cheb_halo;
     DBuf<T> cheb_val, cheb_kdiag;
-    DBuf<int> cheb_nexp, cheb_nbr_hend;
+    DBuf<int> cheb_nexp;
     // Entry positions of one wavefront group's rows without shared-memory bank conflicts.
     // k_cheb_reg's SpMV loads d[slot[o]] for o = 0..13 at once across a warp; a 32-bit load is
     // served per warp (32 lanes, bank = slot mod 32), a 64-bit one per half-warp (16 lanes, bank
@@ -1002,7 +1002,7 @@ struct Ctx : CtxBase {
         // per CTA: neighbour CTAs and halo rows, grouped by owner CTA (in neighbour order: the
         // kernel loads each neighbour's rows as soon as its flag arrives); within a group in
         // first-use order over (position, row), so a warp's halo reads are consecutive too
-        std::vector<int> ptr(pcg_blocks + 1, 0), lst, hptr(pcg_blocks + 1, 0), hl, hend;
+        std::vector<int> ptr(pcg_blocks + 1, 0), lst, hptr(pcg_blocks + 1, 0), hl;
         std::vector<int> oslot((size_t)vk::kChebOff * nn1);
         std::vector<int> nbr_pos(pcg_blocks, -1);
         std::vector<int> hslot(nn1, -1);
@@ -1032,13 +1032,6 @@ struct Ctx : CtxBase {
                              [&](int x, int y) { return nbr_pos[x / chunk] < nbr_pos[y / chunk]; });
             const int h0 = (int)hl.size();
             for (size_t j = 0; j < first.size(); ++j) { hslot[first[j]] = (int)j; hl.push_back(first[j]); }
-            const int nnb = (int)lst.size() - n0;
-            for (int q = 0; q < nnb; ++q) {
-                int e = 0;
-                for (size_t j = 0; j < first.size(); ++j)
-                    if (nbr_pos[first[j] / chunk] <= q) e = (int)j + 1;
-                hend.push_back(e);
-            }
             for (int o = 0; o < vk::kChebOff; ++o)
                 for (int i = r0; i < r1; ++i) {
                     const int c = ocol[(size_t)o * nF + i];
@@ -1079,8 +1072,6 @@ struct Ctx : CtxBase {
             hptr[b + 1] = (int)hl.size();
             cheb_halo_max = std::max(cheb_halo_max, (int)hl.size() - h0);
         }
-        if (hend.empty()) hend.push_back(0);
-        CK(cheb_nbr_hend.alloc(hend.size())); CK(cheb_nbr_hend.upload(hend.data(), hend.size(), stream));
         if (lst.empty()) lst.push_back(0);
         if (hl.empty()) hl.push_back(0);
         // exported rows (read by another CTA) must lead each CTA's range for the early publish;
@@ -1545,7 +1536,7 @@ struct Ctx : CtxBase {
         pa.cheb_ll = cheb_ll.p;
         pa.cheb_lmin = lam_min; pa.cheb_lmax = gersh;
         pa.cheb_slot = cheb_slot.p; pa.cheb_val = cheb_val.p; pa.cheb_kdiag = cheb_kdiag.p;
-        pa.cheb_nexp = cheb_nexp.p; pa.cheb_nbr_hend = cheb_nbr_hend.p;
+        pa.cheb_nexp = cheb_nexp.p;
         pa.cheb_halo_ptr = cheb_halo_ptr.p; pa.cheb_halo = cheb_halo.p;
         pa.cheb_halo_max = cheb_halo_max;
         pa.h = hh.p; pa.omega = poly_omega; pa.ell_kd = ell_kd.p;
