@@ -238,7 +238,7 @@ __device__ __forceinline__ void finish_tet(const LocalArgs<T>& a, int e, const T
 // partial per (warp, node).  At C3 a warp's 32 tets touch ~26 nodes and a node gets ~3 partials
 // instead of ~15 corner vectors.  Deterministic: fixed orders everywhere, no atomics.
 template <typename T>
-__device__ __forceinline__ void local_wred(const LocalArgs<T>& a, T (*stage)[128]) {
+__device__ __forceinline__ void local_wred(const LocalArgs<T>& a, T (*stage)[128], unsigned* scode) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     if ((e & ~31) >= a.nE) return;                 // a warp past the last tet (warp-uniform)
@@ -290,16 +290,18 @@ __device__ __forceinline__ void local_wred(const LocalArgs<T>& a, T (*stage)[128
             f4[1][i] = f[0][i]; f4[2][i] = f[1][i]; f4[3][i] = f[2][i];
         }
     }
+    const int w = e >> 5;
+    const int e0 = w << 5;
+    const int cnt = 4 * min(32, a.nE - e0);
+    // the warp's 128 codes into shared memory (one coalesced load) next to the staged values
+    scode[lane] = __ldg(reinterpret_cast<const unsigned*>(a.wr_code + (size_t)w * 128) + lane);
 #pragma unroll
     for (int n = 0; n < 4; ++n)
 #pragma unroll
         for (int i = 0; i < 3; ++i) stage[i][lane * 4 + n] = f4[n][i];
-    __syncwarp();
-    const int w = e >> 5;
-    const int e0 = w << 5;
-    const int cnt = 4 * min(32, a.nE - e0);
     const int E0 = __ldg(&a.wr_ptr[w]), m = __ldg(&a.wr_ptr[w + 1]) - E0;
-    const unsigned char* code = a.wr_code + (size_t)w * 128;
+    __syncwarp();
+    const unsigned char* code = reinterpret_cast<const unsigned char*>(scode);
     for (int j = lane; j < m; j += 32) {
         const int b = a.wr_beg[E0 + j], en = j + 1 < m ? a.wr_beg[E0 + j + 1] : cnt;
         T sx = 0, sy = 0, sz = 0;
@@ -315,7 +317,8 @@ template <typename T>
 __global__ void __launch_bounds__(128, sizeof(T) == 8 ? VK_LOCAL_MINB64 : VK_LOCAL_MINB) k_local_wred(LocalArgs<T> a) {
     pcg_mark(8);
     __shared__ T stage[4][3][128];
-    local_wred<T>(a, stage[threadIdx.x >> 5]);
+    __shared__ unsigned scode[4][32];
+    local_wred<T>(a, stage[threadIdx.x >> 5], scode[threadIdx.x >> 5]);
 }
 
 template <typename T, int MODE, bool WITH_FRV, int PASS = 0>
