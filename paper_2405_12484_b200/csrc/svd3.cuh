@@ -19,14 +19,25 @@ template <typename T>
 VK_HD void jacobi_rotate(T (&a)[3][3], T (&W)[3][3], int p, int q) {
     const T apq = a[p][q];
     if (apq == T(0)) return;
-    const T theta = (a[q][q] - a[p][p]) / (T(2) * apq);
-    const T at = fabs(theta);
     T t;
-    if (at > T(1e15)) {
-        t = T(0.5) / theta;
+    if constexpr (sizeof(T) == 8) {
+        // t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)), theta = tau / b (tau = a_qq - a_pp,
+        // b = 2 a_pq) multiplied through by |b|: one division instead of two.  The sign rule keeps
+        // theta = -0 -> t = +1; if the squares underflow (|tau|, |b| < 1e-154) and tau = 0 the
+        // denominator is 0 and t = 1 is theta = 0's value.
+        const T tau = a[q][q] - a[p][p], b = T(2) * apq;
+        const T ab = fabs(b), at = fabs(tau), den = at + sqrt(at * at + ab * ab);
+        t = den > T(0) ? ab / den : T(1);
+        t = (tau != T(0) && ((tau < T(0)) != (b < T(0)))) ? -t : t;
     } else {
-        t = T(1) / (at + sqrt(at * at + T(1)));
-        t = theta < T(0) ? -t : t;
+        const T theta = (a[q][q] - a[p][p]) / (T(2) * apq);
+        const T at = fabs(theta);
+        if (at > T(1e15)) {
+            t = T(0.5) / theta;
+        } else {
+            t = T(1) / (at + sqrt(at * at + T(1)));
+            t = theta < T(0) ? -t : t;
+        }
     }
     const T c = rsqrt_(t * t + T(1));
     const T s = t * c;
